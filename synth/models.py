@@ -1,0 +1,143 @@
+"""Workload recipes: the shapes of the paper's models as synthetic layer stacks.
+
+PAPER.md §5.1 (lines 440-444) evaluates Llama-3 70B and Mixtral 8x7B in bf16
+with fp32 copies of params, grads and Adam states; BASELINE.json's configs add a
+Llama-3 8B-shaped stack and the 4-layer MLP of config 1.  The synthetic layer
+keeps the 7 Llama projections at their real shapes; the attention core is a
+token-local surrogate.
+
+The parameter table is listed in first-use order of the forward pass, which is
+the order the fully-sharded rewrite gathers them in (§4.1).
+The compute-op graph (which op consumes which parameter) is also defined here:
+it is the workload's structure, not the method.
+"""
+from dataclasses import dataclass, field
+from typing import List, Tuple
+
+from .gen import std_to_k, K_MLP
+
+WEIGHT_STD = 0.02
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    name: str
+    kind: str            # "llama" | "mlp"
+    hidden: int
+    ffn: int
+    n_heads: int
+    n_kv: int
+    head_dim: int
+    layers: int
+    seq: int = 2048
+    batch: int = 1
+
+    @property
+    def tokens(self) -> int:
+        return self.seq * self.batch
+
+    @property
+    def q_dim(self) -> int:
+        return self.n_heads * self.head_dim
+
+    @property
+    def kv_dim(self) -> int:
+        return self.n_kv * self.head_dim
+
+
+@dataclass(frozen=True)
+class ParamSpec:
+    id: int              # global id == generator tensor_id == S_0 first-use order
+    layer: int
+    name: str
+    shape: Tuple[int, ...]
+    k: float             # generator scale; 0.0 means "constant 1.0" (norm gain)
+    dtype: str           # "bf16" | "fp32"
+
+    @property
+    def numel(self) -> int:
+        n = 1
+        for s in self.shape:
+            n *= s
+        return n
+
+    @property
+    def elem_bytes(self) -> int:
+        return 2 if self.dtype == "bf16" else 4
+
+
+LLAMA_NAMES = ("attn_norm", "wq", "wk", "wv", "wo", "mlp_norm", "wgate", "wup", "wdown")
+
+
+def llama_param_table(cfg: ModelConfig) -> List[ParamSpec]:
+    kw = float(std_to_k(WEIGHT_STD))
+    h, f, qd, kvd = cfg.hidden, cfg.ffn, cfg.q_dim, cfg.kv_dim
+    shapes = {
+        "attn_norm": (h,), "wq": (qd, h), "wk": (kvd, h), "wv": (kvd, h),
+        "wo": (h, qd), "mlp_norm": (h,), "wgate": (f, h), "wup": (f, h),
+        "wdown": (h, f),
+    }
+    out = []
+    for l in range(cfg.layers):
+        for j, nm in enumerate(LLAMA_NAMES):
+            out.append(ParamSpec(id=l * len(LLAMA_NAMES) + j, layer=l, name=nm,
+                                 shape=shapes[nm],
+                                 k=0.0 if nm.endswith("norm") else kw,
+                                 dtype="bf16"))
+    return out
+
+
+def mlp_param_table(cfg: ModelConfig) -> List[ParamSpec]:
+    """Config 1: Linear(256,256)+bias x4, fp32, PyTorch-default U(+-1/16) init."""
+    out = []
+    for l in range(cfg.layers):
+        out.append(ParamSpec(2 * l, l, "w", (cfg.hidden, cfg.hidden), float(K_MLP), "fp32"))
+        out.append(ParamSpec(2 * l + 1, l, "b", (cfg.hidden,), float(K_MLP), "fp32"))
+    return out
+
+
+# --- compute-op graph -------------------------------------------------------
+# Each op: dict(name, kind in {"compute","rs"}, phase in {"fwd","bwd"}, micro,
+# layer, params=[param ids consumed]).  RS(l) is the reduce-scatter + Adam of
+# layer l, placed after the layer's last backward op.
+
+LLAMA_FWD = (("attn_norm", ("attn_norm",)), ("qkv", ("wq", "wk", "wv")),
+             ("attn_mix", ()), ("o_proj", ("wo",)), ("mlp_norm", ("mlp_norm",)),
+             ("gate_up", ("wgate", "wup")), ("act", ()), ("down", ("wdown",)))
+LLAMA_BWD = (("down_bwd", ("wdown",)), ("act_bwd", ()), ("gate_up_bwd", ("wgate", "wup")),
+             ("mlp_norm_bwd", ("mlp_norm",)), ("o_bwd", ("wo",)), ("attn_mix_bwd", ()),
+             ("qkv_bwd", ("wq", "wk", "wv")), ("attn_norm_bwd", ("attn_norm",)))
+
+
+def llama_compute_ops(cfg: ModelConfig, micro_steps: int = 1):
+    P = len(LLAMA_NAMES)
+    pid = lambda l, nm: l * P + LLAMA_NAMES.index(nm)
+    ops = []
+    for mu in range(micro_steps):
+        for l in range(cfg.layers):
+            for nm, ps in LLAMA_FWD:
+                ops.append(dict(name=nm, kind="compute", phase="fwd", micro=mu, layer=l,
+                                params=[pid(l, p) for p in ps]))
+        ops.append(dict(name="loss", kind="compute", phase="fwd", micro=mu,
+                        layer=cfg.layers - 1, params=[]))
+        for l in reversed(range(cfg.layers)):
+            for nm, ps in LLAMA_BWD:
+                ops.append(dict(name=nm, kind="compute", phase="bwd", micro=mu, layer=l,
+                                params=[pid(l, p) for p in ps]))
+            if mu == micro_steps - 1:
+                ops.append(dict(name="rs", kind="rs", phase="bwd", micro=mu, layer=l,
+                                params=[]))
+    return ops
+
+
+LLAMA3_8B = ModelConfig("llama3-8b", "llama", 4096, 14336, 32, 8, 128, 32)
+LLAMA3_70B = ModelConfig("llama3-70b", "llama", 8192, 28672, 64, 8, 128, 80)
+# Mixtral 8x7B attention shapes; the MoE MLP (8 experts, fixed balanced top-2) is
+# a next-round workload.
+MIXTRAL_8X7B = ModelConfig("mixtral-8x7b", "mixtral", 4096, 14336, 32, 8, 128, 32)
+MLP_CONFIG1 = ModelConfig("mlp4x256", "mlp", 256, 256, 1, 1, 256, 4, seq=1, batch=8)
+
+
+def small_llama(layers: int = 2, seq: int = 256, batch: int = 1) -> ModelConfig:
+    """Scaled-down Llama layer for oracle-speed parity: same structure, GQA 2:1."""
+    return ModelConfig("llama-small", "llama", 512, 1024, 4, 2, 128, layers, seq=seq, batch=batch)
