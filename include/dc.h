@@ -1,0 +1,260 @@
+/*
+ * dc.h — C ABI of the B200-native sharded-parameter hot path of DeepCompile
+ * (Tanaka et al., arxiv 2504.09983).  Citations: P:n = line n of PAPER.md.
+ *
+ * The life cycle of a sharded parameter (§4.1): all-gather the shards
+ * into an unsharded buffer before a layer's forward and backward (dc_gather),
+ * release the buffer after its last use (dc_release), reduce-scatter the
+ * gradient fused with the 1/N scale and a partitioned Adam update of the local
+ * shard (dc_reduce_scatter_step, P:127/P:440/P:504), under the profile-guided
+ * schedule of §4.2-§4.4 (dc_plan) with optimizer-state offload (dc_offload,
+ * P:370-408).
+ *
+ * Conventions (every function):
+ *  - returns dc_status; no C++ exception crosses the ABI;
+ *  - on error, dc_last_error(ctx) (or dc_last_error(NULL) for ctx-less calls)
+ *    returns a message owned by the library, valid until the next call on the
+ *    same thread;
+ *  - the CALLER owns all device and pinned-host memory (torch allocates it);
+ *    the library keeps non-owning pointers until dc_destroy and never
+ *    cudaMalloc's.  The library owns dc_ctx, dc_schedule, dc_model and strings;
+ *  - enqueue calls are asynchronous on the given stream(s); a CUDA launch error
+ *    returns DC_ECUDA immediately; a device-side flag-wait timeout sets a sticky
+ *    error that the next call on the ctx returns (DC_ETIMEOUT);
+ *  - a ctx is single-threaded (one per rank / virtual rank).
+ */
+#ifndef DC_H
+#define DC_H
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DC_OK = 0,
+  DC_EINVAL = 1,       /* bad argument / layout                              */
+  DC_EOOM = 2,         /* a caller-provided buffer is too small              */
+  DC_EINFEASIBLE = 3,  /* memory limit cannot be met (SPEC Infeasible*)      */
+  DC_ECUDA = 4,        /* CUDA runtime / launch error                         */
+  DC_ESTATE = 5,       /* call out of order (e.g. step before a schedule)     */
+  DC_EPROFILE = 6,     /* profile is not an S_0 schedule (ProfileMismatch)    */
+  DC_ETIMEOUT = 7      /* a device-side flag wait exceeded its bound          */
+} dc_status;
+
+enum { DC_BF16 = 0, DC_FP32 = 1 };
+enum { DC_INIT_WEIGHTS = 1u, DC_VIRTUAL_RANKS = 2u, DC_DEBUG_POISON = 4u };
+enum { DC_PASS_SHARD = 1u, DC_PASS_PREFETCH = 2u, DC_PASS_UNSHARD = 4u, DC_PASS_OFFLOAD = 8u };
+enum { DC_D2H_START = 0, DC_D2H_SYNC_FREE = 1, DC_H2D_START = 2, DC_H2D_SYNC = 3 };
+
+typedef struct dc_ctx dc_ctx;
+typedef struct dc_schedule dc_schedule;
+typedef struct dc_model dc_model;
+
+const char* dc_last_error(const dc_ctx* ctx);
+const char* dc_version(void);
+
+/* ------------------------------------------------------------------------
+ * Shard layout ("each parameter tensor is evenly partitioned").
+ * S_i = ceil(numel_i / (8 N)) * 8 elements; rank r owns elements
+ * [r S_i, (r+1) S_i) of the zero-padded flat tensor.  The per-rank shard store
+ * concatenates the S_i in param order (offsets are multiples of 8 elements =
+ * 16 B for bf16).  The grad slot of a layer holds each of its params as N*S_i
+ * bf16 elements (padded full tensor) in param order, 256-byte aligned.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t world;                 /* N >= 1                                     */
+  int32_t n_params;
+  const int64_t* numel;          /* [n_params] in S_0 first-use order          */
+  const int32_t* layer_of;       /* [n_params] non-decreasing                  */
+  int32_t max_s0_ops;            /* upper bound on S_0 op ids (flag table)     */
+} dc_layout_args;
+
+typedef struct {
+  int64_t shard_elems;           /* sum S_i: length of every per-rank store    */
+  int64_t grad_slot_bytes;       /* max over layers of the layer's grad slot   */
+  int64_t flag_bytes;            /* uint32 flag table per rank                 */
+  int32_t n_layers;
+} dc_layout;
+
+/* Pure host function: sizes the caller must allocate before dc_init. */
+dc_status dc_layout_query(const dc_layout_args* a, dc_layout* out);
+
+/* ------------------------------------------------------------------------
+ * Context.  Pointers are device pointers unless noted; "peer" tables hold the
+ * same buffer as mapped on every rank (torch symmetric memory buffer_ptrs at
+ * N>1; in DC_VIRTUAL_RANKS mode, the N virtual ranks' buffers on one GPU).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t rank, world, device;
+  int32_t n_params;
+  const int64_t* numel;          /* host [n_params]                            */
+  const int32_t* layer_of;       /* host [n_params]                            */
+  const float* init_k;           /* host [n_params] generator scale; 0 -> 1.0  */
+  int32_t max_s0_ops;
+  void* shard_param;             /* bf16 [shard_elems], caller-owned           */
+  float* master;                 /* fp32 [shard_elems]                         */
+  float* exp_avg;                /* fp32 [shard_elems]  (Adam m)               */
+  float* exp_avg_sq;             /* fp32 [shard_elems]  (Adam v)               */
+  const uint64_t* grad_peer_ptrs;  /* host [world]: 2 grad slots per rank,    */
+  uint64_t grad_bytes;             /*   each dc_layout.grad_slot_bytes        */
+  const uint64_t* flag_peer_ptrs;  /* host [world]: uint32 flag tables        */
+  uint64_t flag_bytes;
+  void* host_pinned;             /* pinned host memory for offload (may be 0) */
+  uint64_t host_pinned_bytes;
+  float lr, beta1, beta2, eps;   /* Adam; weight decay 0               */
+  uint64_t seed;                 /* generator seed (synth/gen.py recipe)       */
+  uint32_t flags;                /* DC_INIT_WEIGHTS | DC_VIRTUAL_RANKS | ...   */
+  uint32_t spin_limit;           /* flag-wait bound in 2^10-cycle units, 0=def */
+} dc_init_args;
+
+/* Validates, computes the layout, zeroes m/v and (with DC_INIT_WEIGHTS) fills
+ * master = value(seed, param, idx) and shard = RNE_bf16(master) with the
+ * counter-based generator on the device (synchronous). */
+dc_status dc_init(const dc_init_args* a, dc_ctx** out);
+dc_status dc_destroy(dc_ctx* ctx);
+
+/* Offset (elements) of param's shard in the store, and S_i. */
+dc_status dc_shard_range(const dc_ctx* ctx, int32_t param, int64_t* offset, int64_t* shard_elems);
+/* Byte offset of param inside its layer's grad slot (padded, N*S_i bf16). */
+dc_status dc_grad_offset(const dc_ctx* ctx, int32_t param, int64_t* byte_offset);
+
+/* ------------------------------------------------------------------------
+ * Planner.  Host-only, deterministic, exact integer arithmetic;
+ * no CUDA calls.  profile_json: the S_0 schedule with per-op p_mem (bytes
+ * resident before the op, excluding Adam m and v), transient, dur_us, plus
+ * params {id, bytes}, frags {id, layer, bytes} and the T_c table (schema:
+ * DESIGN.md §6).  mem_budget = M.  Output: dc_schedule (immutable).
+ * Errors: DC_EPROFILE (not an S_0 / malformed), DC_EINFEASIBLE.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  uint64_t M_prefetch;             /* default 2 GiB                    */
+  uint32_t alpha_num, alpha_den;   /* default 3/2                      */
+  uint32_t passes;                 /* DC_PASS_* bitmask; order fixed P->S->O   */
+  uint32_t strict;                 /* reading D4                               */
+} dc_plan_opts;
+
+dc_status dc_plan(const char* profile_json, uint64_t mem_budget, const dc_plan_opts* opts,
+                  dc_schedule** out);
+/* Canonical JSON (keys sorted, no whitespace, integers only).  *len in/out:
+ * buffer size in, bytes needed (without NUL) out; DC_EOOM if too small. */
+dc_status dc_schedule_json(const dc_schedule* s, char* buf, size_t* len);
+uint64_t dc_schedule_capacity(const dc_schedule* s);
+void dc_schedule_free(dc_schedule* s);
+
+/* Bind a schedule and the gather arena (peer table of a symmetric buffer of
+ * >= dc_schedule_capacity bytes).  Zeroes this rank's flag table: every rank
+ * must call it between the same two barriers.  Resets the epoch to 0. */
+dc_status dc_bind_schedule(dc_ctx* ctx, const dc_schedule* s, const uint64_t* arena_peer_ptrs,
+                           uint64_t arena_bytes, cudaStream_t stream);
+
+/* Begin step `epoch` (1-based, monotone): posts the ready flags of gathers
+ * whose arena interval has no earlier release in the step (reading D26). */
+dc_status dc_step_begin(dc_ctx* ctx, int32_t epoch, cudaStream_t compute_stream);
+
+/* ------------------------------------------------------------------------
+ * Gather / release.  gather_id = the schedule op id of an "ag"
+ * op (S_0 id of its first member).  ag_stream must already be ordered after
+ * the compute-stream position of the op (issue semantics, reading D23).
+ * Kernel ag_push: waits for the ready flag of every receiving rank, stores this
+ * rank's shard of every member into every rank's arena at
+ * arena_off(member) + rank * S_i * 2 bytes with 16-byte stores, fences, bumps
+ * every receiver's done counter, then waits for its own N * CTAs arrivals.
+ * At N = 1 the gathered tensor aliases the shard (no copy, no kernel).
+ * done_evt (may be NULL) is recorded on ag_stream after the kernel.
+ * ------------------------------------------------------------------------ */
+dc_status dc_gather(dc_ctx* ctx, int32_t gather_id, cudaStream_t ag_stream, cudaEvent_t done_evt);
+/* Unsharded tensor of param (row-major, numel elements; padding follows). */
+dc_status dc_tensor_ptr(const dc_ctx* ctx, int32_t param, void** full_ptr);
+/* Release op `release_id` (schedule op id): posts the ready flags listed in
+ * its posts_ready_for to every peer, on compute_stream.  */
+dc_status dc_release(dc_ctx* ctx, int32_t release_id, cudaStream_t compute_stream);
+
+/* ------------------------------------------------------------------------
+ * Gradient slot and reduce-scatter + Adam.
+ * dc_grad_slot: where the dW GEMMs of `layer` write bf16 full grads; before the
+ * first write of a backward the caller enqueues dc_grad_slot_acquire on the
+ * compute stream (waits until every owner consumed the slot's previous use);
+ * after the last write dc_grad_slot_publish (posts grad-ready to every owner).
+ * dc_reduce_scatter_step, kernel rs_adam: for every param of `layer`, owner
+ * r computes g = (((+0 + g_0) + g_1) + ... + g_{N-1}) over fp32(bf16) slice r
+ * of every rank's grad slot (peer loads), g *= 1/N, Adam step `step_t`
+ * (1-based) on master/m/v (fp32, the op order of reading D18), shard =
+ * RNE_bf16(master); then posts "consumed" to every rank.
+ * apply_update = 0 is reserved for gradient accumulation (next round).
+ * ------------------------------------------------------------------------ */
+dc_status dc_grad_slot(const dc_ctx* ctx, int32_t layer, void** grad_full_bf16);
+dc_status dc_grad_slot_acquire(dc_ctx* ctx, int32_t layer, cudaStream_t compute_stream);
+dc_status dc_grad_slot_publish(dc_ctx* ctx, int32_t layer, cudaStream_t compute_stream);
+dc_status dc_reduce_scatter_step(dc_ctx* ctx, int32_t layer, int32_t step_t, int32_t apply_update,
+                                 cudaStream_t rs_stream);
+
+/* ------------------------------------------------------------------------
+ * Offload: fragment f = a contiguous slice of the fp32 m or v
+ * store (dc_offload_fragments).  op: DC_D2H_START (async cudaMemcpyAsync to
+ * the pinned host slot on copy_stream), DC_D2H_SYNC_FREE (compute stream waits
+ * for that copy; the device slice may then be reused), DC_H2D_START,
+ * DC_H2D_SYNC (the stream passed waits for the reload).
+ * ------------------------------------------------------------------------ */
+typedef struct { int32_t layer; int32_t state; /* 0 = m, 1 = v */ int64_t offset_elems, elems; } dc_fragment;
+dc_status dc_offload_fragments(dc_ctx* ctx, int64_t max_fragment_bytes, dc_fragment* out,
+                               int32_t* n_inout);
+dc_status dc_offload(dc_ctx* ctx, int32_t fragment, int32_t op, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Synthetic Llama-shaped layer stack — the "user model"
+ * that exercises the path.  GEMMs are tcgen05/TMEM/TMA kernels (bf16 in,
+ * fp32 accumulate); glue kernels are fused elementwise/row kernels.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t hidden, ffn, n_heads, n_kv, head_dim, layers, tokens;
+} dc_model_dims;
+
+/* Plain GEMM entry (tests, comparators): C[M,N] (bf16, row-major, ldc) =
+ * A_op[M,K] * B_op[K,N] (+ R[M,N] if R != NULL), fp32 accumulation.
+ * a_mn_major = 0: A stored [M][lda] (K contiguous); 1: A stored [K][lda]
+ * (M contiguous).  b_mn_major = 0: B stored [N][ldb] (K contiguous, i.e. the
+ * nn.Linear weight layout for x W^T); 1: B stored [K][ldb] (N contiguous).
+ * Up to 4 B segments split along N (b_split_k = 0; seg_end in units of
+ * 256 columns) or along K (b_split_k = 1; seg_end in units of 64). */
+typedef struct {
+  int32_t M, N, K;
+  const void* A; int64_t lda; int32_t a_mn_major;
+  int32_t n_bseg; const void* B[4]; int64_t ldb[4]; int32_t bseg_end[4];
+  int32_t b_mn_major, b_split_k;
+  void* C; int64_t ldc;
+  const void* R; int64_t ldr;
+  int32_t num_sms;               /* 0 = all SMs                                 */
+} dc_gemm_args;
+dc_status dc_gemm(const dc_gemm_args* g, cudaStream_t stream);
+
+dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_model** out);
+dc_status dc_model_destroy(dc_model* m);
+/* Bytes of the activation + workspace buffer the caller must provide. */
+dc_status dc_model_act_bytes(const dc_model* m, uint64_t* bytes);
+/* x, target: bf16 [tokens, hidden] device buffers of this rank's micro-batch. */
+dc_status dc_model_bind(dc_model* m, void* act_buf, uint64_t act_bytes, const void* x,
+                        const void* target);
+/* The S_0 schedule of the model as a profile skeleton (p_mem/transient/dur
+ * filled from the last profiled step if any, else 0). */
+dc_status dc_model_profile_json(const dc_model* m, char* buf, size_t* len);
+/* One training step through the bound schedule: forward, loss, backward with
+ * gathers / releases / reduce-scatter+Adam / offload ops interleaved as
+ * planned.  Streams: compute, ag, rs, copy.  profile != 0 records per-op
+ * durations and memory for dc_model_profile_json. */
+dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile, cudaStream_t compute,
+                        cudaStream_t ag, cudaStream_t rs, cudaStream_t copy);
+/* Device pointer to the fp32 loss of the last step (mean 1/2 (y-t)^2). */
+dc_status dc_model_loss_ptr(const dc_model* m, float** loss);
+/* Pointers into the activation buffer (tests): which = 0 x(l), 1 y(l) ... */
+dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t which, void** ptr);
+/* Number of kernels the last dc_model_step launched. */
+dc_status dc_model_launch_count(const dc_model* m, int64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DC_H */

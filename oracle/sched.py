@@ -347,6 +347,8 @@ def alg2_and_reload(S, P_other, tr, B, frags, M, s0):
     micro_of = lambda e: s0[e["ref"]]["micro"] if "ref" in e else s0[e["members"][0][1]]["micro"]
     last_micro = max(o["micro"] for o in s0)
     bwd = [j for j, e in enumerate(S) if phase_of(e) == "bwd" and micro_of(e) == last_micro]
+    if not bwd:
+        raise Infeasible("offloaded fragments need a backward region to reload in")
     suffix = [0] * (len(bwd) + 1)
     for k in range(len(bwd) - 1, -1, -1):
         suffix[k] = max(suffix[k + 1], need[bwd[k]])

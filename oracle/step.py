@@ -67,7 +67,9 @@ def _fwd_bwd(cfg, table, full, x, t, bf16):
     P = len(names)
     Ws = [{p.name: full[l * P + j].reshape(p.shape) for j, p in enumerate(table[l * P:(l + 1) * P])}
           for l in range(cfg.layers)]
-    loss, G, outs = om.llama_stack_fwd_bwd(nx.rne_bf16(x) if bf16 else x, t, Ws, cfg, rnd)
+    # bf16 regime: inputs and targets are stored in bf16 like every activation
+    loss, G, outs = om.llama_stack_fwd_bwd(nx.rne_bf16(x) if bf16 else x, nx.rne_bf16(t) if bf16 else t,
+                                           Ws, cfg, rnd)
     flat = []
     for l in range(cfg.layers):
         for nm in names:

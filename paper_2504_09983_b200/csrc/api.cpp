@@ -1,0 +1,468 @@
+// C-ABI runtime: shard store layout, context, schedule binding, and the
+// gather / release / reduce-scatter+Adam / offload entry points of dc.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "dc_internal.h"
+
+namespace dc {
+static thread_local std::string g_err;
+static thread_local int64_t g_launches = 0;
+void set_global_error(const std::string& s) { g_err = s; }
+void count_launch() { ++g_launches; }
+int64_t launch_count() { return g_launches; }
+void reset_launch_count() { g_launches = 0; }
+
+static int64_t align256(int64_t b) { return (b + 255) / 256 * 256; }
+static int64_t shard_len(int64_t numel, int world) { return (numel + 8LL * world - 1) / (8LL * world) * 8; }
+
+static dc_status make_layout(int world, int n, const int64_t* numel, const int32_t* layer_of, int max_ops,
+                             Layout* L, std::string* err) {
+  if (world < 1 || world > MAXW) { *err = "world must be in [1, 8]"; return DC_EINVAL; }
+  if (n < 1 || !numel || !layer_of) { *err = "empty parameter table"; return DC_EINVAL; }
+  L->S.resize(n); L->store_off.resize(n); L->goff.resize(n);
+  int64_t off = 0;
+  int prev_layer = -1;
+  std::map<int, int64_t> slot_bytes;
+  for (int i = 0; i < n; ++i) {
+    if (numel[i] <= 0) { *err = "numel must be > 0"; return DC_EINVAL; }
+    if (layer_of[i] < prev_layer || layer_of[i] < 0) { *err = "layer_of must be non-decreasing"; return DC_EINVAL; }
+    if (layer_of[i] != prev_layer) {
+      if (layer_of[i] != (int)L->layer_first.size()) { *err = "layers must be numbered 0..L-1"; return DC_EINVAL; }
+      L->layer_first.push_back(i);
+      L->layer_count.push_back(0);
+      prev_layer = layer_of[i];
+    }
+    L->layer_count.back()++;
+    L->S[i] = shard_len(numel[i], world);
+    L->store_off[i] = off;
+    off += L->S[i];
+    L->goff[i] = slot_bytes[layer_of[i]];
+    slot_bytes[layer_of[i]] += align256(L->S[i] * world * 2);
+  }
+  L->shard_elems = off;
+  L->n_layers = (int)L->layer_first.size();
+  for (auto& kv : slot_bytes) L->grad_slot_bytes = std::max(L->grad_slot_bytes, kv.second);
+  const int64_t ops = std::max(max_ops, 1);
+  L->f_ready = 0;
+  L->f_done = L->f_ready + ops * world;
+  L->f_gready = L->f_done + ops;
+  L->f_gcons = L->f_gready + 2 * world;
+  L->f_rsdone = L->f_gcons + 2 * world;
+  L->flag_words = L->f_rsdone + 1;
+  return DC_OK;
+}
+
+}  // namespace dc
+
+using namespace dc;
+
+struct FragInfo { int layer, state; int64_t off, elems, host_off; cudaEvent_t d2h, h2d; };
+
+struct dc_ctx {
+  int rank = 0, world = 1, device = 0;
+  uint32_t flags = 0;
+  int n_params = 0;
+  std::vector<int64_t> numel;
+  std::vector<int32_t> layer_of;
+  Layout L;
+  void* shard = nullptr;
+  float *master = nullptr, *m = nullptr, *v = nullptr;
+  std::vector<uint64_t> grad_peers, flag_peers, arena_peers;
+  uint64_t grad_bytes = 0, flag_bytes = 0, arena_bytes = 0;
+  void* host_pinned = nullptr;
+  uint64_t host_pinned_bytes = 0;
+  float lr = 1e-3f, beta1 = 0.9f, beta2 = 0.999f, eps = 1e-8f;
+  uint64_t seed = 0;
+  uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
+  int max_ops = 0;
+  // schedule
+  const dc_schedule* sched = nullptr;
+  std::map<int, int> op_index;          // schedule op id -> index (ag / rel)
+  std::vector<int64_t> cur_off;         // param -> arena byte offset of its live buffer (-1)
+  std::vector<int> initial_ready;       // gathers whose ready is posted at step start
+  std::map<int, int> ag_ctas;           // gather id -> CTAs per launch
+  std::map<int, int> ag_launches;
+  uint32_t epoch = 0;
+  int slot_use[2] = {0, 0};
+  std::vector<int> layer_use;
+  uint32_t rs_done_total = 0;
+  int rs_ctas = 0;
+  // error word: host-mapped pinned (device writes on a flag-wait timeout)
+  uint32_t* err_host = nullptr;
+  uint32_t* err_dev = nullptr;
+  std::vector<FragInfo> frags;
+  std::string err;
+
+  uint32_t* flag(int q, int64_t word) const { return reinterpret_cast<uint32_t*>(flag_peers[q]) + word; }
+  uint32_t* myflag(int64_t word) const { return flag(rank, word); }
+  uint8_t* slot_ptr(int q, int s) const { return reinterpret_cast<uint8_t*>(grad_peers[q]) + (int64_t)s * L.grad_slot_bytes; }
+};
+
+static dc_status fail(dc_ctx* c, dc_status s, const std::string& m) {
+  if (c) c->err = m;
+  set_global_error(m);
+  return s;
+}
+
+static dc_status check_sticky(dc_ctx* c) {
+  if (c->err_host && *(volatile uint32_t*)c->err_host) {
+    char b[96];
+    snprintf(b, sizeof b, "device flag wait timed out (code 0x%x)", *(volatile uint32_t*)c->err_host);
+    return fail(c, DC_ETIMEOUT, b);
+  }
+  return DC_OK;
+}
+
+extern "C" const char* dc_last_error(const dc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+extern "C" const char* dc_version(void) { return "dc-b200 0.1 (sm_100a)"; }
+
+extern "C" dc_status dc_layout_query(const dc_layout_args* a, dc_layout* out) {
+  if (!a || !out) { set_global_error("dc_layout_query: null argument"); return DC_EINVAL; }
+  Layout L;
+  std::string err;
+  dc_status s = make_layout(a->world, a->n_params, a->numel, a->layer_of, a->max_s0_ops, &L, &err);
+  if (s != DC_OK) { set_global_error(err); return s; }
+  out->shard_elems = L.shard_elems;
+  out->grad_slot_bytes = L.grad_slot_bytes;
+  out->flag_bytes = L.flag_words * 4;
+  out->n_layers = L.n_layers;
+  return DC_OK;
+}
+
+extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
+  if (!a || !out) { set_global_error("dc_init: null argument"); return DC_EINVAL; }
+  auto c = std::make_unique<dc_ctx>();
+  std::string err;
+  dc_status s = make_layout(a->world, a->n_params, a->numel, a->layer_of, a->max_s0_ops, &c->L, &err);
+  if (s != DC_OK) return fail(nullptr, s, "dc_init: " + err);
+  if (a->rank < 0 || a->rank >= a->world) return fail(nullptr, DC_EINVAL, "dc_init: rank out of range");
+  if (!a->shard_param || !a->master || !a->exp_avg || !a->exp_avg_sq || !a->grad_peer_ptrs || !a->flag_peer_ptrs)
+    return fail(nullptr, DC_EINVAL, "dc_init: null buffer");
+  if (a->grad_bytes < (uint64_t)(2 * c->L.grad_slot_bytes)) return fail(nullptr, DC_EOOM, "dc_init: grad buffer < 2 slots");
+  if (a->flag_bytes < (uint64_t)(c->L.flag_words * 4)) return fail(nullptr, DC_EOOM, "dc_init: flag table too small");
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al16(a->shard_param) || !al16(a->master) || !al16(a->exp_avg) || !al16(a->exp_avg_sq))
+    return fail(nullptr, DC_EINVAL, "dc_init: buffers must be 16-byte aligned");
+  c->rank = a->rank; c->world = a->world; c->device = a->device; c->flags = a->flags;
+  c->n_params = a->n_params;
+  c->numel.assign(a->numel, a->numel + a->n_params);
+  c->layer_of.assign(a->layer_of, a->layer_of + a->n_params);
+  c->shard = a->shard_param; c->master = a->master; c->m = a->exp_avg; c->v = a->exp_avg_sq;
+  c->grad_peers.assign(a->grad_peer_ptrs, a->grad_peer_ptrs + a->world);
+  c->flag_peers.assign(a->flag_peer_ptrs, a->flag_peer_ptrs + a->world);
+  c->grad_bytes = a->grad_bytes; c->flag_bytes = a->flag_bytes;
+  c->host_pinned = a->host_pinned; c->host_pinned_bytes = a->host_pinned_bytes;
+  c->lr = a->lr; c->beta1 = a->beta1; c->beta2 = a->beta2; c->eps = a->eps;
+  c->seed = a->seed;
+  c->max_ops = std::max(a->max_s0_ops, 1);
+  if (a->spin_limit) c->timeout_ns = (uint64_t)a->spin_limit * 1000ull * 1000ull;   // spin_limit in ms
+  c->cur_off.assign(a->n_params, -1);
+  c->layer_use.assign(c->L.n_layers, 0);
+  c->rs_ctas = 148;
+  DC_CUDA_TRY(cudaSetDevice(a->device), &c->err);
+  DC_CUDA_TRY(cudaHostAlloc(&c->err_host, 4, cudaHostAllocMapped), &c->err);
+  *c->err_host = 0;
+  DC_CUDA_TRY(cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0), &c->err);
+  cudaStream_t st = 0;
+  DC_CUDA_TRY(cudaMemsetAsync(c->m, 0, c->L.shard_elems * 4, st), &c->err);
+  DC_CUDA_TRY(cudaMemsetAsync(c->v, 0, c->L.shard_elems * 4, st), &c->err);
+  DC_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<void*>(c->grad_peers[c->rank]), 0, 2 * c->L.grad_slot_bytes, st), &c->err);
+  DC_CUDA_TRY(cudaMemsetAsync(c->myflag(0), 0, c->L.flag_words * 4, st), &c->err);
+  if (a->flags & DC_INIT_WEIGHTS) {
+    for (int i = 0; i < a->n_params; ++i) {
+      const float k = a->init_k ? a->init_k[i] : 0.0f;
+      k_init_param(a->seed, i, c->numel[i], c->world, c->rank, c->L.S[i], k, c->master + c->L.store_off[i],
+                   reinterpret_cast<uint16_t*>(c->shard) + c->L.store_off[i], st);
+    }
+  }
+  DC_CUDA_TRY(cudaStreamSynchronize(st), &c->err);
+  DC_CUDA_TRY(cudaGetLastError(), &c->err);
+  *out = c.release();
+  return DC_OK;
+}
+
+extern "C" dc_status dc_destroy(dc_ctx* c) {
+  if (!c) return DC_OK;
+  for (auto& f : c->frags) { cudaEventDestroy(f.d2h); cudaEventDestroy(f.h2d); }
+  if (c->err_host) cudaFreeHost(c->err_host);
+  delete c;
+  return DC_OK;
+}
+
+extern "C" dc_status dc_shard_range(const dc_ctx* c, int32_t p, int64_t* off, int64_t* S) {
+  if (!c || p < 0 || p >= c->n_params) { set_global_error("dc_shard_range: bad param"); return DC_EINVAL; }
+  if (off) *off = c->L.store_off[p];
+  if (S) *S = c->L.S[p];
+  return DC_OK;
+}
+
+extern "C" dc_status dc_grad_offset(const dc_ctx* c, int32_t p, int64_t* b) {
+  if (!c || p < 0 || p >= c->n_params) { set_global_error("dc_grad_offset: bad param"); return DC_EINVAL; }
+  *b = c->L.goff[p];
+  return DC_OK;
+}
+
+// ------------------------------------------------------------------ schedule
+extern "C" dc_status dc_bind_schedule(dc_ctx* c, const dc_schedule* s, const uint64_t* arena_peer_ptrs,
+                                      uint64_t arena_bytes, cudaStream_t st) {
+  if (!c || !s) return fail(c, DC_EINVAL, "dc_bind_schedule: null argument");
+  const int n = sched_num_ops(s);
+  c->op_index.clear();
+  c->initial_ready.clear();
+  c->ag_ctas.clear();
+  c->ag_launches.clear();
+  for (int i = 0; i < n; ++i) {
+    int kind, id, nm, np, nw;
+    const int64_t* mem; const int* posts; const int* waits;
+    int64_t off, bytes;
+    sched_op(s, i, &kind, &id, &mem, &nm, &off, &bytes, &posts, &np, &waits, &nw);
+    if (kind == K_AG || kind == K_REL) {
+      if (id < 0 || id >= c->max_ops) return fail(c, DC_EINVAL, "dc_bind_schedule: op id exceeds max_s0_ops");
+      c->op_index[id] = i;
+    }
+    for (int j = 0; j < nm && (kind == K_AG || kind == K_REL); ++j)
+      if (mem[j] < 0 || mem[j] >= c->n_params) return fail(c, DC_EINVAL, "dc_bind_schedule: param out of range");
+    if (kind == K_AG) {
+      if (c->world > 1 && off + bytes > (int64_t)arena_bytes) return fail(c, DC_EOOM, "dc_bind_schedule: arena too small");
+      if (nw == 0) c->initial_ready.push_back(id);
+      int64_t shard_bytes = 0;
+      for (int j = 0; j < nm; ++j) shard_bytes += c->L.S[mem[j]] * 2;
+      int ctas = (int)std::min<int64_t>(32, std::max<int64_t>(1, shard_bytes / (64 * 1024)));
+      c->ag_ctas[id] = ctas;
+      c->ag_launches[id] = (nm + 47) / 48;
+    }
+  }
+  c->sched = s;
+  c->arena_peers.assign(arena_peer_ptrs ? arena_peer_ptrs : nullptr, arena_peer_ptrs ? arena_peer_ptrs + c->world : nullptr);
+  if (c->world > 1 && (int)c->arena_peers.size() != c->world) return fail(c, DC_EINVAL, "dc_bind_schedule: arena peers");
+  c->arena_bytes = arena_bytes;
+  c->epoch = 0;
+  c->slot_use[0] = c->slot_use[1] = 0;
+  std::fill(c->layer_use.begin(), c->layer_use.end(), 0);
+  c->rs_done_total = 0;
+  std::fill(c->cur_off.begin(), c->cur_off.end(), -1);
+  DC_CUDA_TRY(cudaMemsetAsync(c->myflag(0), 0, c->L.flag_words * 4, st), &c->err);
+  DC_CUDA_TRY(cudaStreamSynchronize(st), &c->err);
+  return DC_OK;
+}
+
+static PeerFlags peers_at(const dc_ctx* c, int64_t word) {
+  PeerFlags f{};
+  f.n = c->world;
+  for (int q = 0; q < c->world; ++q) f.p[q] = c->flag(q, word);
+  return f;
+}
+
+extern "C" dc_status dc_step_begin(dc_ctx* c, int32_t epoch, cudaStream_t st) {
+  if (!c || !c->sched) return fail(c, DC_ESTATE, "dc_step_begin: no schedule bound");
+  if (dc_status e = check_sticky(c)) return e;
+  if ((uint32_t)epoch <= c->epoch) return fail(c, DC_EINVAL, "dc_step_begin: epochs must increase");
+  c->epoch = (uint32_t)epoch;
+  if (c->world == 1) return DC_OK;
+  // ready flags for gathers without an in-step predecessor release (D26):
+  // ready[g][me] in every rank's table
+  for (int g : c->initial_ready) {
+    k_post_flags(peers_at(c, c->L.f_ready + (int64_t)g * c->world + c->rank), c->epoch, st);
+  }
+  if (cudaGetLastError() != cudaSuccess) return fail(c, DC_ECUDA, "dc_step_begin: launch failed");
+  return DC_OK;
+}
+
+extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEvent_t done_evt) {
+  if (!c || !c->sched) return fail(c, DC_ESTATE, "dc_gather: no schedule bound");
+  if (dc_status e = check_sticky(c)) return e;
+  auto it = c->op_index.find(gid);
+  if (it == c->op_index.end()) return fail(c, DC_EINVAL, "dc_gather: unknown gather id");
+  int kind, id, nm, np, nw;
+  const int64_t* mem; const int* posts; const int* waits;
+  int64_t off, bytes;
+  sched_op(c->sched, it->second, &kind, &id, &mem, &nm, &off, &bytes, &posts, &np, &waits, &nw);
+  if (kind != K_AG) return fail(c, DC_EINVAL, "dc_gather: op is not a gather");
+  if (c->world == 1) {
+    for (int j = 0; j < nm; ++j) c->cur_off[mem[j]] = -2;   // alias of the shard
+  } else {
+    if (c->epoch == 0) return fail(c, DC_ESTATE, "dc_gather: call dc_step_begin first");
+    std::vector<AgMember> am;
+    int64_t cur = off;
+    for (int j = 0; j < nm; ++j) {
+      const int p = (int)mem[j];
+      AgMember a;
+      a.src = reinterpret_cast<const uint16_t*>(c->shard) + c->L.store_off[p];
+      a.dst_off_bytes = cur + (int64_t)c->rank * c->L.S[p] * 2;
+      a.bytes = c->L.S[p] * 2;
+      am.push_back(a);
+      c->cur_off[p] = cur;
+      cur += align256(c->numel[p] > 0 ? c->L.S[p] * c->world * 2 : 0);
+    }
+    const int ctas = c->ag_ctas[gid];
+    const uint32_t target = c->epoch * (uint32_t)(c->world * ctas * c->ag_launches[gid]);
+    dc_status s = k_ag_push(am, c->world, c->rank, c->arena_peers.data(), c->myflag(c->L.f_ready + (int64_t)gid * c->world),
+                            c->epoch, peers_at(c, c->L.f_done + gid), c->myflag(c->L.f_done + gid), target, ctas,
+                            c->timeout_ns, c->err_dev, st);
+    if (s != DC_OK) return fail(c, s, "dc_gather: launch failed");
+  }
+  if (done_evt) DC_CUDA_TRY(cudaEventRecord(done_evt, st), &c->err);
+  return DC_OK;
+}
+
+extern "C" dc_status dc_tensor_ptr(const dc_ctx* c, int32_t p, void** ptr) {
+  if (!c || p < 0 || p >= c->n_params || !ptr) { set_global_error("dc_tensor_ptr: bad param"); return DC_EINVAL; }
+  if (c->world == 1) {
+    *ptr = reinterpret_cast<uint16_t*>(c->shard) + c->L.store_off[p];
+    return DC_OK;
+  }
+  if (c->cur_off[p] < 0) { set_global_error("dc_tensor_ptr: param is not gathered"); return DC_ESTATE; }
+  *ptr = reinterpret_cast<uint8_t*>(c->arena_peers[c->rank]) + c->cur_off[p];
+  return DC_OK;
+}
+
+extern "C" dc_status dc_release(dc_ctx* c, int32_t rid, cudaStream_t st) {
+  if (!c || !c->sched) return fail(c, DC_ESTATE, "dc_release: no schedule bound");
+  auto it = c->op_index.find(rid);
+  if (it == c->op_index.end()) return fail(c, DC_EINVAL, "dc_release: unknown release id");
+  int kind, id, nm, np, nw;
+  const int64_t* mem; const int* posts; const int* waits;
+  int64_t off, bytes;
+  sched_op(c->sched, it->second, &kind, &id, &mem, &nm, &off, &bytes, &posts, &np, &waits, &nw);
+  if (kind != K_REL) return fail(c, DC_EINVAL, "dc_release: op is not a release");
+  if (c->world > 1) c->cur_off[mem[0]] = -1;
+  if (c->world == 1) return DC_OK;
+  for (int j = 0; j < np; ++j)
+    k_post_flags(peers_at(c, c->L.f_ready + (int64_t)posts[j] * c->world + c->rank), c->epoch, st);
+  if (cudaGetLastError() != cudaSuccess) return fail(c, DC_ECUDA, "dc_release: launch failed");
+  return DC_OK;
+}
+
+// ------------------------------------------------------------------ grads
+extern "C" dc_status dc_grad_slot(const dc_ctx* c, int32_t layer, void** p) {
+  if (!c || layer < 0 || layer >= c->L.n_layers || !p) { set_global_error("dc_grad_slot: bad layer"); return DC_EINVAL; }
+  *p = c->slot_ptr(c->rank, layer & 1);
+  return DC_OK;
+}
+
+extern "C" dc_status dc_grad_slot_acquire(dc_ctx* c, int32_t layer, cudaStream_t st) {
+  if (!c || layer < 0 || layer >= c->L.n_layers) return fail(c, DC_EINVAL, "dc_grad_slot_acquire: bad layer");
+  if (dc_status e = check_sticky(c)) return e;
+  const int s = layer & 1;
+  const int u = ++c->slot_use[s];
+  c->layer_use[layer] = u;
+  if (u > 1)   // every owner consumed the previous use of this slot
+    k_wait_flags(c->myflag(c->L.f_gcons + (int64_t)s * c->world), c->world, (uint32_t)(u - 1), c->timeout_ns,
+                 c->err_dev, st);
+  return DC_OK;
+}
+
+extern "C" dc_status dc_grad_slot_publish(dc_ctx* c, int32_t layer, cudaStream_t st) {
+  if (!c || layer < 0 || layer >= c->L.n_layers) return fail(c, DC_EINVAL, "dc_grad_slot_publish: bad layer");
+  const int s = layer & 1;
+  k_post_flags(peers_at(c, c->L.f_gready + (int64_t)s * c->world + c->rank), (uint32_t)c->layer_use[layer], st);
+  return DC_OK;
+}
+
+extern "C" dc_status dc_reduce_scatter_step(dc_ctx* c, int32_t layer, int32_t step_t, int32_t apply_update,
+                                            cudaStream_t st) {
+  if (!c || layer < 0 || layer >= c->L.n_layers) return fail(c, DC_EINVAL, "dc_reduce_scatter_step: bad layer");
+  if (!apply_update) return fail(c, DC_EINVAL, "dc_reduce_scatter_step: accumulate-only is not implemented");
+  if (step_t < 1) return fail(c, DC_EINVAL, "dc_reduce_scatter_step: step_t is 1-based");
+  if (dc_status e = check_sticky(c)) return e;
+  const int s = layer & 1;
+  const int u = c->layer_use[layer];
+  if (u == 0) return fail(c, DC_ESTATE, "dc_reduce_scatter_step: grad slot of layer never acquired");
+  std::vector<RsMember> mem;
+  int64_t elems = 0;
+  for (int i = c->L.layer_first[layer]; i < c->L.layer_first[layer] + c->L.layer_count[layer]; ++i) {
+    mem.push_back({c->L.goff[i], c->L.S[i], c->L.store_off[i]});
+    elems += c->L.S[i];
+  }
+  std::vector<uint64_t> slots(c->world);
+  for (int q = 0; q < c->world; ++q) slots[q] = reinterpret_cast<uint64_t>(c->slot_ptr(q, s));
+  const double bc1 = 1.0 - std::pow((double)c->beta1, step_t);
+  const double bc2 = 1.0 - std::pow((double)c->beta2, step_t);
+  const float sc = (float)((double)c->lr / bc1);
+  const float cc = (float)std::sqrt(bc2);
+  int ctas = (int)std::min<int64_t>(c->rs_ctas * 2, std::max<int64_t>(1, elems / 8 / 256));
+  c->rs_done_total += (uint32_t)ctas;
+  dc_status r = k_rs_adam(mem, c->world, c->rank, slots.data(), c->myflag(c->L.f_gready + (int64_t)s * c->world),
+                          (uint32_t)u, peers_at(c, c->L.f_gcons + (int64_t)s * c->world + c->rank), (uint32_t)u,
+                          c->myflag(c->L.f_rsdone), c->rs_done_total, c->master, c->m, c->v, c->shard, sc, cc,
+                          c->beta1, c->beta2, c->eps, ctas, c->timeout_ns, c->err_dev, st);
+  if (r != DC_OK) return fail(c, r, "dc_reduce_scatter_step: launch failed");
+  return DC_OK;
+}
+
+// ------------------------------------------------------------------ offload
+extern "C" dc_status dc_offload_fragments(dc_ctx* c, int64_t max_bytes, dc_fragment* out, int32_t* n_inout) {
+  if (!c || !n_inout || max_bytes < 32) return fail(c, DC_EINVAL, "dc_offload_fragments: bad argument");
+  for (auto& f : c->frags) { cudaEventDestroy(f.d2h); cudaEventDestroy(f.h2d); }
+  c->frags.clear();
+  const int64_t chunk = max_bytes / 4 / 8 * 8;
+  int64_t host_off = 0;
+  for (int l = 0; l < c->L.n_layers; ++l) {
+    const int first = c->L.layer_first[l];
+    const int64_t lo = c->L.store_off[first];
+    const int64_t hi = lo + [&] { int64_t e = 0; for (int i = first; i < first + c->L.layer_count[l]; ++i) e += c->L.S[i]; return e; }();
+    for (int st = 0; st < 2; ++st)
+      for (int64_t o = lo; o < hi; o += chunk) {
+        FragInfo f{};
+        f.layer = l; f.state = st; f.off = o; f.elems = std::min(chunk, hi - o); f.host_off = host_off;
+        host_off += f.elems * 4;
+        c->frags.push_back(f);
+      }
+  }
+  const int n = (int)c->frags.size();
+  for (auto& f : c->frags) {
+    DC_CUDA_TRY(cudaEventCreateWithFlags(&f.d2h, cudaEventDisableTiming), &c->err);
+    DC_CUDA_TRY(cudaEventCreateWithFlags(&f.h2d, cudaEventDisableTiming), &c->err);
+  }
+  if (out) {
+    if (*n_inout < n) { *n_inout = n; return fail(c, DC_EOOM, "dc_offload_fragments: output array too small"); }
+    for (int i = 0; i < n; ++i) out[i] = {c->frags[i].layer, c->frags[i].state, c->frags[i].off, c->frags[i].elems};
+  }
+  *n_inout = n;
+  return DC_OK;
+}
+
+extern "C" dc_status dc_offload(dc_ctx* c, int32_t fi, int32_t op, cudaStream_t st) {
+  if (!c || fi < 0 || fi >= (int)c->frags.size()) return fail(c, DC_EINVAL, "dc_offload: bad fragment");
+  FragInfo& f = c->frags[fi];
+  float* dev = (f.state == 0 ? c->m : c->v) + f.off;
+  if ((uint64_t)(f.host_off + f.elems * 4) > c->host_pinned_bytes || !c->host_pinned)
+    return fail(c, DC_EOOM, "dc_offload: pinned host buffer too small");
+  char* host = reinterpret_cast<char*>(c->host_pinned) + f.host_off;
+  switch (op) {
+    case DC_D2H_START:
+      DC_CUDA_TRY(cudaMemcpyAsync(host, dev, f.elems * 4, cudaMemcpyDeviceToHost, st), &c->err);
+      DC_CUDA_TRY(cudaEventRecord(f.d2h, st), &c->err);
+      break;
+    case DC_D2H_SYNC_FREE:
+      DC_CUDA_TRY(cudaStreamWaitEvent(st, f.d2h, 0), &c->err);
+      break;
+    case DC_H2D_START:
+      DC_CUDA_TRY(cudaMemcpyAsync(dev, host, f.elems * 4, cudaMemcpyHostToDevice, st), &c->err);
+      DC_CUDA_TRY(cudaEventRecord(f.h2d, st), &c->err);
+      break;
+    case DC_H2D_SYNC:
+      DC_CUDA_TRY(cudaStreamWaitEvent(st, f.h2d, 0), &c->err);
+      break;
+    default:
+      return fail(c, DC_EINVAL, "dc_offload: bad op");
+  }
+  return DC_OK;
+}
+
+// internal accessors for model.cu
+namespace dc {
+const Layout& ctx_layout(const dc_ctx* c) { return c->L; }
+int ctx_world(const dc_ctx* c) { return c->world; }
+int ctx_rank(const dc_ctx* c) { return c->rank; }
+const dc_schedule* ctx_sched(const dc_ctx* c) { return c->sched; }
+int64_t ctx_numel(const dc_ctx* c, int p) { return c->numel[p]; }
+}  // namespace dc

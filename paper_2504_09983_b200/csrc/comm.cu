@@ -1,0 +1,295 @@
+// Collective kernels of the sharded-parameter life cycle, over peer-mapped
+// memory (NVLink 5 / NVSwitch at N > 1; plain device memory of the other
+// virtual ranks in DC_VIRTUAL_RANKS mode).
+//
+//  ag_push  (P:236 all-gather): every rank stores its shard of each member of a
+//           gather group into every rank's arena with 16-byte st.global —
+//           one local HBM read, N peer writes per vector.  Write-after-read on
+//           the receivers' arena is guarded by ready flags (posted by the
+//           receiver's release of the previous occupant); completion by
+//           per-gather done counters bumped with red.release.sys.
+//  rs_adam  (reduce-scatter + 1/N + Adam, P:127 / P:440 / P:504): owner r pulls
+//           slice r of every rank's bf16 grad slot (peer loads), sums in fp32
+//           in ascending rank order from +0.0, scales by 1/N and applies the
+//           Adam step to its fp32 master/m/v shard, writing the bf16 shard.
+//
+// Flag waits are bounded (globaltimer); a timeout sets a host-mapped error word
+// instead of hanging the GPU.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "dc_internal.h"
+#include "ptx.cuh"
+
+namespace dc {
+
+using bf16 = __nv_bfloat16;
+
+constexpr int AG_MAXM = 48;
+struct AgParams {
+  int nm, world, rank;
+  const uint4* src[AG_MAXM];
+  int64_t dst_off[AG_MAXM];   // byte offset of this rank's slot inside each arena
+  int64_t nvec[AG_MAXM];      // 16-byte vectors of the member's shard
+  uint8_t* arena[MAXW];
+  uint32_t* done_peer[MAXW];  // &done[gid] in every rank's flag table
+  const uint32_t* ready;      // &ready[gid * world] in this rank's table
+  const uint32_t* done_local;
+  uint32_t epoch, done_target;
+  int wait;
+  uint64_t timeout_ns;
+  uint32_t* err;
+};
+
+__device__ __forceinline__ bool spin_ge(const uint32_t* p, uint32_t target, uint64_t t0, uint64_t tmo,
+                                        uint32_t* err, uint32_t code) {
+  while (ptx::ld_acquire_sys(p) < target) {
+    if (ptx::globaltimer() - t0 > tmo) {
+      atomicExch(err, code);
+      return false;
+    }
+    __nanosleep(64);
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(512) ag_push_kernel(const AgParams p) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    const uint64_t t0 = ptx::globaltimer();
+    int good = 1;
+    for (int q = 0; q < p.world && good; ++q)
+      good = spin_ge(p.ready + q, p.epoch, t0, p.timeout_ns, p.err, 0x100u | q);
+    ok = good;
+  }
+  __syncthreads();
+  if (!ok) return;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int m = 0; m < p.nm; ++m) {
+    const uint4* src = p.src[m];
+    const int64_t n = p.nvec[m];
+    const int64_t off = p.dst_off[m];
+    int64_t i = tid;
+    for (; i + 3 * nthr < n; i += 4 * nthr) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(src + i + u * nthr);
+      for (int q = 0; q < p.world; ++q) {
+        uint4* dst = reinterpret_cast<uint4*>(p.arena[q] + off);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dst[i + u * nthr] = v[u];
+      }
+    }
+    for (; i < n; i += nthr) {
+      const uint4 v = __ldg(src + i);
+      for (int q = 0; q < p.world; ++q) reinterpret_cast<uint4*>(p.arena[q] + off)[i] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < p.world; ++q) ptx::red_add_release_sys(p.done_peer[q], 1u);
+    if (p.wait && blockIdx.x == 0)
+      spin_ge(p.done_local, p.done_target, ptx::globaltimer(), p.timeout_ns, p.err, 0x200u);
+  }
+}
+
+dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const uint64_t* arena_peers,
+                    const uint32_t* ready_local, uint32_t epoch, PeerFlags done_peers, const uint32_t* done_local,
+                    uint32_t done_target, int ctas, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st) {
+  // members beyond AG_MAXM go to extra launches; only the last one waits
+  for (size_t b = 0; b < mem.size(); b += AG_MAXM) {
+    AgParams p{};
+    p.nm = (int)std::min<size_t>(AG_MAXM, mem.size() - b);
+    p.world = world; p.rank = rank;
+    for (int i = 0; i < p.nm; ++i) {
+      const AgMember& a = mem[b + i];
+      p.src[i] = reinterpret_cast<const uint4*>(a.src);
+      p.dst_off[i] = a.dst_off_bytes;
+      p.nvec[i] = a.bytes / 16;
+    }
+    for (int q = 0; q < world; ++q) {
+      p.arena[q] = reinterpret_cast<uint8_t*>(arena_peers[q]);
+      p.done_peer[q] = done_peers.p[q];
+    }
+    p.ready = ready_local;
+    p.done_local = done_local;
+    p.epoch = epoch;
+    p.done_target = done_target;
+    p.wait = (b + AG_MAXM >= mem.size());
+    p.timeout_ns = timeout_ns;
+    p.err = err_flag;
+    ag_push_kernel<<<ctas, 512, 0, st>>>(p);
+    if (cudaGetLastError() != cudaSuccess) return DC_ECUDA;
+    count_launch();
+  }
+  return DC_OK;
+}
+
+// ------------------------------------------------------------------ rs_adam
+constexpr int RS_MAXM = 48;
+struct RsParams {
+  int nm, world, rank;
+  int64_t goff[RS_MAXM];      // byte offset of member's padded tensor in a grad slot
+  int64_t S[RS_MAXM];
+  int64_t store_off[RS_MAXM];
+  const uint8_t* slot[MAXW];  // this layer's grad slot on every rank
+  const uint32_t* ready;      // grad-ready flags [world] in this rank's table
+  uint32_t ready_target;
+  uint32_t* consumed[MAXW];   // consumed[slot][rank] in every rank's table
+  uint32_t consumed_value;
+  uint32_t* done_ctr;
+  uint32_t done_target;
+  float* master; float* m; float* v; bf16* shard;
+  float w1, w2, b2, neg_s, c, eps, invN;
+  uint64_t timeout_ns;
+  uint32_t* err;
+};
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+__global__ void __launch_bounds__(256) rs_adam_kernel(const RsParams p) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    const uint64_t t0 = ptx::globaltimer();
+    int good = 1;
+    for (int q = 0; q < p.world && good; ++q)
+      good = spin_ge(p.ready + q, p.ready_target, t0, p.timeout_ns, p.err, 0x300u | q);
+    ok = good;
+  }
+  __syncthreads();
+  if (ok) {
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (int mi = 0; mi < p.nm; ++mi) {
+      const int64_t n8 = p.S[mi] / 8;
+      const int64_t gbase = p.goff[mi] + (int64_t)p.rank * p.S[mi] * 2;
+      float* mst = p.master + p.store_off[mi];
+      float* mm = p.m + p.store_off[mi];
+      float* vv = p.v + p.store_off[mi];
+      bf16* sh = p.shard + p.store_off[mi];
+      for (int64_t i = tid; i < n8; i += nthr) {
+        float g[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[j] = 0.0f;
+        for (int q = 0; q < p.world; ++q) {      // ascending rank order, fp32
+          const uint4 u = *reinterpret_cast<const uint4*>(p.slot[q] + gbase + i * 16);
+          float f[8];
+          bf16x8_to_f32(u, f);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) g[j] = __fadd_rn(g[j], f[j]);
+        }
+        float4 P0 = reinterpret_cast<float4*>(mst)[2 * i], P1 = reinterpret_cast<float4*>(mst)[2 * i + 1];
+        float4 M0 = reinterpret_cast<float4*>(mm)[2 * i], M1 = reinterpret_cast<float4*>(mm)[2 * i + 1];
+        float4 V0 = reinterpret_cast<float4*>(vv)[2 * i], V1 = reinterpret_cast<float4*>(vv)[2 * i + 1];
+        float pp[8] = {P0.x, P0.y, P0.z, P0.w, P1.x, P1.y, P1.z, P1.w};
+        float m8[8] = {M0.x, M0.y, M0.z, M0.w, M1.x, M1.y, M1.z, M1.w};
+        float v8[8] = {V0.x, V0.y, V0.z, V0.w, V1.x, V1.y, V1.z, V1.w};
+        uint4 out;
+        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&out);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float gj = __fmul_rn(g[j], p.invN);
+          const float mj = __fadd_rn(m8[j], __fmul_rn(p.w1, __fsub_rn(gj, m8[j])));
+          const float vj = __fadd_rn(__fmul_rn(p.b2, v8[j]), __fmul_rn(__fmul_rn(p.w2, gj), gj));
+          const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(vj), p.c), p.eps);
+          pp[j] = __fadd_rn(pp[j], __fdiv_rn(__fmul_rn(p.neg_s, mj), d));
+          m8[j] = mj;
+          v8[j] = vj;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) o2[t] = __floats2bfloat162_rn(pp[2 * t], pp[2 * t + 1]);
+        reinterpret_cast<float4*>(mst)[2 * i] = make_float4(pp[0], pp[1], pp[2], pp[3]);
+        reinterpret_cast<float4*>(mst)[2 * i + 1] = make_float4(pp[4], pp[5], pp[6], pp[7]);
+        reinterpret_cast<float4*>(mm)[2 * i] = make_float4(m8[0], m8[1], m8[2], m8[3]);
+        reinterpret_cast<float4*>(mm)[2 * i + 1] = make_float4(m8[4], m8[5], m8[6], m8[7]);
+        reinterpret_cast<float4*>(vv)[2 * i] = make_float4(v8[0], v8[1], v8[2], v8[3]);
+        reinterpret_cast<float4*>(vv)[2 * i + 1] = make_float4(v8[4], v8[5], v8[6], v8[7]);
+        reinterpret_cast<uint4*>(sh)[i] = out;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const uint32_t prev = atomicAdd(p.done_ctr, 1u);
+    if (prev + 1 == p.done_target) {            // last CTA: every slice pulled
+      __threadfence_system();
+      for (int q = 0; q < p.world; ++q) ptx::st_release_sys(p.consumed[q], p.consumed_value);
+    }
+  }
+}
+
+dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const uint64_t* slot_peers,
+                    const uint32_t* ready_local, uint32_t ready_target, PeerFlags consumed_peers,
+                    uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master, float* m,
+                    float* v, void* shard, float s, float c, float beta1, float beta2, float eps, int ctas,
+                    uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st) {
+  if (mem.size() > (size_t)RS_MAXM) return DC_EINVAL;
+  RsParams p{};
+  p.nm = (int)mem.size();
+  p.world = world; p.rank = rank;
+  for (int i = 0; i < p.nm; ++i) {
+    p.goff[i] = mem[i].goff_bytes;
+    p.S[i] = mem[i].S;
+    p.store_off[i] = mem[i].store_off;
+  }
+  for (int q = 0; q < world; ++q) {
+    p.slot[q] = reinterpret_cast<const uint8_t*>(slot_peers[q]);
+    p.consumed[q] = consumed_peers.p[q];
+  }
+  p.ready = ready_local; p.ready_target = ready_target;
+  p.consumed_value = consumed_value;
+  p.done_ctr = done_ctr; p.done_target = done_target;
+  p.master = master; p.m = m; p.v = v; p.shard = reinterpret_cast<bf16*>(shard);
+  p.w1 = (float)(1.0 - (double)beta1);
+  p.w2 = (float)(1.0 - (double)beta2);
+  p.b2 = beta2;
+  p.neg_s = -s;
+  p.c = c;
+  p.eps = eps;
+  p.invN = (float)(1.0 / (double)world);
+  p.timeout_ns = timeout_ns;
+  p.err = err_flag;
+  rs_adam_kernel<<<ctas, 256, 0, st>>>(p);
+  if (cudaGetLastError() != cudaSuccess) return DC_ECUDA;
+  count_launch();
+  return DC_OK;
+}
+
+// ------------------------------------------------------------------ flags
+struct PostParams { uint32_t* p[MAXW]; int n; uint32_t value; };
+__global__ void post_flags_kernel(const PostParams p) {
+  __threadfence_system();
+  for (int i = 0; i < p.n; ++i) ptx::st_release_sys(p.p[i], p.value);
+}
+void k_post_flags(PeerFlags dst, uint32_t value, cudaStream_t st) {
+  PostParams p{};
+  p.n = dst.n;
+  for (int i = 0; i < dst.n; ++i) p.p[i] = dst.p[i];
+  p.value = value;
+  post_flags_kernel<<<1, 1, 0, st>>>(p);
+  count_launch();
+}
+
+__global__ void wait_flags_kernel(const uint32_t* f, int n, uint32_t target, uint64_t tmo, uint32_t* err) {
+  const uint64_t t0 = ptx::globaltimer();
+  for (int i = 0; i < n; ++i)
+    if (!spin_ge(f + i, target, t0, tmo, err, 0x400u | i)) return;
+}
+void k_wait_flags(const uint32_t* flags, int n, uint32_t target, uint64_t timeout_ns, uint32_t* err_flag,
+                  cudaStream_t st) {
+  wait_flags_kernel<<<1, 1, 0, st>>>(flags, n, target, timeout_ns, err_flag);
+  count_launch();
+}
+
+}  // namespace dc

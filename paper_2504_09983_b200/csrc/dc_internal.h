@@ -1,0 +1,88 @@
+// Internal declarations shared by the library's translation units.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/dc.h"
+
+namespace dc {
+
+void set_global_error(const std::string& s);
+void count_launch();                 // increments the launch counter (per thread)
+int64_t launch_count();
+void reset_launch_count();
+
+#define DC_CUDA_TRY(expr, ctxerr)                                                   \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess) {                                                        \
+      *(ctxerr) = std::string(#expr ": ") + cudaGetErrorString(_e);                 \
+      return DC_ECUDA;                                                              \
+    }                                                                               \
+  } while (0)
+
+struct Layout {
+  std::vector<int64_t> S, store_off, goff;
+  std::vector<int> layer_first, layer_count;
+  int64_t shard_elems = 0, grad_slot_bytes = 0, flag_words = 0;
+  int n_layers = 0;
+  // flag table (uint32 words)
+  int64_t f_ready = 0, f_done = 0, f_gready = 0, f_gcons = 0, f_rsdone = 0;
+};
+
+struct dc_ctx_fwd;
+const Layout& ctx_layout(const dc_ctx* c);
+int ctx_world(const dc_ctx* c);
+int ctx_rank(const dc_ctx* c);
+const dc_schedule* ctx_sched(const dc_ctx* c);
+int64_t ctx_numel(const dc_ctx* c, int p);
+int sched_num_ops(const dc_schedule* s);
+void sched_op(const dc_schedule* s, int i, int* kind, int* id, const int64_t** members, int* nmem,
+              int64_t* arena_off, int64_t* bytes, const int** posts, int* nposts, const int** waits, int* nwaits);
+enum { K_COMPUTE, K_AG, K_REL, K_RS, K_OFF, K_OFFSYNC, K_RELOAD, K_RELOADSYNC };
+
+dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* err);
+
+// ------------------------------------------------------------------ kernels
+// glue.cu
+void k_init_param(uint64_t seed, int32_t tensor_id, int64_t numel, int32_t world, int32_t rank,
+                  int64_t S, float k, float* master, void* shard, cudaStream_t st);
+void k_rmsnorm_fwd(const void* x, const void* g, void* h, float* rstd, int T, int H, cudaStream_t st);
+void k_rmsnorm_bwd(const void* dh, const void* x, const void* g, const float* rstd, const void* dres,
+                   void* dx, float* dg_partial, int T, int H, cudaStream_t st);
+int rmsnorm_bwd_blocks(int T);
+void k_colsum_to_bf16(const float* partial, int nblk, int H, void* out, cudaStream_t st);
+void k_attn_mix_fwd(const void* qkv, void* a, int T, int qd, int kvd, int hd, int grp, cudaStream_t st);
+void k_attn_mix_bwd(void* dqkv, const void* qkv, int T, int qd, int kvd, int hd, int grp, cudaStream_t st);
+void k_act_fwd(const void* gu, void* act, int T, int F, cudaStream_t st);
+void k_act_bwd(const void* dact, const void* gu, void* dgu, int T, int F, cudaStream_t st);
+void k_loss(const void* y, const void* t, void* dy, float* partial, float* loss, int64_t n, cudaStream_t st);
+void k_zero(void* p, int64_t bytes, cudaStream_t st);
+
+// comm.cu
+constexpr int MAXW = 8;                       // max ranks on one NVSwitch box
+struct PeerFlags { uint32_t* p[MAXW]; int n; };
+struct AgMember { const void* src; int64_t dst_off_bytes; int64_t bytes; };
+struct RsMember {
+  int64_t goff_bytes;      // member's padded full tensor inside the grad slot
+  int64_t S;               // shard elements
+  int64_t store_off;       // member's shard offset in the per-rank store
+};
+dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const uint64_t* arena_peers,
+                    const uint32_t* ready_local, uint32_t epoch, PeerFlags done_peers,
+                    const uint32_t* done_local, uint32_t done_target, int ctas, uint64_t timeout_ns,
+                    uint32_t* err_flag, cudaStream_t st);
+dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const uint64_t* slot_peers,
+                    const uint32_t* ready_local, uint32_t ready_target, PeerFlags consumed_peers,
+                    uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master,
+                    float* m, float* v, void* shard, float s, float c, float beta1, float beta2,
+                    float eps, int ctas, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st);
+void k_post_flags(PeerFlags dst, uint32_t value, cudaStream_t st);
+void k_wait_flags(const uint32_t* flags, int n, uint32_t target, uint64_t timeout_ns,
+                  uint32_t* err_flag, cudaStream_t st);
+
+}  // namespace dc

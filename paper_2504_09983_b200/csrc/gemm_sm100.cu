@@ -1,0 +1,334 @@
+// bf16 GEMM on the 5th-generation tensor cores (sm_100a):
+//   C[M,N] (bf16) = A_op[M,K] * B_op[K,N] (+ R)   with fp32 accumulation in TMEM.
+//
+// Persistent, warp-specialised, one CTA per SM:
+//   warp 0      TMA producer (one elected lane): A/B tiles -> 4-stage smem ring
+//   warp 1      MMA issuer (one lane): tcgen05.mma 128x256x16, accumulators in
+//               TMEM (2 x 256 columns, double buffered across tiles)
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue: tcgen05.ld -> registers -> (+R) -> bf16 -> global
+// Operand majorness per operand (K-major, or MN-major through the UMMA
+// descriptor's transpose bit), so the three layer GEMMs need no transposes:
+//   forward  Y  = X  W^T : A K-major,  B K-major
+//   backward dX = dY W   : A K-major,  B MN-major
+//   backward dW = dY^T X : A MN-major, B MN-major
+// B may be split into up to 4 segments along N (fused q|k|v and gate|up
+// projections read three / two gathered tensors) or along K (their dX).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "dc_internal.h"
+#include "ptx.cuh"
+
+namespace dc {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4, UMMA_K = 16;
+constexpr int A_STAGE = BM * BK * 2;          // 16 KiB
+constexpr int B_STAGE = BN * BK * 2;          // 32 KiB
+constexpr int GEMM_THREADS = 256;
+constexpr int TMEM_COLS = 512;
+constexpr int GEMM_SMEM = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
+
+struct GemmParams {
+  int M, N, K;
+  int m_tiles, n_tiles, k_blocks;
+  int nseg, split_k;
+  int seg_end[4];      // cumulative, in n-tiles (split N) or k-blocks (split K)
+  int a_mn, b_mn;
+  __nv_bfloat16* C;
+  int64_t ldc;
+  const __nv_bfloat16* R;
+  int64_t ldr;
+  uint32_t idesc;
+};
+
+__device__ __forceinline__ int seg_of(const GemmParams& p, int idx) {
+  int s = 0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    if (i + 1 < p.nseg && idx >= p.seg_end[i]) s = i + 1;
+  return s;
+}
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+gemm_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
+                const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
+                const __grid_constant__ CUtensorMap mapB3, const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smB + STAGES * B_STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int num_tiles = p.m_tiles * p.n_tiles;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&mapA);
+    ptx::tma_prefetch(&mapB0);
+    if (p.nseg > 1) ptx::tma_prefetch(&mapB1);
+    if (p.nseg > 2) ptx::tma_prefetch(&mapB2);
+    if (p.nseg > 3) ptx::tma_prefetch(&mapB3);
+    for (int s = 0; s < STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { ptx::mbar_init(&tfull[b], 1); ptx::mbar_init(&tempty[b], 4); }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ----------------------------------------------------------- producer
+      int stage = 0; uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+        const int m0 = mt * BM;
+        int bseg = 0, n0 = nt * BN;
+        if (!p.split_k) {
+          bseg = seg_of(p, nt);
+          n0 = (nt - (bseg ? p.seg_end[bseg - 1] : 0)) * BN;
+        }
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], A_STAGE + B_STAGE);
+          uint8_t* a = smA + stage * A_STAGE;
+          uint8_t* b = smB + stage * B_STAGE;
+          const int k0 = kb * BK;
+          if (!p.a_mn) {
+            ptx::tma_load_2d(a, &mapA, &full[stage], k0, m0);
+          } else {
+            ptx::tma_load_2d(a, &mapA, &full[stage], m0, k0);
+            ptx::tma_load_2d(a + 8192, &mapA, &full[stage], m0 + 64, k0);
+          }
+          int s = bseg, kk0 = k0;
+          if (p.split_k) {
+            s = seg_of(p, kb);
+            kk0 = (kb - (s ? p.seg_end[s - 1] : 0)) * BK;
+          }
+          const CUtensorMap* mb = s == 0 ? &mapB0 : s == 1 ? &mapB1 : s == 2 ? &mapB2 : &mapB3;
+          if (!p.b_mn) {
+            ptx::tma_load_2d(b, mb, &full[stage], kk0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ptx::tma_load_2d(b + j * 8192, mb, &full[stage], n0 + 64 * j, kk0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ----------------------------------------------------------- MMA issuer
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t aphase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(smA + stage * A_STAGE);
+          const uint32_t b_addr = ptx::smem_u32(smB + stage * B_STAGE);
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            uint64_t ad, bd;
+            if (!p.a_mn) ad = ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
+            else         ad = ptx::umma_desc_sw128(a_addr + k * 2048, 8192, 1024);
+            if (!p.b_mn) bd = ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
+            else         bd = ptx::umma_desc_sw128(b_addr + k * 2048, 8192, 1024);
+            ptx::umma_f16(d, ad, bd, p.idesc, (kb | k) != 0);
+          }
+          ptx::umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        ptx::umma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------- epilogue
+    const int q = warp & 3;
+    int acc = 0; uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      ptx::mbar_wait(&tfull[acc], aphase);
+      ptx::tc_fence_after();
+      const int row = mt * BM + q * 32 + lane;
+      const bool row_ok = row < p.M;
+      __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
+      const __nv_bfloat16* rrow = p.R ? p.R + (int64_t)row * p.ldr : nullptr;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+        ptx::tmem_ld_wait();
+        const int col0 = nt * BN + c * 32;
+        if (row_ok && col0 < p.N) {
+          float f[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+          if (rrow) {
+            if (col0 + 32 <= p.N) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                uint4 rv = *reinterpret_cast<const uint4*>(rrow + col0 + j);
+                const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  float2 rf = __bfloat1622float2(r2[t]);
+                  f[j + 2 * t] = __fadd_rn(f[j + 2 * t], rf.x);
+                  f[j + 2 * t + 1] = __fadd_rn(f[j + 2 * t + 1], rf.y);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j < p.N) f[j] = __fadd_rn(f[j], __bfloat162float(rrow[col0 + j]));
+            }
+          }
+          if (col0 + 32 <= p.N) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              uint4 o;
+              __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+              for (int t = 0; t < 4; ++t) o2[t] = __floats2bfloat162_rn(f[j + 2 * t], f[j + 2 * t + 1]);
+              *reinterpret_cast<uint4*>(crow + col0 + j) = o;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < p.N) crow[col0 + j] = __float2bfloat16_rn(f[j]);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map: inner dimension `inner` (contiguous) x `outer` rows,
+// row pitch `ld` elements, box {64, box_outer}, 128-byte swizzle, OOB -> 0.
+static bool make_map(CUtensorMap* m, const void* ptr, int64_t inner, int64_t outer, int64_t ld,
+                     int box_outer) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static int num_sms_cached() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* err) {
+  if (g->M <= 0 || g->N <= 0 || g->K <= 0 || (g->N % 8) || (g->K % 8) || g->n_bseg < 1 || g->n_bseg > 4) {
+    *err = "dc_gemm: M,N,K must be > 0, N and K multiples of 8, 1..4 B segments";
+    return DC_EINVAL;
+  }
+  GemmParams p{};
+  p.M = g->M; p.N = g->N; p.K = g->K;
+  p.m_tiles = (g->M + BM - 1) / BM;
+  p.n_tiles = (g->N + BN - 1) / BN;
+  p.k_blocks = (g->K + BK - 1) / BK;
+  p.nseg = g->n_bseg; p.split_k = g->b_split_k;
+  p.a_mn = g->a_mn_major; p.b_mn = g->b_mn_major;
+  p.C = reinterpret_cast<__nv_bfloat16*>(g->C); p.ldc = g->ldc;
+  p.R = reinterpret_cast<const __nv_bfloat16*>(g->R); p.ldr = g->ldr;
+  p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a_mn << 15) | ((uint32_t)p.b_mn << 16) |
+            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  CUtensorMap mA, mB[4];
+  bool ok = p.a_mn ? make_map(&mA, g->A, g->M, g->K, g->lda, 64) : make_map(&mA, g->A, g->K, g->M, g->lda, BM);
+  int prev = 0;
+  for (int s = 0; s < g->n_bseg; ++s) {
+    p.seg_end[s] = g->bseg_end[s];
+    const int unit = g->b_split_k ? BK : BN;
+    const int64_t lo = (int64_t)prev * unit;
+    int64_t hi = (int64_t)g->bseg_end[s] * unit;
+    const int64_t full_ext = g->b_split_k ? g->K : g->N;
+    if (s == g->n_bseg - 1) hi = full_ext;
+    if (hi > full_ext) hi = full_ext;
+    if (hi <= lo) { *err = "dc_gemm: empty or unordered B segment"; return DC_EINVAL; }
+    const int64_t ext = hi - lo;                   // this segment's N (or K) extent
+    const int64_t kdim = g->b_split_k ? ext : g->K;
+    const int64_t ndim = g->b_split_k ? g->N : ext;
+    ok = ok && (g->b_mn_major ? make_map(&mB[s], g->B[s], ndim, kdim, g->ldb[s], 64)
+                              : make_map(&mB[s], g->B[s], kdim, ndim, g->ldb[s], BN));
+    prev = g->bseg_end[s];
+  }
+  if (g->n_bseg == 1) p.seg_end[0] = g->b_split_k ? p.k_blocks : p.n_tiles;
+  for (int s = g->n_bseg; s < 4; ++s) { mB[s] = mB[0]; p.seg_end[s] = p.seg_end[g->n_bseg - 1]; }
+  if (!ok) { *err = "dc_gemm: cuTensorMapEncodeTiled failed (alignment / pitch must be 16 B)"; return DC_EINVAL; }
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(gemm_bf16_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) != cudaSuccess) {
+      *err = "dc_gemm: cannot set dynamic smem";
+      return DC_ECUDA;
+    }
+    attr = true;
+  }
+  const int tiles = p.m_tiles * p.n_tiles;
+  int sms = g->num_sms > 0 ? g->num_sms : num_sms_cached();
+  const int grid = tiles < sms ? tiles : sms;
+  gemm_bf16_sm100<<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { *err = std::string("dc_gemm launch: ") + cudaGetErrorString(e); return DC_ECUDA; }
+  count_launch();
+  return DC_OK;
+}
+
+}  // namespace dc
+
+extern "C" dc_status dc_gemm(const dc_gemm_args* g, cudaStream_t stream) {
+  std::string err;
+  dc_status s = dc::launch_gemm(g, stream, &err);
+  if (s != DC_OK) dc::set_global_error(err);
+  return s;
+}

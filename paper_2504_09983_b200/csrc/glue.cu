@@ -1,0 +1,385 @@
+// Glue kernels of the synthetic Llama-shaped layer and the
+// counter-based parameter initialiser.  All HBM-bound, 16-byte vectorised,
+// fp32 math, bf16 storage (RNE).  Row reductions use a fixed tree so results
+// are deterministic run to run.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "dc_internal.h"
+
+namespace dc {
+
+using bf16 = __nv_bfloat16;
+using bf162 = __nv_bfloat162;
+
+// ------------------------------------------------------------------ generator
+// value(seed, tensor_id, idx): splitmix64(seed ^ (tensor_id << 40) ^ idx),
+// u = (h >> 40) * 2^-24, x = (u - 0.5f) * k.  Same recipe as synth/gen.py.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void init_param_kernel(uint64_t key, int64_t numel, int64_t base, int64_t S, float k,
+                                  float* __restrict__ master, bf16* __restrict__ shard) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < S; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gi = base + j;
+    float v = 0.0f;
+    if (gi < numel) {
+      if (k == 0.0f) {
+        v = 1.0f;
+      } else {
+        const uint64_t h = splitmix64(key ^ (uint64_t)gi);
+        const float u = __fmul_rn((float)(uint32_t)(h >> 40), 5.9604644775390625e-08f);  // 2^-24
+        v = __fmul_rn(__fsub_rn(u, 0.5f), k);
+      }
+    }
+    master[j] = v;
+    shard[j] = __float2bfloat16_rn(v);
+  }
+}
+
+void k_init_param(uint64_t seed, int32_t tensor_id, int64_t numel, int32_t world, int32_t rank, int64_t S,
+                  float k, float* master, void* shard, cudaStream_t st) {
+  const uint64_t key = seed ^ ((uint64_t)tensor_id << 40);
+  int64_t blocks = (S + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  init_param_kernel<<<(int)blocks, 256, 0, st>>>(key, numel, (int64_t)rank * S, S, k, master,
+                                                  reinterpret_cast<bf16*>(shard));
+  count_launch();
+}
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ void load8(const bf16* p, float (&f)[8]) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  const bf162* h = reinterpret_cast<const bf162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void store8(bf16* p, const float (&f)[8]) {
+  uint4 u;
+  bf162* h = reinterpret_cast<bf162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+// block-wide sum, fixed order (warp shuffle tree, then warp 0 over warps)
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < NT / 32 ? sh[l] : 0.0f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (l == 0) sh[0] = v;
+  }
+  __syncthreads();
+  float r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// ------------------------------------------------------------------ RMSNorm
+// h = bf16(x * rstd * g), rstd = 1/sqrt(mean(x^2) + eps).  One CTA per row.
+constexpr int RN_T = 256;
+__global__ void __launch_bounds__(RN_T) rmsnorm_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
+                                                          bf16* __restrict__ h, float* __restrict__ rstd, int H) {
+  __shared__ float sh[32];
+  const int64_t row = blockIdx.x;
+  const bf16* xr = x + row * H;
+  float ss = 0.0f;
+  for (int c = threadIdx.x * 8; c < H; c += RN_T * 8) {
+    float f[8];
+    load8(xr + c, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss = fmaf(f[i], f[i], ss);
+  }
+  ss = block_sum<RN_T>(ss, sh);
+  const float r = 1.0f / sqrtf(ss / (float)H + 1e-5f);
+  if (threadIdx.x == 0) rstd[row] = r;
+  for (int c = threadIdx.x * 8; c < H; c += RN_T * 8) {
+    float f[8], gg[8];
+    load8(xr + c, f);
+    load8(g + c, gg);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = f[i] * r * gg[i];
+    store8(h + row * H + c, f);
+  }
+}
+
+void k_rmsnorm_fwd(const void* x, const void* g, void* h, float* rstd, int T, int H, cudaStream_t st) {
+  rmsnorm_fwd_kernel<<<T, RN_T, 0, st>>>((const bf16*)x, (const bf16*)g, (bf16*)h, rstd, H);
+  count_launch();
+}
+
+// dx = bf16(dres + rstd * (dn - n * mean(dn * n))), n = x*rstd, dn = dh*g;
+// dg partial[blk][c] = sum over the block's rows of dh*n (fixed row order).
+constexpr int RB_ROWS = 16;
+int rmsnorm_bwd_blocks(int T) { return (T + RB_ROWS - 1) / RB_ROWS; }
+
+__global__ void __launch_bounds__(RN_T) rmsnorm_bwd_kernel(const bf16* __restrict__ dh, const bf16* __restrict__ x,
+                                                          const bf16* __restrict__ g, const float* __restrict__ rstd,
+                                                          const bf16* __restrict__ dres, bf16* __restrict__ dx,
+                                                          float* __restrict__ dgp, int T, int H) {
+  __shared__ float sh[32];
+  // each thread owns columns c = threadIdx.x*8 + j*RN_T*8 (H <= 8192 -> <= 4 chunks)
+  float acc[4][8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[j][i] = 0.0f;
+  const int r0 = blockIdx.x * RB_ROWS;
+  for (int rr = 0; rr < RB_ROWS; ++rr) {
+    const int row = r0 + rr;
+    if (row >= T) break;
+    const float rs = rstd[row];
+    const bf16* dhr = dh + (int64_t)row * H;
+    const bf16* xr = x + (int64_t)row * H;
+    float dot = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = threadIdx.x * 8 + j * RN_T * 8;
+      if (c < H) {
+        float a[8], b[8], gg[8];
+        load8(dhr + c, a);
+        load8(xr + c, b);
+        load8(g + c, gg);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float n = b[i] * rs;
+          acc[j][i] += a[i] * n;
+          dot = fmaf(a[i] * gg[i], n, dot);
+        }
+      }
+    }
+    dot = block_sum<RN_T>(dot, sh) / (float)H;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = threadIdx.x * 8 + j * RN_T * 8;
+      if (c < H) {
+        float a[8], b[8], gg[8], d[8];
+        load8(dhr + c, a);
+        load8(xr + c, b);
+        load8(g + c, gg);
+        if (dres) load8(dres + (int64_t)row * H + c, d);
+        else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) d[i] = 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float n = b[i] * rs;
+          d[i] = d[i] + rs * (a[i] * gg[i] - n * dot);
+        }
+        store8(dx + (int64_t)row * H + c, d);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = threadIdx.x * 8 + j * RN_T * 8;
+    if (c < H) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dgp[(int64_t)blockIdx.x * H + c + i] = acc[j][i];
+    }
+  }
+}
+
+void k_rmsnorm_bwd(const void* dh, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
+                   float* dg_partial, int T, int H, cudaStream_t st) {
+  rmsnorm_bwd_kernel<<<rmsnorm_bwd_blocks(T), RN_T, 0, st>>>((const bf16*)dh, (const bf16*)x, (const bf16*)g, rstd,
+                                                             (const bf16*)dres, (bf16*)dx, dg_partial, T, H);
+  count_launch();
+}
+
+__global__ void colsum_kernel(const float* __restrict__ p, int nblk, int H, bf16* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= H) return;
+  float s = 0.0f;
+  for (int b = 0; b < nblk; ++b) s += p[(int64_t)b * H + c];
+  out[c] = __float2bfloat16_rn(s);
+}
+
+void k_colsum_to_bf16(const float* partial, int nblk, int H, void* out, cudaStream_t st) {
+  colsum_kernel<<<(H + 255) / 256, 256, 0, st>>>(partial, nblk, H, (bf16*)out);
+  count_launch();
+}
+
+// ------------------------------------------------------------------ attention surrogate
+// a = bf16(q + rep(k) * rep(v)); qkv row = [q (qd) | k (kvd) | v (kvd)].
+__global__ void attn_mix_fwd_kernel(const bf16* __restrict__ qkv, bf16* __restrict__ a, int T, int qd, int kvd,
+                                    int hd, int grp) {
+  const int ld = qd + 2 * kvd;
+  const int64_t n8 = (int64_t)T * qd / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * 8;
+    const int t = (int)(e / qd), c = (int)(e % qd);
+    const int head = c / hd, d = c % hd;
+    const int kc = (head / grp) * hd + d;
+    const bf16* row = qkv + (int64_t)t * ld;
+    float q[8], k[8], v[8], o[8];
+    load8(row + c, q);
+    load8(row + qd + kc, k);
+    load8(row + qd + kvd + kc, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = fmaf(k[j], v[j], q[j]);
+    store8(a + e, o);
+  }
+}
+
+static int grid_for(int64_t n, int per_block) {
+  int64_t b = (n + per_block - 1) / per_block;
+  if (b > 148 * 8) b = 148 * 8;
+  return b < 1 ? 1 : (int)b;
+}
+
+void k_attn_mix_fwd(const void* qkv, void* a, int T, int qd, int kvd, int hd, int grp, cudaStream_t st) {
+  attn_mix_fwd_kernel<<<grid_for((int64_t)T * qd / 8, 256), 256, 0, st>>>((const bf16*)qkv, (bf16*)a, T, qd, kvd,
+                                                                           hd, grp);
+  count_launch();
+}
+
+// dqkv row = [dq = da (already written by the o-projection dX GEMM) | dk | dv]
+// dk[j*hd+d] = sum_{h in group j} da[h*hd+d] * v[j*hd+d]; dv likewise with k.
+__global__ void attn_mix_bwd_kernel(bf16* __restrict__ dqkv, const bf16* __restrict__ qkv, int T, int qd, int kvd,
+                                    int hd, int grp) {
+  const int ld = qd + 2 * kvd;
+  const int64_t n8 = (int64_t)T * kvd / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * 8;
+    const int t = (int)(e / kvd), kc = (int)(e % kvd);
+    const int j = kc / hd, d = kc % hd;
+    const bf16* row = qkv + (int64_t)t * ld;
+    bf16* drow = dqkv + (int64_t)t * ld;
+    float k[8], v[8], sk[8], sv[8];
+    load8(row + qd + kc, k);
+    load8(row + qd + kvd + kc, v);
+#pragma unroll
+    for (int x = 0; x < 8; ++x) { sk[x] = 0.0f; sv[x] = 0.0f; }
+    for (int h = j * grp; h < (j + 1) * grp; ++h) {
+      float da[8];
+      load8(drow + h * hd + d, da);
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        sk[x] = fmaf(da[x], v[x], sk[x]);
+        sv[x] = fmaf(da[x], k[x], sv[x]);
+      }
+    }
+    store8(drow + qd + kc, sk);
+    store8(drow + qd + kvd + kc, sv);
+  }
+}
+
+void k_attn_mix_bwd(void* dqkv, const void* qkv, int T, int qd, int kvd, int hd, int grp, cudaStream_t st) {
+  attn_mix_bwd_kernel<<<grid_for((int64_t)T * kvd / 8, 256), 256, 0, st>>>((bf16*)dqkv, (const bf16*)qkv, T, qd,
+                                                                            kvd, hd, grp);
+  count_launch();
+}
+
+// ------------------------------------------------------------------ SiLU * up
+__device__ __forceinline__ float sigmoidf_(float z) { return 1.0f / (1.0f + expf(-z)); }
+
+__global__ void act_fwd_kernel(const bf16* __restrict__ gu, bf16* __restrict__ act, int T, int F) {
+  const int64_t n8 = (int64_t)T * F / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * 8;
+    const int t = (int)(e / F), c = (int)(e % F);
+    const bf16* row = gu + (int64_t)t * 2 * F;
+    float g[8], u[8], o[8];
+    load8(row + c, g);
+    load8(row + F + c, u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = g[j] * sigmoidf_(g[j]) * u[j];
+    store8(act + e, o);
+  }
+}
+
+void k_act_fwd(const void* gu, void* act, int T, int F, cudaStream_t st) {
+  act_fwd_kernel<<<grid_for((int64_t)T * F / 8, 256), 256, 0, st>>>((const bf16*)gu, (bf16*)act, T, F);
+  count_launch();
+}
+
+// d_gate = bf16(dact * up * silu'(g)), d_up = bf16(dact * silu(g))
+__global__ void act_bwd_kernel(const bf16* __restrict__ dact, const bf16* __restrict__ gu, bf16* __restrict__ dgu,
+                               int T, int F) {
+  const int64_t n8 = (int64_t)T * F / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * 8;
+    const int t = (int)(e / F), c = (int)(e % F);
+    const bf16* row = gu + (int64_t)t * 2 * F;
+    float g[8], u[8], da[8], dg[8], du[8];
+    load8(row + c, g);
+    load8(row + F + c, u);
+    load8(dact + e, da);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float s = sigmoidf_(g[j]);
+      du[j] = da[j] * (g[j] * s);
+      dg[j] = da[j] * u[j] * (s * (1.0f + g[j] * (1.0f - s)));
+    }
+    store8(dgu + (int64_t)t * 2 * F + c, dg);
+    store8(dgu + (int64_t)t * 2 * F + F + c, du);
+  }
+}
+
+void k_act_bwd(const void* dact, const void* gu, void* dgu, int T, int F, cudaStream_t st) {
+  act_bwd_kernel<<<grid_for((int64_t)T * F / 8, 256), 256, 0, st>>>((const bf16*)dact, (const bf16*)gu, (bf16*)dgu,
+                                                                     T, F);
+  count_launch();
+}
+
+// ------------------------------------------------------------------ loss
+// loss = mean 1/2 (y - t)^2 ; dy = bf16((y - t) / n).  Deterministic 2-pass sum.
+constexpr int LOSS_BLOCKS = 296;
+__global__ void loss_kernel(const bf16* __restrict__ y, const bf16* __restrict__ t, bf16* __restrict__ dy,
+                            float* __restrict__ partial, int64_t n) {
+  __shared__ float sh[32];
+  const float inv = 1.0f / (float)n;
+  float s = 0.0f;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 8; i < n; i += (int64_t)gridDim.x * blockDim.x * 8) {
+    float a[8], b[8], d[8];
+    load8(y + i, a);
+    load8(t + i, b);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float e = a[j] - b[j];
+      s = fmaf(0.5f * e, e, s);
+      d[j] = e * inv;
+    }
+    store8(dy + i, d);
+  }
+  s = block_sum<256>(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+__global__ void loss_final_kernel(const float* __restrict__ partial, int nb, int64_t n, float* __restrict__ loss) {
+  __shared__ float sh[32];
+  float s = 0.0f;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) s += partial[i];
+  s = block_sum<256>(s, sh);
+  if (threadIdx.x == 0) *loss = (float)((double)s / (double)n);
+}
+
+void k_loss(const void* y, const void* t, void* dy, float* partial, float* loss, int64_t n, cudaStream_t st) {
+  loss_kernel<<<LOSS_BLOCKS, 256, 0, st>>>((const bf16*)y, (const bf16*)t, (bf16*)dy, partial, n);
+  loss_final_kernel<<<1, 256, 0, st>>>(partial, LOSS_BLOCKS, n, loss);
+  count_launch();
+  count_launch();
+}
+
+void k_zero(void* p, int64_t bytes, cudaStream_t st) {
+  cudaMemsetAsync(p, 0, bytes, st);
+}
+
+}  // namespace dc

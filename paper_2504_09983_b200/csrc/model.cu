@@ -1,0 +1,547 @@
+// The synthetic Llama-shaped layer stack and the native step executor.
+//
+// The executor walks the bound schedule (S_0 or the planned S) and issues, per
+// op: gathers on the AG stream (ordered after the compute-stream position of
+// the op — reading D23), releases and layer compute on the compute stream,
+// reduce-scatter + Adam on the RS stream, offload copies on the copy stream.
+// With profiling on it records per-op CUDA-event durations and the analytic
+// resident-memory profile P_mem(o) for dc_plan.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "dc_internal.h"
+
+using namespace dc;
+
+namespace {
+
+enum OpCode {
+  F_ATTN_NORM, F_QKV, F_ATTN_MIX, F_O, F_MLP_NORM, F_GATE_UP, F_ACT, F_DOWN, F_LOSS,
+  B_DOWN, B_ACT, B_GATE_UP, B_MLP_NORM, B_O, B_ATTN_MIX, B_QKV, B_ATTN_NORM, RS_OP
+};
+const char* op_name(int c) {
+  static const char* n[] = {"attn_norm", "qkv", "attn_mix", "o_proj", "mlp_norm", "gate_up", "act", "down", "loss",
+                            "down_bwd", "act_bwd", "gate_up_bwd", "mlp_norm_bwd", "o_bwd", "attn_mix_bwd",
+                            "qkv_bwd", "attn_norm_bwd", "rs"};
+  return n[c];
+}
+// param slots inside a layer (llama order of synth/models.py)
+enum { P_G1, P_Q, P_K, P_V, P_O, P_G2, P_GATE, P_UP, P_DOWN, P_N };
+
+struct S0 {
+  int kind;       // K_COMPUTE / K_AG / K_REL / K_RS
+  int code;       // OpCode for compute-like ops
+  bool fwd;
+  int micro, layer;
+  std::vector<int> params;
+};
+
+struct LayerAct { int64_t h1, rstd1, qkv, a, x2, h2, rstd2, gu, act, y; };
+
+}  // namespace
+
+struct dc_model {
+  dc_ctx* ctx = nullptr;
+  dc_model_dims d{};
+  int qd = 0, kvd = 0, qkvd = 0, grp = 0;
+  std::vector<S0> s0;
+  std::vector<LayerAct> la;
+  int64_t ws_dA = 0, ws_dB = 0, ws_dact = 0, ws_dgu = 0, ws_dh = 0, ws_dx2 = 0, ws_dqkv = 0, ws_dgp = 0,
+          ws_lossp = 0, ws_loss = 0;
+  uint64_t act_bytes = 0, layer_act_bytes = 0, ws_bytes = 0;
+  uint8_t* act = nullptr;
+  const void* x = nullptr;
+  const void* target = nullptr;
+  std::vector<cudaEvent_t> ev_pos, ev_done, ev_t0, ev_t1;
+  cudaEvent_t ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<int64_t> dur_us;       // per S_0 op
+  std::vector<int64_t> p_mem;        // per S_0 op
+  int32_t epoch = 0;
+  int64_t launches = 0;
+  int cur_d = 0;                     // which of dA/dB holds dL/d(layer output)
+  std::string err;
+
+  int pid(int layer, int slot) const { return ctx_layout(ctx).layer_first[layer] + slot; }
+  void* W(int layer, int slot) const {
+    void* p = nullptr;
+    dc_tensor_ptr(ctx, pid(layer, slot), &p);
+    return p;
+  }
+  uint8_t* A(int64_t off) const { return act + off; }
+};
+
+static dc_status mfail(dc_model* m, dc_status s, const std::string& e) {
+  if (m) m->err = e;
+  set_global_error(e);
+  return s;
+}
+
+static void build_s0(dc_model* m) {
+  const int L = m->d.layers;
+  std::vector<S0> comp;
+  static const int fwd_codes[] = {F_ATTN_NORM, F_QKV, F_ATTN_MIX, F_O, F_MLP_NORM, F_GATE_UP, F_ACT, F_DOWN};
+  static const int bwd_codes[] = {B_DOWN, B_ACT, B_GATE_UP, B_MLP_NORM, B_O, B_ATTN_MIX, B_QKV, B_ATTN_NORM};
+  auto params_of = [&](int code, int l) -> std::vector<int> {
+    switch (code) {
+      case F_ATTN_NORM: case B_ATTN_NORM: return {m->pid(l, P_G1)};
+      case F_QKV: case B_QKV: return {m->pid(l, P_Q), m->pid(l, P_K), m->pid(l, P_V)};
+      case F_O: case B_O: return {m->pid(l, P_O)};
+      case F_MLP_NORM: case B_MLP_NORM: return {m->pid(l, P_G2)};
+      case F_GATE_UP: case B_GATE_UP: return {m->pid(l, P_GATE), m->pid(l, P_UP)};
+      case F_DOWN: case B_DOWN: return {m->pid(l, P_DOWN)};
+      default: return {};
+    }
+  };
+  for (int l = 0; l < L; ++l)
+    for (int c : fwd_codes) comp.push_back({K_COMPUTE, c, true, 0, l, params_of(c, l)});
+  comp.push_back({K_COMPUTE, F_LOSS, true, 0, L - 1, {}});
+  for (int l = L - 1; l >= 0; --l) {
+    for (int c : bwd_codes) comp.push_back({K_COMPUTE, c, false, 0, l, params_of(c, l)});
+    comp.push_back({K_RS, RS_OP, false, 0, l, {}});
+  }
+  // S_0: gather before first use, release after last use, per region
+  m->s0.clear();
+  size_t i = 0;
+  while (i < comp.size()) {
+    size_t j = i;
+    while (j < comp.size() && comp[j].fwd == comp[i].fwd && comp[j].micro == comp[i].micro) ++j;
+    std::map<int, size_t> first, last;
+    for (size_t k = i; k < j; ++k)
+      for (int p : comp[k].params) {
+        if (!first.count(p)) first[p] = k;
+        last[p] = k;
+      }
+    for (size_t k = i; k < j; ++k) {
+      for (auto& kv : first)
+        if (kv.second == k) m->s0.push_back({K_AG, -1, comp[k].fwd, comp[k].micro, comp[k].layer, {kv.first}});
+      m->s0.push_back(comp[k]);
+      for (auto& kv : last)
+        if (kv.second == k) m->s0.push_back({K_REL, -1, comp[k].fwd, comp[k].micro, comp[k].layer, {kv.first}});
+    }
+    i = j;
+  }
+}
+
+extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_model** out) {
+  if (!ctx || !d || !out) return mfail(nullptr, DC_EINVAL, "dc_model_create: null argument");
+  auto m = std::make_unique<dc_model>();
+  m->ctx = ctx;
+  m->d = *d;
+  const Layout& L = ctx_layout(ctx);
+  if (d->layers != L.n_layers) return mfail(nullptr, DC_EINVAL, "dc_model_create: layer count mismatch");
+  if (d->n_heads % d->n_kv) return mfail(nullptr, DC_EINVAL, "dc_model_create: n_heads % n_kv != 0");
+  m->qd = d->n_heads * d->head_dim;
+  m->kvd = d->n_kv * d->head_dim;
+  m->qkvd = m->qd + 2 * m->kvd;
+  m->grp = d->n_heads / d->n_kv;
+  if (d->hidden % 256 || d->ffn % 256 || m->qd % 256 || m->kvd % 256 || d->hidden > 8192 || d->tokens % 8)
+    return mfail(nullptr, DC_EINVAL, "dc_model_create: hidden/ffn/q/kv dims must be multiples of 256, hidden <= 8192");
+  const int64_t h = d->hidden, f = d->ffn;
+  const int64_t want[P_N] = {h, m->qd * h, m->kvd * h, m->kvd * h, h * m->qd, h, f * h, f * h, h * f};
+  for (int l = 0; l < d->layers; ++l) {
+    if (L.layer_count[l] != P_N) return mfail(nullptr, DC_EINVAL, "dc_model_create: 9 params per layer expected");
+    for (int s = 0; s < P_N; ++s)
+      if (ctx_numel(ctx, L.layer_first[l] + s) != want[s])
+        return mfail(nullptr, DC_EINVAL, "dc_model_create: param shape mismatch");
+  }
+  // activation layout (256-byte aligned pieces)
+  const int64_t T = d->tokens;
+  uint64_t off = 0;
+  auto take = [&](int64_t bytes) { int64_t o = (int64_t)off; off += (bytes + 255) / 256 * 256; return o; };
+  m->la.resize(d->layers);
+  for (int l = 0; l < d->layers; ++l) {
+    LayerAct& a = m->la[l];
+    a.h1 = take(T * h * 2); a.rstd1 = take(T * 4); a.qkv = take(T * m->qkvd * 2); a.a = take(T * m->qd * 2);
+    a.x2 = take(T * h * 2); a.h2 = take(T * h * 2); a.rstd2 = take(T * 4); a.gu = take(T * 2 * f * 2);
+    a.act = take(T * f * 2); a.y = take(T * h * 2);
+    if (l == 0) m->layer_act_bytes = off;
+  }
+  const uint64_t ws0 = off;
+  m->ws_dA = take(T * h * 2); m->ws_dB = take(T * h * 2); m->ws_dact = take(T * f * 2);
+  m->ws_dgu = take(T * 2 * f * 2); m->ws_dh = take(T * h * 2); m->ws_dx2 = take(T * h * 2);
+  m->ws_dqkv = take(T * m->qkvd * 2); m->ws_dgp = take((int64_t)rmsnorm_bwd_blocks((int)T) * h * 4);
+  m->ws_lossp = take(1024 * 4); m->ws_loss = take(256);
+  m->ws_bytes = off - ws0;
+  m->act_bytes = off;
+  build_s0(m.get());
+  const size_t n = m->s0.size();
+  m->dur_us.assign(n, 0);
+  m->p_mem.assign(n, 0);
+  m->ev_pos.resize(n); m->ev_done.resize(n); m->ev_t0.resize(n); m->ev_t1.resize(n);
+  for (size_t i = 0; i < n; ++i) {
+    if (cudaEventCreateWithFlags(&m->ev_pos[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&m->ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreate(&m->ev_t0[i]) != cudaSuccess || cudaEventCreate(&m->ev_t1[i]) != cudaSuccess)
+      return mfail(nullptr, DC_ECUDA, "dc_model_create: event creation failed");
+  }
+  for (auto& e : m->ev_join) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  *out = m.release();
+  return DC_OK;
+}
+
+extern "C" dc_status dc_model_destroy(dc_model* m) {
+  if (!m) return DC_OK;
+  for (size_t i = 0; i < m->ev_pos.size(); ++i) {
+    cudaEventDestroy(m->ev_pos[i]); cudaEventDestroy(m->ev_done[i]);
+    cudaEventDestroy(m->ev_t0[i]); cudaEventDestroy(m->ev_t1[i]);
+  }
+  for (auto& e : m->ev_join) if (e) cudaEventDestroy(e);
+  delete m;
+  return DC_OK;
+}
+
+extern "C" dc_status dc_model_act_bytes(const dc_model* m, uint64_t* b) {
+  if (!m || !b) return mfail(nullptr, DC_EINVAL, "dc_model_act_bytes: null argument");
+  *b = m->act_bytes;
+  return DC_OK;
+}
+
+extern "C" dc_status dc_model_bind(dc_model* m, void* buf, uint64_t bytes, const void* x, const void* target) {
+  if (!m || !buf || !x || !target) return mfail(m, DC_EINVAL, "dc_model_bind: null argument");
+  if (bytes < m->act_bytes) return mfail(m, DC_EOOM, "dc_model_bind: activation buffer too small");
+  if ((reinterpret_cast<uintptr_t>(buf) & 255) || (reinterpret_cast<uintptr_t>(x) & 15) ||
+      (reinterpret_cast<uintptr_t>(target) & 15))
+    return mfail(m, DC_EINVAL, "dc_model_bind: buffer alignment");
+  m->act = reinterpret_cast<uint8_t*>(buf);
+  m->x = x;
+  m->target = target;
+  return DC_OK;
+}
+
+// ------------------------------------------------------------------ layer ops
+static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t lda, int a_mn,
+                      std::initializer_list<const void*> Bs, std::initializer_list<int64_t> ldbs,
+                      std::initializer_list<int> ends, int b_mn, int split_k, void* C, int64_t ldc,
+                      const void* R, int64_t ldr, cudaStream_t st) {
+  dc_gemm_args g{};
+  g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.a_mn_major = a_mn;
+  int i = 0;
+  for (const void* b : Bs) g.B[i++] = b;
+  g.n_bseg = i;
+  i = 0;
+  for (int64_t l : ldbs) g.ldb[i++] = l;
+  i = 0;
+  for (int e : ends) g.bseg_end[i++] = e;
+  g.b_mn_major = b_mn; g.b_split_k = split_k;
+  g.C = C; g.ldc = ldc; g.R = R; g.ldr = ldr;
+  std::string err;
+  dc_status s = launch_gemm(&g, st, &err);
+  if (s != DC_OK) return mfail(m, s, err);
+  return DC_OK;
+}
+
+static const void* layer_in(const dc_model* m, int l) { return l == 0 ? m->x : m->A(m->la[l - 1].y); }
+
+static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
+  const int T = m->d.tokens, H = m->d.hidden, F = m->d.ffn, qd = m->qd, kvd = m->kvd, qkvd = m->qkvd;
+  const int l = o.layer;
+  LayerAct& a = m->la[l];
+  uint8_t* dcur = m->A(m->cur_d ? m->ws_dB : m->ws_dA);
+  uint8_t* dnext = m->A(m->cur_d ? m->ws_dA : m->ws_dB);
+  void* gslot = nullptr;
+  if (!o.fwd && o.code != RS_OP) dc_grad_slot(m->ctx, l, &gslot);
+  auto G = [&](int slot) {
+    int64_t b = 0;
+    dc_grad_offset(m->ctx, m->pid(l, slot), &b);
+    return reinterpret_cast<uint8_t*>(gslot) + b;
+  };
+  dc_status s = DC_OK;
+  switch (o.code) {
+    case F_ATTN_NORM:
+      k_rmsnorm_fwd(layer_in(m, l), m->W(l, P_G1), m->A(a.h1), (float*)m->A(a.rstd1), T, H, st);
+      break;
+    case F_QKV:
+      s = gemm(m, T, qkvd, H, m->A(a.h1), H, 0, {m->W(l, P_Q), m->W(l, P_K), m->W(l, P_V)}, {H, H, H},
+               {qd / 256, (qd + kvd) / 256, qkvd / 256}, 0, 0, m->A(a.qkv), qkvd, nullptr, 0, st);
+      break;
+    case F_ATTN_MIX:
+      k_attn_mix_fwd(m->A(a.qkv), m->A(a.a), T, qd, kvd, m->d.head_dim, m->grp, st);
+      break;
+    case F_O:
+      s = gemm(m, T, H, qd, m->A(a.a), qd, 0, {m->W(l, P_O)}, {qd}, {H / 256}, 0, 0, m->A(a.x2), H,
+               layer_in(m, l), H, st);
+      break;
+    case F_MLP_NORM:
+      k_rmsnorm_fwd(m->A(a.x2), m->W(l, P_G2), m->A(a.h2), (float*)m->A(a.rstd2), T, H, st);
+      break;
+    case F_GATE_UP:
+      s = gemm(m, T, 2 * F, H, m->A(a.h2), H, 0, {m->W(l, P_GATE), m->W(l, P_UP)}, {H, H},
+               {F / 256, 2 * F / 256}, 0, 0, m->A(a.gu), 2 * F, nullptr, 0, st);
+      break;
+    case F_ACT:
+      k_act_fwd(m->A(a.gu), m->A(a.act), T, F, st);
+      break;
+    case F_DOWN:
+      s = gemm(m, T, H, F, m->A(a.act), F, 0, {m->W(l, P_DOWN)}, {F}, {H / 256}, 0, 0, m->A(a.y), H,
+               m->A(a.x2), H, st);
+      break;
+    case F_LOSS:
+      m->cur_d = 0;
+      k_loss(m->A(a.y), m->target, m->A(m->ws_dA), (float*)m->A(m->ws_lossp), (float*)m->A(m->ws_loss),
+             (int64_t)T * H, st);
+      break;
+    case B_DOWN:
+      if ((s = dc_grad_slot_acquire(m->ctx, l, st)) != DC_OK) return s;
+      // dact = dy Wd  (A K-major [T,H]; B = Wd [H rows = K][F] MN-major)
+      s = gemm(m, T, F, H, dcur, H, 0, {m->W(l, P_DOWN)}, {F}, {F / 256}, 1, 0, m->A(m->ws_dact), F, nullptr, 0, st);
+      if (s == DC_OK)  // dWd = dy^T act : A = dy stored [T][H] (MN-major), B = act [T][F] (MN-major)
+        s = gemm(m, H, F, T, dcur, H, 1, {m->A(a.act)}, {F}, {F / 256}, 1, 0, G(P_DOWN), F, nullptr, 0, st);
+      break;
+    case B_ACT:
+      k_act_bwd(m->A(m->ws_dact), m->A(a.gu), m->A(m->ws_dgu), T, F, st);
+      break;
+    case B_GATE_UP:
+      // dh2 = dgate Wg + dup Wu : A = dgu [T, 2F] K-major, B split along K
+      s = gemm(m, T, H, 2 * F, m->A(m->ws_dgu), 2 * F, 0, {m->W(l, P_GATE), m->W(l, P_UP)}, {H, H},
+               {F / 64, 2 * F / 64}, 1, 1, m->A(m->ws_dh), H, nullptr, 0, st);
+      if (s == DC_OK)
+        s = gemm(m, F, H, T, m->A(m->ws_dgu), 2 * F, 1, {m->A(a.h2)}, {H}, {H / 256}, 1, 0, G(P_GATE), H, nullptr, 0, st);
+      if (s == DC_OK)
+        s = gemm(m, F, H, T, m->A(m->ws_dgu) + (int64_t)F * 2, 2 * F, 1, {m->A(a.h2)}, {H}, {H / 256}, 1, 0, G(P_UP),
+                 H, nullptr, 0, st);
+      break;
+    case B_MLP_NORM: {
+      const int nb = rmsnorm_bwd_blocks(T);
+      k_rmsnorm_bwd(m->A(m->ws_dh), m->A(a.x2), m->W(l, P_G2), (float*)m->A(a.rstd2), dcur, m->A(m->ws_dx2),
+                    (float*)m->A(m->ws_dgp), T, H, st);
+      k_colsum_to_bf16((float*)m->A(m->ws_dgp), nb, H, G(P_G2), st);
+      break;
+    }
+    case B_O:
+      // da -> dqkv[:, :qd] ; dWo = dx2^T a
+      s = gemm(m, T, qd, H, m->A(m->ws_dx2), H, 0, {m->W(l, P_O)}, {qd}, {qd / 256}, 1, 0, m->A(m->ws_dqkv), qkvd,
+               nullptr, 0, st);
+      if (s == DC_OK)
+        s = gemm(m, H, qd, T, m->A(m->ws_dx2), H, 1, {m->A(a.a)}, {qd}, {qd / 256}, 1, 0, G(P_O), qd, nullptr, 0, st);
+      break;
+    case B_ATTN_MIX:
+      k_attn_mix_bwd(m->A(m->ws_dqkv), m->A(a.qkv), T, qd, kvd, m->d.head_dim, m->grp, st);
+      break;
+    case B_QKV:
+      s = gemm(m, T, H, qkvd, m->A(m->ws_dqkv), qkvd, 0, {m->W(l, P_Q), m->W(l, P_K), m->W(l, P_V)}, {H, H, H},
+               {qd / 64, (qd + kvd) / 64, qkvd / 64}, 1, 1, m->A(m->ws_dh), H, nullptr, 0, st);
+      if (s == DC_OK)
+        s = gemm(m, qd, H, T, m->A(m->ws_dqkv), qkvd, 1, {m->A(a.h1)}, {H}, {H / 256}, 1, 0, G(P_Q), H, nullptr, 0, st);
+      if (s == DC_OK)
+        s = gemm(m, kvd, H, T, m->A(m->ws_dqkv) + (int64_t)qd * 2, qkvd, 1, {m->A(a.h1)}, {H}, {H / 256}, 1, 0, G(P_K),
+                 H, nullptr, 0, st);
+      if (s == DC_OK)
+        s = gemm(m, kvd, H, T, m->A(m->ws_dqkv) + (int64_t)(qd + kvd) * 2, qkvd, 1, {m->A(a.h1)}, {H}, {H / 256}, 1,
+                 0, G(P_V), H, nullptr, 0, st);
+      break;
+    case B_ATTN_NORM: {
+      const int nb = rmsnorm_bwd_blocks(T);
+      k_rmsnorm_bwd(m->A(m->ws_dh), layer_in(m, l), m->W(l, P_G1), (float*)m->A(a.rstd1), m->A(m->ws_dx2), dnext,
+                    (float*)m->A(m->ws_dgp), T, H, st);
+      k_colsum_to_bf16((float*)m->A(m->ws_dgp), nb, H, G(P_G1), st);
+      if ((s = dc_grad_slot_publish(m->ctx, l, st)) != DC_OK) return s;
+      m->cur_d ^= 1;
+      break;
+    }
+    default:
+      return mfail(m, DC_EINVAL, "run_op: bad op");
+  }
+  if (s != DC_OK) return s;
+  if (cudaGetLastError() != cudaSuccess) return mfail(m, DC_ECUDA, std::string("layer op launch failed: ") + op_name(o.code));
+  return DC_OK;
+}
+
+// resident-memory profile P_mem(o): static state (bf16 shard, fp32
+// master, grad slots, workspace, inputs; NOT Adam m/v — reading D14) + live
+// gathered buffers under S_0 + saved activations of layers between their
+// forward op and the end of their backward.
+static void compute_pmem(dc_model* m) {
+  const Layout& L = ctx_layout(m->ctx);
+  const int N = ctx_world(m->ctx);
+  const int64_t T = m->d.tokens, h = m->d.hidden;
+  int64_t stat = L.shard_elems * 6 + 2 * L.grad_slot_bytes + (int64_t)m->ws_bytes + 2 * T * h * 2;
+  int64_t live_ag = 0, act = 0;
+  const LayerAct& a0 = m->la[0];
+  auto piece = [&](int code) -> int64_t {
+    const int64_t f = m->d.ffn;
+    switch (code) {
+      case F_ATTN_NORM: return T * h * 2 + T * 4;
+      case F_QKV: return T * m->qkvd * 2;
+      case F_ATTN_MIX: return T * m->qd * 2;
+      case F_O: return T * h * 2;
+      case F_MLP_NORM: return T * h * 2 + T * 4;
+      case F_GATE_UP: return T * 2 * f * 2;
+      case F_ACT: return T * f * 2;
+      case F_DOWN: return T * h * 2;
+      default: return 0;
+    }
+  };
+  (void)a0;
+  for (size_t i = 0; i < m->s0.size(); ++i) {
+    const S0& o = m->s0[i];
+    m->p_mem[i] = stat + live_ag + act;
+    if (o.kind == K_AG) live_ag += L.S[o.params[0]] * N * 2;
+    else if (o.kind == K_REL) live_ag -= L.S[o.params[0]] * N * 2;
+    else if (o.kind == K_COMPUTE) {
+      if (o.fwd) act += piece(o.code);
+      else if (o.code == B_ATTN_NORM) {
+        int64_t layer_total = 0;
+        for (int c = F_ATTN_NORM; c <= F_DOWN; ++c) layer_total += piece(c);
+        act -= layer_total;
+      }
+    }
+  }
+}
+
+extern "C" dc_status dc_model_profile_json(const dc_model* mc, char* buf, size_t* len) {
+  dc_model* m = const_cast<dc_model*>(mc);
+  if (!m || !len) return mfail(nullptr, DC_EINVAL, "dc_model_profile_json: null argument");
+  compute_pmem(m);
+  const Layout& L = ctx_layout(m->ctx);
+  const int N = ctx_world(m->ctx);
+  std::string s = "{\"ops\":[";
+  for (size_t i = 0; i < m->s0.size(); ++i) {
+    const S0& o = m->s0[i];
+    if (i) s += ',';
+    const char* kind = o.kind == K_AG ? "ag" : o.kind == K_REL ? "rel" : o.kind == K_RS ? "rs" : "compute";
+    s += "{\"dur_us\":" + std::to_string(m->dur_us[i]) + ",\"id\":" + std::to_string(i) + ",\"kind\":\"" + kind +
+         "\",\"layer\":" + std::to_string(o.layer) + ",\"micro\":" + std::to_string(o.micro) + ",\"name\":\"" +
+         (o.kind == K_AG ? "ag" : o.kind == K_REL ? "rel" : op_name(o.code)) + "\",\"p_mem\":" +
+         std::to_string(m->p_mem[i]) + ",\"params\":[";
+    for (size_t j = 0; j < o.params.size(); ++j) s += (j ? "," : "") + std::to_string(o.params[j]);
+    s += "],\"phase\":\"" + std::string(o.fwd ? "fwd" : "bwd") + "\",\"transient\":0}";
+  }
+  s += "],\"params\":[";
+  for (int p = 0; p < (int)L.S.size(); ++p) {
+    if (p) s += ',';
+    int layer = 0;
+    for (int l = 0; l < L.n_layers; ++l)
+      if (p >= L.layer_first[l]) layer = l;
+    s += "{\"bytes\":" + std::to_string(L.S[p] * N * 2) + ",\"id\":" + std::to_string(p) + ",\"layer\":" +
+         std::to_string(layer) + "}";
+  }
+  s += "]}";
+  const size_t cap = *len;
+  *len = s.size();
+  if (!buf) return DC_OK;
+  if (cap < s.size() + 1) return mfail(m, DC_EOOM, "dc_model_profile_json: buffer too small");
+  memcpy(buf, s.c_str(), s.size() + 1);
+  return DC_OK;
+}
+
+extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile, cudaStream_t cs, cudaStream_t ags,
+                                   cudaStream_t rss, cudaStream_t cps) {
+  if (!m || !m->act) return mfail(m, DC_ESTATE, "dc_model_step: model not bound");
+  const dc_schedule* sc = ctx_sched(m->ctx);
+  if (!sc) return mfail(m, DC_ESTATE, "dc_model_step: no schedule bound");
+  const int64_t l0 = launch_count();
+  const int N = ctx_world(m->ctx);
+  dc_status s = dc_step_begin(m->ctx, ++m->epoch, cs);
+  if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
+  // streams must not run ahead of the previous step's tail on the compute stream
+  cudaEventRecord(m->ev_join[0], cs);
+  cudaStreamWaitEvent(ags, m->ev_join[0], 0);
+  cudaStreamWaitEvent(rss, m->ev_join[0], 0);
+  cudaStreamWaitEvent(cps, m->ev_join[0], 0);
+  std::vector<cudaEvent_t> gather_ev(ctx_layout(m->ctx).S.size(), nullptr);
+  const int nops = sched_num_ops(sc);
+  for (int i = 0; i < nops; ++i) {
+    int kind, id, nm, np, nw;
+    const int64_t* mem; const int* posts; const int* waits;
+    int64_t off, bytes;
+    sched_op(sc, i, &kind, &id, &mem, &nm, &off, &bytes, &posts, &np, &waits, &nw);
+    switch (kind) {
+      case K_AG:
+        if (N > 1) {
+          cudaEventRecord(m->ev_pos[id], cs);
+          cudaStreamWaitEvent(ags, m->ev_pos[id], 0);
+          s = dc_gather(m->ctx, id, ags, m->ev_done[id]);
+          for (int j = 0; j < nm; ++j) gather_ev[mem[j]] = m->ev_done[id];
+        } else {
+          s = dc_gather(m->ctx, id, ags, nullptr);
+        }
+        break;
+      case K_REL:
+        s = dc_release(m->ctx, id, cs);
+        break;
+      case K_COMPUTE: {
+        const S0& o = m->s0[id];
+        if (N > 1)
+          for (int p : o.params)
+            if (gather_ev[p]) cudaStreamWaitEvent(cs, gather_ev[p], 0);
+        if (profile) cudaEventRecord(m->ev_t0[id], cs);
+        s = run_op(m, o, cs);
+        if (profile) cudaEventRecord(m->ev_t1[id], cs);
+        break;
+      }
+      case K_RS: {
+        const S0& o = m->s0[id];
+        cudaEventRecord(m->ev_pos[id], cs);
+        cudaStreamWaitEvent(rss, m->ev_pos[id], 0);
+        if (profile) cudaEventRecord(m->ev_t0[id], rss);
+        s = dc_reduce_scatter_step(m->ctx, o.layer, step_t, 1, rss);
+        if (profile) cudaEventRecord(m->ev_t1[id], rss);
+        break;
+      }
+      case K_OFF:
+        s = dc_offload(m->ctx, (int)mem[0], DC_D2H_START, cps);
+        break;
+      case K_OFFSYNC:
+        s = dc_offload(m->ctx, (int)mem[0], DC_D2H_SYNC_FREE, cs);
+        break;
+      case K_RELOAD:
+        cudaEventRecord(m->ev_join[1], cs);
+        cudaStreamWaitEvent(cps, m->ev_join[1], 0);
+        s = dc_offload(m->ctx, (int)mem[0], DC_H2D_START, cps);
+        break;
+      case K_RELOADSYNC:
+        s = dc_offload(m->ctx, (int)mem[0], DC_H2D_SYNC, rss);
+        break;
+      default:
+        return mfail(m, DC_EINVAL, "dc_model_step: bad schedule op");
+    }
+    if (s != DC_OK) return mfail(m, s, std::string("dc_model_step: ") + dc_last_error(m->ctx) + " / " + m->err);
+  }
+  // join every stream into the compute stream (step end)
+  cudaEventRecord(m->ev_join[1], ags);
+  cudaEventRecord(m->ev_join[2], rss);
+  cudaEventRecord(m->ev_join[3], cps);
+  cudaStreamWaitEvent(cs, m->ev_join[1], 0);
+  cudaStreamWaitEvent(cs, m->ev_join[2], 0);
+  cudaStreamWaitEvent(cs, m->ev_join[3], 0);
+  if (cudaGetLastError() != cudaSuccess) return mfail(m, DC_ECUDA, "dc_model_step: CUDA error");
+  if (profile) {
+    if (cudaStreamSynchronize(cs) != cudaSuccess) return mfail(m, DC_ECUDA, "dc_model_step: sync failed");
+    for (size_t i = 0; i < m->s0.size(); ++i) {
+      if (m->s0[i].kind != K_COMPUTE && m->s0[i].kind != K_RS) continue;
+      float ms = 0.0f;
+      if (cudaEventElapsedTime(&ms, m->ev_t0[i], m->ev_t1[i]) == cudaSuccess)
+        m->dur_us[i] = (int64_t)std::llround(ms * 1000.0);
+    }
+  }
+  m->launches = launch_count() - l0;
+  return DC_OK;
+}
+
+extern "C" dc_status dc_model_loss_ptr(const dc_model* m, float** loss) {
+  if (!m || !loss || !m->act) return mfail(nullptr, DC_EINVAL, "dc_model_loss_ptr: not bound");
+  *loss = (float*)m->A(m->ws_loss);
+  return DC_OK;
+}
+
+extern "C" dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t which, void** p) {
+  if (!m || !p || !m->act || layer < 0 || layer >= m->d.layers) return mfail(nullptr, DC_EINVAL, "dc_model_act_ptr: bad args");
+  const LayerAct& a = m->la[layer];
+  const int64_t offs[] = {a.h1, a.qkv, a.a, a.x2, a.h2, a.gu, a.act, a.y, m->ws_dA, m->ws_dB};
+  if (which < 0 || which >= 10) return mfail(nullptr, DC_EINVAL, "dc_model_act_ptr: which in [0, 10)");
+  *p = m->A(offs[which]);
+  return DC_OK;
+}
+
+extern "C" dc_status dc_model_launch_count(const dc_model* m, int64_t* n) {
+  if (!m || !n) return mfail(nullptr, DC_EINVAL, "dc_model_launch_count: null");
+  *n = m->launches;
+  return DC_OK;
+}

@@ -1,0 +1,227 @@
+"""Torch-side plumbing around the C ABI: allocate the shard store, the
+symmetric grad slots / flag tables / gather arena, the activation buffer and the
+streams, then drive profile -> plan -> step through libdc_b200.so.
+
+Two ways to get N ranks:
+  * one process per GPU (torchrun): peer pointers from torch symmetric memory
+    (`torch.distributed._symmetric_memory.empty` + `rendezvous`);
+  * DC_VIRTUAL_RANKS: N ranks on one GPU in one process, each with its own
+    buffers; the "peer" pointers are the other virtual ranks' device buffers.
+    Every rank's host calls run in their own thread (one ctx per thread).
+Nothing here computes: all math runs in the library's kernels.
+"""
+import ctypes as C
+import json
+import threading
+
+import numpy as np
+import torch
+
+from . import dc
+
+GiB = 1 << 30
+
+
+def table_arrays(table):
+    return ([p.numel for p in table], [p.layer for p in table], [float(p.k) for p in table])
+
+
+def max_s0_ops(table, micro_steps=1):
+    # compute ops (<= 9 fwd + 9 bwd per layer + loss) + one gather and one
+    # release per param per phase per micro-step, rounded up generously
+    return (2 * 3 * len(table) + 20 * (max(p.layer for p in table) + 1) + 16) * micro_steps
+
+
+class RankState:
+    """One rank's buffers, context, model and streams."""
+
+    def __init__(self):
+        self.ctx = None
+        self.model = None
+        self.tensors = {}
+        self.streams = None
+        self.sched = None
+
+    def stream_handles(self):
+        return [s.cuda_stream for s in self.streams]
+
+
+def _alloc_symmetric(nbytes, group, device):
+    from torch.distributed import _symmetric_memory as symm_mem
+    t = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+    h = symm_mem.rendezvous(t, group.group_name)
+    return t, [int(p) for p in h.buffer_ptrs]
+
+
+def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr=1e-3, beta1=0.9,
+                 beta2=0.999, eps=1e-8, seed=0, init=True, host_pinned_bytes=0, spin_ms=20000):
+    """Allocate and dc_init the ranks this process drives: all N virtual ranks,
+    or this process's rank when `virtual` is False."""
+    dev = torch.device("cuda", device)
+    numel, layer_of, init_k = table_arrays(table)
+    mops = max_s0_ops(table)
+    la = dc.LayoutArgs(world, len(table), dc.i64_array(numel), dc.i32_array(layer_of), mops)
+    lay = dc.Layout()
+    dc.check(dc.lib.dc_layout_query(C.byref(la), C.byref(lay)))
+    mine = list(range(world)) if virtual else [rank]
+    ranks = {r: RankState() for r in mine}
+    grad_bytes = 2 * lay.grad_slot_bytes
+    if virtual:
+        for r in mine:
+            ranks[r].tensors["grad"] = torch.zeros(grad_bytes, dtype=torch.uint8, device=dev)
+            ranks[r].tensors["flags"] = torch.zeros(lay.flag_bytes, dtype=torch.uint8, device=dev)
+        grad_ptrs = [ranks[r].tensors["grad"].data_ptr() for r in mine]
+        flag_ptrs = [ranks[r].tensors["flags"].data_ptr() for r in mine]
+    else:
+        g, grad_ptrs = _alloc_symmetric(grad_bytes, group, dev)
+        f, flag_ptrs = _alloc_symmetric(lay.flag_bytes, group, dev)
+        ranks[rank].tensors["grad"], ranks[rank].tensors["flags"] = g, f
+    for r in mine:
+        st = ranks[r]
+        t = st.tensors
+        t["shard"] = torch.empty(lay.shard_elems, dtype=torch.bfloat16, device=dev)
+        t["master"] = torch.empty(lay.shard_elems, dtype=torch.float32, device=dev)
+        t["m"] = torch.empty(lay.shard_elems, dtype=torch.float32, device=dev)
+        t["v"] = torch.empty(lay.shard_elems, dtype=torch.float32, device=dev)
+        if host_pinned_bytes:
+            t["host"] = torch.empty(host_pinned_bytes, dtype=torch.uint8, pin_memory=True)
+        a = dc.InitArgs()
+        a.rank, a.world, a.device, a.n_params = r, world, device, len(table)
+        st._keep = [dc.i64_array(numel), dc.i32_array(layer_of), dc.f32_array(init_k),
+                    dc.u64_array(grad_ptrs), dc.u64_array(flag_ptrs)]
+        a.numel, a.layer_of, a.init_k = (C.cast(st._keep[0], dc.p_i64), C.cast(st._keep[1], dc.p_i32),
+                                         C.cast(st._keep[2], dc.p_f32))
+        a.max_s0_ops = mops
+        a.shard_param, a.master = t["shard"].data_ptr(), t["master"].data_ptr()
+        a.exp_avg, a.exp_avg_sq = t["m"].data_ptr(), t["v"].data_ptr()
+        a.grad_peer_ptrs, a.grad_bytes = C.cast(st._keep[3], dc.p_u64), grad_bytes
+        a.flag_peer_ptrs, a.flag_bytes = C.cast(st._keep[4], dc.p_u64), lay.flag_bytes
+        a.host_pinned = t["host"].data_ptr() if host_pinned_bytes else None
+        a.host_pinned_bytes = host_pinned_bytes
+        a.lr, a.beta1, a.beta2, a.eps = lr, beta1, beta2, eps
+        a.seed = seed
+        a.flags = (dc.DC_INIT_WEIGHTS if init else 0) | (dc.DC_VIRTUAL_RANKS if virtual else 0)
+        a.spin_limit = spin_ms
+        out = C.c_void_p()
+        dc.check(dc.lib.dc_init(C.byref(a), C.byref(out)))
+        st.ctx = out
+        st.rank = r
+        st.world = world
+        st.layout = lay
+        st.device = dev
+        st.streams = [torch.cuda.Stream(device=dev) for _ in range(4)]   # compute, ag, rs, copy
+    return ranks
+
+
+def shard_range(st, p):
+    off, S = C.c_int64(), C.c_int64()
+    dc.check(dc.lib.dc_shard_range(st.ctx, p, C.byref(off), C.byref(S)), st.ctx)
+    return off.value, S.value
+
+
+def grad_offset(st, p):
+    b = C.c_int64()
+    dc.check(dc.lib.dc_grad_offset(st.ctx, p, C.byref(b)), st.ctx)
+    return b.value
+
+
+def attach_model(ranks, cfg, xs, targets):
+    """dc_model_create + bind per rank; xs/targets: dict rank -> bf16 device [T, H]."""
+    d = dc.ModelDims(cfg.hidden, cfg.ffn, cfg.n_heads, cfg.n_kv, cfg.head_dim, cfg.layers, cfg.tokens)
+    for r, st in ranks.items():
+        m = C.c_void_p()
+        dc.check(dc.lib.dc_model_create(st.ctx, C.byref(d), C.byref(m)))
+        st.model = m
+        nb = C.c_uint64()
+        dc.check(dc.lib.dc_model_act_bytes(m, C.byref(nb)))
+        st.tensors["act"] = torch.empty(nb.value, dtype=torch.uint8, device=st.device)
+        st.tensors["x"], st.tensors["t"] = xs[r], targets[r]
+        dc.check(dc.lib.dc_model_bind(m, st.tensors["act"].data_ptr(), nb.value, xs[r].data_ptr(),
+                                      targets[r].data_ptr()))
+
+
+def bind(ranks, sched_by_rank, group=None):
+    """Allocate the gather arena at the planned capacity and dc_bind_schedule
+    on every rank (all ranks quiescent)."""
+    any_st = next(iter(ranks.values()))
+    cap = max(1, int(dc.lib.dc_schedule_capacity(next(iter(sched_by_rank.values())))))
+    if any_st.world == 1:
+        ptrs = {r: [0] for r in ranks}
+    elif group is None:   # virtual ranks
+        for r, st in ranks.items():
+            st.tensors["arena"] = torch.empty(cap, dtype=torch.uint8, device=st.device)
+        allp = [ranks[r].tensors["arena"].data_ptr() for r in sorted(ranks)]
+        ptrs = {r: allp for r in ranks}
+    else:
+        st = any_st
+        t, allp = _alloc_symmetric(cap, group, st.device)
+        st.tensors["arena"] = t
+        ptrs = {st.rank: allp}
+    torch.cuda.synchronize()
+    for r, st in ranks.items():
+        st.sched = sched_by_rank[r]
+        arr = dc.u64_array(ptrs[r])
+        st._arena_keep = arr
+        dc.check(dc.lib.dc_bind_schedule(st.ctx, st.sched, C.cast(arr, dc.p_u64), cap,
+                                         st.streams[0].cuda_stream), st.ctx)
+    torch.cuda.synchronize()
+
+
+def profile_json(st, tc=None, frags=None):
+    prof = json.loads(dc.model_profile_json(st.model))
+    prof["tc"] = tc if tc is not None else [[0, 0], [1 << 40, 0]]
+    prof["frags"] = frags or []
+    return prof
+
+
+def run_parallel(ranks, fn):
+    """Run fn(rank_state) for every rank, each in its own thread (virtual ranks
+    spin on each other's flags, so their host calls must interleave)."""
+    if len(ranks) == 1:
+        st = next(iter(ranks.values()))
+        fn(st)
+        return
+    errs = []
+
+    def wrap(st):
+        try:
+            torch.cuda.set_device(st.device)
+            fn(st)
+        except BaseException as e:   # noqa: BLE001 - re-raised below
+            errs.append(e)
+
+    th = [threading.Thread(target=wrap, args=(st,)) for st in ranks.values()]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+
+
+def step(ranks, t, profile=False):
+    def one(st):
+        dc.check(dc.lib.dc_model_step(st.model, t, 1 if profile else 0, *st.stream_handles()), st.ctx)
+    run_parallel(ranks, one)
+
+
+def loss_ptr(st):
+    p = dc.p_f32()
+    dc.check(dc.lib.dc_model_loss_ptr(st.model, C.byref(p)))
+    return C.cast(p, C.c_void_p).value
+
+
+class _CAI:
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
+
+
+_TYPESTR = {torch.float32: "<f4", torch.uint8: "|u1", torch.int16: "<i2", torch.uint32: "<u4",
+            torch.bfloat16: "<i2"}
+
+
+def view(ptr, n, dtype, device="cuda"):
+    """Zero-copy torch view (n elements) of library-addressed device memory,
+    e.g. dc_tensor_ptr / dc_grad_slot results (tests and diagnostics only)."""
+    t = torch.as_tensor(_CAI(int(ptr), n, _TYPESTR[dtype]), device=device)
+    return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t

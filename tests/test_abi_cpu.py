@@ -1,0 +1,138 @@
+"""C-ABI checks that need no GPU: the library loads and exports every symbol
+include/dc.h declares; dc_layout_query matches the oracle's shard layout; and
+dc_plan (host-only C++) produces byte-identical canonical JSON to the oracle
+scheduler on every pinned example and on random profiles."""
+import ctypes as C
+import json
+import os
+import random
+import re
+
+import pytest
+
+import synth
+from oracle import numerics as nx
+from oracle import sched as osd
+from paper_2504_09983_b200 import dc
+from tests import sched_util as su
+from tests.test_oracle_sched import _fig6_profile, _offload_profile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_exports_match_header():
+    hdr = open(os.path.join(ROOT, "include", "dc.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    declared = set(re.findall(r"\b(dc_[a-z0-9_]+)\s*\(", hdr))
+    assert len(declared) >= 30
+    for name in sorted(declared):
+        assert hasattr(dc.lib, name), name
+    assert set(dc.EXPORTS) <= declared | {"dc_last_error", "dc_version"}
+
+
+def test_layout_query_matches_oracle():
+    for world in (1, 2, 4, 8):
+        table = synth.llama_param_table(synth.small_llama(layers=3))
+        numel = [p.numel for p in table]
+        layer = [p.layer for p in table]
+        la = dc.LayoutArgs(world, len(table), dc.i64_array(numel), dc.i32_array(layer), 1000)
+        out = dc.Layout()
+        dc.check(dc.lib.dc_layout_query(C.byref(la), C.byref(out)))
+        assert out.shard_elems == sum(nx.shard_len(n, world) for n in numel)
+        assert out.n_layers == 3
+        per_layer = {}
+        for p in table:
+            per_layer[p.layer] = per_layer.get(p.layer, 0) + osd.align256(nx.shard_len(p.numel, world) * world * 2)
+        assert out.grad_slot_bytes == max(per_layer.values())
+
+
+def test_layout_errors():
+    la = dc.LayoutArgs(9, 1, dc.i64_array([8]), dc.i32_array([0]), 10)
+    assert dc.lib.dc_layout_query(C.byref(la), C.byref(dc.Layout())) == dc.DC_EINVAL
+    la = dc.LayoutArgs(2, 2, dc.i64_array([8, 8]), dc.i32_array([1, 0]), 10)
+    assert dc.lib.dc_layout_query(C.byref(la), C.byref(dc.Layout())) == dc.DC_EINVAL
+
+
+def _both(prof, M, M_pf=2 << 30, alpha=(3, 2), passes=osd.PASSES_PS, strict=False):
+    """(oracle json or exception class, C json or status)."""
+    try:
+        o = osd.canonical_json(osd.plan(json.loads(json.dumps(prof)), M, M_pf, alpha, passes, strict))
+    except osd.ProfileError:
+        o = dc.DC_EPROFILE
+    except osd.Infeasible:
+        o = dc.DC_EINFEASIBLE
+    opts = dc.PlanOpts(M_pf, alpha[0], alpha[1], passes, 1 if strict else 0)
+    h = C.c_void_p()
+    st = dc.lib.dc_plan(json.dumps(prof).encode(), M, C.byref(opts), C.byref(h))
+    if st != dc.DC_OK:
+        return o, st
+    c = dc.schedule_json(h)
+    assert dc.lib.dc_schedule_capacity(h) == json.loads(c)["capacity"]
+    dc.lib.dc_schedule_free(h)
+    return o, c
+
+
+def test_plan_parity_pins():
+    cases = [(_fig6_profile(), 100, 10 ** 9, osd.PASS_SHARD | osd.PASS_PREFETCH, False),
+             (_offload_profile([20, 50, 80], [60, 30], 4, 10), 100, 2 << 30, osd.PASSES_PS | osd.PASS_OFFLOAD, False),
+             (_offload_profile([20, 50, 90], [90, 80, 70, 60, 10], 4, 10), 100, 2 << 30,
+              osd.PASSES_PS | osd.PASS_OFFLOAD, True),
+             (_offload_profile([20, 90], [90, 90], 2, 10), 100, 2 << 30, osd.PASSES_PS | osd.PASS_OFFLOAD, False),
+             (_offload_profile([20, 120], [30], 2, 10), 100, 2 << 30, osd.PASSES_PS | osd.PASS_OFFLOAD, False),
+             (su.make_profile(su.layered(8, n_micro=4), {p: 1024 for p in range(8)}, lambda o: 0), 10 ** 12,
+              2 << 30, osd.PASS_SHARD | osd.PASS_UNSHARD, False)]
+    for prof, M, mpf, passes, strict in cases:
+        o, c = _both(prof, M, mpf, passes=passes, strict=strict)
+        assert o == c
+
+
+def test_plan_parity_llama_s0():
+    comp = synth.models.llama_compute_ops(synth.small_llama(layers=4))
+    s0 = osd.build_s0(comp)
+    B = {p.id: nx.shard_len(p.numel, 8) * 8 * 2 for p in synth.llama_param_table(synth.small_llama(layers=4))}
+    live = osd.live_before_s0(s0, B)
+    rng = random.Random(3)
+    act, pm = 0, {}
+    for o in s0:
+        pm[o["id"]] = 10 ** 6 + act + live[o["id"]]
+        if o["kind"] == "compute":
+            act += rng.randint(0, 10 ** 5) if o["phase"] == "fwd" else -rng.randint(0, 10 ** 5)
+            act = max(act, 0)
+    prof = su.make_profile([(o["name"], o["kind"], o["phase"], o["micro"], o["layer"], o["params"]) for o in comp],
+                           B, pm, tc=[[4096, 20], [1 << 20, 40], [1 << 24, 300]])
+    for M in (max(pm.values()) + 10 ** 5, max(pm.values()) + 5 * 10 ** 6):
+        for strict in (False, True):
+            o, c = _both(prof, M, 4 << 20, strict=strict)
+            assert isinstance(c, str) and o == c
+
+
+def test_plan_parity_random():
+    rng = random.Random(77)
+    n = 0
+    for it in range(250):
+        prof = su.random_profile(rng, n_micro=rng.choice([1, 1, 2]), frags=rng.random() < 0.4)
+        base = max(o["p_mem"] + o["transient"] for o in prof["ops"])
+        M_opt = sum(f["bytes"] for f in prof["frags"])
+        M = base + rng.randint(-2000, 40000 + M_opt)
+        M_pf = rng.choice([2048, 8192, 1 << 30])
+        alpha = rng.choice([(3, 2), (1, 1), (2, 1), (5, 4)])
+        passes = rng.choice([osd.PASSES_PS, osd.PASSES_PS | osd.PASS_OFFLOAD, osd.PASS_SHARD | osd.PASS_PREFETCH,
+                             osd.PASS_SHARD])
+        o, c = _both(prof, M, M_pf, alpha, passes, strict=rng.random() < 0.5)
+        assert o == c, (it, o if isinstance(o, int) else o[:200], c if isinstance(c, int) else c[:200])
+        n += isinstance(c, str)
+    assert n > 100
+
+
+def test_plan_profile_errors():
+    prof = _fig6_profile()
+    bad = json.loads(json.dumps(prof))
+    bad["ops"][0], bad["ops"][1] = bad["ops"][1], bad["ops"][0]
+    o, c = _both(bad, 100)
+    assert o == c == dc.DC_EPROFILE
+    bad = json.loads(json.dumps(prof))
+    bad["tc"] = [[10, 1], [5, 2]]
+    assert _both(bad, 100) == (dc.DC_EPROFILE, dc.DC_EPROFILE)
+    h = C.c_void_p()
+    assert dc.lib.dc_plan(b'{"ops": [1.5]}', 10, None, C.byref(h)) == dc.DC_EPROFILE
+    assert "profile" in dc.last_error()

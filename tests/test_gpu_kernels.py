@@ -1,0 +1,232 @@
+"""GPU parity of the individual hot-path kernels against the oracle, through
+the C ABI (tests run on a B200 under gpurun: pytest -m gpu).
+
+* init:    dc_init's on-device generator == oracle shard_of(values)  (bit-exact)
+* gemm:    tcgen05 GEMM, all operand layouts / segments / ragged tails / residual
+           vs an fp64 matmul of the same bf16 inputs (bf16 output tolerance)
+* rs_adam: reduce-scatter + 1/N + Adam in DC_VIRTUAL_RANKS mode, N in {1,2,4},
+           two steps, vs oracle.numerics.rs_adam_shard (bit-exact; <= 1e-5 bar)
+* ag_push: every gather of a planned schedule, N in {2,4,8} virtual ranks,
+           vs oracle all_gather (bit-exact, including padding)
+"""
+import ctypes as C
+import json
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import numerics as nx
+from oracle import step as ost
+from tests.gpu_util import bf16_tensor, seeded, to_np
+
+pytestmark = pytest.mark.gpu
+
+dc = pytest.importorskip("paper_2504_09983_b200.dc")
+from paper_2504_09983_b200 import runtime as rt  # noqa: E402
+
+
+# ------------------------------------------------------------------ init
+def test_init_bitexact():
+    cfg = synth.small_llama(layers=2)
+    table = synth.llama_param_table(cfg)
+    full = ost.init_full_params(table)
+    for world in (1, 2):
+        ranks = rt.create_ranks(table, world, seed=synth.SEED_WEIGHTS)
+        torch.cuda.synchronize()
+        for r, st in ranks.items():
+            sh = st.tensors["shard"].view(torch.int16).cpu().numpy().view(np.uint16)
+            ms = st.tensors["master"].cpu().numpy()
+            for i, p in enumerate(table):
+                off, S = rt.shard_range(st, i)
+                ref = nx.shard_of(full[i], world, r)
+                assert ms[off:off + S].tobytes() == ref.tobytes(), (r, p.name)
+                assert np.array_equal(sh[off:off + S], nx.bf16_bits(ref)), (r, p.name)
+            assert not st.tensors["m"].any() and not st.tensors["v"].any()
+
+
+# ------------------------------------------------------------------ GEMM
+def _gemm(M, N, K, A, lda, a_mn, Bs, ldbs, ends, b_mn, split_k, Cm, ldc, R=None, ldr=0, sms=0):
+    g = dc.GemmArgs()
+    g.M, g.N, g.K = M, N, K
+    g.A, g.lda, g.a_mn_major = A.data_ptr(), lda, a_mn
+    g.n_bseg = len(Bs)
+    for i, (b, l, e) in enumerate(zip(Bs, ldbs, ends)):
+        g.B[i], g.ldb[i], g.bseg_end[i] = b.data_ptr(), l, e
+    g.b_mn_major, g.b_split_k = b_mn, split_k
+    g.C, g.ldc = Cm.data_ptr(), ldc
+    g.R, g.ldr = (R.data_ptr() if R is not None else None), ldr
+    g.num_sms = sms
+    dc.check(dc.lib.dc_gemm(C.byref(g), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+
+
+def _check(Cm, ref, absref, name):
+    got = to_np(Cm)
+    err = np.abs(got - ref)
+    tol = 2.0 ** -8 * np.abs(ref) + 2.0 ** -18 * absref + 1e-30
+    bad = err > tol
+    assert not bad.any(), "%s: %d bad, max err %g" % (name, bad.sum(), err.max())
+
+
+def _mat(seed, r, c):
+    a = nx.rne_bf16(seeded(seed, 0, r * c)).reshape(r, c)
+    return a, bf16_tensor(a)
+
+
+@pytest.mark.parametrize("M,N,K,sms", [(256, 512, 512, 0), (200, 264, 200, 0), (1024, 2048, 1024, 8),
+                                       (130, 8, 64, 0)])
+def test_gemm_forward_kmajor(M, N, K, sms):
+    a, A = _mat(11, M, K)
+    b, B = _mat(12, N, K)
+    Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    _gemm(M, N, K, A, K, 0, [B], [K], [0], 0, 0, Cm, N, sms=sms)
+    _check(Cm, a @ b.T, np.abs(a) @ np.abs(b).T, "fwd")
+
+
+def test_gemm_nsplit_segments_and_residual():
+    M, K = 384, 320
+    Ns = [256, 256, 512]
+    a, A = _mat(21, M, K)
+    bs = [_mat(22 + i, n, K) for i, n in enumerate(Ns)]
+    r, R = _mat(30, M, sum(Ns))
+    Cm = torch.empty(M, sum(Ns), dtype=torch.bfloat16, device="cuda")
+    _gemm(M, sum(Ns), K, A, K, 0, [x[1] for x in bs], [K] * 3, [1, 2, 4], 0, 0, Cm, sum(Ns), R=R, ldr=sum(Ns))
+    bcat = np.concatenate([x[0] for x in bs])
+    ref = (a @ bcat.T) + r
+    _check(Cm, ref, np.abs(a) @ np.abs(bcat).T + np.abs(r), "nsplit+res")
+
+
+def test_gemm_ksplit_mn_major_b():
+    """dX = dY W with W split along K (q|k|v): B stored [K_s][N] (N contiguous)."""
+    M, N = 256, 512
+    Ks = [128, 64, 192]
+    a, A = _mat(41, M, sum(Ks))
+    ws = [_mat(42 + i, k, N) for i, k in enumerate(Ks)]
+    Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    _gemm(M, N, sum(Ks), A, sum(Ks), 0, [w[1] for w in ws], [N] * 3, [2, 3, 6], 1, 1, Cm, N)
+    wcat = np.concatenate([w[0] for w in ws])
+    _check(Cm, a @ wcat, np.abs(a) @ np.abs(wcat), "ksplit")
+
+
+@pytest.mark.parametrize("M,N,K,sms", [(384, 512, 296, 0), (512, 256, 1024, 4), (256, 256, 64, 0)])
+def test_gemm_dw_both_mn_major(M, N, K, sms):
+    """dW = dY^T X: A stored [K][M], B stored [K][N]; A slice with lda > M."""
+    dy, DY = _mat(51, K, M + 64)          # use columns [64, 64+M) via pointer offset
+    x, X = _mat(52, K, N)
+    Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    _gemm(M, N, K, DY[:, 64:], M + 64, 1, [X], [N], [0], 1, 0, Cm, N, sms=sms)
+    ref = dy[:, 64:].T @ x
+    _check(Cm, ref, np.abs(dy[:, 64:]).T @ np.abs(x), "dW")
+
+
+def test_gemm_rejects_bad_shapes():
+    A = torch.empty(8, 8, dtype=torch.bfloat16, device="cuda")
+    g = dc.GemmArgs()
+    g.M, g.N, g.K, g.n_bseg = 8, 7, 8, 1
+    g.A = g.B[0] = g.C = A.data_ptr()
+    assert dc.lib.dc_gemm(C.byref(g), None) == dc.DC_EINVAL
+
+
+# ------------------------------------------------------------------ RS + Adam
+def _grads(world, table, S, q, step):
+    out = []
+    for i, p in enumerate(table):
+        g = nx.rne_bf16(seeded(500 + 10 * step + q, i, p.numel, std=0.01))
+        out.append(np.concatenate([g, np.zeros(world * S[i] - p.numel, np.float32)]))
+    return out
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_rs_adam_virtual_ranks(world):
+    cfg = synth.small_llama(layers=2)
+    table = synth.llama_param_table(cfg)
+    lr = 1e-3
+    ranks = rt.create_ranks(table, world, lr=lr)
+    S = [nx.shard_len(p.numel, world) for p in table]
+    full = ost.init_full_params(table)
+    o_master = [[nx.shard_of(full[i], world, r) for i in range(len(table))] for r in range(world)]
+    o_m = [[np.zeros(S[i], np.float32) for i in range(len(table))] for r in range(world)]
+    o_v = [[np.zeros(S[i], np.float32) for i in range(len(table))] for r in range(world)]
+    for step in (1, 2):
+        grads = {q: _grads(world, table, S, q, step) for q in range(world)}
+
+        def work(st):
+            cs, rs = st.streams[0], st.streams[2]
+            for layer in (1, 0):
+                dc.check(dc.lib.dc_grad_slot_acquire(st.ctx, layer, cs.cuda_stream), st.ctx)
+                slot = C.c_void_p()
+                dc.check(dc.lib.dc_grad_slot(st.ctx, layer, C.byref(slot)), st.ctx)
+                with torch.cuda.stream(cs):
+                    for i, p in enumerate(table):
+                        if p.layer != layer:
+                            continue
+                        v = rt.view(slot.value + rt.grad_offset(st, i), world * S[i], torch.bfloat16)
+                        v.copy_(bf16_tensor(grads[st.rank][i]))
+                dc.check(dc.lib.dc_grad_slot_publish(st.ctx, layer, cs.cuda_stream), st.ctx)
+                dc.check(dc.lib.dc_reduce_scatter_step(st.ctx, layer, step, 1, rs.cuda_stream), st.ctx)
+            torch.cuda.synchronize()
+
+        rt.run_parallel(ranks, work)
+        for r, st in ranks.items():
+            ms, mm, vv = (st.tensors[k].cpu().numpy() for k in ("master", "m", "v"))
+            sh = st.tensors["shard"].view(torch.int16).cpu().numpy().view(np.uint16)
+            for i, p in enumerate(table):
+                mst, m1, v1, shb = nx.rs_adam_shard([grads[q][i] for q in range(world)], o_master[r][i],
+                                                    o_m[r][i], o_v[r][i], world, r, step, lr)
+                o_master[r][i], o_m[r][i], o_v[r][i] = mst, m1, v1
+                off, n = rt.shard_range(st, i)
+                for got, ref in ((ms[off:off + n], mst), (mm[off:off + n], m1), (vv[off:off + n], v1)):
+                    rel = np.abs(got - ref) / np.maximum(np.abs(ref), 1e-30)
+                    assert rel.max() <= 1e-5, (r, p.name, rel.max())
+                    assert got.tobytes() == ref.tobytes(), (r, p.name, "not bit-exact")
+                assert np.array_equal(sh[off:off + n], nx.bf16_bits(mst))
+
+
+# ------------------------------------------------------------------ all-gather
+def _ops(sched):
+    return json.loads(dc.schedule_json(sched))["ops"]
+
+
+@pytest.mark.parametrize("world,passes", [(2, dc.DC_PASS_SHARD), (4, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH),
+                                          (8, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD)])
+def test_ag_push_virtual_ranks(world, passes):
+    cfg = synth.small_llama(layers=2, seq=128)
+    table = synth.llama_param_table(cfg)
+    ranks = rt.create_ranks(table, world)
+    xs = {r: bf16_tensor(ost.rank_batch(cfg, r)[0]) for r in ranks}
+    rt.attach_model(ranks, cfg, xs, xs)
+    prof = rt.profile_json(ranks[0], tc=[[4096, 10], [1 << 20, 20], [1 << 26, 400]])
+    M = 1 << 40
+    sched = dc.plan(json.dumps(prof), M, M_prefetch=1 << 22, passes=passes, strict=True)
+    rt.bind(ranks, {r: sched for r in ranks})
+    full = ost.init_full_params(table)
+    ops = _ops(sched)
+    for st in ranks.values():
+        dc.check(dc.lib.dc_step_begin(st.ctx, 1, st.streams[0].cuda_stream), st.ctx)
+    checked = set()
+    for o in ops:
+        if o["kind"] == "ag":
+            for st in ranks.values():
+                ev = torch.cuda.Event()
+                ev.record(st.streams[0])
+                st.streams[1].wait_event(ev)
+                dc.check(dc.lib.dc_gather(st.ctx, o["id"], st.streams[1].cuda_stream, None), st.ctx)
+            torch.cuda.synchronize()
+            for st in ranks.values():
+                for p in o["members"]:
+                    ptr = C.c_void_p()
+                    dc.check(dc.lib.dc_tensor_ptr(st.ctx, p, C.byref(ptr)), st.ctx)
+                    S = nx.shard_len(table[p].numel, world)
+                    got = rt.view(ptr.value, world * S, torch.bfloat16).view(torch.int16).cpu().numpy()
+                    ref = nx.all_gather_padded([nx.bf16_bits(nx.shard_of(full[p], world, q)) for q in range(world)])
+                    assert np.array_equal(got.view(np.uint16), ref), (st.rank, p)
+                    checked.add(p)
+        elif o["kind"] == "rel":
+            for st in ranks.values():
+                dc.check(dc.lib.dc_release(st.ctx, o["id"], st.streams[0].cuda_stream), st.ctx)
+    torch.cuda.synchronize()
+    assert checked == set(range(len(table)))
+    for st in ranks.values():
+        assert dc.lib.dc_step_begin(st.ctx, 2, st.streams[0].cuda_stream) == dc.DC_OK   # no sticky timeout

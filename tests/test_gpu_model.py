@@ -1,0 +1,116 @@
+"""End-to-end parity of the sharded step (dc_model_step through a planned
+schedule) against the oracle's N-rank simulated sharded step.
+
+Tolerances (BASELINE.json north star): bf16 layer outputs, loss and grads
+<= 2e-2 relative (norm-wise); the updated fp32 master: Adam's step-1 update is
+-lr * g / (|g| + eps), so elements whose bf16 gradient sign agrees match to a
+few ulp and the rest differ by at most 2 lr (checked: all within 2.02 lr and
+>= 95 % within 1e-6).
+"""
+import ctypes as C
+import json
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import numerics as nx
+from oracle import step as ost
+from tests.gpu_util import bf16_tensor, rel_norm, to_np
+
+pytestmark = pytest.mark.gpu
+
+dc = pytest.importorskip("paper_2504_09983_b200.dc")
+from paper_2504_09983_b200 import runtime as rt  # noqa: E402
+
+LR = 1e-3
+
+
+def _setup(cfg, world, passes, M=1 << 40, prefetch=1 << 22):
+    table = synth.llama_param_table(cfg)
+    ranks = rt.create_ranks(table, world, lr=LR)
+    xs, ts = {}, {}
+    for r in ranks:
+        x, t = ost.rank_batch(cfg, r)
+        xs[r], ts[r] = bf16_tensor(x), bf16_tensor(t)
+    rt.attach_model(ranks, cfg, xs, ts)
+    prof = rt.profile_json(ranks[0], tc=[[4096, 10], [1 << 20, 20], [1 << 26, 400]])
+    sched = dc.plan(json.dumps(prof), M, M_prefetch=prefetch, passes=passes, strict=True)
+    rt.bind(ranks, {r: sched for r in ranks})
+    return table, ranks
+
+
+def _loss(st):
+    return rt.view(rt.loss_ptr(st), 1, torch.float32).item()
+
+
+@pytest.mark.parametrize("world,passes", [(1, dc.DC_PASS_SHARD),
+                                          (2, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH),
+                                          (2, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD)])
+def test_step_matches_oracle(world, passes):
+    cfg = synth.small_llama(layers=2, seq=256)
+    table, ranks = _setup(cfg, world, passes)
+    oracle = ost.ShardedState(table, world, bf16=True)
+    o_losses, o_grads = ost.sharded_step(oracle, cfg, lr=LR)
+    # per-rank layer outputs from the oracle (same gathered weights on every rank)
+    rt.step(ranks, 1)
+    torch.cuda.synchronize()
+    for r, st in ranks.items():
+        assert abs(_loss(st) - o_losses[r]) <= 2e-2 * abs(o_losses[r])
+        # grads left in the two slots: layer 1 in slot 1, layer 0 in slot 0
+        for layer in (0, 1):
+            slot = C.c_void_p()
+            dc.check(dc.lib.dc_grad_slot(st.ctx, layer, C.byref(slot)), st.ctx)
+            for i, p in enumerate(table):
+                if p.layer != layer:
+                    continue
+                S = nx.shard_len(p.numel, world)
+                got = to_np(rt.view(slot.value + rt.grad_offset(st, i), world * S, torch.bfloat16))
+                ref = o_grads[r][i]
+                assert rel_norm(got[:p.numel], ref[:p.numel]) <= 2e-2, (r, p.name, rel_norm(got, ref))
+                assert not got[p.numel:].any()            # padding stays zero
+        ms = st.tensors["master"].cpu().numpy()
+        close, tot = 0, 0
+        for i, p in enumerate(table):
+            off, n = rt.shard_range(st, i)
+            d = np.abs(ms[off:off + n].astype(np.float64) - oracle.master[r][i])
+            assert d.max() <= 2.02 * LR, (r, p.name, d.max())
+            close += int((d <= 1e-6).sum())
+            tot += n
+        assert close >= 0.95 * tot, close / tot
+
+
+def test_layer_outputs_and_two_steps():
+    cfg = synth.small_llama(layers=2, seq=256)
+    table, ranks = _setup(cfg, 1, dc.DC_PASS_SHARD)
+    st = ranks[0]
+    ref = ost.ShardedState(table, 1, bf16=True)
+    full = ref.gathered(0)
+    P = 9
+    Ws = [{p.name: full[l * P + j].reshape(p.shape) for j, p in enumerate(table[l * P:(l + 1) * P])}
+          for l in range(cfg.layers)]
+    x, t = ost.rank_batch(cfg, 0)
+    from oracle import model as om
+    _, _, outs = om.llama_stack_fwd_bwd(nx.rne_bf16(x), nx.rne_bf16(t), Ws, cfg, nx.rne_bf16)
+    rt.step(ranks, 1, profile=True)
+    torch.cuda.synchronize()
+    for l in range(cfg.layers):
+        y = C.c_void_p()
+        dc.check(dc.lib.dc_model_act_ptr(st.model, l, 7, C.byref(y)))
+        got = to_np(rt.view(y.value, cfg.tokens * cfg.hidden, torch.bfloat16)).reshape(cfg.tokens, cfg.hidden)
+        assert rel_norm(got, outs[l]) <= 2e-2, (l, rel_norm(got, outs[l]))
+    l1 = _loss(st)
+    o1, _ = ost.sharded_step(ref, cfg, lr=LR)
+    o2, _ = ost.sharded_step(ref, cfg, lr=LR)
+    rt.step(ranks, 2)
+    torch.cuda.synchronize()
+    l2 = _loss(st)
+    assert abs(l1 - o1[0]) <= 2e-2 * o1[0] and abs(l2 - o2[0]) <= 2e-2 * o2[0]
+    assert l2 < l1
+    # profiling filled durations of every compute op
+    prof = json.loads(dc.model_profile_json(st.model))
+    assert all(o["dur_us"] > 0 for o in prof["ops"] if o["kind"] == "compute")
+    n = C.c_int64()
+    dc.check(dc.lib.dc_model_launch_count(st.model, C.byref(n)))
+    assert n.value > 20
