@@ -1,0 +1,423 @@
+"""Benchmark: the sharded training step of a Llama-3-8B-shaped layer stack
+(BASELINE.json configs[1]) through the C ABI, one process per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--layers L]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference      # the CPU oracle, same metric/config
+
+Flow (§3 / §5.5): S_0 warm-up steps (5) with per-op profiling
+-> profile MAX-reduced over ranks -> dc_plan (prefetch + unshard, strict) ->
+W warm-up steps -> K timed steps (CUDA events on the compute stream, barrier +
+synchronize on both sides, max over ranks) -> K end-to-end steps with pinned
+host inputs copied in and the loss read back -> CPU oracle sample.
+Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/sec/box (device-timed, max over ranks) at 1/2/4/8 B200; AG/RS GB/s vs 900 GB/s"
+GiB = 1 << 30
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=2)
+    ap.add_argument("--seq", type=int, default=2048)
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--passes", default="PS", help="S0 | P | S | PS")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-json", default="", help="write the rank-0 profile / plan here")
+    return ap.parse_args()
+
+
+def peaks():
+    p = {"hbm_gbs": 6546.6, "bf16_tflops": 1647.5, "bf16_tflops_sustained": 1402.6, "source": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({k: m[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in m})
+        p["source"] = "measured (MEASURED_PEAKS.json)"
+    except (OSError, ValueError):
+        pass
+    return p
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [r.split(", ") for r in out.strip().splitlines() if r.count(",") >= 7]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].strip() == "Active"})
+        load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+BAD_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+# ----------------------------------------------------------------------------- oracle sample
+class OracleSample:
+    """The CPU oracle on a bounded sample of the workload: ONE layer of the
+    stack at `tokens` tokens, N=1 — forward + backward (bf16-emulated, fp64
+    GEMMs) + reduce-scatter + Adam over the layer's 218 M parameters.
+    Weights are generated once (untimed); step() returns seconds."""
+
+    def __init__(self, cfg, tokens):
+        import synth
+        from oracle import numerics as nx
+        self.cfg, self.tokens, self.t = cfg, tokens, 0
+        self.table = synth.llama_param_table(cfg)[:9]
+        self.W, self.masters = {}, []
+        for p in self.table:
+            v = (np.ones(p.numel, np.float32) if p.k == 0.0 else synth.values(0, p.id, 0, p.numel, p.k))
+            self.masters.append(v)
+            self.W[p.name] = nx.rne_bf16(v).reshape(p.shape)
+        n = tokens * cfg.hidden
+        self.x = nx.rne_bf16(synth.values(1000, 0, 0, n, synth.K_UNIT)).reshape(tokens, cfg.hidden)
+        self.y_t = nx.rne_bf16(synth.values(2000, 0, 0, n, synth.K_UNIT)).reshape(tokens, cfg.hidden)
+        self.ms = [np.zeros_like(v) for v in self.masters]
+        self.vs = [np.zeros_like(v) for v in self.masters]
+
+    def step(self):
+        from oracle import model as om
+        from oracle import numerics as nx
+        self.t += 1
+        t0 = time.perf_counter()
+        y, c = om.llama_layer_fwd(self.x, self.W, self.cfg, nx.rne_bf16)
+        _, dy = om.mse_loss(y, self.y_t)
+        _, G = om.llama_layer_bwd(nx.rne_bf16(dy), c, self.W, self.cfg, nx.rne_bf16)
+        for i, p in enumerate(self.table):
+            g = nx.reduce_scatter([np.asarray(G[p.name], np.float32).reshape(-1)], 1, 0)
+            self.masters[i], self.ms[i], self.vs[i] = nx.adam_update(
+                self.masters[i], self.ms[i], self.vs[i], nx.scale_mean(g, 1), self.t)
+        return time.perf_counter() - t0
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    """--impl reference: the oracle (this tier's reference arm) on host cores."""
+    import synth
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import dataclasses
+    cfg = dataclasses.replace(synth.LLAMA3_8B, layers=args.layers, seq=args.seq, batch=args.batch)
+    T = 32
+    sample_run = OracleSample(cfg, T)
+    secs = []
+    for _ in range(args.warmup):
+        sample_run.step()
+    for _ in range(args.steps):
+        secs.append(sample_run.step())
+    per_step = float(np.mean(secs))
+    # tokens/s of the whole L-layer stack: T tokens need L layer-samples
+    val = T / (per_step * args.layers)
+    sample = "1 Llama-3-8B-shaped layer, %d tokens, N=1: oracle fwd+bwd+RS+Adam; scaled x%d layers" % (T, args.layers)
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * args.layers * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (oracle)",
+            "data": "synthetic",
+            "config": {"workload": "llama3-8b-stack (BASELINE configs[1]), oracle sample", "seq_len": args.seq,
+                       "global_batch": args.batch, "layers": args.layers},
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+GEMM_OPS = ("qkv", "o_proj", "gate_up", "down", "down_bwd", "gate_up_bwd", "o_bwd", "qkv_bwd")
+
+
+def gemm_flops(name, cfg, T):
+    h, f, qd = cfg.hidden, cfg.ffn, cfg.q_dim
+    qkvd = qd + 2 * cfg.kv_dim
+    fwd = {"qkv": 2 * T * h * qkvd, "o_proj": 2 * T * qd * h, "gate_up": 2 * T * h * 2 * f, "down": 2 * T * f * h}
+    bwd = {"down_bwd": 2 * fwd["down"], "gate_up_bwd": 2 * fwd["gate_up"], "o_bwd": 2 * fwd["o_proj"],
+           "qkv_bwd": 2 * fwd["qkv"]}
+    return {**fwd, **bwd}[name]
+
+
+def measure_tc(group, world, dev, torch, dist):
+    """T_c(V) table for the planner at N > 1: all-gather time vs full bytes,
+    MAX over ranks (reading D12).  Measured with the NCCL comparator (same
+    link), integer µs."""
+    pts = []
+    for lg in range(16, 31, 2):
+        full = 1 << lg
+        x = torch.empty(full // world // 2, dtype=torch.bfloat16, device=dev)
+        out = torch.empty(full // 2, dtype=torch.bfloat16, device=dev)
+        for _ in range(3):
+            dist.all_gather_into_tensor(out, x, group=group)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(5):
+            dist.all_gather_into_tensor(out, x, group=group)
+        e1.record()
+        torch.cuda.synchronize()
+        us = torch.tensor([e0.elapsed_time(e1) * 1000 / 5], device=dev)
+        dist.all_reduce(us, op=dist.ReduceOp.MAX, group=group)
+        pts.append([full, max(1, int(round(us.item())))])
+    for i in range(1, len(pts)):
+        pts[i][1] = max(pts[i][1], pts[i - 1][1])
+    return pts
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2504_09983_b200 import dc, runtime as rt
+
+    world = args.gpus
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    base = synth.LLAMA3_8B
+    cfg = synth.ModelConfig(base.name, base.kind, base.hidden, base.ffn, base.n_heads, base.n_kv, base.head_dim,
+                            args.layers, seq=args.seq, batch=args.batch)
+    T = cfg.tokens
+    table = synth.llama_param_table(cfg)
+    lr = 1.5e-5
+    if world == 1:
+        ranks = rt.create_ranks(table, 1, local, virtual=True, lr=lr)
+    else:
+        ranks = rt.create_ranks(table, world, local, virtual=False, group=group, rank=rank, lr=lr)
+    st = ranks[rank]
+    from oracle import numerics as nx          # bf16 rounding of the synthetic inputs only
+    x_np = synth.values(synth.seed_inputs(rank), 0, 0, T * cfg.hidden, synth.K_UNIT)
+    t_np = synth.values(synth.seed_targets(rank), 0, 0, T * cfg.hidden, synth.K_UNIT)
+    x_host = torch.from_numpy(nx.bf16_bits(x_np).view(np.int16)).view(torch.bfloat16).pin_memory()
+    t_host = torch.from_numpy(nx.bf16_bits(t_np).view(np.int16)).view(torch.bfloat16).pin_memory()
+    x_dev = x_host.to(dev).view(T, cfg.hidden)
+    t_dev = t_host.to(dev).view(T, cfg.hidden)
+    rt.attach_model(ranks, cfg, {rank: x_dev}, {rank: t_dev})
+    cs = st.streams[0]
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(group=group)
+
+    # ---- S_0 warm-up + profile (five warm-up iterations, then profile)
+    prof0 = rt.profile_json(st)
+    s0 = dc.plan(json.dumps(prof0), 1 << 50, passes=dc.DC_PASS_SHARD)
+    rt.bind(ranks, {rank: s0}, group=group)
+    step_no = 0
+    for i in range(5):
+        step_no += 1
+        rt.step(ranks, step_no, profile=(i == 4))
+    barrier()
+    tc = measure_tc(group, world, dev, torch, dist) if world > 1 else [[0, 0], [1 << 40, 0]]
+    prof = rt.profile_json(st, tc=tc)
+    if world > 1:   # element-wise MAX over ranks (reading D12)
+        vals = torch.tensor([[o["p_mem"], o["transient"], o["dur_us"]] for o in prof["ops"]], dtype=torch.int64,
+                            device=dev)
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX, group=group)
+        for o, v in zip(prof["ops"], vals.tolist()):
+            o["p_mem"], o["transient"], o["dur_us"] = v
+    total = torch.cuda.get_device_properties(dev).total_memory
+    M = int(0.9 * (total - 7 * GiB))
+    passes = dc.DC_PASS_SHARD | (dc.DC_PASS_PREFETCH if "P" in args.passes else 0) | \
+        (dc.DC_PASS_UNSHARD if "S" in args.passes and args.passes != "S0" else 0)
+    t_plan = time.perf_counter()
+    sched = dc.plan(json.dumps(prof), M, passes=passes, strict=True)
+    t_plan = time.perf_counter() - t_plan
+    plan = json.loads(dc.schedule_json(sched))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier(group=group)
+    rt.bind(ranks, {rank: sched}, group=group)
+    if world > 1:
+        dist.barrier(group=group)
+    if args.profile_json and rank == 0:
+        with open(args.profile_json, "w") as f:
+            json.dump({"profile": prof, "plan": plan, "M": M}, f)
+
+    # ---- warm-up with the planned schedule
+    for _ in range(max(3, args.warmup)):
+        step_no += 1
+        rt.step(ranks, step_no)
+    barrier()
+
+    # ---- timed region (device-timed on the compute stream, max over ranks)
+    def timed(k, profile_last=True):
+        nonlocal step_no
+        clocks = rt_clocks = None
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        clk = Clocks(local)
+        clk.start()
+        time.sleep(0.3)
+        e0.record(cs)
+        launches = 0
+        for i in range(k):
+            step_no += 1
+            rt.step(ranks, step_no, profile=2 if (profile_last and i == k - 1) else 0)
+            n = rt.C.c_int64()
+            dc.check(dc.lib.dc_model_launch_count(st.model, rt.C.byref(n)))
+            launches += n.value
+        e1.record(cs)
+        barrier()
+        clocks = clk.stop()
+        rt.poll(ranks)
+        ms = torch.tensor([e0.elapsed_time(e1) / k], device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=group)
+        return ms.item(), clocks, launches
+
+    ms, clocks, launches = timed(args.steps)
+    if clocks["reasons"] and BAD_REASONS & set(clocks["reasons"]):
+        ms, clocks, launches = timed(args.steps)          # re-measure once
+        clocks["remeasured"] = True
+    tokens_box = world * T
+    value = tokens_box / (ms / 1e3)
+
+    # ---- per-op breakdown of the last timed step (events recorded in-region)
+    last = rt.profile_json(st)
+    by = {}
+    gemm_us, gemm_fl = 0, 0
+    for o in last["ops"]:
+        if o["kind"] in ("compute", "rs"):
+            by.setdefault(o["name"], 0)
+            by[o["name"]] += o["dur_us"]
+            if o["name"] in GEMM_OPS:
+                gemm_us += o["dur_us"]
+                gemm_fl += gemm_flops(o["name"], cfg, T)
+    pk = peaks()
+    achieved = gemm_fl / (gemm_us * 1e-6) / 1e12 if gemm_us else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    roofline = {"bound": "tensor", "kernel": "gemm_bf16_sm100 (tcgen05, all layer GEMMs)",
+                "achieved": achieved, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                "frac": achieved / pk["bf16_tflops_sustained"] if achieved else None, "traffic": traffic,
+                "peak_source": pk["source"] + ", sustained bf16 (kernel inside a long step)",
+                "flops_per_step": gemm_fl, "gemm_ms_per_step": gemm_us / 1e3}
+    shard_elems = st.layout.shard_elems
+    rs_us = by.get("rs", 0)
+    rs_bytes = (28 + 2 * (world - 1)) * shard_elems
+    kernels = {"op_ms_per_step": {k: round(v / 1e3, 3) for k, v in sorted(by.items())},
+               "rs_adam": {"bytes_per_step": rs_bytes, "ms_per_step": rs_us / 1e3,
+                           "achieved_gbs": rs_bytes / (rs_us * 1e-6) / 1e9 if rs_us else None,
+                           "peak_gbs": pk["hbm_gbs"], "bound": "hbm" if world == 1 else "nvlink+hbm"}}
+
+    # ---- end to end through the public API with HOST buffers
+    loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
+    lp = rt.view(rt.loss_ptr(st), 1, torch.float32, device=dev)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cs)
+    for _ in range(args.steps):
+        with torch.cuda.stream(cs):
+            x_dev.view(-1).copy_(x_host, non_blocking=True)
+            t_dev.view(-1).copy_(t_host, non_blocking=True)
+        step_no += 1
+        rt.step(ranks, step_no)
+        with torch.cuda.stream(cs):
+            loss_host.copy_(lp, non_blocking=True)
+        cs.synchronize()
+        _ = float(loss_host.item())
+    e1.record(cs)
+    barrier()
+    ems = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    if world > 1:
+        dist.all_reduce(ems, op=dist.ReduceOp.MAX, group=group)
+    e2e = {"value": tokens_box / (ems.item() / 1e3), "unit": "tokens/s",
+           "h2d_bytes_per_step": 2 * T * cfg.hidden * 2, "d2h_bytes_per_step": 4,
+           "loss": float(loss_host.item())}
+
+    # ---- CPU oracle timed on host cores (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        Ts = 128
+        sample_run = OracleSample(cfg, Ts)
+        sec = min(sample_run.step() for _ in range(2))
+        cpu = {"value": Ts / (sec * cfg.layers), "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": "1 Llama-3-8B-shaped layer, %d tokens, N=1: oracle fwd+bwd+RS+Adam (best of 2, %.1f s); "
+                         "tokens/s scaled to the %d-layer stack" % (Ts, sec, cfg.layers)}
+
+    coll = None
+    if world > 1:
+        ag_us = sum(o["dur_us"] for o in last["ops"] if o["kind"] == "ag")
+        coll = {"note": "AG busbw = (N-1)/N x gathered bytes / gather time (incl. flag waits)",
+                "ag_busbw_gbs": (world - 1) / world * sum(p["bytes"] for p in last["params"]) * 2 / (ag_us * 1e-6) / 1e9
+                if ag_us else None, "nvlink_peak_gbs": 900}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": "llama3-8b-stack (BASELINE configs[1]): L=%d h=4096 f=14336 32/8 heads, "
+                                       "seq %d, b=%d per GPU, ZeRO-3 + proactive prefetch%s" %
+                                       (cfg.layers, args.seq, args.batch, " + selective unshard" if "S" in args.passes else ""),
+                           "model": "llama3-8b-shaped synthetic stack (random init)", "global_batch": world * args.batch,
+                           "seq_len": args.seq, "parallelism": "fsdp%d" % world, "passes": args.passes,
+                           "mem_budget_M": M, "plan_ms": round(t_plan * 1e3, 2),
+                           "unshard_params": len(plan["unshard"]),
+                           "l2": "working set (~120 GB/GPU of weights, states, activations) >> 126 MB L2; no flush"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clocks, "kernels": kernels, "collectives": coll}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

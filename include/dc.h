@@ -105,10 +105,10 @@ typedef struct {
   uint64_t flag_bytes;
   void* host_pinned;             /* pinned host memory for offload (may be 0) */
   uint64_t host_pinned_bytes;
-  float lr, beta1, beta2, eps;   /* Adam; weight decay 0               */
+  double lr, beta1, beta2, eps;  /* Adam; weight decay 0; host scalars  */
   uint64_t seed;                 /* generator seed (synth/gen.py recipe)       */
   uint32_t flags;                /* DC_INIT_WEIGHTS | DC_VIRTUAL_RANKS | ...   */
-  uint32_t spin_limit;           /* flag-wait bound in 2^10-cycle units, 0=def */
+  uint32_t spin_limit;           /* flag-wait bound in ms, 0 = 20000           */
 } dc_init_args;
 
 /* Validates, computes the layout, zeroes m/v and (with DC_INIT_WEIGHTS) fills
@@ -116,6 +116,9 @@ typedef struct {
  * counter-based generator on the device (synchronous). */
 dc_status dc_init(const dc_init_args* a, dc_ctx** out);
 dc_status dc_destroy(dc_ctx* ctx);
+/* Non-blocking check of the sticky device error word (DC_ETIMEOUT if any flag
+ * wait of this ctx timed out since dc_init); DC_OK otherwise. */
+dc_status dc_poll(dc_ctx* ctx);
 
 /* Offset (elements) of param's shard in the store, and S_i. */
 dc_status dc_shard_range(const dc_ctx* ctx, int32_t param, int64_t* offset, int64_t* shard_elems);
@@ -243,13 +246,16 @@ dc_status dc_model_bind(dc_model* m, void* act_buf, uint64_t act_bytes, const vo
 dc_status dc_model_profile_json(const dc_model* m, char* buf, size_t* len);
 /* One training step through the bound schedule: forward, loss, backward with
  * gathers / releases / reduce-scatter+Adam / offload ops interleaved as
- * planned.  Streams: compute, ag, rs, copy.  profile != 0 records per-op
- * durations and memory for dc_model_profile_json. */
+ * planned.  Streams: compute, ag, rs, copy.  profile: 0 off; 1 record per-op
+ * CUDA events around every compute / RS op and read them now (synchronises);
+ * 2 record only (read by the next dc_model_profile_json, no sync). */
 dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile, cudaStream_t compute,
                         cudaStream_t ag, cudaStream_t rs, cudaStream_t copy);
 /* Device pointer to the fp32 loss of the last step (mean 1/2 (y-t)^2). */
 dc_status dc_model_loss_ptr(const dc_model* m, float** loss);
-/* Pointers into the activation buffer (tests): which = 0 x(l), 1 y(l) ... */
+/* Pointers into the activation buffer of layer l (tests): which = 0 h1, 1 qkv,
+ * 2 a, 3 x2, 4 h2, 5 gate|up, 6 act, 7 y (layer output), 8 / 9 the two
+ * backward gradient ping-pong buffers. */
 dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t which, void** ptr);
 /* Number of kernels the last dc_model_step launched. */
 dc_status dc_model_launch_count(const dc_model* m, int64_t* n);

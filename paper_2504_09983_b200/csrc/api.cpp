@@ -79,7 +79,7 @@ struct dc_ctx {
   uint64_t grad_bytes = 0, flag_bytes = 0, arena_bytes = 0;
   void* host_pinned = nullptr;
   uint64_t host_pinned_bytes = 0;
-  float lr = 1e-3f, beta1 = 0.9f, beta2 = 0.999f, eps = 1e-8f;
+  double lr = 1e-3, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
   uint64_t seed = 0;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_ops = 0;
@@ -90,7 +90,8 @@ struct dc_ctx {
   std::vector<int> initial_ready;       // gathers whose ready is posted at step start
   std::map<int, int> ag_ctas;           // gather id -> CTAs per launch
   std::map<int, int> ag_launches;
-  uint32_t epoch = 0;
+  uint32_t epoch = 0;                   // caller's step number (monotone)
+  uint32_t fepoch = 0;                  // flag epoch: steps since the last bind
   int slot_use[2] = {0, 0};
   std::vector<int> layer_use;
   uint32_t rs_done_total = 0;
@@ -168,6 +169,9 @@ extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
   c->layer_use.assign(c->L.n_layers, 0);
   c->rs_ctas = 148;
   DC_CUDA_TRY(cudaSetDevice(a->device), &c->err);
+  DC_CUDA_TRY(preload_glue_kernels(), &c->err);
+  DC_CUDA_TRY(preload_comm_kernels(), &c->err);
+  DC_CUDA_TRY(preload_gemm_kernels(), &c->err);
   DC_CUDA_TRY(cudaHostAlloc(&c->err_host, 4, cudaHostAllocMapped), &c->err);
   *c->err_host = 0;
   DC_CUDA_TRY(cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0), &c->err);
@@ -195,6 +199,11 @@ extern "C" dc_status dc_destroy(dc_ctx* c) {
   if (c->err_host) cudaFreeHost(c->err_host);
   delete c;
   return DC_OK;
+}
+
+extern "C" dc_status dc_poll(dc_ctx* c) {
+  if (!c) return fail(nullptr, DC_EINVAL, "dc_poll: null ctx");
+  return check_sticky(c);
 }
 
 extern "C" dc_status dc_shard_range(const dc_ctx* c, int32_t p, int64_t* off, int64_t* S) {
@@ -245,6 +254,7 @@ extern "C" dc_status dc_bind_schedule(dc_ctx* c, const dc_schedule* s, const uin
   if (c->world > 1 && (int)c->arena_peers.size() != c->world) return fail(c, DC_EINVAL, "dc_bind_schedule: arena peers");
   c->arena_bytes = arena_bytes;
   c->epoch = 0;
+  c->fepoch = 0;
   c->slot_use[0] = c->slot_use[1] = 0;
   std::fill(c->layer_use.begin(), c->layer_use.end(), 0);
   c->rs_done_total = 0;
@@ -266,11 +276,12 @@ extern "C" dc_status dc_step_begin(dc_ctx* c, int32_t epoch, cudaStream_t st) {
   if (dc_status e = check_sticky(c)) return e;
   if ((uint32_t)epoch <= c->epoch) return fail(c, DC_EINVAL, "dc_step_begin: epochs must increase");
   c->epoch = (uint32_t)epoch;
+  ++c->fepoch;
   if (c->world == 1) return DC_OK;
   // ready flags for gathers without an in-step predecessor release (D26):
   // ready[g][me] in every rank's table
   for (int g : c->initial_ready) {
-    k_post_flags(peers_at(c, c->L.f_ready + (int64_t)g * c->world + c->rank), c->epoch, st);
+    k_post_flags(peers_at(c, c->L.f_ready + (int64_t)g * c->world + c->rank), c->fepoch, st);
   }
   if (cudaGetLastError() != cudaSuccess) return fail(c, DC_ECUDA, "dc_step_begin: launch failed");
   return DC_OK;
@@ -289,7 +300,7 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
   if (c->world == 1) {
     for (int j = 0; j < nm; ++j) c->cur_off[mem[j]] = -2;   // alias of the shard
   } else {
-    if (c->epoch == 0) return fail(c, DC_ESTATE, "dc_gather: call dc_step_begin first");
+    if (c->fepoch == 0) return fail(c, DC_ESTATE, "dc_gather: call dc_step_begin first");
     std::vector<AgMember> am;
     int64_t cur = off;
     for (int j = 0; j < nm; ++j) {
@@ -303,9 +314,9 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
       cur += align256(c->numel[p] > 0 ? c->L.S[p] * c->world * 2 : 0);
     }
     const int ctas = c->ag_ctas[gid];
-    const uint32_t target = c->epoch * (uint32_t)(c->world * ctas * c->ag_launches[gid]);
+    const uint32_t target = c->fepoch * (uint32_t)(c->world * ctas * c->ag_launches[gid]);
     dc_status s = k_ag_push(am, c->world, c->rank, c->arena_peers.data(), c->myflag(c->L.f_ready + (int64_t)gid * c->world),
-                            c->epoch, peers_at(c, c->L.f_done + gid), c->myflag(c->L.f_done + gid), target, ctas,
+                            c->fepoch, peers_at(c, c->L.f_done + gid), c->myflag(c->L.f_done + gid), target, ctas,
                             c->timeout_ns, c->err_dev, st);
     if (s != DC_OK) return fail(c, s, "dc_gather: launch failed");
   }
@@ -336,7 +347,7 @@ extern "C" dc_status dc_release(dc_ctx* c, int32_t rid, cudaStream_t st) {
   if (c->world > 1) c->cur_off[mem[0]] = -1;
   if (c->world == 1) return DC_OK;
   for (int j = 0; j < np; ++j)
-    k_post_flags(peers_at(c, c->L.f_ready + (int64_t)posts[j] * c->world + c->rank), c->epoch, st);
+    k_post_flags(peers_at(c, c->L.f_ready + (int64_t)posts[j] * c->world + c->rank), c->fepoch, st);
   if (cudaGetLastError() != cudaSuccess) return fail(c, DC_ECUDA, "dc_release: launch failed");
   return DC_OK;
 }
@@ -384,9 +395,9 @@ extern "C" dc_status dc_reduce_scatter_step(dc_ctx* c, int32_t layer, int32_t st
   }
   std::vector<uint64_t> slots(c->world);
   for (int q = 0; q < c->world; ++q) slots[q] = reinterpret_cast<uint64_t>(c->slot_ptr(q, s));
-  const double bc1 = 1.0 - std::pow((double)c->beta1, step_t);
-  const double bc2 = 1.0 - std::pow((double)c->beta2, step_t);
-  const float sc = (float)((double)c->lr / bc1);
+  const double bc1 = 1.0 - std::pow(c->beta1, step_t);
+  const double bc2 = 1.0 - std::pow(c->beta2, step_t);
+  const float sc = (float)(c->lr / bc1);
   const float cc = (float)std::sqrt(bc2);
   int ctas = (int)std::min<int64_t>(c->rs_ctas * 2, std::max<int64_t>(1, elems / 8 / 256));
   c->rs_done_total += (uint32_t)ctas;

@@ -53,17 +53,10 @@ __device__ __forceinline__ bool spin_ge(const uint32_t* p, uint32_t target, uint
   return true;
 }
 
+// Flag waits run in separate one-thread kernels on the same stream (before the
+// push: every receiver's ready flag; after it: this rank's done counter), so a
+// waiting rank occupies one SM slot, never a whole grid of spinning CTAs.
 __global__ void __launch_bounds__(512) ag_push_kernel(const AgParams p) {
-  __shared__ int ok;
-  if (threadIdx.x == 0) {
-    const uint64_t t0 = ptx::globaltimer();
-    int good = 1;
-    for (int q = 0; q < p.world && good; ++q)
-      good = spin_ge(p.ready + q, p.epoch, t0, p.timeout_ns, p.err, 0x100u | q);
-    ok = good;
-  }
-  __syncthreads();
-  if (!ok) return;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   for (int m = 0; m < p.nm; ++m) {
@@ -90,15 +83,22 @@ __global__ void __launch_bounds__(512) ag_push_kernel(const AgParams p) {
   if (threadIdx.x == 0) {
     __threadfence_system();
     for (int q = 0; q < p.world; ++q) ptx::red_add_release_sys(p.done_peer[q], 1u);
-    if (p.wait && blockIdx.x == 0)
-      spin_ge(p.done_local, p.done_target, ptx::globaltimer(), p.timeout_ns, p.err, 0x200u);
   }
+}
+
+__global__ void wait_flags_kernel(const uint32_t* f, int n, uint32_t target, uint64_t tmo, uint32_t* err,
+                                  uint32_t code) {
+  const uint64_t t0 = ptx::globaltimer();
+  for (int i = 0; i < n; ++i)
+    if (!spin_ge(f + i, target, t0, tmo, err, code | i)) return;
 }
 
 dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const uint64_t* arena_peers,
                     const uint32_t* ready_local, uint32_t epoch, PeerFlags done_peers, const uint32_t* done_local,
                     uint32_t done_target, int ctas, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st) {
-  // members beyond AG_MAXM go to extra launches; only the last one waits
+  wait_flags_kernel<<<1, 1, 0, st>>>(ready_local, world, epoch, timeout_ns, err_flag, 0x100u);
+  count_launch();
+  // members beyond AG_MAXM go to extra launches
   for (size_t b = 0; b < mem.size(); b += AG_MAXM) {
     AgParams p{};
     p.nm = (int)std::min<size_t>(AG_MAXM, mem.size() - b);
@@ -124,7 +124,9 @@ dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const
     if (cudaGetLastError() != cudaSuccess) return DC_ECUDA;
     count_launch();
   }
-  return DC_OK;
+  wait_flags_kernel<<<1, 1, 0, st>>>(done_local, 1, done_target, timeout_ns, err_flag, 0x200u);
+  count_launch();
+  return cudaGetLastError() == cudaSuccess ? DC_OK : DC_ECUDA;
 }
 
 // ------------------------------------------------------------------ rs_adam
@@ -158,16 +160,7 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
 }
 
 __global__ void __launch_bounds__(256) rs_adam_kernel(const RsParams p) {
-  __shared__ int ok;
-  if (threadIdx.x == 0) {
-    const uint64_t t0 = ptx::globaltimer();
-    int good = 1;
-    for (int q = 0; q < p.world && good; ++q)
-      good = spin_ge(p.ready + q, p.ready_target, t0, p.timeout_ns, p.err, 0x300u | q);
-    ok = good;
-  }
-  __syncthreads();
-  if (ok) {
+  {   // grad-ready of every rank was awaited by the preceding wait kernel
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     for (int mi = 0; mi < p.nm; ++mi) {
@@ -232,7 +225,7 @@ __global__ void __launch_bounds__(256) rs_adam_kernel(const RsParams p) {
 dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const uint64_t* slot_peers,
                     const uint32_t* ready_local, uint32_t ready_target, PeerFlags consumed_peers,
                     uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master, float* m,
-                    float* v, void* shard, float s, float c, float beta1, float beta2, float eps, int ctas,
+                    float* v, void* shard, float s, float c, double beta1, double beta2, double eps, int ctas,
                     uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st) {
   if (mem.size() > (size_t)RS_MAXM) return DC_EINVAL;
   RsParams p{};
@@ -251,15 +244,17 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
   p.consumed_value = consumed_value;
   p.done_ctr = done_ctr; p.done_target = done_target;
   p.master = master; p.m = m; p.v = v; p.shard = reinterpret_cast<bf16*>(shard);
-  p.w1 = (float)(1.0 - (double)beta1);
-  p.w2 = (float)(1.0 - (double)beta2);
-  p.b2 = beta2;
+  p.w1 = (float)(1.0 - beta1);          // fp32(1 - b1) rounded once from double
+  p.w2 = (float)(1.0 - beta2);
+  p.b2 = (float)beta2;
   p.neg_s = -s;
   p.c = c;
-  p.eps = eps;
+  p.eps = (float)eps;
   p.invN = (float)(1.0 / (double)world);
   p.timeout_ns = timeout_ns;
   p.err = err_flag;
+  wait_flags_kernel<<<1, 1, 0, st>>>(ready_local, world, ready_target, timeout_ns, err_flag, 0x300u);
+  count_launch();
   rs_adam_kernel<<<ctas, 256, 0, st>>>(p);
   if (cudaGetLastError() != cudaSuccess) return DC_ECUDA;
   count_launch();
@@ -281,15 +276,24 @@ void k_post_flags(PeerFlags dst, uint32_t value, cudaStream_t st) {
   count_launch();
 }
 
-__global__ void wait_flags_kernel(const uint32_t* f, int n, uint32_t target, uint64_t tmo, uint32_t* err) {
-  const uint64_t t0 = ptx::globaltimer();
-  for (int i = 0; i < n; ++i)
-    if (!spin_ge(f + i, target, t0, tmo, err, 0x400u | i)) return;
-}
 void k_wait_flags(const uint32_t* flags, int n, uint32_t target, uint64_t timeout_ns, uint32_t* err_flag,
                   cudaStream_t st) {
-  wait_flags_kernel<<<1, 1, 0, st>>>(flags, n, target, timeout_ns, err_flag);
+  wait_flags_kernel<<<1, 1, 0, st>>>(flags, n, target, timeout_ns, err_flag, 0x400u);
   count_launch();
 }
 
+}  // namespace dc
+
+namespace dc {
+// Force-load this file's kernels (CUDA lazy loading would otherwise load a
+// kernel at its first launch, which can block behind a spinning flag wait of
+// another rank sharing the GPU).
+cudaError_t preload_comm_kernels() {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, ag_push_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, wait_flags_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, post_flags_kernel);
+  return e;
+}
 }  // namespace dc

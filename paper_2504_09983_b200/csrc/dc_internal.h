@@ -62,6 +62,11 @@ void k_act_fwd(const void* gu, void* act, int T, int F, cudaStream_t st);
 void k_act_bwd(const void* dact, const void* gu, void* dgu, int T, int F, cudaStream_t st);
 void k_loss(const void* y, const void* t, void* dy, float* partial, float* loss, int64_t n, cudaStream_t st);
 void k_zero(void* p, int64_t bytes, cudaStream_t st);
+// force-load every kernel of the library (lazy module loading at first launch
+// can block behind another rank's spinning flag wait on the same GPU)
+cudaError_t preload_glue_kernels();
+cudaError_t preload_comm_kernels();
+cudaError_t preload_gemm_kernels();
 
 // comm.cu
 constexpr int MAXW = 8;                       // max ranks on one NVSwitch box
@@ -79,8 +84,8 @@ dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const
 dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const uint64_t* slot_peers,
                     const uint32_t* ready_local, uint32_t ready_target, PeerFlags consumed_peers,
                     uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master,
-                    float* m, float* v, void* shard, float s, float c, float beta1, float beta2,
-                    float eps, int ctas, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st);
+                    float* m, float* v, void* shard, float s, float c, double beta1, double beta2,
+                    double eps, int ctas, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st);
 void k_post_flags(PeerFlags dst, uint32_t value, cudaStream_t st);
 void k_wait_flags(const uint32_t* flags, int n, uint32_t target, uint64_t timeout_ns,
                   uint32_t* err_flag, cudaStream_t st);

@@ -332,3 +332,13 @@ extern "C" dc_status dc_gemm(const dc_gemm_args* g, cudaStream_t stream) {
   if (s != DC_OK) dc::set_global_error(err);
   return s;
 }
+
+namespace dc {
+cudaError_t preload_gemm_kernels() {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, gemm_bf16_sm100);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm_bf16_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+  return e;
+}
+}  // namespace dc

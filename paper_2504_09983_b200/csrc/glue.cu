@@ -383,3 +383,19 @@ void k_zero(void* p, int64_t bytes, cudaStream_t st) {
 }
 
 }  // namespace dc
+
+namespace dc {
+cudaError_t preload_glue_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {(const void*)init_param_kernel, (const void*)rmsnorm_fwd_kernel,
+                       (const void*)rmsnorm_bwd_kernel, (const void*)colsum_kernel,
+                       (const void*)attn_mix_fwd_kernel, (const void*)attn_mix_bwd_kernel,
+                       (const void*)act_fwd_kernel, (const void*)act_bwd_kernel,
+                       (const void*)loss_kernel, (const void*)loss_final_kernel};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+}  // namespace dc

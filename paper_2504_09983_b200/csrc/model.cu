@@ -66,6 +66,7 @@ struct dc_model {
   int32_t epoch = 0;
   int64_t launches = 0;
   int cur_d = 0;                     // which of dA/dB holds dL/d(layer output)
+  bool profile_pending = false;      // per-op events recorded, not yet read
   std::string err;
 
   int pid(int layer, int slot) const { return ctx_layout(ctx).layer_first[layer] + slot; }
@@ -288,7 +289,7 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
              (int64_t)T * H, st);
       break;
     case B_DOWN:
-      if ((s = dc_grad_slot_acquire(m->ctx, l, st)) != DC_OK) return s;
+      // (the executor has enqueued dc_grad_slot_acquire for this layer)
       // dact = dy Wd  (A K-major [T,H]; B = Wd [H rows = K][F] MN-major)
       s = gemm(m, T, F, H, dcur, H, 0, {m->W(l, P_DOWN)}, {F}, {F / 256}, 1, 0, m->A(m->ws_dact), F, nullptr, 0, st);
       if (s == DC_OK)  // dWd = dy^T act : A = dy stored [T][H] (MN-major), B = act [T][F] (MN-major)
@@ -395,9 +396,26 @@ static void compute_pmem(dc_model* m) {
   }
 }
 
+// Read the per-op CUDA-event durations of the last profiled step (µs).
+static dc_status collect_profile(dc_model* m) {
+  for (size_t i = 0; i < m->s0.size(); ++i) {
+    if (m->s0[i].kind != K_COMPUTE && m->s0[i].kind != K_RS) continue;
+    if (cudaEventSynchronize(m->ev_t1[i]) != cudaSuccess) return mfail(m, DC_ECUDA, "profile: event sync failed");
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, m->ev_t0[i], m->ev_t1[i]) == cudaSuccess)
+      m->dur_us[i] = std::max<int64_t>(1, (int64_t)std::llround(ms * 1000.0));
+  }
+  m->profile_pending = false;
+  return DC_OK;
+}
+
 extern "C" dc_status dc_model_profile_json(const dc_model* mc, char* buf, size_t* len) {
   dc_model* m = const_cast<dc_model*>(mc);
   if (!m || !len) return mfail(nullptr, DC_EINVAL, "dc_model_profile_json: null argument");
+  if (m->profile_pending) {
+    dc_status s = collect_profile(m);
+    if (s != DC_OK) return s;
+  }
   compute_pmem(m);
   const Layout& L = ctx_layout(m->ctx);
   const int N = ctx_world(m->ctx);
@@ -471,6 +489,10 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
         if (N > 1)
           for (int p : o.params)
             if (gather_ev[p]) cudaStreamWaitEvent(cs, gather_ev[p], 0);
+        if (o.code == B_DOWN) {   // first grad-slot write of the layer's backward
+          s = dc_grad_slot_acquire(m->ctx, o.layer, cs);
+          if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
+        }
         if (profile) cudaEventRecord(m->ev_t0[id], cs);
         s = run_op(m, o, cs);
         if (profile) cudaEventRecord(m->ev_t1[id], cs);
@@ -512,16 +534,11 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
   cudaStreamWaitEvent(cs, m->ev_join[2], 0);
   cudaStreamWaitEvent(cs, m->ev_join[3], 0);
   if (cudaGetLastError() != cudaSuccess) return mfail(m, DC_ECUDA, "dc_model_step: CUDA error");
-  if (profile) {
-    if (cudaStreamSynchronize(cs) != cudaSuccess) return mfail(m, DC_ECUDA, "dc_model_step: sync failed");
-    for (size_t i = 0; i < m->s0.size(); ++i) {
-      if (m->s0[i].kind != K_COMPUTE && m->s0[i].kind != K_RS) continue;
-      float ms = 0.0f;
-      if (cudaEventElapsedTime(&ms, m->ev_t0[i], m->ev_t1[i]) == cudaSuccess)
-        m->dur_us[i] = (int64_t)std::llround(ms * 1000.0);
-    }
-  }
   m->launches = launch_count() - l0;
+  if (profile) {
+    m->profile_pending = true;
+    if (profile == 1) return collect_profile(m);   // 2: events only, read later
+  }
   return DC_OK;
 }
 

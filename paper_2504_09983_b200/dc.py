@@ -52,7 +52,7 @@ class InitArgs(C.Structure):
                 ("grad_peer_ptrs", p_u64), ("grad_bytes", C.c_uint64),
                 ("flag_peer_ptrs", p_u64), ("flag_bytes", C.c_uint64),
                 ("host_pinned", vp), ("host_pinned_bytes", C.c_uint64),
-                ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
                 ("seed", C.c_uint64), ("flags", C.c_uint32), ("spin_limit", C.c_uint32)]
 
 
@@ -85,6 +85,7 @@ _sig = {
     "dc_layout_query": (C.c_int, [C.POINTER(LayoutArgs), C.POINTER(Layout)]),
     "dc_init": (C.c_int, [C.POINTER(InitArgs), C.POINTER(vp)]),
     "dc_destroy": (C.c_int, [vp]),
+    "dc_poll": (C.c_int, [vp]),
     "dc_shard_range": (C.c_int, [vp, C.c_int32, p_i64, p_i64]),
     "dc_grad_offset": (C.c_int, [vp, C.c_int32, p_i64]),
     "dc_plan": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(PlanOpts), C.POINTER(vp)]),

@@ -200,9 +200,19 @@ def run_parallel(ranks, fn):
 
 
 def step(ranks, t, profile=False):
+    """One dc_model_step per rank (profile: False/0, True/1 = record+read,
+    2 = record only)."""
+    mode = int(profile) if not isinstance(profile, bool) else (1 if profile else 0)
+
     def one(st):
-        dc.check(dc.lib.dc_model_step(st.model, t, 1 if profile else 0, *st.stream_handles()), st.ctx)
+        dc.check(dc.lib.dc_model_step(st.model, t, mode, *st.stream_handles()), st.ctx)
     run_parallel(ranks, one)
+
+
+def poll(ranks):
+    """Raise if any rank's device flag wait timed out (sticky error word)."""
+    for st in ranks.values():
+        dc.check(dc.lib.dc_poll(st.ctx), st.ctx)
 
 
 def loss_ptr(st):

@@ -165,10 +165,14 @@ def test_rs_adam_virtual_ranks(world):
                         v = rt.view(slot.value + rt.grad_offset(st, i), world * S[i], torch.bfloat16)
                         v.copy_(bf16_tensor(grads[st.rank][i]))
                 dc.check(dc.lib.dc_grad_slot_publish(st.ctx, layer, cs.cuda_stream), st.ctx)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                rs.wait_event(ev)                    # local order, as the executor does
                 dc.check(dc.lib.dc_reduce_scatter_step(st.ctx, layer, step, 1, rs.cuda_stream), st.ctx)
             torch.cuda.synchronize()
 
         rt.run_parallel(ranks, work)
+        rt.poll(ranks)
         for r, st in ranks.items():
             ms, mm, vv = (st.tensors[k].cpu().numpy() for k in ("master", "m", "v"))
             sh = st.tensors["shard"].view(torch.int16).cpu().numpy().view(np.uint16)
@@ -227,6 +231,7 @@ def test_ag_push_virtual_ranks(world, passes):
             for st in ranks.values():
                 dc.check(dc.lib.dc_release(st.ctx, o["id"], st.streams[0].cuda_stream), st.ctx)
     torch.cuda.synchronize()
+    rt.poll(ranks)
     assert checked == set(range(len(table)))
     for st in ranks.values():
         assert dc.lib.dc_step_begin(st.ctx, 2, st.streams[0].cuda_stream) == dc.DC_OK   # no sticky timeout

@@ -56,6 +56,7 @@ def test_step_matches_oracle(world, passes):
     # per-rank layer outputs from the oracle (same gathered weights on every rank)
     rt.step(ranks, 1)
     torch.cuda.synchronize()
+    rt.poll(ranks)
     for r, st in ranks.items():
         assert abs(_loss(st) - o_losses[r]) <= 2e-2 * abs(o_losses[r])
         # grads left in the two slots: layer 1 in slot 1, layer 0 in slot 0
@@ -105,6 +106,7 @@ def test_layer_outputs_and_two_steps():
     o2, _ = ost.sharded_step(ref, cfg, lr=LR)
     rt.step(ranks, 2)
     torch.cuda.synchronize()
+    rt.poll(ranks)
     l2 = _loss(st)
     assert abs(l1 - o1[0]) <= 2e-2 * o1[0] and abs(l2 - o2[0]) <= 2e-2 * o2[0]
     assert l2 < l1
