@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -167,7 +168,8 @@ extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
   if (a->spin_limit) c->timeout_ns = (uint64_t)a->spin_limit * 1000ull * 1000ull;   // spin_limit in ms
   c->cur_off.assign(a->n_params, -1);
   c->layer_use.assign(c->L.n_layers, 0);
-  c->rs_ctas = 148;
+  c->rs_ctas = 296;                     // rs_adam grid, two CTAs per SM (DC_RS_CTAS overrides)
+  if (const char* e = getenv("DC_RS_CTAS")) c->rs_ctas = std::max(1, atoi(e));
   DC_CUDA_TRY(cudaSetDevice(a->device), &c->err);
   DC_CUDA_TRY(preload_glue_kernels(), &c->err);
   DC_CUDA_TRY(preload_comm_kernels(), &c->err);
@@ -399,7 +401,7 @@ extern "C" dc_status dc_reduce_scatter_step(dc_ctx* c, int32_t layer, int32_t st
   const double bc2 = 1.0 - std::pow(c->beta2, step_t);
   const float sc = (float)(c->lr / bc1);
   const float cc = (float)std::sqrt(bc2);
-  int ctas = (int)std::min<int64_t>(c->rs_ctas * 2, std::max<int64_t>(1, elems / 8 / 256));
+  int ctas = (int)std::min<int64_t>(c->rs_ctas, std::max<int64_t>(1, elems / 8 / 256));
   c->rs_done_total += (uint32_t)ctas;
   dc_status r = k_rs_adam(mem, c->world, c->rank, slots.data(), c->myflag(c->L.f_gready + (int64_t)s * c->world),
                           (uint32_t)u, peers_at(c, c->L.f_gcons + (int64_t)s * c->world + c->rank), (uint32_t)u,

@@ -159,8 +159,30 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
   }
 }
 
+// Streaming accesses of rs_adam carry an L2 evict-first policy: the kernel
+// moves ~28 B per parameter once, and runs beside the layer GEMMs whose
+// operand tiles live in L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ld_stream(const void* ptr, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st_stream(void* ptr, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
+               :: "l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
+}
+
+constexpr int RS_UNR = 2;   // groups of 8 elements per thread per iteration (loads hoisted)
+
 __global__ void __launch_bounds__(256) rs_adam_kernel(const RsParams p) {
   {   // grad-ready of every rank was awaited by the preceding wait kernel
+    const uint64_t pol = policy_evict_first();
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     for (int mi = 0; mi < p.nm; ++mi) {
@@ -170,44 +192,71 @@ __global__ void __launch_bounds__(256) rs_adam_kernel(const RsParams p) {
       float* mm = p.m + p.store_off[mi];
       float* vv = p.v + p.store_off[mi];
       bf16* sh = p.shard + p.store_off[mi];
-      for (int64_t i = tid; i < n8; i += nthr) {
-        float g[8];
+      for (int64_t i0 = tid; i0 < n8; i0 += nthr * RS_UNR) {
+        float g[RS_UNR][8], pp[RS_UNR][8], m8[RS_UNR][8], v8[RS_UNR][8];
+        uint4 P[RS_UNR][2], Mv[RS_UNR][2], V[RS_UNR][2];
+        // issue every load of the RS_UNR groups before any math
 #pragma unroll
-        for (int j = 0; j < 8; ++j) g[j] = 0.0f;
-        for (int q = 0; q < p.world; ++q) {      // ascending rank order, fp32
-          const uint4 u = *reinterpret_cast<const uint4*>(p.slot[q] + gbase + i * 16);
-          float f[8];
-          bf16x8_to_f32(u, f);
+        for (int u = 0; u < RS_UNR; ++u) {
+          const int64_t i = i0 + u * nthr;
+          if (i < n8) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) g[j] = __fadd_rn(g[j], f[j]);
-        }
-        float4 P0 = reinterpret_cast<float4*>(mst)[2 * i], P1 = reinterpret_cast<float4*>(mst)[2 * i + 1];
-        float4 M0 = reinterpret_cast<float4*>(mm)[2 * i], M1 = reinterpret_cast<float4*>(mm)[2 * i + 1];
-        float4 V0 = reinterpret_cast<float4*>(vv)[2 * i], V1 = reinterpret_cast<float4*>(vv)[2 * i + 1];
-        float pp[8] = {P0.x, P0.y, P0.z, P0.w, P1.x, P1.y, P1.z, P1.w};
-        float m8[8] = {M0.x, M0.y, M0.z, M0.w, M1.x, M1.y, M1.z, M1.w};
-        float v8[8] = {V0.x, V0.y, V0.z, V0.w, V1.x, V1.y, V1.z, V1.w};
-        uint4 out;
-        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&out);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float gj = __fmul_rn(g[j], p.invN);
-          const float mj = __fadd_rn(m8[j], __fmul_rn(p.w1, __fsub_rn(gj, m8[j])));
-          const float vj = __fadd_rn(__fmul_rn(p.b2, v8[j]), __fmul_rn(__fmul_rn(p.w2, gj), gj));
-          const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(vj), p.c), p.eps);
-          pp[j] = __fadd_rn(pp[j], __fdiv_rn(__fmul_rn(p.neg_s, mj), d));
-          m8[j] = mj;
-          v8[j] = vj;
+            for (int h = 0; h < 2; ++h) {
+              P[u][h] = ld_stream(mst + 8 * i + 4 * h, pol);
+              Mv[u][h] = ld_stream(mm + 8 * i + 4 * h, pol);
+              V[u][h] = ld_stream(vv + 8 * i + 4 * h, pol);
+            }
+          }
         }
 #pragma unroll
-        for (int t = 0; t < 4; ++t) o2[t] = __floats2bfloat162_rn(pp[2 * t], pp[2 * t + 1]);
-        reinterpret_cast<float4*>(mst)[2 * i] = make_float4(pp[0], pp[1], pp[2], pp[3]);
-        reinterpret_cast<float4*>(mst)[2 * i + 1] = make_float4(pp[4], pp[5], pp[6], pp[7]);
-        reinterpret_cast<float4*>(mm)[2 * i] = make_float4(m8[0], m8[1], m8[2], m8[3]);
-        reinterpret_cast<float4*>(mm)[2 * i + 1] = make_float4(m8[4], m8[5], m8[6], m8[7]);
-        reinterpret_cast<float4*>(vv)[2 * i] = make_float4(v8[0], v8[1], v8[2], v8[3]);
-        reinterpret_cast<float4*>(vv)[2 * i + 1] = make_float4(v8[4], v8[5], v8[6], v8[7]);
-        reinterpret_cast<uint4*>(sh)[i] = out;
+        for (int u = 0; u < RS_UNR; ++u) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) g[u][j] = 0.0f;
+          const int64_t i = i0 + u * nthr;
+          if (i < n8) {
+            for (int q = 0; q < p.world; ++q) {    // ascending rank order, fp32
+              const uint4 w = ld_stream(p.slot[q] + gbase + i * 16, pol);
+              float f[8];
+              bf16x8_to_f32(w, f);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) g[u][j] = __fadd_rn(g[u][j], f[j]);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < RS_UNR; ++u) {
+          const int64_t i = i0 + u * nthr;
+          if (i >= n8) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float* pf = reinterpret_cast<const float*>(&P[u][h]);
+            const float* mf = reinterpret_cast<const float*>(&Mv[u][h]);
+            const float* vf = reinterpret_cast<const float*>(&V[u][h]);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) { pp[u][4 * h + t] = pf[t]; m8[u][4 * h + t] = mf[t]; v8[u][4 * h + t] = vf[t]; }
+          }
+          uint4 out;
+          __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&out);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float gj = __fmul_rn(g[u][j], p.invN);
+            const float mj = __fadd_rn(m8[u][j], __fmul_rn(p.w1, __fsub_rn(gj, m8[u][j])));
+            const float vj = __fadd_rn(__fmul_rn(p.b2, v8[u][j]), __fmul_rn(__fmul_rn(p.w2, gj), gj));
+            const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(vj), p.c), p.eps);
+            pp[u][j] = __fadd_rn(pp[u][j], __fdiv_rn(__fmul_rn(p.neg_s, mj), d));
+            m8[u][j] = mj;
+            v8[u][j] = vj;
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t) o2[t] = __floats2bfloat162_rn(pp[u][2 * t], pp[u][2 * t + 1]);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            st_stream(mst + 8 * i + 4 * h, *reinterpret_cast<const uint4*>(&pp[u][4 * h]), pol);
+            st_stream(mm + 8 * i + 4 * h, *reinterpret_cast<const uint4*>(&m8[u][4 * h]), pol);
+            st_stream(vv + 8 * i + 4 * h, *reinterpret_cast<const uint4*>(&v8[u][4 * h]), pol);
+          }
+          st_stream(sh + 8 * i, out, pol);
+        }
       }
     }
   }

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "dc_internal.h"
@@ -315,7 +316,8 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
     attr = true;
   }
   const int tiles = p.m_tiles * p.n_tiles;
-  int sms = g->num_sms > 0 ? g->num_sms : num_sms_cached();
+  static const int env_sms = getenv("DC_GEMM_SMS") ? atoi(getenv("DC_GEMM_SMS")) : 0;
+  int sms = g->num_sms > 0 ? g->num_sms : (env_sms > 0 ? env_sms : num_sms_cached());
   const int grid = tiles < sms ? tiles : sms;
   gemm_bf16_sm100<<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
   cudaError_t e = cudaGetLastError();

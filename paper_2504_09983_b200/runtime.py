@@ -12,6 +12,7 @@ Nothing here computes: all math runs in the library's kernels.
 """
 import ctypes as C
 import json
+import os
 import threading
 
 import numpy as np
@@ -109,7 +110,11 @@ def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr
         st.world = world
         st.layout = lay
         st.device = dev
-        st.streams = [torch.cuda.Stream(device=dev) for _ in range(4)]   # compute, ag, rs, copy
+        # compute, ag, rs, copy.  DC_STREAM_PRIO=compute gives the compute
+        # stream the higher priority (rs_adam then fills in behind the GEMMs)
+        prio = os.environ.get("DC_STREAM_PRIO", "none")
+        st.streams = [torch.cuda.Stream(device=dev, priority=(-1 if (i == 0 and prio == "compute") else 0))
+                      for i in range(4)]
     return ranks
 
 
