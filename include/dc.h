@@ -231,6 +231,7 @@ typedef struct {
   void* C; int64_t ldc;
   const void* R; int64_t ldr;
   int32_t num_sms;               /* 0 = all SMs                                 */
+  int32_t kernel;                /* 0 auto (CTA pairs), 1 one-CTA tiles, 2 pairs */
 } dc_gemm_args;
 dc_status dc_gemm(const dc_gemm_args* g, cudaStream_t stream);
 

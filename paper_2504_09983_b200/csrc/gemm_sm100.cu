@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -229,6 +230,198 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   }
 }
 
+// ------------------------------------------------------------------ CTA-pair kernel
+// cta_group::2: a cluster of 2 CTAs on one TPC computes a 256 x 256 tile.  CTA
+// r stages rows [128r, 128r+128) of A and columns [128r, 128r+128) of B (16 KiB
+// each per 64-deep K block), so each SM moves half the operand bytes of the
+// 1-CTA kernel per MMA; 6 stages fit in 192 KiB.  The leader (rank 0) issues
+// tcgen05.mma.cta_group::2 (M = 256) and commits, multicast to both CTAs, the
+// smem-slot release and the accumulator-ready barriers.  Each CTA's TMEM holds
+// its 128 rows x 256 fp32 columns (x2 buffers = 512 columns).
+constexpr int BM2 = 256, BN2 = 256, STAGES2 = 6;
+constexpr int A2_STAGE = 128 * BK * 2;        // 16 KiB per CTA
+constexpr int B2_STAGE = 128 * BK * 2;        // 16 KiB per CTA
+constexpr int GEMM2_SMEM = STAGES2 * (A2_STAGE + B2_STAGE) + 1024 + 256;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
+                 const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
+                 const __grid_constant__ CUtensorMap mapB3, const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES2 * A2_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smB + STAGES2 * B2_STAGE);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* tfull = empty + STAGES2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+  const int num_tiles = p.m_tiles * p.n_tiles;      // 256 x 256 tiles
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&mapA);
+    ptx::tma_prefetch(&mapB0);
+    if (p.nseg > 1) ptx::tma_prefetch(&mapB1);
+    if (p.nseg > 2) ptx::tma_prefetch(&mapB2);
+    if (p.nseg > 3) ptx::tma_prefetch(&mapB3);
+    for (int s = 0; s < STAGES2; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { ptx::mbar_init(&tfull[b], 1); ptx::mbar_init(&tempty[b], 8); }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, TMEM_COLS);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ----------------------------------------------------------- producer (both CTAs)
+      int stage = 0; uint32_t phase = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+        const int m0 = mt * BM2 + (int)rank * 128;
+        int bseg = 0, n0 = nt * BN2;
+        if (!p.split_k) {
+          bseg = seg_of(p, nt);
+          n0 = (nt - (bseg ? p.seg_end[bseg - 1] : 0)) * BN2;
+        }
+        n0 += (int)rank * 128;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (A2_STAGE + B2_STAGE));
+          const uint32_t lbar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+          uint8_t* a = smA + stage * A2_STAGE;
+          uint8_t* b = smB + stage * B2_STAGE;
+          const int k0 = kb * BK;
+          if (!p.a_mn) {
+            ptx::tma_load_2d_2sm(a, &mapA, lbar, k0, m0);
+          } else {
+            ptx::tma_load_2d_2sm(a, &mapA, lbar, m0, k0);
+            ptx::tma_load_2d_2sm(a + 8192, &mapA, lbar, m0 + 64, k0);
+          }
+          int s = bseg, kk0 = k0;
+          if (p.split_k) {
+            s = seg_of(p, kb);
+            kk0 = (kb - (s ? p.seg_end[s - 1] : 0)) * BK;
+          }
+          const CUtensorMap* mb = s == 0 ? &mapB0 : s == 1 ? &mapB1 : s == 2 ? &mapB2 : &mapB3;
+          if (!p.b_mn) {
+            ptx::tma_load_2d_2sm(b, mb, lbar, kk0, n0);
+          } else {
+            ptx::tma_load_2d_2sm(b, mb, lbar, n0, kk0);
+            ptx::tma_load_2d_2sm(b + 8192, mb, lbar, n0 + 64, kk0);
+          }
+          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ----------------------------------------------------------- MMA issuer (leader)
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t aphase = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN2;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(smA + stage * A2_STAGE);
+          const uint32_t b_addr = ptx::smem_u32(smB + stage * B2_STAGE);
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            uint64_t ad, bd;
+            if (!p.a_mn) ad = ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
+            else         ad = ptx::umma_desc_sw128(a_addr + k * 2048, 8192, 1024);
+            if (!p.b_mn) bd = ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
+            else         bd = ptx::umma_desc_sw128(b_addr + k * 2048, 8192, 1024);
+            ptx::umma_f16_2sm(d, ad, bd, p.idesc, (kb | k) != 0);
+          }
+          ptx::umma_commit_2sm_mc(&empty[stage], 0x3);
+          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+        }
+        ptx::umma_commit_2sm_mc(&tfull[acc], 0x3);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------- epilogue (both CTAs)
+    const int q = warp & 3;
+    int acc = 0; uint32_t aphase = 0;
+    for (int tile = pair; tile < num_tiles; tile += npairs) {
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      ptx::mbar_wait(&tfull[acc], aphase);
+      ptx::tc_fence_after();
+      const int row = mt * BM2 + (int)rank * 128 + q * 32 + lane;
+      const bool row_ok = row < p.M;
+      __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
+      const __nv_bfloat16* rrow = p.R ? p.R + (int64_t)row * p.ldr : nullptr;
+#pragma unroll 1
+      for (int c = 0; c < BN2 / 32; ++c) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN2 + c * 32, v);
+        ptx::tmem_ld_wait();
+        const int col0 = nt * BN2 + c * 32;
+        if (row_ok && col0 < p.N) {
+          float f[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+          if (rrow) {
+            if (col0 + 32 <= p.N) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                uint4 rv = *reinterpret_cast<const uint4*>(rrow + col0 + j);
+                const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  float2 rf = __bfloat1622float2(r2[t]);
+                  f[j + 2 * t] = __fadd_rn(f[j + 2 * t], rf.x);
+                  f[j + 2 * t + 1] = __fadd_rn(f[j + 2 * t + 1], rf.y);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j < p.N) f[j] = __fadd_rn(f[j], __bfloat162float(rrow[col0 + j]));
+            }
+          }
+          if (col0 + 32 <= p.N) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              uint4 o;
+              __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+              for (int t = 0; t < 4; ++t) o2[t] = __floats2bfloat162_rn(f[j + 2 * t], f[j + 2 * t + 1]);
+              *reinterpret_cast<uint4*>(crow + col0 + j) = o;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < p.N) crow[col0 + j] = __float2bfloat16_rn(f[j]);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_2sm(tmem_base, TMEM_COLS);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -274,9 +467,16 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
     *err = "dc_gemm: M,N,K must be > 0, N and K multiples of 8, 1..4 B segments";
     return DC_EINVAL;
   }
+  static const int env_sms = getenv("DC_GEMM_SMS") ? atoi(getenv("DC_GEMM_SMS")) : 0;
+  static const int env_kernel = getenv("DC_GEMM_KERNEL") ? atoi(getenv("DC_GEMM_KERNEL")) : 0;
+  int sms = g->num_sms > 0 ? g->num_sms : (env_sms > 0 ? env_sms : num_sms_cached());
+  const int kind = g->kernel ? g->kernel : (env_kernel ? env_kernel : 2);
+  const bool pair = kind == 2 && sms >= 2;
+  const int tm = pair ? BM2 : BM;                // tile rows
+  const int rows_per_cta = 128;                  // A rows / B cols staged by one CTA
   GemmParams p{};
   p.M = g->M; p.N = g->N; p.K = g->K;
-  p.m_tiles = (g->M + BM - 1) / BM;
+  p.m_tiles = (g->M + tm - 1) / tm;
   p.n_tiles = (g->N + BN - 1) / BN;
   p.k_blocks = (g->K + BK - 1) / BK;
   p.nseg = g->n_bseg; p.split_k = g->b_split_k;
@@ -284,9 +484,10 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
   p.C = reinterpret_cast<__nv_bfloat16*>(g->C); p.ldc = g->ldc;
   p.R = reinterpret_cast<const __nv_bfloat16*>(g->R); p.ldr = g->ldr;
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a_mn << 15) | ((uint32_t)p.b_mn << 16) |
-            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(tm >> 4) << 24);
   CUtensorMap mA, mB[4];
-  bool ok = p.a_mn ? make_map(&mA, g->A, g->M, g->K, g->lda, 64) : make_map(&mA, g->A, g->K, g->M, g->lda, BM);
+  bool ok = p.a_mn ? make_map(&mA, g->A, g->M, g->K, g->lda, 64)
+                   : make_map(&mA, g->A, g->K, g->M, g->lda, rows_per_cta);
   int prev = 0;
   for (int s = 0; s < g->n_bseg; ++s) {
     p.seg_end[s] = g->bseg_end[s];
@@ -301,25 +502,27 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
     const int64_t kdim = g->b_split_k ? ext : g->K;
     const int64_t ndim = g->b_split_k ? g->N : ext;
     ok = ok && (g->b_mn_major ? make_map(&mB[s], g->B[s], ndim, kdim, g->ldb[s], 64)
-                              : make_map(&mB[s], g->B[s], kdim, ndim, g->ldb[s], BN));
+                              : make_map(&mB[s], g->B[s], kdim, ndim, g->ldb[s], pair ? rows_per_cta : BN));
     prev = g->bseg_end[s];
   }
   if (g->n_bseg == 1) p.seg_end[0] = g->b_split_k ? p.k_blocks : p.n_tiles;
   for (int s = g->n_bseg; s < 4; ++s) { mB[s] = mB[0]; p.seg_end[s] = p.seg_end[g->n_bseg - 1]; }
   if (!ok) { *err = "dc_gemm: cuTensorMapEncodeTiled failed (alignment / pitch must be 16 B)"; return DC_EINVAL; }
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(gemm_bf16_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) != cudaSuccess) {
-      *err = "dc_gemm: cannot set dynamic smem";
-      return DC_ECUDA;
-    }
-    attr = true;
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [] { attr_err = preload_gemm_kernels(); });
+  if (attr_err != cudaSuccess) {
+    *err = std::string("dc_gemm: kernel setup failed: ") + cudaGetErrorString(attr_err);
+    return DC_ECUDA;
   }
   const int tiles = p.m_tiles * p.n_tiles;
-  static const int env_sms = getenv("DC_GEMM_SMS") ? atoi(getenv("DC_GEMM_SMS")) : 0;
-  int sms = g->num_sms > 0 ? g->num_sms : (env_sms > 0 ? env_sms : num_sms_cached());
-  const int grid = tiles < sms ? tiles : sms;
-  gemm_bf16_sm100<<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+  if (pair) {
+    const int pairs = std::min(tiles, sms / 2);
+    gemm2_bf16_sm100<<<2 * pairs, GEMM_THREADS, GEMM2_SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+  } else {
+    const int grid = tiles < sms ? tiles : sms;
+    gemm_bf16_sm100<<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { *err = std::string("dc_gemm launch: ") + cudaGetErrorString(e); return DC_ECUDA; }
   count_launch();
@@ -341,6 +544,9 @@ cudaError_t preload_gemm_kernels() {
   cudaError_t e = cudaFuncGetAttributes(&a, gemm_bf16_sm100);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(gemm_bf16_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm2_bf16_sm100);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm2_bf16_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM2_SMEM);
   return e;
 }
 }  // namespace dc

@@ -47,7 +47,7 @@ def test_init_bitexact():
 
 
 # ------------------------------------------------------------------ GEMM
-def _gemm(M, N, K, A, lda, a_mn, Bs, ldbs, ends, b_mn, split_k, Cm, ldc, R=None, ldr=0, sms=0):
+def _gemm(M, N, K, A, lda, a_mn, Bs, ldbs, ends, b_mn, split_k, Cm, ldc, R=None, ldr=0, sms=0, kernel=0):
     g = dc.GemmArgs()
     g.M, g.N, g.K = M, N, K
     g.A, g.lda, g.a_mn_major = A.data_ptr(), lda, a_mn
@@ -58,6 +58,7 @@ def _gemm(M, N, K, A, lda, a_mn, Bs, ldbs, ends, b_mn, split_k, Cm, ldc, R=None,
     g.C, g.ldc = Cm.data_ptr(), ldc
     g.R, g.ldr = (R.data_ptr() if R is not None else None), ldr
     g.num_sms = sms
+    g.kernel = kernel
     dc.check(dc.lib.dc_gemm(C.byref(g), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
 
@@ -75,48 +76,55 @@ def _mat(seed, r, c):
     return a, bf16_tensor(a)
 
 
+KERNELS = pytest.mark.parametrize("kernel", [1, 2], ids=["cta1", "cta_pair"])
+
+
+@KERNELS
 @pytest.mark.parametrize("M,N,K,sms", [(256, 512, 512, 0), (200, 264, 200, 0), (1024, 2048, 1024, 8),
-                                       (130, 8, 64, 0)])
-def test_gemm_forward_kmajor(M, N, K, sms):
+                                       (130, 8, 64, 0), (600, 776, 136, 6)])
+def test_gemm_forward_kmajor(M, N, K, sms, kernel):
     a, A = _mat(11, M, K)
     b, B = _mat(12, N, K)
     Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
-    _gemm(M, N, K, A, K, 0, [B], [K], [0], 0, 0, Cm, N, sms=sms)
+    _gemm(M, N, K, A, K, 0, [B], [K], [0], 0, 0, Cm, N, sms=sms, kernel=kernel)
     _check(Cm, a @ b.T, np.abs(a) @ np.abs(b).T, "fwd")
 
 
-def test_gemm_nsplit_segments_and_residual():
+@KERNELS
+def test_gemm_nsplit_segments_and_residual(kernel):
     M, K = 384, 320
     Ns = [256, 256, 512]
     a, A = _mat(21, M, K)
     bs = [_mat(22 + i, n, K) for i, n in enumerate(Ns)]
     r, R = _mat(30, M, sum(Ns))
     Cm = torch.empty(M, sum(Ns), dtype=torch.bfloat16, device="cuda")
-    _gemm(M, sum(Ns), K, A, K, 0, [x[1] for x in bs], [K] * 3, [1, 2, 4], 0, 0, Cm, sum(Ns), R=R, ldr=sum(Ns))
+    _gemm(M, sum(Ns), K, A, K, 0, [x[1] for x in bs], [K] * 3, [1, 2, 4], 0, 0, Cm, sum(Ns), R=R, ldr=sum(Ns), kernel=kernel)
     bcat = np.concatenate([x[0] for x in bs])
     ref = (a @ bcat.T) + r
     _check(Cm, ref, np.abs(a) @ np.abs(bcat).T + np.abs(r), "nsplit+res")
 
 
-def test_gemm_ksplit_mn_major_b():
+@KERNELS
+def test_gemm_ksplit_mn_major_b(kernel):
     """dX = dY W with W split along K (q|k|v): B stored [K_s][N] (N contiguous)."""
     M, N = 256, 512
     Ks = [128, 64, 192]
     a, A = _mat(41, M, sum(Ks))
     ws = [_mat(42 + i, k, N) for i, k in enumerate(Ks)]
     Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
-    _gemm(M, N, sum(Ks), A, sum(Ks), 0, [w[1] for w in ws], [N] * 3, [2, 3, 6], 1, 1, Cm, N)
+    _gemm(M, N, sum(Ks), A, sum(Ks), 0, [w[1] for w in ws], [N] * 3, [2, 3, 6], 1, 1, Cm, N, kernel=kernel)
     wcat = np.concatenate([w[0] for w in ws])
     _check(Cm, a @ wcat, np.abs(a) @ np.abs(wcat), "ksplit")
 
 
+@KERNELS
 @pytest.mark.parametrize("M,N,K,sms", [(384, 512, 296, 0), (512, 256, 1024, 4), (256, 256, 64, 0)])
-def test_gemm_dw_both_mn_major(M, N, K, sms):
+def test_gemm_dw_both_mn_major(M, N, K, sms, kernel):
     """dW = dY^T X: A stored [K][M], B stored [K][N]; A slice with lda > M."""
     dy, DY = _mat(51, K, M + 64)          # use columns [64, 64+M) via pointer offset
     x, X = _mat(52, K, N)
     Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
-    _gemm(M, N, K, DY[:, 64:], M + 64, 1, [X], [N], [0], 1, 0, Cm, N, sms=sms)
+    _gemm(M, N, K, DY[:, 64:], M + 64, 1, [X], [N], [0], 1, 0, Cm, N, sms=sms, kernel=kernel)
     ref = dy[:, 64:].T @ x
     _check(Cm, ref, np.abs(dy[:, 64:]).T @ np.abs(x), "dW")
 
