@@ -265,11 +265,7 @@ def main():
     tc = measure_tc(group, world, dev, torch, dist) if world > 1 else [[0, 0], [1 << 40, 0]]
     prof = rt.profile_json(st, tc=tc)
     if world > 1:   # element-wise MAX over ranks (reading D12)
-        vals = torch.tensor([[o["p_mem"], o["transient"], o["dur_us"]] for o in prof["ops"]], dtype=torch.int64,
-                            device=dev)
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX, group=group)
-        for o, v in zip(prof["ops"], vals.tolist()):
-            o["p_mem"], o["transient"], o["dur_us"] = v
+        prof = rt.max_reduce_profile(prof, group, device=dev)
     total = torch.cuda.get_device_properties(dev).total_memory
     M = int(0.9 * (total - 7 * GiB))
     passes = dc.DC_PASS_SHARD | (dc.DC_PASS_PREFETCH if "P" in args.passes else 0) | \

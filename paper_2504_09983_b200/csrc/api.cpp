@@ -457,6 +457,10 @@ extern "C" dc_status dc_offload(dc_ctx* c, int32_t fi, int32_t op, cudaStream_t 
       break;
     case DC_D2H_SYNC_FREE:
       DC_CUDA_TRY(cudaStreamWaitEvent(st, f.d2h, 0), &c->err);
+      // debug: the device slice is "freed" — poison it (all-ones = NaN) so a
+      // missing or misordered reload corrupts the update instead of passing
+      if (c->flags & DC_DEBUG_POISON)
+        DC_CUDA_TRY(cudaMemsetAsync(dev, 0xFF, f.elems * 4, st), &c->err);
       break;
     case DC_H2D_START:
       DC_CUDA_TRY(cudaMemcpyAsync(dev, host, f.elems * 4, cudaMemcpyHostToDevice, st), &c->err);

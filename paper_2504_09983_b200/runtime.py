@@ -55,7 +55,7 @@ def _alloc_symmetric(nbytes, group, device):
 
 
 def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr=1e-3, beta1=0.9,
-                 beta2=0.999, eps=1e-8, seed=0, init=True, host_pinned_bytes=0, spin_ms=20000):
+                 beta2=0.999, eps=1e-8, seed=0, init=True, host_pinned_bytes=0, spin_ms=20000, extra_flags=0):
     """Allocate and dc_init the ranks this process drives: all N virtual ranks,
     or this process's rank when `virtual` is False."""
     dev = torch.device("cuda", device)
@@ -101,7 +101,7 @@ def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr
         a.host_pinned_bytes = host_pinned_bytes
         a.lr, a.beta1, a.beta2, a.eps = lr, beta1, beta2, eps
         a.seed = seed
-        a.flags = (dc.DC_INIT_WEIGHTS if init else 0) | (dc.DC_VIRTUAL_RANKS if virtual else 0)
+        a.flags = (dc.DC_INIT_WEIGHTS if init else 0) | (dc.DC_VIRTUAL_RANKS if virtual else 0) | extra_flags
         a.spin_limit = spin_ms
         out = C.c_void_p()
         dc.check(dc.lib.dc_init(C.byref(a), C.byref(out)))
@@ -170,6 +170,38 @@ def bind(ranks, sched_by_rank, group=None):
         dc.check(dc.lib.dc_bind_schedule(st.ctx, st.sched, C.cast(arr, dc.p_u64), cap,
                                          st.streams[0].cuda_stream), st.ctx)
     torch.cuda.synchronize()
+
+
+def max_reduce_profile(prof, group, device="cpu"):
+    """Element-wise MAX of (p_mem, transient, dur_us) over the ranks of `group`
+    (reading D12: every rank must plan from the same profile, or the symmetric
+    arena and the flag protocol diverge).  Works over gloo (cpu) and nccl."""
+    import torch.distributed as dist
+    vals = torch.tensor([[o["p_mem"], o["transient"], o["dur_us"]] for o in prof["ops"]], dtype=torch.int64,
+                        device=device)
+    dist.all_reduce(vals, op=dist.ReduceOp.MAX, group=group)
+    out = json.loads(json.dumps(prof))
+    for o, v in zip(out["ops"], vals.tolist()):
+        o["p_mem"], o["transient"], o["dur_us"] = v
+    if out.get("tc"):
+        tcv = torch.tensor([t[1] for t in out["tc"]], dtype=torch.int64, device=device)
+        dist.all_reduce(tcv, op=dist.ReduceOp.MAX, group=group)
+        out["tc"] = [[t[0], int(v)] for t, v in zip(out["tc"], tcv.tolist())]
+    return out
+
+
+def plan_digest(sched_json):
+    import hashlib
+    return hashlib.sha256(sched_json.encode()).hexdigest()
+
+
+def offload_fragments(st, max_fragment_bytes):
+    """dc_offload_fragments -> planner fragment records {id, layer, bytes}."""
+    n = C.c_int32(0)
+    dc.check(dc.lib.dc_offload_fragments(st.ctx, max_fragment_bytes, None, C.byref(n)), st.ctx)
+    arr = (dc.Fragment * n.value)()
+    dc.check(dc.lib.dc_offload_fragments(st.ctx, max_fragment_bytes, arr, C.byref(n)), st.ctx)
+    return [dict(id=i, layer=f.layer, bytes=f.elems * 4) for i, f in enumerate(arr)]
 
 
 def profile_json(st, tc=None, frags=None):
