@@ -130,7 +130,7 @@ dc_status dc_grad_offset(const dc_ctx* ctx, int32_t param, int64_t* byte_offset)
  * no CUDA calls.  profile_json: the S_0 schedule with per-op p_mem (bytes
  * resident before the op, excluding Adam m and v), transient, dur_us, plus
  * params {id, bytes}, frags {id, layer, bytes} and the T_c table (schema:
- * DESIGN.md §6).  mem_budget = M.  Output: dc_schedule (immutable).
+ * DESIGN.md §11).  mem_budget = M.  Output: dc_schedule (immutable).
  * Errors: DC_EPROFILE (not an S_0 / malformed), DC_EINFEASIBLE.
  * ------------------------------------------------------------------------ */
 typedef struct {
