@@ -258,6 +258,12 @@ dc_status dc_model_loss_ptr(const dc_model* m, float** loss);
  * 2 a, 3 x2, 4 h2, 5 gate|up, 6 act, 7 y (layer output), 8 / 9 the two
  * backward gradient ping-pong buffers. */
 dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t which, void** ptr);
+/* Options: "fused_adam" (default 0; N = 1 only) — the reduce-scatter is the
+ * identity at N = 1, so each weight's Adam update (the rs_adam arithmetic on
+ * fp32(bf16(grad)), bit-identical) can run in the epilogue of its dW GEMM,
+ * leaving only the norm gains to rs_adam.  Ignored for a step whose schedule
+ * offloads optimizer state (the reload lands after the dW GEMMs). */
+dc_status dc_model_set_option(dc_model* m, const char* key, int64_t value);
 /* Number of kernels the last dc_model_step launched. */
 dc_status dc_model_launch_count(const dc_model* m, int64_t* n);
 

@@ -380,18 +380,34 @@ extern "C" dc_status dc_grad_slot_publish(dc_ctx* c, int32_t layer, cudaStream_t
   return DC_OK;
 }
 
-extern "C" dc_status dc_reduce_scatter_step(dc_ctx* c, int32_t layer, int32_t step_t, int32_t apply_update,
-                                            cudaStream_t st) {
-  if (!c || layer < 0 || layer >= c->L.n_layers) return fail(c, DC_EINVAL, "dc_reduce_scatter_step: bad layer");
-  if (!apply_update) return fail(c, DC_EINVAL, "dc_reduce_scatter_step: accumulate-only is not implemented");
-  if (step_t < 1) return fail(c, DC_EINVAL, "dc_reduce_scatter_step: step_t is 1-based");
+namespace dc {
+void ctx_adam_scalars(const dc_ctx* c, int step_t, EpiAdam* o) {
+  const double bc1 = 1.0 - std::pow(c->beta1, step_t);
+  const double bc2 = 1.0 - std::pow(c->beta2, step_t);
+  o->w1 = (float)(1.0 - c->beta1);
+  o->w2 = (float)(1.0 - c->beta2);
+  o->b2 = (float)c->beta2;
+  o->neg_s = -(float)(c->lr / bc1);
+  o->c = (float)std::sqrt(bc2);
+  o->eps = (float)c->eps;
+}
+
+void ctx_param_state(const dc_ctx* c, int p, float** master, float** m, float** v, void** shard) {
+  const int64_t o = c->L.store_off[p];
+  *master = c->master + o;
+  *m = c->m + o;
+  *v = c->v + o;
+  *shard = reinterpret_cast<uint16_t*>(c->shard) + o;
+}
+
+dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, const std::vector<int>& params, cudaStream_t st) {
   if (dc_status e = check_sticky(c)) return e;
   const int s = layer & 1;
   const int u = c->layer_use[layer];
   if (u == 0) return fail(c, DC_ESTATE, "dc_reduce_scatter_step: grad slot of layer never acquired");
   std::vector<RsMember> mem;
   int64_t elems = 0;
-  for (int i = c->L.layer_first[layer]; i < c->L.layer_first[layer] + c->L.layer_count[layer]; ++i) {
+  for (int i : params) {
     mem.push_back({c->L.goff[i], c->L.S[i], c->L.store_off[i]});
     elems += c->L.S[i];
   }
@@ -409,6 +425,17 @@ extern "C" dc_status dc_reduce_scatter_step(dc_ctx* c, int32_t layer, int32_t st
                           c->beta1, c->beta2, c->eps, ctas, c->timeout_ns, c->err_dev, st);
   if (r != DC_OK) return fail(c, r, "dc_reduce_scatter_step: launch failed");
   return DC_OK;
+}
+}  // namespace dc
+
+extern "C" dc_status dc_reduce_scatter_step(dc_ctx* c, int32_t layer, int32_t step_t, int32_t apply_update,
+                                            cudaStream_t st) {
+  if (!c || layer < 0 || layer >= c->L.n_layers) return fail(c, DC_EINVAL, "dc_reduce_scatter_step: bad layer");
+  if (!apply_update) return fail(c, DC_EINVAL, "dc_reduce_scatter_step: accumulate-only is not implemented");
+  if (step_t < 1) return fail(c, DC_EINVAL, "dc_reduce_scatter_step: step_t is 1-based");
+  std::vector<int> params;
+  for (int i = c->L.layer_first[layer]; i < c->L.layer_first[layer] + c->L.layer_count[layer]; ++i) params.push_back(i);
+  return reduce_scatter_params(c, layer, step_t, params, st);
 }
 
 // ------------------------------------------------------------------ offload

@@ -45,7 +45,24 @@ void sched_op(const dc_schedule* s, int i, int* kind, int* id, const int64_t** m
               int64_t* arena_off, int64_t* bytes, const int** posts, int* nposts, const int** waits, int* nwaits);
 enum { K_COMPUTE, K_AG, K_REL, K_RS, K_OFF, K_OFFSYNC, K_RELOAD, K_RELOADSYNC };
 
-dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* err);
+// Fused reduce-scatter + Adam epilogue (N = 1): the GEMM's C[row, col] is the
+// gradient of element row * N + col of one parameter.
+struct EpiAdam {
+  float* master;
+  float* m;
+  float* v;
+  void* shard;
+  float w1, w2, b2, neg_s, c, eps;
+};
+dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* err,
+                      const EpiAdam* adam = nullptr);
+// Adam scalars of step t from the ctx hyper-parameters (reading D18)
+void ctx_adam_scalars(const dc_ctx* c, int step_t, EpiAdam* out);
+// shard-store pointers of a param (fp32 master/m/v, bf16 shard) on this rank
+void ctx_param_state(const dc_ctx* c, int param, float** master, float** m, float** v, void** shard);
+// dc_reduce_scatter_step restricted to a subset of the layer's params
+dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, const std::vector<int>& params,
+                                cudaStream_t st);
 
 // ------------------------------------------------------------------ kernels
 // glue.cu

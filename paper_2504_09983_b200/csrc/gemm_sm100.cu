@@ -46,6 +46,15 @@ struct GemmParams {
   const __nv_bfloat16* R;
   int64_t ldr;
   uint32_t idesc;
+  // epilogue mode 1 (fused reduce-scatter + Adam at N = 1): C[row, col] is the
+  // gradient of element row * ldc + col of a parameter whose fp32 master/m/v
+  // and bf16 shard are given; Adam scalars as in rs_adam (reading D18)
+  int epi;
+  float* master;
+  float* m;
+  float* v;
+  __nv_bfloat16* shard;
+  float w1, w2, b2, neg_s, c, eps;
 };
 
 __device__ __forceinline__ int seg_of(const GemmParams& p, int idx) {
@@ -54,6 +63,105 @@ __device__ __forceinline__ int seg_of(const GemmParams& p, int idx) {
   for (int i = 0; i < 3; ++i)
     if (i + 1 < p.nseg && idx >= p.seg_end[i]) s = i + 1;
   return s;
+}
+
+
+// One 32-column chunk of an accumulator row (thread = row) -> global memory.
+// Mode 0: C = bf16(acc [+ R]).  Mode 1 (N = 1 fused reduce-scatter + Adam):
+// g = fp32(bf16(acc)) is exactly the value the grad slot would hold, x 1/N
+// (= 1), then the fp32 Adam step of rs_adam on master/m/v (same op order,
+// same intrinsics, no FMA) and the bf16 shard; nothing is written to C.
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int col0, const uint32_t (&v)[32]) {
+  float f[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+  const bool full = col0 + 32 <= p.N;
+  if (p.epi == 1) {
+    const int64_t e0 = (int64_t)row * p.ldc + col0;
+    if (full) {
+      float4 P[8], Mv[8], V[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        P[t] = reinterpret_cast<const float4*>(p.master + e0)[t];
+        Mv[t] = reinterpret_cast<const float4*>(p.m + e0)[t];
+        V[t] = reinterpret_cast<const float4*>(p.v + e0)[t];
+      }
+      uint4 sh[4];
+      __nv_bfloat162* s2 = reinterpret_cast<__nv_bfloat162*>(sh);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        float pp[4] = {P[t].x, P[t].y, P[t].z, P[t].w};
+        float mm[4] = {Mv[t].x, Mv[t].y, Mv[t].z, Mv[t].w};
+        float vv[4] = {V[t].x, V[t].y, V[t].z, V[t].w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float g = __bfloat162float(__float2bfloat16_rn(f[4 * t + u]));
+          const float mj = __fadd_rn(mm[u], __fmul_rn(p.w1, __fsub_rn(g, mm[u])));
+          const float vj = __fadd_rn(__fmul_rn(p.b2, vv[u]), __fmul_rn(__fmul_rn(p.w2, g), g));
+          const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(vj), p.c), p.eps);
+          pp[u] = __fadd_rn(pp[u], __fdiv_rn(__fmul_rn(p.neg_s, mj), d));
+          mm[u] = mj;
+          vv[u] = vj;
+        }
+        reinterpret_cast<float4*>(p.master + e0)[t] = make_float4(pp[0], pp[1], pp[2], pp[3]);
+        reinterpret_cast<float4*>(p.m + e0)[t] = make_float4(mm[0], mm[1], mm[2], mm[3]);
+        reinterpret_cast<float4*>(p.v + e0)[t] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+        s2[2 * t] = __floats2bfloat162_rn(pp[0], pp[1]);
+        s2[2 * t + 1] = __floats2bfloat162_rn(pp[2], pp[3]);
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) reinterpret_cast<uint4*>(p.shard + e0)[t] = sh[t];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (col0 + j >= p.N) continue;
+        const int64_t e = e0 + j;
+        const float g = __bfloat162float(__float2bfloat16_rn(f[j]));
+        const float mj = __fadd_rn(p.m[e], __fmul_rn(p.w1, __fsub_rn(g, p.m[e])));
+        const float vj = __fadd_rn(__fmul_rn(p.b2, p.v[e]), __fmul_rn(__fmul_rn(p.w2, g), g));
+        const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(vj), p.c), p.eps);
+        const float pj = __fadd_rn(p.master[e], __fdiv_rn(__fmul_rn(p.neg_s, mj), d));
+        p.master[e] = pj; p.m[e] = mj; p.v[e] = vj;
+        p.shard[e] = __float2bfloat16_rn(pj);
+      }
+    }
+    return;
+  }
+  __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
+  if (p.R) {
+    const __nv_bfloat16* rrow = p.R + (int64_t)row * p.ldr;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint4 rv = *reinterpret_cast<const uint4*>(rrow + col0 + j);
+        const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          float2 rf = __bfloat1622float2(r2[t]);
+          f[j + 2 * t] = __fadd_rn(f[j + 2 * t], rf.x);
+          f[j + 2 * t + 1] = __fadd_rn(f[j + 2 * t + 1], rf.y);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < p.N) f[j] = __fadd_rn(f[j], __bfloat162float(rrow[col0 + j]));
+    }
+  }
+  if (full) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint4 o;
+      __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) o2[t] = __floats2bfloat162_rn(f[j + 2 * t], f[j + 2 * t + 1]);
+      *reinterpret_cast<uint4*>(crow + col0 + j) = o;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col0 + j < p.N) crow[col0 + j] = __float2bfloat16_rn(f[j]);
+  }
 }
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -170,52 +278,13 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       ptx::tc_fence_after();
       const int row = mt * BM + q * 32 + lane;
       const bool row_ok = row < p.M;
-      __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
-      const __nv_bfloat16* rrow = p.R ? p.R + (int64_t)row * p.ldr : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
         ptx::tmem_ld_wait();
         const int col0 = nt * BN + c * 32;
-        if (row_ok && col0 < p.N) {
-          float f[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-          if (rrow) {
-            if (col0 + 32 <= p.N) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 8) {
-                uint4 rv = *reinterpret_cast<const uint4*>(rrow + col0 + j);
-                const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                  float2 rf = __bfloat1622float2(r2[t]);
-                  f[j + 2 * t] = __fadd_rn(f[j + 2 * t], rf.x);
-                  f[j + 2 * t + 1] = __fadd_rn(f[j + 2 * t + 1], rf.y);
-                }
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (col0 + j < p.N) f[j] = __fadd_rn(f[j], __bfloat162float(rrow[col0 + j]));
-            }
-          }
-          if (col0 + 32 <= p.N) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              uint4 o;
-              __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-              for (int t = 0; t < 4; ++t) o2[t] = __floats2bfloat162_rn(f[j + 2 * t], f[j + 2 * t + 1]);
-              *reinterpret_cast<uint4*>(crow + col0 + j) = o;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j < p.N) crow[col0 + j] = __float2bfloat16_rn(f[j]);
-          }
-        }
+        if (row_ok && col0 < p.N) epilogue_chunk(p, row, col0, v);
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -361,52 +430,13 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       ptx::tc_fence_after();
       const int row = mt * BM2 + (int)rank * 128 + q * 32 + lane;
       const bool row_ok = row < p.M;
-      __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
-      const __nv_bfloat16* rrow = p.R ? p.R + (int64_t)row * p.ldr : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN2 / 32; ++c) {
         uint32_t v[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN2 + c * 32, v);
         ptx::tmem_ld_wait();
         const int col0 = nt * BN2 + c * 32;
-        if (row_ok && col0 < p.N) {
-          float f[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-          if (rrow) {
-            if (col0 + 32 <= p.N) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 8) {
-                uint4 rv = *reinterpret_cast<const uint4*>(rrow + col0 + j);
-                const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                  float2 rf = __bfloat1622float2(r2[t]);
-                  f[j + 2 * t] = __fadd_rn(f[j + 2 * t], rf.x);
-                  f[j + 2 * t + 1] = __fadd_rn(f[j + 2 * t + 1], rf.y);
-                }
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (col0 + j < p.N) f[j] = __fadd_rn(f[j], __bfloat162float(rrow[col0 + j]));
-            }
-          }
-          if (col0 + 32 <= p.N) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              uint4 o;
-              __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-              for (int t = 0; t < 4; ++t) o2[t] = __floats2bfloat162_rn(f[j + 2 * t], f[j + 2 * t + 1]);
-              *reinterpret_cast<uint4*>(crow + col0 + j) = o;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j < p.N) crow[col0 + j] = __float2bfloat16_rn(f[j]);
-          }
-        }
+        if (row_ok && col0 < p.N) epilogue_chunk(p, row, col0, v);
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -462,7 +492,7 @@ static int num_sms_cached() {
   return n;
 }
 
-dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* err) {
+dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* err, const EpiAdam* adam) {
   if (g->M <= 0 || g->N <= 0 || g->K <= 0 || (g->N % 8) || (g->K % 8) || g->n_bseg < 1 || g->n_bseg > 4) {
     *err = "dc_gemm: M,N,K must be > 0, N and K multiples of 8, 1..4 B segments";
     return DC_EINVAL;
@@ -483,6 +513,13 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
   p.a_mn = g->a_mn_major; p.b_mn = g->b_mn_major;
   p.C = reinterpret_cast<__nv_bfloat16*>(g->C); p.ldc = g->ldc;
   p.R = reinterpret_cast<const __nv_bfloat16*>(g->R); p.ldr = g->ldr;
+  if (adam) {
+    if (g->ldc != g->N || g->R) { *err = "dc_gemm: fused Adam epilogue needs ldc == N and no residual"; return DC_EINVAL; }
+    p.epi = 1;
+    p.master = adam->master; p.m = adam->m; p.v = adam->v;
+    p.shard = reinterpret_cast<__nv_bfloat16*>(adam->shard);
+    p.w1 = adam->w1; p.w2 = adam->w2; p.b2 = adam->b2; p.neg_s = adam->neg_s; p.c = adam->c; p.eps = adam->eps;
+  }
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a_mn << 15) | ((uint32_t)p.b_mn << 16) |
             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(tm >> 4) << 24);
   CUtensorMap mA, mB[4];

@@ -67,6 +67,9 @@ struct dc_model {
   int64_t launches = 0;
   int cur_d = 0;                     // which of dA/dB holds dL/d(layer output)
   bool profile_pending = false;      // per-op events recorded, not yet read
+  bool fused_adam = false;           // N = 1: Adam in the dW GEMM epilogues (option)
+  bool fused_active = false;         // ... and the bound schedule has no offload
+  int step_t = 0;
   std::string err;
 
   int pid(int layer, int slot) const { return ctx_layout(ctx).layer_first[layer] + slot; }
@@ -172,6 +175,9 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   m->ws_bytes = off - ws0;
   m->act_bytes = off;
   build_s0(m.get());
+  // opt-in (dc_model_set_option): bit-identical, but the epilogue becomes
+  // HBM-bound and slows the dW GEMMs more than it saves (profiles/r01)
+  m->fused_adam = false;
   const size_t n = m->s0.size();
   m->dur_us.assign(n, 0);
   m->p_mem.assign(n, 0);
@@ -220,7 +226,7 @@ extern "C" dc_status dc_model_bind(dc_model* m, void* buf, uint64_t bytes, const
 static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t lda, int a_mn,
                       std::initializer_list<const void*> Bs, std::initializer_list<int64_t> ldbs,
                       std::initializer_list<int> ends, int b_mn, int split_k, void* C, int64_t ldc,
-                      const void* R, int64_t ldr, cudaStream_t st) {
+                      const void* R, int64_t ldr, cudaStream_t st, const EpiAdam* adam = nullptr) {
   dc_gemm_args g{};
   g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.a_mn_major = a_mn;
   int i = 0;
@@ -233,7 +239,7 @@ static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t l
   g.b_mn_major = b_mn; g.b_split_k = split_k;
   g.C = C; g.ldc = ldc; g.R = R; g.ldr = ldr;
   std::string err;
-  dc_status s = launch_gemm(&g, st, &err);
+  dc_status s = launch_gemm(&g, st, &err, adam);
   if (s != DC_OK) return mfail(m, s, err);
   return DC_OK;
 }
@@ -252,6 +258,15 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
     int64_t b = 0;
     dc_grad_offset(m->ctx, m->pid(l, slot), &b);
     return reinterpret_cast<uint8_t*>(gslot) + b;
+  };
+  // fused reduce-scatter + Adam in the dW epilogue (N = 1): the update of the
+  // param's shard replaces the grad-slot write
+  EpiAdam epi{};
+  auto ADAM = [&](int slot) -> const EpiAdam* {
+    if (!m->fused_active) return nullptr;
+    ctx_adam_scalars(m->ctx, m->step_t, &epi);
+    ctx_param_state(m->ctx, m->pid(l, slot), &epi.master, &epi.m, &epi.v, &epi.shard);
+    return &epi;
   };
   dc_status s = DC_OK;
   switch (o.code) {
@@ -293,7 +308,7 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       // dact = dy Wd  (A K-major [T,H]; B = Wd [H rows = K][F] MN-major)
       s = gemm(m, T, F, H, dcur, H, 0, {m->W(l, P_DOWN)}, {F}, {F / 256}, 1, 0, m->A(m->ws_dact), F, nullptr, 0, st);
       if (s == DC_OK)  // dWd = dy^T act : A = dy stored [T][H] (MN-major), B = act [T][F] (MN-major)
-        s = gemm(m, H, F, T, dcur, H, 1, {m->A(a.act)}, {F}, {F / 256}, 1, 0, G(P_DOWN), F, nullptr, 0, st);
+        s = gemm(m, H, F, T, dcur, H, 1, {m->A(a.act)}, {F}, {F / 256}, 1, 0, G(P_DOWN), F, nullptr, 0, st, ADAM(P_DOWN));
       break;
     case B_ACT:
       k_act_bwd(m->A(m->ws_dact), m->A(a.gu), m->A(m->ws_dgu), T, F, st);
@@ -303,10 +318,10 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       s = gemm(m, T, H, 2 * F, m->A(m->ws_dgu), 2 * F, 0, {m->W(l, P_GATE), m->W(l, P_UP)}, {H, H},
                {F / 64, 2 * F / 64}, 1, 1, m->A(m->ws_dh), H, nullptr, 0, st);
       if (s == DC_OK)
-        s = gemm(m, F, H, T, m->A(m->ws_dgu), 2 * F, 1, {m->A(a.h2)}, {H}, {H / 256}, 1, 0, G(P_GATE), H, nullptr, 0, st);
+        s = gemm(m, F, H, T, m->A(m->ws_dgu), 2 * F, 1, {m->A(a.h2)}, {H}, {H / 256}, 1, 0, G(P_GATE), H, nullptr, 0, st, ADAM(P_GATE));
       if (s == DC_OK)
         s = gemm(m, F, H, T, m->A(m->ws_dgu) + (int64_t)F * 2, 2 * F, 1, {m->A(a.h2)}, {H}, {H / 256}, 1, 0, G(P_UP),
-                 H, nullptr, 0, st);
+                 H, nullptr, 0, st, ADAM(P_UP));
       break;
     case B_MLP_NORM: {
       const int nb = rmsnorm_bwd_blocks(T);
@@ -320,7 +335,7 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       s = gemm(m, T, qd, H, m->A(m->ws_dx2), H, 0, {m->W(l, P_O)}, {qd}, {qd / 256}, 1, 0, m->A(m->ws_dqkv), qkvd,
                nullptr, 0, st);
       if (s == DC_OK)
-        s = gemm(m, H, qd, T, m->A(m->ws_dx2), H, 1, {m->A(a.a)}, {qd}, {qd / 256}, 1, 0, G(P_O), qd, nullptr, 0, st);
+        s = gemm(m, H, qd, T, m->A(m->ws_dx2), H, 1, {m->A(a.a)}, {qd}, {qd / 256}, 1, 0, G(P_O), qd, nullptr, 0, st, ADAM(P_O));
       break;
     case B_ATTN_MIX:
       k_attn_mix_bwd(m->A(m->ws_dqkv), m->A(a.qkv), T, qd, kvd, m->d.head_dim, m->grp, st);
@@ -329,13 +344,13 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       s = gemm(m, T, H, qkvd, m->A(m->ws_dqkv), qkvd, 0, {m->W(l, P_Q), m->W(l, P_K), m->W(l, P_V)}, {H, H, H},
                {qd / 64, (qd + kvd) / 64, qkvd / 64}, 1, 1, m->A(m->ws_dh), H, nullptr, 0, st);
       if (s == DC_OK)
-        s = gemm(m, qd, H, T, m->A(m->ws_dqkv), qkvd, 1, {m->A(a.h1)}, {H}, {H / 256}, 1, 0, G(P_Q), H, nullptr, 0, st);
+        s = gemm(m, qd, H, T, m->A(m->ws_dqkv), qkvd, 1, {m->A(a.h1)}, {H}, {H / 256}, 1, 0, G(P_Q), H, nullptr, 0, st, ADAM(P_Q));
       if (s == DC_OK)
         s = gemm(m, kvd, H, T, m->A(m->ws_dqkv) + (int64_t)qd * 2, qkvd, 1, {m->A(a.h1)}, {H}, {H / 256}, 1, 0, G(P_K),
-                 H, nullptr, 0, st);
+                 H, nullptr, 0, st, ADAM(P_K));
       if (s == DC_OK)
         s = gemm(m, kvd, H, T, m->A(m->ws_dqkv) + (int64_t)(qd + kvd) * 2, qkvd, 1, {m->A(a.h1)}, {H}, {H / 256}, 1,
-                 0, G(P_V), H, nullptr, 0, st);
+                 0, G(P_V), H, nullptr, 0, st, ADAM(P_V));
       break;
     case B_ATTN_NORM: {
       const int nb = rmsnorm_bwd_blocks(T);
@@ -456,6 +471,18 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
   if (!sc) return mfail(m, DC_ESTATE, "dc_model_step: no schedule bound");
   const int64_t l0 = launch_count();
   const int N = ctx_world(m->ctx);
+  if (step_t < 1) return mfail(m, DC_EINVAL, "dc_model_step: step_t is 1-based");
+  m->step_t = step_t;
+  // an offloaded fragment is reloaded before its layer's RS op (reading D17),
+  // i.e. after the dW GEMMs: the fused update needs every state resident
+  m->fused_active = m->fused_adam;
+  for (int i = 0, n = sched_num_ops(sc); i < n && m->fused_active; ++i) {
+    int kind, id, nm, np, nw;
+    const int64_t* mem; const int* posts; const int* waits;
+    int64_t off, bytes;
+    sched_op(sc, i, &kind, &id, &mem, &nm, &off, &bytes, &posts, &np, &waits, &nw);
+    if (kind >= K_OFF) m->fused_active = false;
+  }
   dc_status s = dc_step_begin(m->ctx, ++m->epoch, cs);
   if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
   // streams must not run ahead of the previous step's tail on the compute stream
@@ -503,7 +530,10 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
         cudaEventRecord(m->ev_pos[id], cs);
         cudaStreamWaitEvent(rss, m->ev_pos[id], 0);
         if (profile) cudaEventRecord(m->ev_t0[id], rss);
-        s = dc_reduce_scatter_step(m->ctx, o.layer, step_t, 1, rss);
+        if (m->fused_active)   // the weights were updated in their dW epilogues; the norm gains remain
+          s = reduce_scatter_params(m->ctx, o.layer, step_t, {m->pid(o.layer, P_G1), m->pid(o.layer, P_G2)}, rss);
+        else
+          s = dc_reduce_scatter_step(m->ctx, o.layer, step_t, 1, rss);
         if (profile) cudaEventRecord(m->ev_t1[id], rss);
         break;
       }
@@ -555,6 +585,16 @@ extern "C" dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t 
   if (which < 0 || which >= 10) return mfail(nullptr, DC_EINVAL, "dc_model_act_ptr: which in [0, 10)");
   *p = m->A(offs[which]);
   return DC_OK;
+}
+
+extern "C" dc_status dc_model_set_option(dc_model* m, const char* key, int64_t value) {
+  if (!m || !key) return mfail(nullptr, DC_EINVAL, "dc_model_set_option: null argument");
+  if (!strcmp(key, "fused_adam")) {
+    if (value && ctx_world(m->ctx) != 1) return mfail(m, DC_EINVAL, "fused_adam needs N == 1");
+    m->fused_adam = value != 0;
+    return DC_OK;
+  }
+  return mfail(m, DC_EINVAL, std::string("dc_model_set_option: unknown key ") + key);
 }
 
 extern "C" dc_status dc_model_launch_count(const dc_model* m, int64_t* n) {

@@ -114,6 +114,7 @@ _sig = {
     "dc_model_loss_ptr": (C.c_int, [vp, C.POINTER(p_f32)]),
     "dc_model_act_ptr": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(vp)]),
     "dc_model_launch_count": (C.c_int, [vp, p_i64]),
+    "dc_model_set_option": (C.c_int, [vp, C.c_char_p, C.c_int64]),
 }
 EXPORTS = tuple(_sig)
 for _name, (_res, _args) in _sig.items():

@@ -27,7 +27,7 @@ from paper_2504_09983_b200 import runtime as rt  # noqa: E402
 LR = 1e-3
 
 
-def _setup(cfg, world, passes, M=1 << 40, prefetch=1 << 22):
+def _setup(cfg, world, passes, M=1 << 40, prefetch=1 << 22, fused=None):
     table = synth.llama_param_table(cfg)
     ranks = rt.create_ranks(table, world, lr=LR)
     xs, ts = {}, {}
@@ -35,6 +35,9 @@ def _setup(cfg, world, passes, M=1 << 40, prefetch=1 << 22):
         x, t = ost.rank_batch(cfg, r)
         xs[r], ts[r] = bf16_tensor(x), bf16_tensor(t)
     rt.attach_model(ranks, cfg, xs, ts)
+    if fused is not None:
+        for st in ranks.values():
+            dc.check(dc.lib.dc_model_set_option(st.model, b"fused_adam", int(fused)))
     prof = rt.profile_json(ranks[0], tc=[[4096, 10], [1 << 20, 20], [1 << 26, 400]])
     sched = dc.plan(json.dumps(prof), M, M_prefetch=prefetch, passes=passes, strict=True)
     rt.bind(ranks, {r: sched for r in ranks})
@@ -45,12 +48,12 @@ def _loss(st):
     return rt.view(rt.loss_ptr(st), 1, torch.float32).item()
 
 
-@pytest.mark.parametrize("world,passes", [(1, dc.DC_PASS_SHARD),
-                                          (2, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH),
-                                          (2, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD)])
-def test_step_matches_oracle(world, passes):
+@pytest.mark.parametrize("world,passes,fused", [(1, dc.DC_PASS_SHARD, 0), (1, dc.DC_PASS_SHARD, 1),
+                                                (2, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH, 0),
+                                                (2, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD, 0)])
+def test_step_matches_oracle(world, passes, fused):
     cfg = synth.small_llama(layers=2, seq=256)
-    table, ranks = _setup(cfg, world, passes)
+    table, ranks = _setup(cfg, world, passes, fused=fused)
     oracle = ost.ShardedState(table, world, bf16=True)
     o_losses, o_grads = ost.sharded_step(oracle, cfg, lr=LR)
     # per-rank layer outputs from the oracle (same gathered weights on every rank)
@@ -64,8 +67,8 @@ def test_step_matches_oracle(world, passes):
             slot = C.c_void_p()
             dc.check(dc.lib.dc_grad_slot(st.ctx, layer, C.byref(slot)), st.ctx)
             for i, p in enumerate(table):
-                if p.layer != layer:
-                    continue
+                if p.layer != layer or (fused and not p.name.endswith("norm")):
+                    continue                 # fused: weight grads never reach the slot
                 S = nx.shard_len(p.numel, world)
                 got = to_np(rt.view(slot.value + rt.grad_offset(st, i), world * S, torch.bfloat16))
                 ref = o_grads[r][i]
@@ -116,3 +119,20 @@ def test_layer_outputs_and_two_steps():
     n = C.c_int64()
     dc.check(dc.lib.dc_model_launch_count(st.model, C.byref(n)))
     assert n.value > 20
+
+
+def test_fused_adam_bitexact_vs_rs_adam():
+    """N = 1: Adam in the dW epilogue == grad slot + rs_adam, bit for bit."""
+    cfg = synth.small_llama(layers=2, seq=256)
+    _, a = _setup(cfg, 1, dc.DC_PASS_SHARD, fused=1)
+    _, b = _setup(cfg, 1, dc.DC_PASS_SHARD, fused=0)
+    for t in (1, 2, 3):
+        rt.step(a, t)
+        rt.step(b, t)
+        torch.cuda.synchronize()
+        for k in ("master", "m", "v", "shard"):
+            x, y = a[0].tensors[k], b[0].tensors[k]
+            assert torch.equal(x.view(torch.int16) if k == "shard" else x.view(torch.int32),
+                               y.view(torch.int16) if k == "shard" else y.view(torch.int32)), (t, k)
+        assert _loss(a[0]) == _loss(b[0])
+    assert dc.lib.dc_model_set_option(a[0].model, b"nope", 1) == dc.DC_EINVAL
