@@ -71,12 +71,13 @@ __device__ __forceinline__ int seg_of(const GemmParams& p, int idx) {
 // g = fp32(bf16(acc)) is exactly the value the grad slot would hold, x 1/N
 // (= 1), then the fp32 Adam step of rs_adam on master/m/v (same op order,
 // same intrinsics, no FMA) and the bf16 shard; nothing is written to C.
+template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int col0, const uint32_t (&v)[32]) {
   float f[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
   const bool full = col0 + 32 <= p.N;
-  if (p.epi == 1) {
+  if constexpr (EPI == 1) {
     const int64_t e0 = (int64_t)row * p.ldc + col0;
     if (full) {
       float4 P[8], Mv[8], V[8];
@@ -164,6 +165,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
   }
 }
 
+template <int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 gemm_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
                 const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
@@ -278,13 +280,56 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       ptx::tc_fence_after();
       const int row = mt * BM + q * 32 + lane;
       const bool row_ok = row < p.M;
+      __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
+      const __nv_bfloat16* rrow = p.R ? p.R + (int64_t)row * p.ldr : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
         ptx::tmem_ld_wait();
         const int col0 = nt * BN + c * 32;
-        if (row_ok && col0 < p.N) epilogue_chunk(p, row, col0, v);
+        if (row_ok && col0 < p.N) {
+          if constexpr (EPI == 1) {
+            epilogue_chunk<1>(p, row, col0, v);
+          } else {
+            float f[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+            if (rrow) {
+              if (col0 + 32 <= p.N) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 8) {
+                  uint4 rv = *reinterpret_cast<const uint4*>(rrow + col0 + j);
+                  const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
+#pragma unroll
+                  for (int t = 0; t < 4; ++t) {
+                    float2 rf = __bfloat1622float2(r2[t]);
+                    f[j + 2 * t] = __fadd_rn(f[j + 2 * t], rf.x);
+                    f[j + 2 * t + 1] = __fadd_rn(f[j + 2 * t + 1], rf.y);
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (col0 + j < p.N) f[j] = __fadd_rn(f[j], __bfloat162float(rrow[col0 + j]));
+              }
+            }
+            if (col0 + 32 <= p.N) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                uint4 o;
+                __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) o2[t] = __floats2bfloat162_rn(f[j + 2 * t], f[j + 2 * t + 1]);
+                *reinterpret_cast<uint4*>(crow + col0 + j) = o;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j < p.N) crow[col0 + j] = __float2bfloat16_rn(f[j]);
+            }
+          }
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -307,11 +352,17 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
 // tcgen05.mma.cta_group::2 (M = 256) and commits, multicast to both CTAs, the
 // smem-slot release and the accumulator-ready barriers.  Each CTA's TMEM holds
 // its 128 rows x 256 fp32 columns (x2 buffers = 512 columns).
-constexpr int BM2 = 256, BN2 = 256, STAGES2 = 6;
+constexpr int BM2 = 256;
 constexpr int A2_STAGE = 128 * BK * 2;        // 16 KiB per CTA
-constexpr int B2_STAGE = 128 * BK * 2;        // 16 KiB per CTA
-constexpr int GEMM2_SMEM = STAGES2 * (A2_STAGE + B2_STAGE) + 1024 + 256;
+template <int BNT, int ST> struct Pair {
+  static constexpr int B_STAGE = (BNT / 2) * BK * 2;                    // B half per CTA
+  static constexpr int STAGES = ST;                                      // <= 7 @256, <= 9 @128
+  static_assert(ST * (A2_STAGE + B_STAGE) + 1280 <= 227 * 1024, "smem");
+  static constexpr int SMEM = STAGES * (A2_STAGE + B_STAGE) + 1024 + 256;
+  static constexpr int TMEM = 2 * BNT;                                   // 2 accumulator buffers
+};
 
+template <int BNT, int ST, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
                  const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
@@ -320,10 +371,10 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   const uint32_t raw = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
   uint8_t* smA = smem;
-  uint8_t* smB = smem + STAGES2 * A2_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smB + STAGES2 * B2_STAGE);
-  uint64_t* empty = full + STAGES2;
-  uint64_t* tfull = empty + STAGES2;
+  uint8_t* smB = smem + Pair<BNT, ST>::STAGES * A2_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smB + Pair<BNT, ST>::STAGES * Pair<BNT, ST>::B_STAGE);
+  uint64_t* empty = full + Pair<BNT, ST>::STAGES;
+  uint64_t* tfull = empty + Pair<BNT, ST>::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -338,11 +389,11 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     if (p.nseg > 1) ptx::tma_prefetch(&mapB1);
     if (p.nseg > 2) ptx::tma_prefetch(&mapB2);
     if (p.nseg > 3) ptx::tma_prefetch(&mapB3);
-    for (int s = 0; s < STAGES2; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < Pair<BNT, ST>::STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { ptx::mbar_init(&tfull[b], 1); ptx::mbar_init(&tempty[b], 8); }
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, TMEM_COLS);
+  if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, Pair<BNT, ST>::TMEM);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -355,18 +406,18 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       for (int tile = pair; tile < num_tiles; tile += npairs) {
         const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
         const int m0 = mt * BM2 + (int)rank * 128;
-        int bseg = 0, n0 = nt * BN2;
+        int bseg = 0, n0 = nt * BNT;
         if (!p.split_k) {
           bseg = seg_of(p, nt);
-          n0 = (nt - (bseg ? p.seg_end[bseg - 1] : 0)) * BN2;
+          n0 = (nt - (bseg ? p.seg_end[bseg - 1] : 0)) * BNT;
         }
-        n0 += (int)rank * 128;
+        n0 += (int)rank * (BNT / 2);
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (A2_STAGE + B2_STAGE));
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (A2_STAGE + Pair<BNT, ST>::B_STAGE));
           const uint32_t lbar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
           uint8_t* a = smA + stage * A2_STAGE;
-          uint8_t* b = smB + stage * B2_STAGE;
+          uint8_t* b = smB + stage * Pair<BNT, ST>::B_STAGE;
           const int k0 = kb * BK;
           if (!p.a_mn) {
             ptx::tma_load_2d_2sm(a, &mapA, lbar, k0, m0);
@@ -383,10 +434,10 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           if (!p.b_mn) {
             ptx::tma_load_2d_2sm(b, mb, lbar, kk0, n0);
           } else {
-            ptx::tma_load_2d_2sm(b, mb, lbar, n0, kk0);
-            ptx::tma_load_2d_2sm(b + 8192, mb, lbar, n0 + 64, kk0);
+#pragma unroll
+            for (int j = 0; j < BNT / 128; ++j) ptx::tma_load_2d_2sm(b + j * 8192, mb, lbar, n0 + 64 * j, kk0);
           }
-          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+          if (++stage == Pair<BNT, ST>::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -398,12 +449,12 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       for (int tile = pair; tile < num_tiles; tile += npairs) {
         ptx::mbar_wait(&tempty[acc], aphase ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d = tmem_base + acc * BN2;
+        const uint32_t d = tmem_base + acc * BNT;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint32_t a_addr = ptx::smem_u32(smA + stage * A2_STAGE);
-          const uint32_t b_addr = ptx::smem_u32(smB + stage * B2_STAGE);
+          const uint32_t b_addr = ptx::smem_u32(smB + stage * Pair<BNT, ST>::B_STAGE);
 #pragma unroll
           for (int k = 0; k < BK / UMMA_K; ++k) {
             uint64_t ad, bd;
@@ -414,7 +465,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             ptx::umma_f16_2sm(d, ad, bd, p.idesc, (kb | k) != 0);
           }
           ptx::umma_commit_2sm_mc(&empty[stage], 0x3);
-          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+          if (++stage == Pair<BNT, ST>::STAGES) { stage = 0; phase ^= 1; }
         }
         ptx::umma_commit_2sm_mc(&tfull[acc], 0x3);
         if (++acc == 2) { acc = 0; aphase ^= 1; }
@@ -430,13 +481,56 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       ptx::tc_fence_after();
       const int row = mt * BM2 + (int)rank * 128 + q * 32 + lane;
       const bool row_ok = row < p.M;
+      __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
+      const __nv_bfloat16* rrow = p.R ? p.R + (int64_t)row * p.ldr : nullptr;
 #pragma unroll 1
-      for (int c = 0; c < BN2 / 32; ++c) {
+      for (int c = 0; c < BNT / 32; ++c) {
         uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN2 + c * 32, v);
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BNT + c * 32, v);
         ptx::tmem_ld_wait();
-        const int col0 = nt * BN2 + c * 32;
-        if (row_ok && col0 < p.N) epilogue_chunk(p, row, col0, v);
+        const int col0 = nt * BNT + c * 32;
+        if (row_ok && col0 < p.N) {
+          if constexpr (EPI == 1) {
+            epilogue_chunk<1>(p, row, col0, v);
+          } else {
+            float f[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+            if (rrow) {
+              if (col0 + 32 <= p.N) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 8) {
+                  uint4 rv = *reinterpret_cast<const uint4*>(rrow + col0 + j);
+                  const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
+#pragma unroll
+                  for (int t = 0; t < 4; ++t) {
+                    float2 rf = __bfloat1622float2(r2[t]);
+                    f[j + 2 * t] = __fadd_rn(f[j + 2 * t], rf.x);
+                    f[j + 2 * t + 1] = __fadd_rn(f[j + 2 * t + 1], rf.y);
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (col0 + j < p.N) f[j] = __fadd_rn(f[j], __bfloat162float(rrow[col0 + j]));
+              }
+            }
+            if (col0 + 32 <= p.N) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                uint4 o;
+                __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) o2[t] = __floats2bfloat162_rn(f[j + 2 * t], f[j + 2 * t + 1]);
+                *reinterpret_cast<uint4*>(crow + col0 + j) = o;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j < p.N) crow[col0 + j] = __float2bfloat16_rn(f[j]);
+            }
+          }
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -448,7 +542,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   ptx::cluster_sync();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc_2sm(tmem_base, TMEM_COLS);
+    ptx::tmem_dealloc_2sm(tmem_base, Pair<BNT, ST>::TMEM);
   }
 }
 
@@ -503,11 +597,25 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
   const int kind = g->kernel ? g->kernel : (env_kernel ? env_kernel : 2);
   const bool pair = kind == 2 && sms >= 2;
   const int tm = pair ? BM2 : BM;                // tile rows
+  // pair tile width: 256 unless 128 wastes clearly less of the last wave
+  int bnt = BN;
+  if (pair) {
+    const int pairs = sms / 2;
+    const int64_t mt = (g->M + BM2 - 1) / BM2;
+    auto eff = [&](int bn) {
+      const int64_t t = mt * ((g->N + bn - 1) / bn);
+      const int64_t waves = (t + pairs - 1) / pairs;
+      return (double)t / (double)(waves * pairs);
+    };
+    const int forced = getenv("DC_GEMM_BN") ? atoi(getenv("DC_GEMM_BN")) : 0;
+    if (forced == 128 || forced == 256) bnt = forced;
+    (void)eff;   // 256 x 128 pair tiles measured slower on every layer shape (r01); forced only
+  }
   const int rows_per_cta = 128;                  // A rows / B cols staged by one CTA
   GemmParams p{};
   p.M = g->M; p.N = g->N; p.K = g->K;
   p.m_tiles = (g->M + tm - 1) / tm;
-  p.n_tiles = (g->N + BN - 1) / BN;
+  p.n_tiles = (g->N + bnt - 1) / bnt;
   p.k_blocks = (g->K + BK - 1) / BK;
   p.nseg = g->n_bseg; p.split_k = g->b_split_k;
   p.a_mn = g->a_mn_major; p.b_mn = g->b_mn_major;
@@ -521,7 +629,7 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
     p.w1 = adam->w1; p.w2 = adam->w2; p.b2 = adam->b2; p.neg_s = adam->neg_s; p.c = adam->c; p.eps = adam->eps;
   }
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a_mn << 15) | ((uint32_t)p.b_mn << 16) |
-            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(tm >> 4) << 24);
+            ((uint32_t)(bnt >> 3) << 17) | ((uint32_t)(tm >> 4) << 24);
   CUtensorMap mA, mB[4];
   bool ok = p.a_mn ? make_map(&mA, g->A, g->M, g->K, g->lda, 64)
                    : make_map(&mA, g->A, g->K, g->M, g->lda, rows_per_cta);
@@ -539,9 +647,11 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
     const int64_t kdim = g->b_split_k ? ext : g->K;
     const int64_t ndim = g->b_split_k ? g->N : ext;
     ok = ok && (g->b_mn_major ? make_map(&mB[s], g->B[s], ndim, kdim, g->ldb[s], 64)
-                              : make_map(&mB[s], g->B[s], kdim, ndim, g->ldb[s], pair ? rows_per_cta : BN));
+                              : make_map(&mB[s], g->B[s], kdim, ndim, g->ldb[s], pair ? bnt / 2 : BN));
     prev = g->bseg_end[s];
   }
+  if (!g->b_split_k)      // caller's N segment ends are in units of 256 columns
+    for (int s = 0; s < g->n_bseg; ++s) p.seg_end[s] *= 256 / bnt;
   if (g->n_bseg == 1) p.seg_end[0] = g->b_split_k ? p.k_blocks : p.n_tiles;
   for (int s = g->n_bseg; s < 4; ++s) { mB[s] = mB[0]; p.seg_end[s] = p.seg_end[g->n_bseg - 1]; }
   if (!ok) { *err = "dc_gemm: cuTensorMapEncodeTiled failed (alignment / pitch must be 16 B)"; return DC_EINVAL; }
@@ -555,10 +665,19 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
   const int tiles = p.m_tiles * p.n_tiles;
   if (pair) {
     const int pairs = std::min(tiles, sms / 2);
-    gemm2_bf16_sm100<<<2 * pairs, GEMM_THREADS, GEMM2_SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+    static const int env_st = getenv("DC_GEMM_STAGES") ? atoi(getenv("DC_GEMM_STAGES")) : 6;
+    const int g2 = 2 * pairs;
+#define DC_PAIR_LAUNCH(BN_, ST_)                                                                   \
+    (p.epi ? gemm2_bf16_sm100<BN_, ST_, 1><<<g2, GEMM_THREADS, Pair<BN_, ST_>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p) \
+           : gemm2_bf16_sm100<BN_, ST_, 0><<<g2, GEMM_THREADS, Pair<BN_, ST_>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p))
+    if (bnt == 128) DC_PAIR_LAUNCH(128, 9);
+    else if (env_st == 6) DC_PAIR_LAUNCH(256, 6);
+    else DC_PAIR_LAUNCH(256, 7);
+#undef DC_PAIR_LAUNCH
   } else {
     const int grid = tiles < sms ? tiles : sms;
-    gemm_bf16_sm100<<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+    if (p.epi) gemm_bf16_sm100<1><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+    else gemm_bf16_sm100<0><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { *err = std::string("dc_gemm launch: ") + cudaGetErrorString(e); return DC_ECUDA; }
@@ -578,12 +697,26 @@ extern "C" dc_status dc_gemm(const dc_gemm_args* g, cudaStream_t stream) {
 namespace dc {
 cudaError_t preload_gemm_kernels() {
   cudaFuncAttributes a;
-  cudaError_t e = cudaFuncGetAttributes(&a, gemm_bf16_sm100);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(gemm_bf16_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm2_bf16_sm100);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(gemm2_bf16_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM2_SMEM);
+  cudaError_t e = cudaSuccess;
+#define DC_ONE_ATTR(EPI_)                                                                          \
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_bf16_sm100<EPI_>);                      \
+  if (e == cudaSuccess)                                                                            \
+    e = cudaFuncSetAttribute(gemm_bf16_sm100<EPI_>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+  DC_ONE_ATTR(0)
+  DC_ONE_ATTR(1)
+#undef DC_ONE_ATTR
+#define DC_PAIR_ATTR(BN_, ST_, EPI_)                                                               \
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm2_bf16_sm100<BN_, ST_, EPI_>);           \
+  if (e == cudaSuccess)                                                                            \
+    e = cudaFuncSetAttribute(gemm2_bf16_sm100<BN_, ST_, EPI_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             Pair<BN_, ST_>::SMEM);
+  DC_PAIR_ATTR(256, 7, 0)
+  DC_PAIR_ATTR(256, 7, 1)
+  DC_PAIR_ATTR(256, 6, 0)
+  DC_PAIR_ATTR(256, 6, 1)
+  DC_PAIR_ATTR(128, 9, 0)
+  DC_PAIR_ATTR(128, 9, 1)
+#undef DC_PAIR_ATTR
   return e;
 }
 }  // namespace dc

@@ -11,6 +11,7 @@ the C ABI (tests run on a B200 under gpurun: pytest -m gpu).
 """
 import ctypes as C
 import json
+import os
 
 import numpy as np
 import pytest
@@ -58,7 +59,9 @@ def _gemm(M, N, K, A, lda, a_mn, Bs, ldbs, ends, b_mn, split_k, Cm, ldc, R=None,
     g.C, g.ldc = Cm.data_ptr(), ldc
     g.R, g.ldr = (R.data_ptr() if R is not None else None), ldr
     g.num_sms = sms
-    g.kernel = kernel
+    # kernel 1: one-CTA tiles; 2: CTA pairs 256 x 256; 3: CTA pairs 256 x 128
+    os.environ["DC_GEMM_BN"] = "128" if kernel == 3 else "256"
+    g.kernel = 2 if kernel == 3 else kernel
     dc.check(dc.lib.dc_gemm(C.byref(g), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
 
@@ -76,7 +79,7 @@ def _mat(seed, r, c):
     return a, bf16_tensor(a)
 
 
-KERNELS = pytest.mark.parametrize("kernel", [1, 2], ids=["cta1", "cta_pair"])
+KERNELS = pytest.mark.parametrize("kernel", [1, 2, 3], ids=["cta1", "pair256", "pair128"])
 
 
 @KERNELS
