@@ -262,7 +262,12 @@ dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t which, void
  * identity at N = 1, so each weight's Adam update (the rs_adam arithmetic on
  * fp32(bf16(grad)), bit-identical) can run in the epilogue of its dW GEMM,
  * leaving only the norm gains to rs_adam.  Ignored for a step whose schedule
- * offloads optimizer state (the reload lands after the dW GEMMs). */
+ * offloads optimizer state (the reload lands after the dW GEMMs).
+ * "side_adam" (default 0; N = 1 only): layer l's reduce-scatter + Adam (the
+ * rs_adam arithmetic, bit-identical) is sliced across layer l-1's backward
+ * GEMM launches and streamed by idle warps of the CTA-pair GEMM, so the
+ * HBM-bound update overlaps tensor-bound work instead of competing for SMs;
+ * layer 0's update stays an rs_adam launch.  Same offload exclusion. */
 dc_status dc_model_set_option(dc_model* m, const char* key, int64_t value);
 /* Number of kernels the last dc_model_step launched. */
 dc_status dc_model_launch_count(const dc_model* m, int64_t* n);

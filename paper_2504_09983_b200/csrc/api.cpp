@@ -400,6 +400,38 @@ void ctx_param_state(const dc_ctx* c, int p, float** master, float** m, float** 
   *shard = reinterpret_cast<uint16_t*>(c->shard) + o;
 }
 
+dc_status ctx_side_job(dc_ctx* c, int layer, int step_t, SideJob* o) {
+  if (c->world != 1) return fail(c, DC_EINVAL, "side job: N == 1 only");
+  if (c->layer_use[layer] == 0) return fail(c, DC_ESTATE, "side job: grad slot of layer never acquired");
+  const int first = c->L.layer_first[layer], n = c->L.layer_count[layer];
+  if (n > 9) return fail(c, DC_EINVAL, "side job: at most 9 params per layer");
+  *o = SideJob{};
+  o->nm = n;
+  o->cum[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    o->goff[i] = c->L.goff[first + i];
+    o->store_off[i] = c->L.store_off[first + i];
+    o->cum[i + 1] = o->cum[i] + c->L.S[first + i] / 8;
+  }
+  o->slot = c->slot_ptr(c->rank, layer & 1);
+  o->master = c->master;
+  o->m = c->m;
+  o->v = c->v;
+  o->shard = reinterpret_cast<__nv_bfloat16*>(c->shard);
+  EpiAdam a{};
+  ctx_adam_scalars(c, step_t, &a);
+  o->w1 = a.w1; o->w2 = a.w2; o->b2 = a.b2; o->neg_s = a.neg_s; o->c = a.c; o->eps = a.eps;
+  o->g0 = 0;
+  o->g1 = o->cum[n];
+  return DC_OK;
+}
+
+dc_status ctx_post_consumed(dc_ctx* c, int layer, cudaStream_t st) {
+  const int s = layer & 1;
+  k_post_flags(peers_at(c, c->L.f_gcons + (int64_t)s * c->world + c->rank), (uint32_t)c->layer_use[layer], st);
+  return cudaGetLastError() == cudaSuccess ? DC_OK : fail(c, DC_ECUDA, "post consumed: launch failed");
+}
+
 dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, const std::vector<int>& params, cudaStream_t st) {
   if (dc_status e = check_sticky(c)) return e;
   const int s = layer & 1;

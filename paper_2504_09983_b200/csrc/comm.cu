@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "adam.cuh"
 #include "dc_internal.h"
 #include "ptx.cuh"
 
@@ -149,40 +150,13 @@ struct RsParams {
   uint32_t* err;
 };
 
-__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float2 t = __bfloat1622float2(h[i]);
-    f[2 * i] = t.x;
-    f[2 * i + 1] = t.y;
-  }
-}
-
-// Streaming accesses of rs_adam carry an L2 evict-first policy: the kernel
-// moves ~28 B per parameter once, and runs beside the layer GEMMs whose
-// operand tiles live in L2.
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ uint4 ld_stream(const void* ptr, uint64_t pol) {
-  uint4 r;
-  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ void st_stream(void* ptr, uint4 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
-               :: "l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
-}
-
 constexpr int RS_UNR = 2;   // groups of 8 elements per thread per iteration (loads hoisted)
 
+template <int MAXQ>
 __global__ void __launch_bounds__(256) rs_adam_kernel(const RsParams p) {
   {   // grad-ready of every rank was awaited by the preceding wait kernel
     const uint64_t pol = policy_evict_first();
+    const AdamScalars a{p.w1, p.w2, p.b2, p.neg_s, p.c, p.eps, p.invN};
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     for (int mi = 0; mi < p.nm; ++mi) {
@@ -193,69 +167,21 @@ __global__ void __launch_bounds__(256) rs_adam_kernel(const RsParams p) {
       float* vv = p.v + p.store_off[mi];
       bf16* sh = p.shard + p.store_off[mi];
       for (int64_t i0 = tid; i0 < n8; i0 += nthr * RS_UNR) {
-        float g[RS_UNR][8], pp[RS_UNR][8], m8[RS_UNR][8], v8[RS_UNR][8];
-        uint4 P[RS_UNR][2], Mv[RS_UNR][2], V[RS_UNR][2];
-        // issue every load of the RS_UNR groups before any math
+        Group8<MAXQ> x[RS_UNR];
 #pragma unroll
-        for (int u = 0; u < RS_UNR; ++u) {
+        for (int u = 0; u < RS_UNR; ++u) {     // every load of RS_UNR groups before any math
           const int64_t i = i0 + u * nthr;
           if (i < n8) {
+            const uint8_t* gp[MAXQ];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              P[u][h] = ld_stream(mst + 8 * i + 4 * h, pol);
-              Mv[u][h] = ld_stream(mm + 8 * i + 4 * h, pol);
-              V[u][h] = ld_stream(vv + 8 * i + 4 * h, pol);
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < RS_UNR; ++u) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) g[u][j] = 0.0f;
-          const int64_t i = i0 + u * nthr;
-          if (i < n8) {
-            for (int q = 0; q < p.world; ++q) {    // ascending rank order, fp32
-              const uint4 w = ld_stream(p.slot[q] + gbase + i * 16, pol);
-              float f[8];
-              bf16x8_to_f32(w, f);
-#pragma unroll
-              for (int j = 0; j < 8; ++j) g[u][j] = __fadd_rn(g[u][j], f[j]);
-            }
+            for (int q = 0; q < MAXQ; ++q) gp[q] = q < p.world ? p.slot[q] + gbase + i * 16 : nullptr;
+            load_group8<MAXQ>(x[u], gp, p.world, mst + 8 * i, mm + 8 * i, vv + 8 * i, pol);
           }
         }
 #pragma unroll
         for (int u = 0; u < RS_UNR; ++u) {
           const int64_t i = i0 + u * nthr;
-          if (i >= n8) continue;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const float* pf = reinterpret_cast<const float*>(&P[u][h]);
-            const float* mf = reinterpret_cast<const float*>(&Mv[u][h]);
-            const float* vf = reinterpret_cast<const float*>(&V[u][h]);
-#pragma unroll
-            for (int t = 0; t < 4; ++t) { pp[u][4 * h + t] = pf[t]; m8[u][4 * h + t] = mf[t]; v8[u][4 * h + t] = vf[t]; }
-          }
-          uint4 out;
-          __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&out);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float gj = __fmul_rn(g[u][j], p.invN);
-            const float mj = __fadd_rn(m8[u][j], __fmul_rn(p.w1, __fsub_rn(gj, m8[u][j])));
-            const float vj = __fadd_rn(__fmul_rn(p.b2, v8[u][j]), __fmul_rn(__fmul_rn(p.w2, gj), gj));
-            const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(vj), p.c), p.eps);
-            pp[u][j] = __fadd_rn(pp[u][j], __fdiv_rn(__fmul_rn(p.neg_s, mj), d));
-            m8[u][j] = mj;
-            v8[u][j] = vj;
-          }
-#pragma unroll
-          for (int t = 0; t < 4; ++t) o2[t] = __floats2bfloat162_rn(pp[u][2 * t], pp[u][2 * t + 1]);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            st_stream(mst + 8 * i + 4 * h, *reinterpret_cast<const uint4*>(&pp[u][4 * h]), pol);
-            st_stream(mm + 8 * i + 4 * h, *reinterpret_cast<const uint4*>(&m8[u][4 * h]), pol);
-            st_stream(vv + 8 * i + 4 * h, *reinterpret_cast<const uint4*>(&v8[u][4 * h]), pol);
-          }
-          st_stream(sh + 8 * i, out, pol);
+          if (i < n8) finish_group8<MAXQ>(x[u], p.world, mst + 8 * i, mm + 8 * i, vv + 8 * i, sh + 8 * i, a, pol);
         }
       }
     }
@@ -304,7 +230,10 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
   p.err = err_flag;
   wait_flags_kernel<<<1, 1, 0, st>>>(ready_local, world, ready_target, timeout_ns, err_flag, 0x300u);
   count_launch();
-  rs_adam_kernel<<<ctas, 256, 0, st>>>(p);
+  if (world == 1) rs_adam_kernel<1><<<ctas, 256, 0, st>>>(p);
+  else if (world == 2) rs_adam_kernel<2><<<ctas, 256, 0, st>>>(p);
+  else if (world <= 4) rs_adam_kernel<4><<<ctas, 256, 0, st>>>(p);
+  else rs_adam_kernel<MAXW><<<ctas, 256, 0, st>>>(p);
   if (cudaGetLastError() != cudaSuccess) return DC_ECUDA;
   count_launch();
   return DC_OK;
@@ -341,7 +270,10 @@ cudaError_t preload_comm_kernels() {
   cudaFuncAttributes a;
   cudaError_t e = cudaFuncGetAttributes(&a, ag_push_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, wait_flags_kernel);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel<1>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel<2>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel<4>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel<MAXW>);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, post_flags_kernel);
   return e;
 }

@@ -54,8 +54,27 @@ struct EpiAdam {
   void* shard;
   float w1, w2, b2, neg_s, c, eps;
 };
+// GEMM side job: groups [g0, g1) of 8 elements over a layer's params
+// (concatenated in order; member i spans groups [cum[i], cum[i+1]))
+struct SideJob {
+  int nm;
+  int64_t cum[10];
+  int64_t goff[9];          // byte offset of member i's grads in `slot`
+  int64_t store_off[9];     // member i's offset in the shard store
+  const uint8_t* slot;
+  float* master;
+  float* m;
+  float* v;
+  __nv_bfloat16* shard;
+  float w1, w2, b2, neg_s, c, eps;
+  int64_t g0, g1;
+};
 dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* err,
-                      const EpiAdam* adam = nullptr);
+                      const EpiAdam* adam = nullptr, const SideJob* side = nullptr);
+// the reduce-scatter + Adam of `layer` as a side job template (N = 1 only);
+// and the consumed-flag post that normally ends rs_adam
+dc_status ctx_side_job(dc_ctx* c, int layer, int step_t, SideJob* out);
+dc_status ctx_post_consumed(dc_ctx* c, int layer, cudaStream_t st);
 // Adam scalars of step t from the ctx hyper-parameters (reading D18)
 void ctx_adam_scalars(const dc_ctx* c, int step_t, EpiAdam* out);
 // shard-store pointers of a param (fp32 master/m/v, bf16 shard) on this rank

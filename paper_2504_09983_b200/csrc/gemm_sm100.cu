@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "adam.cuh"
 #include "dc_internal.h"
 #include "ptx.cuh"
 
@@ -55,6 +56,10 @@ struct GemmParams {
   float* v;
   __nv_bfloat16* shard;
   float w1, w2, b2, neg_s, c, eps;
+  // side job (pair kernel, N = 1): groups [g0, g1) of 8 shard elements of a
+  // previous layer's reduce-scatter + Adam, streamed by 6 otherwise idle warps
+  // while the tensor cores run this GEMM (same arithmetic as rs_adam)
+  SideJob side;
 };
 
 __device__ __forceinline__ int seg_of(const GemmParams& p, int idx) {
@@ -344,6 +349,40 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   }
 }
 
+// ------------------------------------------------------------------ GEMM side job
+constexpr int SIDE_WARPS = 6;               // warps 2, 3, 8, 9, 10, 11 of the pair kernel
+__device__ __forceinline__ void side_job(const SideJob& sj, int side_warp, int lane) {
+  const int64_t nthr = (int64_t)gridDim.x * SIDE_WARPS * 32;
+  const int64_t t = (int64_t)blockIdx.x * SIDE_WARPS * 32 + side_warp * 32 + lane;
+  const uint64_t pol = policy_evict_first();
+  const AdamScalars a{sj.w1, sj.w2, sj.b2, sj.neg_s, sj.c, sj.eps, 1.0f};
+  for (int64_t g = sj.g0 + t; g < sj.g1; g += 2 * nthr) {
+    Group8<1> x[2];
+    int mi[2];
+    int64_t j[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {          // both groups' loads before any math
+      const int64_t gg = g + u * nthr;
+      mi[u] = 0;
+      for (int i = 1; i < sj.nm; ++i)
+        if (gg >= sj.cum[i]) mi[u] = i;
+      j[u] = gg - sj.cum[mi[u]];
+      if (gg < sj.g1) {
+        const uint8_t* gp = sj.slot + sj.goff[mi[u]] + j[u] * 16;
+        const int64_t e = sj.store_off[mi[u]] + 8 * j[u];
+        load_group8<1>(x[u], &gp, 1, sj.master + e, sj.m + e, sj.v + e, pol);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (g + u * nthr < sj.g1) {
+        const int64_t e = sj.store_off[mi[u]] + 8 * j[u];
+        finish_group8<1>(x[u], 1, sj.master + e, sj.m + e, sj.v + e, sj.shard + e, a, pol);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ CTA-pair kernel
 // cta_group::2: a cluster of 2 CTAs on one TPC computes a 256 x 256 tile.  CTA
 // r stages rows [128r, 128r+128) of A and columns [128r, 128r+128) of B (16 KiB
@@ -362,8 +401,10 @@ template <int BNT, int ST> struct Pair {
   static constexpr int TMEM = 2 * BNT;                                   // 2 accumulator buffers
 };
 
+constexpr int GEMM2_THREADS = 384;          // + side-job warps 8..11
+
 template <int BNT, int ST, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
 gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
                  const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
                  const __grid_constant__ CUtensorMap mapB3, const GemmParams p) {
@@ -471,7 +512,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         if (++acc == 2) { acc = 0; aphase ^= 1; }
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 8) {
     // ------------------------------------------------------------- epilogue (both CTAs)
     const int q = warp & 3;
     int acc = 0; uint32_t aphase = 0;
@@ -537,6 +578,9 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
       if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
+  } else if (p.side.nm > 0) {
+    // ------------------------------------------------------------- side job (warps 2, 3, 8..11)
+    side_job(p.side, warp < 4 ? warp - 2 : warp - 6, lane);
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();
@@ -586,7 +630,8 @@ static int num_sms_cached() {
   return n;
 }
 
-dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* err, const EpiAdam* adam) {
+dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* err, const EpiAdam* adam,
+                      const SideJob* side) {
   if (g->M <= 0 || g->N <= 0 || g->K <= 0 || (g->N % 8) || (g->K % 8) || g->n_bseg < 1 || g->n_bseg > 4) {
     *err = "dc_gemm: M,N,K must be > 0, N and K multiples of 8, 1..4 B segments";
     return DC_EINVAL;
@@ -628,6 +673,10 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
     p.shard = reinterpret_cast<__nv_bfloat16*>(adam->shard);
     p.w1 = adam->w1; p.w2 = adam->w2; p.b2 = adam->b2; p.neg_s = adam->neg_s; p.c = adam->c; p.eps = adam->eps;
   }
+  if (side && side->nm > 0) {
+    if (!pair) { *err = "dc_gemm: a side job needs the CTA-pair kernel"; return DC_EINVAL; }
+    p.side = *side;
+  }
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a_mn << 15) | ((uint32_t)p.b_mn << 16) |
             ((uint32_t)(bnt >> 3) << 17) | ((uint32_t)(tm >> 4) << 24);
   CUtensorMap mA, mB[4];
@@ -668,8 +717,8 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
     static const int env_st = getenv("DC_GEMM_STAGES") ? atoi(getenv("DC_GEMM_STAGES")) : 6;
     const int g2 = 2 * pairs;
 #define DC_PAIR_LAUNCH(BN_, ST_)                                                                   \
-    (p.epi ? gemm2_bf16_sm100<BN_, ST_, 1><<<g2, GEMM_THREADS, Pair<BN_, ST_>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p) \
-           : gemm2_bf16_sm100<BN_, ST_, 0><<<g2, GEMM_THREADS, Pair<BN_, ST_>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p))
+    (p.epi ? gemm2_bf16_sm100<BN_, ST_, 1><<<g2, GEMM2_THREADS, Pair<BN_, ST_>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p) \
+           : gemm2_bf16_sm100<BN_, ST_, 0><<<g2, GEMM2_THREADS, Pair<BN_, ST_>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p))
     if (bnt == 128) DC_PAIR_LAUNCH(128, 9);
     else if (env_st == 6) DC_PAIR_LAUNCH(256, 6);
     else DC_PAIR_LAUNCH(256, 7);

@@ -69,6 +69,13 @@ struct dc_model {
   bool profile_pending = false;      // per-op events recorded, not yet read
   bool fused_adam = false;           // N = 1: Adam in the dW GEMM epilogues (option)
   bool fused_active = false;         // ... and the bound schedule has no offload
+  bool side_adam = false;            // N = 1: RS + Adam as GEMM side jobs (option)
+  bool side_active = false;
+  int pending_layer = -1;            // layer whose RS + Adam rides on the current GEMMs
+  SideJob pending{};
+  int64_t pending_assigned = 0;      // groups handed out so far
+  __int128 pending_mnk = 0;          // sum of M*N*K of the hosting GEMMs so far
+  int64_t bwd_mnk = 0;               // sum of M*N*K of one layer's backward GEMMs
   int step_t = 0;
   std::string err;
 
@@ -178,6 +185,16 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   // opt-in (dc_model_set_option): bit-identical, but the epilogue becomes
   // HBM-bound and slows the dW GEMMs more than it saves (profiles/r01)
   m->fused_adam = false;
+  // opt-in: bit-identical and relieves the SM contention, but the 1 kW power
+  // cap lowers the clock by as much as the overlap gains (profiles/r01)
+  m->side_adam = false;
+  {
+    const int64_t T_ = d->tokens, H_ = d->hidden, F_ = d->ffn, qd_ = m->qd, kvd_ = m->kvd, qkvd_ = m->qkvd;
+    m->bwd_mnk = T_ * F_ * H_ + H_ * F_ * T_ +                       // down_bwd: dX, dW
+                 T_ * H_ * 2 * F_ + 2 * (F_ * H_ * T_) +            // gate_up_bwd: dX, dWg, dWu
+                 T_ * qd_ * H_ + H_ * qd_ * T_ +                    // o_bwd: dX, dW
+                 T_ * H_ * qkvd_ + qd_ * H_ * T_ + 2 * (kvd_ * H_ * T_);   // qkv_bwd: dX, dWq/k/v
+  }
   const size_t n = m->s0.size();
   m->dur_us.assign(n, 0);
   m->p_mem.assign(n, 0);
@@ -227,6 +244,22 @@ static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t l
                       std::initializer_list<const void*> Bs, std::initializer_list<int64_t> ldbs,
                       std::initializer_list<int> ends, int b_mn, int split_k, void* C, int64_t ldc,
                       const void* R, int64_t ldr, cudaStream_t st, const EpiAdam* adam = nullptr) {
+  // a backward GEMM carries its share of the pending layer's RS + Adam
+  SideJob sj{};
+  const SideJob* side = nullptr;
+  if (m->pending_layer >= 0) {
+    m->pending_mnk += (__int128)M * N * K;
+    const int64_t G = m->pending.g1;
+    int64_t target = (int64_t)((__int128)G * m->pending_mnk / m->bwd_mnk);
+    if (target > G) target = G;
+    if (target > m->pending_assigned) {
+      sj = m->pending;
+      sj.g0 = m->pending_assigned;
+      sj.g1 = target;
+      m->pending_assigned = target;
+      side = &sj;
+    }
+  }
   dc_gemm_args g{};
   g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.a_mn_major = a_mn;
   int i = 0;
@@ -239,7 +272,7 @@ static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t l
   g.b_mn_major = b_mn; g.b_split_k = split_k;
   g.C = C; g.ldc = ldc; g.R = R; g.ldr = ldr;
   std::string err;
-  dc_status s = launch_gemm(&g, st, &err, adam);
+  dc_status s = launch_gemm(&g, st, &err, adam, side);
   if (s != DC_OK) return mfail(m, s, err);
   return DC_OK;
 }
@@ -358,6 +391,11 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
                     (float*)m->A(m->ws_dgp), T, H, st);
       k_colsum_to_bf16((float*)m->A(m->ws_dgp), nb, H, G(P_G1), st);
       if ((s = dc_grad_slot_publish(m->ctx, l, st)) != DC_OK) return s;
+      if (m->pending_layer >= 0) {     // the hosted RS + Adam is complete (stream order)
+        if (m->pending_assigned != m->pending.g1) return mfail(m, DC_ESTATE, "side job not fully assigned");
+        if ((s = ctx_post_consumed(m->ctx, m->pending_layer, st)) != DC_OK) return s;
+        m->pending_layer = -1;
+      }
       m->cur_d ^= 1;
       break;
     }
@@ -476,12 +514,14 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
   // an offloaded fragment is reloaded before its layer's RS op (reading D17),
   // i.e. after the dW GEMMs: the fused update needs every state resident
   m->fused_active = m->fused_adam;
-  for (int i = 0, n = sched_num_ops(sc); i < n && m->fused_active; ++i) {
+  m->side_active = m->side_adam && !m->fused_adam;
+  m->pending_layer = -1;
+  for (int i = 0, n = sched_num_ops(sc); i < n && (m->fused_active || m->side_active); ++i) {
     int kind, id, nm, np, nw;
     const int64_t* mem; const int* posts; const int* waits;
     int64_t off, bytes;
     sched_op(sc, i, &kind, &id, &mem, &nm, &off, &bytes, &posts, &np, &waits, &nw);
-    if (kind >= K_OFF) m->fused_active = false;
+    if (kind >= K_OFF) m->fused_active = m->side_active = false;
   }
   dc_status s = dc_step_begin(m->ctx, ++m->epoch, cs);
   if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
@@ -532,7 +572,12 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
         if (profile) cudaEventRecord(m->ev_t0[id], rss);
         if (m->fused_active)   // the weights were updated in their dW epilogues; the norm gains remain
           s = reduce_scatter_params(m->ctx, o.layer, step_t, {m->pid(o.layer, P_G1), m->pid(o.layer, P_G2)}, rss);
-        else
+        else if (m->side_active && o.layer > 0) {   // rides on layer l-1's backward GEMMs
+          s = ctx_side_job(m->ctx, o.layer, step_t, &m->pending);
+          m->pending_layer = o.layer;
+          m->pending_assigned = 0;
+          m->pending_mnk = 0;
+        } else
           s = dc_reduce_scatter_step(m->ctx, o.layer, step_t, 1, rss);
         if (profile) cudaEventRecord(m->ev_t1[id], rss);
         break;
@@ -589,6 +634,11 @@ extern "C" dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t 
 
 extern "C" dc_status dc_model_set_option(dc_model* m, const char* key, int64_t value) {
   if (!m || !key) return mfail(nullptr, DC_EINVAL, "dc_model_set_option: null argument");
+  if (!strcmp(key, "side_adam")) {
+    if (value && ctx_world(m->ctx) != 1) return mfail(m, DC_EINVAL, "side_adam needs N == 1");
+    m->side_adam = value != 0;
+    return DC_OK;
+  }
   if (!strcmp(key, "fused_adam")) {
     if (value && ctx_world(m->ctx) != 1) return mfail(m, DC_EINVAL, "fused_adam needs N == 1");
     m->fused_adam = value != 0;

@@ -47,11 +47,42 @@ class RankState:
         return [s.cuda_stream for s in self.streams]
 
 
+_IPC_KEEP = []   # imported peer storages must outlive every use of their pointers
+
+
+def _alloc_symmetric_ipc(nbytes, group, device):
+    """Peer-mapped buffer through CUDA IPC: every rank exports its allocation's
+    IPC handle over the process group and opens the others' (works between
+    processes on one device, and across NVLink-connected devices)."""
+    import torch.distributed as dist
+    t = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+    h = t.untyped_storage()._share_cuda_()
+    handles = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, h, group=group)
+    me = dist.get_rank(group)
+    ptrs = []
+    for q, hq in enumerate(handles):
+        if q == me:
+            ptrs.append(t.data_ptr())
+        else:
+            st = torch.UntypedStorage._new_shared_cuda(*hq)
+            _IPC_KEEP.append(st)
+            ptrs.append(st.data_ptr())
+    return t, ptrs
+
+
 def _alloc_symmetric(nbytes, group, device):
-    from torch.distributed import _symmetric_memory as symm_mem
-    t = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
-    h = symm_mem.rendezvous(t, group.group_name)
-    return t, [int(p) for p in h.buffer_ptrs]
+    """Symmetric buffer for the peer tables: torch symmetric memory by default
+    (DC_SYMM=ipc selects CUDA IPC; it is also the fallback)."""
+    if os.environ.get("DC_SYMM", "symm_mem") == "ipc":
+        return _alloc_symmetric_ipc(nbytes, group, device)
+    try:
+        from torch.distributed import _symmetric_memory as symm_mem
+        t = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+        h = symm_mem.rendezvous(t, group.group_name)
+        return t, [int(p) for p in h.buffer_ptrs]
+    except RuntimeError:
+        return _alloc_symmetric_ipc(nbytes, group, device)
 
 
 def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr=1e-3, beta1=0.9,

@@ -136,3 +136,24 @@ def test_fused_adam_bitexact_vs_rs_adam():
                                y.view(torch.int16) if k == "shard" else y.view(torch.int32)), (t, k)
         assert _loss(a[0]) == _loss(b[0])
     assert dc.lib.dc_model_set_option(a[0].model, b"nope", 1) == dc.DC_EINVAL
+
+
+def test_side_job_adam_bitexact_vs_rs_adam():
+    """N = 1: layer l's RS + Adam streamed by the GEMM side warps of layer l-1's
+    backward == the rs_adam kernel, bit for bit (3 layers: two hosted, one not)."""
+    cfg = synth.small_llama(layers=3, seq=256)
+    _, a = _setup(cfg, 1, dc.DC_PASS_SHARD)
+    _, b = _setup(cfg, 1, dc.DC_PASS_SHARD)
+    dc.check(dc.lib.dc_model_set_option(a[0].model, b"side_adam", 1))
+    dc.check(dc.lib.dc_model_set_option(b[0].model, b"side_adam", 0))
+    for t in (1, 2, 3):
+        rt.step(a, t)
+        rt.step(b, t)
+        torch.cuda.synchronize()
+        rt.poll(a)
+        rt.poll(b)
+        for k in ("master", "m", "v", "shard"):
+            x, y = a[0].tensors[k], b[0].tensors[k]
+            assert torch.equal(x.view(torch.int16) if k == "shard" else x.view(torch.int32),
+                               y.view(torch.int16) if k == "shard" else y.view(torch.int32)), (t, k)
+    assert not torch.isnan(a[0].tensors["master"]).any()

@@ -1,0 +1,117 @@
+"""The one-process-per-rank path (what torchrun runs at N > 1) on a single
+GPU: two processes share cuda:0, peer pointers come from torch symmetric
+memory (IPC-mapped between the processes), host collectives use gloo.  Each
+rank profiles, the profile is MAX-reduced, both plan identically, bind and run
+two sharded steps through the C ABI; results vs the oracle's 2-rank step."""
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_dir):
+    # torch symmetric memory rejects two ranks on one device: peer-map via CUDA IPC
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), DC_SYMM="ipc")
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import synth
+    from oracle import numerics as nx
+    from oracle import step as ost
+    from paper_2504_09983_b200 import dc, runtime as rt
+    cfg = synth.small_llama(layers=2, seq=128)
+    table = synth.llama_param_table(cfg)
+    ranks = rt.create_ranks(table, world, 0, virtual=False, group=dist.group.WORLD, rank=rank, lr=1e-3,
+                            spin_ms=60000)
+    st = ranks[rank]
+    x, t = ost.rank_batch(cfg, rank)
+    bf = lambda a: torch.from_numpy(nx.bf16_bits(a).view(np.int16).copy()).cuda().view(torch.bfloat16)
+    rt.attach_model(ranks, cfg, {rank: bf(x)}, {rank: bf(t)})
+    prof = rt.profile_json(st, tc=[[4096, 10], [1 << 20, 20 + rank], [1 << 26, 400]])
+    prof = rt.max_reduce_profile(prof, dist.group.WORLD)
+    sched = dc.plan(json.dumps(prof), 1 << 40, M_prefetch=1 << 22,
+                    passes=dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD, strict=True)
+    digests = [None] * world
+    dist.all_gather_object(digests, rt.plan_digest(dc.schedule_json(sched)))
+    torch.cuda.synchronize()
+    dist.barrier()
+    rt.bind(ranks, {rank: sched}, group=dist.group.WORLD)
+    dist.barrier()
+    losses = []
+    for step in (1, 2):
+        rt.step(ranks, step)
+        torch.cuda.synchronize()
+        rt.poll(ranks)
+        losses.append(rt.view(rt.loss_ptr(st), 1, torch.float32).item())
+        dist.barrier()
+    np.save(os.path.join(out_dir, "master%d.npy" % rank), st.tensors["master"].cpu().numpy())
+    with open(os.path.join(out_dir, "r%d.json" % rank), "w") as f:
+        json.dump({"losses": losses, "digests": digests}, f)
+    torch.cuda.synchronize()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_processes_one_gpu(tmp_path):
+    import synth
+    from oracle import numerics as nx
+    from oracle import step as ost
+    port = _free_port()
+    mp.start_processes(_worker, args=(2, port, str(tmp_path)), nprocs=2, start_method="spawn")
+    r = [json.load(open(tmp_path / ("r%d.json" % q))) for q in range(2)]
+    assert r[0]["digests"][0] == r[0]["digests"][1]
+    cfg = synth.small_llama(layers=2, seq=128)
+    table = synth.llama_param_table(cfg)
+    oracle = ost.ShardedState(table, 2, bf16=True)
+    o1, _ = ost.sharded_step(oracle, cfg, lr=1e-3)
+    o2, _ = ost.sharded_step(oracle, cfg, lr=1e-3)
+    # the same 2-rank run in DC_VIRTUAL_RANKS mode (same kernels, same order)
+    from paper_2504_09983_b200 import dc, runtime as rt
+    vr = rt.create_ranks(table, 2, 0, lr=1e-3)
+    bf = lambda a: torch.from_numpy(nx.bf16_bits(a).view(np.int16).copy()).cuda().view(torch.bfloat16)
+    xs = {q: bf(ost.rank_batch(cfg, q)[0]) for q in range(2)}
+    ts = {q: bf(ost.rank_batch(cfg, q)[1]) for q in range(2)}
+    rt.attach_model(vr, cfg, xs, ts)
+    profs = []
+    for q in range(2):
+        p = rt.profile_json(vr[q], tc=[[4096, 10], [1 << 20, 20 + q], [1 << 26, 400]])
+        profs.append(p)
+    prof = json.loads(json.dumps(profs[0]))
+    for o, o1_ in zip(prof["ops"], profs[1]["ops"]):
+        o["p_mem"] = max(o["p_mem"], o1_["p_mem"])
+    prof["tc"][1][1] = 21
+    sched = dc.plan(json.dumps(prof), 1 << 40, M_prefetch=1 << 22,
+                    passes=dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD, strict=True)
+    assert rt.plan_digest(dc.schedule_json(sched)) == r[0]["digests"][0]
+    rt.bind(vr, {q: sched for q in range(2)})
+    vl = []
+    for step in (1, 2):
+        rt.step(vr, step)
+        torch.cuda.synchronize()
+        vl.append([rt.view(rt.loss_ptr(vr[q]), 1, torch.float32).item() for q in range(2)])
+    for q in range(2):
+        l1, l2 = r[q]["losses"]
+        assert abs(l1 - o1[q]) <= 2e-2 * o1[q] and abs(l2 - o2[q]) <= 2e-2 * o2[q]
+        assert [l1, l2] == [vl[0][q], vl[1][q]]
+        ms = np.load(tmp_path / ("master%d.npy" % q))
+        assert ms.tobytes() == vr[q].tensors["master"].cpu().numpy().tobytes()   # bit-identical
+        off = 0
+        for i, p in enumerate(table):
+            S = nx.shard_len(p.numel, 2)
+            d = np.abs(ms[off:off + S].astype(np.float64) - oracle.master[q][i])
+            assert d.max() <= 4.1e-3, (q, p.name, d.max())      # two steps of |update| <= ~lr each
+            off += S
