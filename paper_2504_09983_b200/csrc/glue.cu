@@ -129,17 +129,22 @@ void k_rmsnorm_fwd(const void* x, const void* g, void* h, float* rstd, int T, in
 constexpr int RB_ROWS = 16;
 int rmsnorm_bwd_blocks(int T) { return (T + RB_ROWS - 1) / RB_ROWS; }
 
+// One pass per row: dh and x are loaded once into registers (CH chunks of 8
+// columns per thread, H = CH * 2048), the gain once per CTA.
+template <int CH>
 __global__ void __launch_bounds__(RN_T) rmsnorm_bwd_kernel(const bf16* __restrict__ dh, const bf16* __restrict__ x,
                                                           const bf16* __restrict__ g, const float* __restrict__ rstd,
                                                           const bf16* __restrict__ dres, bf16* __restrict__ dx,
                                                           float* __restrict__ dgp, int T, int H) {
   __shared__ float sh[32];
-  // each thread owns columns c = threadIdx.x*8 + j*RN_T*8 (H <= 8192 -> <= 4 chunks)
-  float acc[4][8];
+  float acc[CH][8], gg[CH][8];
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
+  for (int j = 0; j < CH; ++j) {
+    const int c = threadIdx.x * 8 + j * RN_T * 8;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[j][i] = 0.0f;
+    for (int i = 0; i < 8; ++i) { acc[j][i] = 0.0f; gg[j][i] = 0.0f; }
+    if (c < H) load8(g + c, gg[j]);
+  }
   const int r0 = blockIdx.x * RB_ROWS;
   for (int rr = 0; rr < RB_ROWS; ++rr) {
     const int row = r0 + rr;
@@ -147,48 +152,41 @@ __global__ void __launch_bounds__(RN_T) rmsnorm_bwd_kernel(const bf16* __restric
     const float rs = rstd[row];
     const bf16* dhr = dh + (int64_t)row * H;
     const bf16* xr = x + (int64_t)row * H;
+    float a[CH][8], n[CH][8], d[CH][8];
     float dot = 0.0f;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < CH; ++j) {
       const int c = threadIdx.x * 8 + j * RN_T * 8;
-      if (c < H) {
-        float a[8], b[8], gg[8];
-        load8(dhr + c, a);
-        load8(xr + c, b);
-        load8(g + c, gg);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float n = b[i] * rs;
-          acc[j][i] += a[i] * n;
-          dot = fmaf(a[i] * gg[i], n, dot);
-        }
+      for (int i = 0; i < 8; ++i) { a[j][i] = 0.0f; n[j][i] = 0.0f; d[j][i] = 0.0f; }
+      if (c < H) {
+        load8(dhr + c, a[j]);
+        load8(xr + c, n[j]);
+        if (dres) load8(dres + (int64_t)row * H + c, d[j]);
       }
     }
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        n[j][i] = n[j][i] * rs;
+        acc[j][i] += a[j][i] * n[j][i];
+        dot = fmaf(a[j][i] * gg[j][i], n[j][i], dot);
+      }
     dot = block_sum<RN_T>(dot, sh) / (float)H;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < CH; ++j) {
       const int c = threadIdx.x * 8 + j * RN_T * 8;
-      if (c < H) {
-        float a[8], b[8], gg[8], d[8];
-        load8(dhr + c, a);
-        load8(xr + c, b);
-        load8(g + c, gg);
-        if (dres) load8(dres + (int64_t)row * H + c, d);
-        else {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) d[i] = 0.0f;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float n = b[i] * rs;
-          d[i] = d[i] + rs * (a[i] * gg[i] - n * dot);
-        }
-        store8(dx + (int64_t)row * H + c, d);
+      for (int i = 0; i < 8; ++i) {
+        const float base = dres ? d[j][i] : 0.0f;
+        d[j][i] = base + rs * (a[j][i] * gg[j][i] - n[j][i] * dot);
       }
+      if (c < H) store8(dx + (int64_t)row * H + c, d[j]);
     }
   }
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < CH; ++j) {
     const int c = threadIdx.x * 8 + j * RN_T * 8;
     if (c < H) {
 #pragma unroll
@@ -199,8 +197,15 @@ __global__ void __launch_bounds__(RN_T) rmsnorm_bwd_kernel(const bf16* __restric
 
 void k_rmsnorm_bwd(const void* dh, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
                    float* dg_partial, int T, int H, cudaStream_t st) {
-  rmsnorm_bwd_kernel<<<rmsnorm_bwd_blocks(T), RN_T, 0, st>>>((const bf16*)dh, (const bf16*)x, (const bf16*)g, rstd,
-                                                             (const bf16*)dres, (bf16*)dx, dg_partial, T, H);
+  const int ch = (H + RN_T * 8 - 1) / (RN_T * 8);
+#define DC_RB(CH_)                                                                                  \
+  rmsnorm_bwd_kernel<CH_><<<rmsnorm_bwd_blocks(T), RN_T, 0, st>>>((const bf16*)dh, (const bf16*)x,     \
+      (const bf16*)g, rstd, (const bf16*)dres, (bf16*)dx, dg_partial, T, H)
+  if (ch == 1) DC_RB(1);
+  else if (ch == 2) DC_RB(2);
+  else if (ch == 3) DC_RB(3);
+  else DC_RB(4);
+#undef DC_RB
   count_launch();
 }
 
@@ -388,7 +393,8 @@ namespace dc {
 cudaError_t preload_glue_kernels() {
   cudaFuncAttributes a;
   const void* fns[] = {(const void*)init_param_kernel, (const void*)rmsnorm_fwd_kernel,
-                       (const void*)rmsnorm_bwd_kernel, (const void*)colsum_kernel,
+                       (const void*)rmsnorm_bwd_kernel<1>, (const void*)rmsnorm_bwd_kernel<2>,
+                       (const void*)rmsnorm_bwd_kernel<3>, (const void*)rmsnorm_bwd_kernel<4>, (const void*)colsum_kernel,
                        (const void*)attn_mix_fwd_kernel, (const void*)attn_mix_bwd_kernel,
                        (const void*)act_fwd_kernel, (const void*)act_bwd_kernel,
                        (const void*)loss_kernel, (const void*)loss_final_kernel};
