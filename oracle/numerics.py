@@ -78,9 +78,16 @@ def reduce_scatter(grads_padded, world: int, rank: int):
     return acc
 
 
-def scale_mean(g, world: int):
-    """Data-parallel mean: g * (1/N) in fp32 (exact for N a power of two)."""
-    return (g * F32(1.0 / world)).astype(F32)
+def scale_mean(g, world: int, micro_steps: int = 1):
+    """Data-parallel mean over N ranks and n accumulated micro-steps:
+    g * fp32(1/(N n)), one rounding (exact for N n a power of two)."""
+    return (g * F32(1.0 / (world * micro_steps))).astype(F32)
+
+
+def accumulate(acc, rs):
+    """Gradient accumulation of the partitioned fp32 gradient shard (ZeRO-3
+    semantics): acc_0 = rs_0, acc_mu = acc_{mu-1} + rs_mu."""
+    return np.asarray(rs, F32).copy() if acc is None else (acc + np.asarray(rs, F32)).astype(F32)
 
 
 # ---------------------------------------------------------------------------
@@ -117,10 +124,13 @@ def adam_update(p, m, v, g, step: int, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8
 
 
 def rs_adam_shard(grads_bf16_padded, master, m, v, world, rank, step, lr, beta1=0.9,
-                  beta2=0.999, eps=1e-8):
-    """What dc_reduce_scatter_step computes for one tensor on owner `rank`:
-    RS of bf16 grads accumulated in fp32, x 1/N, Adam on the fp32 master/m/v
-    shard, bf16 (RNE) param shard written back.  Returns (master, m, v, shard_bf16)."""
-    g = scale_mean(reduce_scatter([np.asarray(x, F32) for x in grads_bf16_padded], world, rank), world)
+                  beta2=0.999, eps=1e-8, acc=None, micro_steps=1):
+    """What dc_reduce_scatter_step computes for one tensor on owner `rank` at
+    the last micro-step: RS of bf16 grads summed in fp32, added to the
+    accumulated shard of the earlier micro-steps (if any), x 1/(N n), Adam on
+    the fp32 master/m/v shard, bf16 (RNE) param shard written back.
+    Returns (master, m, v, shard_bf16)."""
+    rs = reduce_scatter([np.asarray(x, F32) for x in grads_bf16_padded], world, rank)
+    g = scale_mean(accumulate(acc, rs) if acc is not None else rs, world, micro_steps)
     p2, m2, v2 = adam_update(master, m, v, g, step, lr, beta1, beta2, eps)
     return p2, m2, v2, rne_bf16(p2)

@@ -26,11 +26,11 @@ def init_full_params(table):
     return out
 
 
-def rank_batch(cfg, rank):
-    """Rank r's synthetic micro-batch (inputs std 1, targets std 1)."""
+def rank_batch(cfg, rank, micro=0):
+    """Rank r's synthetic micro-batch `micro` (inputs std 1, targets std 1)."""
     n = cfg.tokens * cfg.hidden
-    x = synth.values(synth.seed_inputs(rank), 0, 0, n, synth.K_UNIT).reshape(cfg.tokens, cfg.hidden)
-    t = synth.values(synth.seed_targets(rank), 0, 0, n, synth.K_UNIT).reshape(cfg.tokens, cfg.hidden)
+    x = synth.values(synth.seed_inputs(rank, micro), 0, 0, n, synth.K_UNIT).reshape(cfg.tokens, cfg.hidden)
+    t = synth.values(synth.seed_targets(rank, micro), 0, 0, n, synth.K_UNIT).reshape(cfg.tokens, cfg.hidden)
     return x, t
 
 
@@ -77,24 +77,36 @@ def _fwd_bwd(cfg, table, full, x, t, bf16):
     return loss, flat, outs
 
 
-def sharded_step(state: ShardedState, cfg, lr, world=None):
-    """One sharded step over all simulated ranks.  Returns per-rank losses and
-    per-rank padded grads (the arena grad-slot contents)."""
+def sharded_step(state: ShardedState, cfg, lr, micro_steps=1):
+    """One sharded optimizer step over all simulated ranks with n micro-steps
+    (§4.3: n forward/backward passes, then one update).
+    Every micro-step's bf16 grads are reduce-scattered (fp32, rank order) and
+    accumulated into the partitioned fp32 gradient shard; the last micro-step
+    applies x 1/(N n) and Adam.  Returns per-rank losses (of the last
+    micro-step) and the last micro-step's padded grads (grad-slot contents)."""
     N = state.world
     state.t += 1
-    losses, grads_padded = [], []
-    for r in range(N):
-        full = state.gathered(r)
-        x, t = rank_batch(cfg, r)
-        loss, flat, _ = _fwd_bwd(cfg, state.table, full, x, t, state.bf16)
-        losses.append(loss)
-        grads_padded.append([np.concatenate([g, np.zeros(N * state.S[i] - g.size, F32)])
-                             for i, g in enumerate(flat)])
+    acc = [[None] * len(state.table) for _ in range(N)]
+    for mu in range(micro_steps):
+        losses, grads_padded = [], []
+        for r in range(N):
+            full = state.gathered(r)
+            x, t = rank_batch(cfg, r, mu)
+            loss, flat, _ = _fwd_bwd(cfg, state.table, full, x, t, state.bf16)
+            losses.append(loss)
+            grads_padded.append([np.concatenate([g, np.zeros(N * state.S[i] - g.size, F32)])
+                                 for i, g in enumerate(flat)])
+        if mu < micro_steps - 1:
+            for r in range(N):
+                for i in range(len(state.table)):
+                    rs = nx.reduce_scatter([grads_padded[q][i] for q in range(N)], N, r)
+                    acc[r][i] = nx.accumulate(acc[r][i], rs)
+    state.acc = acc          # accumulated shards of micro-steps 0..n-2 (tests inspect it)
     for r in range(N):
         for i in range(len(state.table)):
             mst, m, v, sh = nx.rs_adam_shard([grads_padded[q][i] for q in range(N)],
                                              state.master[r][i], state.m[r][i], state.v[r][i],
-                                             N, r, state.t, lr)
+                                             N, r, state.t, lr, acc=acc[r][i], micro_steps=micro_steps)
             state.master[r][i], state.m[r][i], state.v[r][i] = mst, m, v
             state.shard[r][i] = sh if state.bf16 else mst.copy()
     return losses, grads_padded
@@ -114,23 +126,28 @@ class ReplicatedState:
         return [nx.rne_bf16(x) if self.bf16 else x for x in self.master]
 
 
-def replicated_step(state: ReplicatedState, cfg, lr):
-    """All-reduce (fp32, ascending rank from +0.0) -> x1/N -> Adam on full tensors."""
+def replicated_step(state: ReplicatedState, cfg, lr, micro_steps=1):
+    """Plain data parallelism: per micro-step an all-reduce (fp32, ascending
+    rank from +0.0) accumulated over micro-steps, x 1/(N n), Adam on the full
+    tensors."""
     N = state.world
     state.t += 1
     full = state.params()
-    per_rank = []
-    losses = []
-    for r in range(N):
-        x, t = rank_batch(cfg, r)
-        loss, flat, _ = _fwd_bwd(cfg, state.table, full, x, t, state.bf16)
-        losses.append(loss)
-        per_rank.append(flat)
+    total = [None] * len(state.table)
+    for mu in range(micro_steps):
+        per_rank, losses = [], []
+        for r in range(N):
+            x, t = rank_batch(cfg, r, mu)
+            loss, flat, _ = _fwd_bwd(cfg, state.table, full, x, t, state.bf16)
+            losses.append(loss)
+            per_rank.append(flat)
+        for i in range(len(state.table)):
+            ar = np.zeros(state.table[i].numel, F32)
+            for q in range(N):
+                ar = (ar + per_rank[q][i]).astype(F32)
+            total[i] = nx.accumulate(total[i], ar)
     for i in range(len(state.table)):
-        acc = np.zeros(state.table[i].numel, F32)
-        for q in range(N):
-            acc = (acc + per_rank[q][i]).astype(F32)
-        g = nx.scale_mean(acc, N)
+        g = nx.scale_mean(total[i], N, micro_steps)
         state.master[i], state.m[i], state.v[i] = nx.adam_update(
             state.master[i], state.m[i], state.v[i], g, state.t, lr)
     return losses

@@ -21,12 +21,13 @@ _C2 = np.uint64(0x94D049BB133111EB)
 SEED_WEIGHTS = 0
 
 
-def seed_inputs(rank: int) -> int:
-    return 1000 + rank
+def seed_inputs(rank: int, micro: int = 0) -> int:
+    """Inputs of rank r's micro-batch `micro` (gradient accumulation)."""
+    return 1000 + rank + 4096 * micro
 
 
-def seed_targets(rank: int) -> int:
-    return 2000 + rank
+def seed_targets(rank: int, micro: int = 0) -> int:
+    return 2000 + rank + 4096 * micro
 
 
 def splitmix64(x):

@@ -262,3 +262,64 @@ def test_llama_sharded_equals_unsharded_bitexact():
     for i, p in enumerate(table):
         got = nx.all_gather([sh.master[r][i] for r in range(N)], p.numel)
         assert got.tobytes() == rp.master[i].tobytes()
+
+
+# ---------------------------------------------------------------- gradient accumulation
+def test_micro_seeds_distinct_and_micro0_unchanged():
+    assert synth.seed_inputs(3) == synth.seed_inputs(3, 0) == 1003
+    seeds = {synth.seed_inputs(r, m) for r in range(8) for m in range(16)} | \
+            {synth.seed_targets(r, m) for r in range(8) for m in range(16)}
+    assert len(seeds) == 2 * 8 * 16
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_mlp_accumulated_equals_full_batch(n):
+    """n micro-steps x N ranks x b samples == the gradient of the mean loss over
+    all N n b samples (§4.3: the update uses the gradient of
+    the whole mini-batch), up to summation order.  A dropped 1/n, a missing
+    micro-step or a double-counted one fails this."""
+    cfg = synth.MLP_CONFIG1
+    table = synth.mlp_param_table(cfg)
+    N = 2
+    full = ost.init_full_params(table)
+    params = [(full[2 * l].reshape(256, 256), full[2 * l + 1]) for l in range(4)]
+    xs, ts = zip(*[ost.rank_batch(cfg, r, m) for m in range(n) for r in range(N)])
+    _, g_full = om.mlp_fwd_bwd(np.concatenate(xs), np.concatenate(ts), params)
+    sh = ost.ShardedState(table, N, bf16=False)
+    _, gp = ost.sharded_step(sh, cfg, lr=1e-3, micro_steps=n)
+    for i, p in enumerate(table):
+        red = np.concatenate([
+            nx.scale_mean(nx.accumulate(sh.acc[r][i], nx.reduce_scatter([gp[q][i] for q in range(N)], N, r)),
+                          N, n) for r in range(N)])[:p.numel]
+        ref = (g_full[i // 2][i % 2]).reshape(-1)
+        assert np.max(np.abs(red - ref)) <= 1e-5 * np.max(np.abs(ref))
+
+
+def test_accumulation_of_identical_micro_batches_is_exact():
+    """Special case: n = 2 identical micro-batches give exactly the n = 1
+    update (x + x is exact in fp32 and 1/(2N) is a power of two)."""
+    g = synth.values(77, 0, 0, 1000, synth.K_UNIT)
+    one = nx.scale_mean(g, 2, 1)
+    two = nx.scale_mean(nx.accumulate(nx.accumulate(None, g), g), 2, 2)
+    assert one.tobytes() == two.tobytes()
+
+
+@pytest.mark.parametrize("kind", ["mlp", "llama"])
+def test_sharded_equals_replicated_with_accumulation(kind):
+    """§5.6 invariant with n = 2 micro-steps: per-micro RS + fp32 accumulation
+    of the shard == per-micro all-reduce + accumulation of the full gradient."""
+    if kind == "mlp":
+        cfg, table, lr, bf = synth.MLP_CONFIG1, synth.mlp_param_table(synth.MLP_CONFIG1), 1e-3, False
+    else:
+        cfg = synth.small_llama(layers=1, seq=64)
+        table, lr, bf = synth.llama_param_table(cfg), 1.5e-5, True
+    N = 2
+    sh = ost.ShardedState(table, N, bf16=bf)
+    rp = ost.ReplicatedState(table, N, bf16=bf)
+    for _ in range(2):
+        l1, _ = ost.sharded_step(sh, cfg, lr=lr, micro_steps=2)
+        l2 = ost.replicated_step(rp, cfg, lr=lr, micro_steps=2)
+        assert l1 == l2
+    for i, p in enumerate(table):
+        got = nx.all_gather([sh.master[r][i] for r in range(N)], p.numel)
+        assert got.tobytes() == rp.master[i].tobytes()
