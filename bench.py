@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=2)
     ap.add_argument("--seq", type=int, default=2048)
     ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--micro", type=int, default=1, help="gradient-accumulation micro-steps per step (P:362)")
     ap.add_argument("--passes", default="PS", help="S0 | P | S | PS")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default="", help="write the rank-0 profile / plan here")
@@ -233,18 +234,22 @@ def main():
     T = cfg.tokens
     table = synth.llama_param_table(cfg)
     lr = 1.5e-5
+    n_micro = max(1, args.micro)
     if world == 1:
-        ranks = rt.create_ranks(table, 1, local, virtual=True, lr=lr)
+        ranks = rt.create_ranks(table, 1, local, virtual=True, lr=lr, micro_steps=n_micro)
     else:
-        ranks = rt.create_ranks(table, world, local, virtual=False, group=group, rank=rank, lr=lr)
+        ranks = rt.create_ranks(table, world, local, virtual=False, group=group, rank=rank, lr=lr,
+                                micro_steps=n_micro)
     st = ranks[rank]
     from oracle import numerics as nx          # bf16 rounding of the synthetic inputs only
-    x_np = synth.values(synth.seed_inputs(rank), 0, 0, T * cfg.hidden, synth.K_UNIT)
-    t_np = synth.values(synth.seed_targets(rank), 0, 0, T * cfg.hidden, synth.K_UNIT)
+    x_np = np.concatenate([synth.values(synth.seed_inputs(rank, mu), 0, 0, T * cfg.hidden, synth.K_UNIT)
+                           for mu in range(n_micro)])
+    t_np = np.concatenate([synth.values(synth.seed_targets(rank, mu), 0, 0, T * cfg.hidden, synth.K_UNIT)
+                           for mu in range(n_micro)])
     x_host = torch.from_numpy(nx.bf16_bits(x_np).view(np.int16)).view(torch.bfloat16).pin_memory()
     t_host = torch.from_numpy(nx.bf16_bits(t_np).view(np.int16)).view(torch.bfloat16).pin_memory()
-    x_dev = x_host.to(dev).view(T, cfg.hidden)
-    t_dev = t_host.to(dev).view(T, cfg.hidden)
+    x_dev = x_host.to(dev).view(n_micro, T, cfg.hidden)
+    t_dev = t_host.to(dev).view(n_micro, T, cfg.hidden)
     rt.attach_model(ranks, cfg, {rank: x_dev}, {rank: t_dev})
     cs = st.streams[0]
 
@@ -320,7 +325,7 @@ def main():
     if clocks["reasons"] and BAD_REASONS & set(clocks["reasons"]):
         ms, clocks, launches = timed(args.steps)          # re-measure once
         clocks["remeasured"] = True
-    tokens_box = world * T
+    tokens_box = world * T * n_micro
     value = tokens_box / (ms / 1e3)
 
     # ---- per-op breakdown of the last timed step (events recorded in-region)
@@ -349,15 +354,20 @@ def main():
                 "flops_per_step": gemm_fl, "gemm_ms_per_step": gemm_us / 1e3}
     shard_elems = st.layout.shard_elems
     rs_us = by.get("rs", 0)
-    rs_bytes = (28 + 2 * (world - 1)) * shard_elems
+    # per shard element: bf16 grads of N ranks + fp32 master/m/v r+w + bf16 shard w
+    # (28 + 2(N-1) B at n = 1); with accumulation the first micro-step writes the
+    # fp32 accumulator, the middle ones read+write it and the last one reads it
+    per = 2 * world
+    rs_bytes = ((per + 26) if n_micro == 1 else
+                (per + 4) + (n_micro - 2) * (per + 8) + (per + 26 + 4)) * shard_elems
     kernels = {"op_ms_per_step": {k: round(v / 1e3, 3) for k, v in sorted(by.items())},
                "rs_adam": {"bytes_per_step": rs_bytes, "ms_per_step": rs_us / 1e3,
                            "achieved_gbs": rs_bytes / (rs_us * 1e-6) / 1e9 if rs_us else None,
                            "peak_gbs": pk["hbm_gbs"], "bound": "hbm" if world == 1 else "nvlink+hbm"}}
 
     # ---- end to end through the public API with HOST buffers
-    loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
-    lp = rt.view(rt.loss_ptr(st), 1, torch.float32, device=dev)
+    loss_host = torch.empty(n_micro, dtype=torch.float32).pin_memory()
+    lp = rt.view(rt.loss_ptr(st), n_micro, torch.float32, device=dev)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(cs)
@@ -370,15 +380,15 @@ def main():
         with torch.cuda.stream(cs):
             loss_host.copy_(lp, non_blocking=True)
         cs.synchronize()
-        _ = float(loss_host.item())
+        _ = loss_host.tolist()
     e1.record(cs)
     barrier()
     ems = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
     if world > 1:
         dist.all_reduce(ems, op=dist.ReduceOp.MAX, group=group)
     e2e = {"value": tokens_box / (ems.item() / 1e3), "unit": "tokens/s",
-           "h2d_bytes_per_step": 2 * T * cfg.hidden * 2, "d2h_bytes_per_step": 4,
-           "loss": float(loss_host.item())}
+           "h2d_bytes_per_step": 2 * n_micro * T * cfg.hidden * 2, "d2h_bytes_per_step": 4 * n_micro,
+           "loss": loss_host.tolist()[-1]}
 
     # ---- CPU oracle timed on host cores (rank 0, N = 1 only)
     cpu = None
@@ -401,9 +411,12 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                 "config": {"workload": "llama3-8b-stack (BASELINE configs[1]): L=%d h=4096 f=14336 32/8 heads, "
-                                       "seq %d, b=%d per GPU, ZeRO-3 + proactive prefetch%s" %
-                                       (cfg.layers, args.seq, args.batch, " + selective unshard" if "S" in args.passes else ""),
-                           "model": "llama3-8b-shaped synthetic stack (random init)", "global_batch": world * args.batch,
+                                       "seq %d, b=%d per GPU, ZeRO-3 + proactive prefetch%s%s" %
+                                       (cfg.layers, args.seq, args.batch,
+                                        " + selective unshard" if "S" in args.passes else "",
+                                        ", grad accumulation %d" % n_micro if n_micro > 1 else ""),
+                           "model": "llama3-8b-shaped synthetic stack (random init)",
+                           "global_batch": world * args.batch * n_micro, "micro_steps": n_micro,
                            "seq_len": args.seq, "parallelism": "fsdp%d" % world, "passes": args.passes,
                            "mem_budget_M": M, "plan_ms": round(t_plan * 1e3, 2),
                            "unshard_params": len(plan["unshard"]),

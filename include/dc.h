@@ -109,6 +109,10 @@ typedef struct {
   uint64_t seed;                 /* generator seed (synth/gen.py recipe)       */
   uint32_t flags;                /* DC_INIT_WEIGHTS | DC_VIRTUAL_RANKS | ...   */
   uint32_t spin_limit;           /* flag-wait bound in ms, 0 = 20000           */
+  int32_t micro_steps;           /* n gradient-accumulation micro-steps per    */
+                                 /*   optimizer step; 0 -> 1          */
+  float* grad_acc;               /* fp32 [shard_elems], caller-owned; required */
+                                 /*   when micro_steps > 1, else may be NULL   */
 } dc_init_args;
 
 /* Validates, computes the layout, zeroes m/v and (with DC_INIT_WEIGHTS) fills
@@ -183,16 +187,22 @@ dc_status dc_release(dc_ctx* ctx, int32_t release_id, cudaStream_t compute_strea
  * compute stream (waits until every owner consumed the slot's previous use);
  * after the last write dc_grad_slot_publish (posts grad-ready to every owner).
  * dc_reduce_scatter_step, kernel rs_adam: for every param of `layer`, owner
- * r computes g = (((+0 + g_0) + g_1) + ... + g_{N-1}) over fp32(bf16) slice r
- * of every rank's grad slot (peer loads), g *= 1/N, Adam step `step_t`
- * (1-based) on master/m/v (fp32, the op order of reading D18), shard =
- * RNE_bf16(master); then posts "consumed" to every rank.
- * apply_update = 0 is reserved for gradient accumulation (next round).
+ * r computes rs = (((+0 + g_0) + g_1) + ... + g_{N-1}) over fp32(bf16) slice r
+ * of every rank's grad slot (peer loads); then, by micro-step `micro` in
+ * [0, n) of the n = micro_steps of dc_init (gradient accumulation, P:362,
+ * ZeRO-3 semantics P:478 — the accumulated gradient stays partitioned):
+ *   n = 1:          g = rs * fp32(1/N), Adam
+ *   micro = 0:      acc = rs                      (grad_acc shard, fp32)
+ *   0 < micro < n-1: acc = acc + rs
+ *   micro = n-1:    g = (acc + rs) * fp32(1/(N n)), Adam
+ * Adam = step `step_t` (1-based) on master/m/v (fp32, the op order of reading
+ * D18), shard = RNE_bf16(master).  Every mode then posts "consumed" to every
+ * rank.  DC_EINVAL for micro outside [0, n).
  * ------------------------------------------------------------------------ */
 dc_status dc_grad_slot(const dc_ctx* ctx, int32_t layer, void** grad_full_bf16);
 dc_status dc_grad_slot_acquire(dc_ctx* ctx, int32_t layer, cudaStream_t compute_stream);
 dc_status dc_grad_slot_publish(dc_ctx* ctx, int32_t layer, cudaStream_t compute_stream);
-dc_status dc_reduce_scatter_step(dc_ctx* ctx, int32_t layer, int32_t step_t, int32_t apply_update,
+dc_status dc_reduce_scatter_step(dc_ctx* ctx, int32_t layer, int32_t step_t, int32_t micro,
                                  cudaStream_t rs_stream);
 
 /* ------------------------------------------------------------------------
@@ -239,20 +249,22 @@ dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_model** out);
 dc_status dc_model_destroy(dc_model* m);
 /* Bytes of the activation + workspace buffer the caller must provide. */
 dc_status dc_model_act_bytes(const dc_model* m, uint64_t* bytes);
-/* x, target: bf16 [tokens, hidden] device buffers of this rank's micro-batch. */
+/* x, target: bf16 [n][tokens][hidden] device buffers: this rank's n =
+ * micro_steps (dc_init) micro-batches, contiguous. */
 dc_status dc_model_bind(dc_model* m, void* act_buf, uint64_t act_bytes, const void* x,
                         const void* target);
 /* The S_0 schedule of the model as a profile skeleton (p_mem/transient/dur
  * filled from the last profiled step if any, else 0). */
 dc_status dc_model_profile_json(const dc_model* m, char* buf, size_t* len);
-/* One training step through the bound schedule: forward, loss, backward with
- * gathers / releases / reduce-scatter+Adam / offload ops interleaved as
- * planned.  Streams: compute, ag, rs, copy.  profile: 0 off; 1 record per-op
+/* One training step through the bound schedule: per micro-step forward,
+ * loss, backward with gathers / releases / reduce-scatter (+ Adam on the last
+ * micro-step) / offload ops interleaved as planned.  Streams: compute, ag, rs, copy.  profile: 0 off; 1 record per-op
  * CUDA events around every compute / RS op and read them now (synchronises);
  * 2 record only (read by the next dc_model_profile_json, no sync). */
 dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile, cudaStream_t compute,
                         cudaStream_t ag, cudaStream_t rs, cudaStream_t copy);
-/* Device pointer to the fp32 loss of the last step (mean 1/2 (y-t)^2). */
+/* Device pointer to fp32 [n]: the loss (mean 1/2 (y-t)^2) of every
+ * micro-step of the last step. */
 dc_status dc_model_loss_ptr(const dc_model* m, float** loss);
 /* Pointers into the activation buffer of layer l (tests): which = 0 h1, 1 qkv,
  * 2 a, 3 x2, 4 h2, 5 gate|up, 6 act, 7 y (layer output), 8 / 9 the two
@@ -262,7 +274,8 @@ dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t which, void
  * identity at N = 1, so each weight's Adam update (the rs_adam arithmetic on
  * fp32(bf16(grad)), bit-identical) can run in the epilogue of its dW GEMM,
  * leaving only the norm gains to rs_adam.  Ignored for a step whose schedule
- * offloads optimizer state (the reload lands after the dW GEMMs).
+ * offloads optimizer state (the reload lands after the dW GEMMs) and with
+ * gradient accumulation (micro_steps > 1).
  * "side_adam" (default 0; N = 1 only): layer l's reduce-scatter + Adam (the
  * rs_adam arithmetic, bit-identical) is sliced across layer l-1's backward
  * GEMM launches and streamed by idle warps of the CTA-pair GEMM, so the

@@ -87,6 +87,7 @@ def sharded_step(state: ShardedState, cfg, lr, micro_steps=1):
     N = state.world
     state.t += 1
     acc = [[None] * len(state.table) for _ in range(N)]
+    state.micro_losses = []     # [micro][rank]
     for mu in range(micro_steps):
         losses, grads_padded = [], []
         for r in range(N):
@@ -96,6 +97,7 @@ def sharded_step(state: ShardedState, cfg, lr, micro_steps=1):
             losses.append(loss)
             grads_padded.append([np.concatenate([g, np.zeros(N * state.S[i] - g.size, F32)])
                                  for i, g in enumerate(flat)])
+        state.micro_losses.append(losses)
         if mu < micro_steps - 1:
             for r in range(N):
                 for i in range(len(state.table)):

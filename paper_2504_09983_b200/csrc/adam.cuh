@@ -2,7 +2,8 @@
 // DESIGN.md for the operand order), shared by every kernel that applies it:
 // rs_adam (comm.cu), the fused dW epilogue and the GEMM side job
 // (gemm_sm100.cu).  Correctly rounded fp32 intrinsics, no FMA contraction:
-//   g = sum * (1/N)
+//   g = sum * (1/(N n))          (n accumulated micro-steps; sum includes the
+//                                 accumulated fp32 shard: acc + rs, reading D27)
 //   m = m + (1-b1) * (g - m)
 //   v = (b2 * v) + ((1-b2) * g) * g
 //   d = sqrt(v) / c + eps
@@ -60,38 +61,56 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
 //   load_group8:   fp32 master/m/v and the bf16 grads of `world` ranks
 //   finish_group8: grads summed in ascending rank order from +0.0 (bf16 ->
 //                  fp32), Adam on master/m/v, RNE bf16 shard, streaming stores
+//   ACC:           the final micro-step of gradient accumulation adds the
+//                  fp32 accumulated shard: g = acc + sum (one rounding)
 template <int MAXQ>
 struct Group8 {
-  uint4 P[2], M[2], V[2], G[MAXQ];
+  uint4 P[2], M[2], V[2], A[2], G[MAXQ];
 };
 
-template <int MAXQ>
+template <int MAXQ, bool ACC = false>
 __device__ __forceinline__ void load_group8(Group8<MAXQ>& x, const uint8_t* const* gptr, int world,
-                                            const float* mst, const float* mm, const float* vv, uint64_t pol) {
+                                            const float* mst, const float* mm, const float* vv, uint64_t pol,
+                                            const float* acc = nullptr) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     x.P[h] = ld_stream(mst + 4 * h, pol);
     x.M[h] = ld_stream(mm + 4 * h, pol);
     x.V[h] = ld_stream(vv + 4 * h, pol);
+    if constexpr (ACC) x.A[h] = ld_stream(acc + 4 * h, pol);
   }
 #pragma unroll
   for (int q = 0; q < MAXQ; ++q)
     if (q < world) x.G[q] = ld_stream(gptr[q], pol);
 }
 
+// sum over ranks in ascending order from +0.0 of the bf16 grads (fp32)
 template <int MAXQ>
-__device__ __forceinline__ void finish_group8(const Group8<MAXQ>& x, int world, float* mst, float* mm, float* vv,
-                                              __nv_bfloat16* sh, const AdamScalars& a, uint64_t pol) {
-  float g[8];
+__device__ __forceinline__ void sum_ranks8(const uint4* G, int world, float (&g)[8]) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) g[j] = 0.0f;
 #pragma unroll
   for (int q = 0; q < MAXQ; ++q) {
     if (q < world) {
       float f[8];
-      bf16x8_to_f32(x.G[q], f);
+      bf16x8_to_f32(G[q], f);
 #pragma unroll
       for (int j = 0; j < 8; ++j) g[j] = __fadd_rn(g[j], f[j]);
+    }
+  }
+}
+
+template <int MAXQ, bool ACC = false>
+__device__ __forceinline__ void finish_group8(const Group8<MAXQ>& x, int world, float* mst, float* mm, float* vv,
+                                              __nv_bfloat16* sh, const AdamScalars& a, uint64_t pol) {
+  float g[8];
+  sum_ranks8<MAXQ>(x.G, world, g);
+  if constexpr (ACC) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float* af = reinterpret_cast<const float*>(&x.A[h]);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) g[4 * h + t] = __fadd_rn(af[t], g[4 * h + t]);
     }
   }
   float pp[8], m8[8], v8[8];

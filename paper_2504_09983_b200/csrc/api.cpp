@@ -76,6 +76,8 @@ struct dc_ctx {
   Layout L;
   void* shard = nullptr;
   float *master = nullptr, *m = nullptr, *v = nullptr;
+  float* grad_acc = nullptr;            // fp32 accumulated grad shard (micro_steps > 1)
+  int micro_steps = 1;
   std::vector<uint64_t> grad_peers, flag_peers, arena_peers;
   uint64_t grad_bytes = 0, flag_bytes = 0, arena_bytes = 0;
   void* host_pinned = nullptr;
@@ -151,13 +153,17 @@ extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
   if (a->grad_bytes < (uint64_t)(2 * c->L.grad_slot_bytes)) return fail(nullptr, DC_EOOM, "dc_init: grad buffer < 2 slots");
   if (a->flag_bytes < (uint64_t)(c->L.flag_words * 4)) return fail(nullptr, DC_EOOM, "dc_init: flag table too small");
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (!al16(a->shard_param) || !al16(a->master) || !al16(a->exp_avg) || !al16(a->exp_avg_sq))
+  if (!al16(a->shard_param) || !al16(a->master) || !al16(a->exp_avg) || !al16(a->exp_avg_sq) || !al16(a->grad_acc))
     return fail(nullptr, DC_EINVAL, "dc_init: buffers must be 16-byte aligned");
+  if (a->micro_steps < 0 || a->micro_steps > 4096) return fail(nullptr, DC_EINVAL, "dc_init: micro_steps in [0, 4096]");
+  if (a->micro_steps > 1 && !a->grad_acc) return fail(nullptr, DC_EINVAL, "dc_init: micro_steps > 1 needs grad_acc");
   c->rank = a->rank; c->world = a->world; c->device = a->device; c->flags = a->flags;
   c->n_params = a->n_params;
   c->numel.assign(a->numel, a->numel + a->n_params);
   c->layer_of.assign(a->layer_of, a->layer_of + a->n_params);
   c->shard = a->shard_param; c->master = a->master; c->m = a->exp_avg; c->v = a->exp_avg_sq;
+  c->micro_steps = std::max(1, a->micro_steps);
+  c->grad_acc = a->grad_acc;
   c->grad_peers.assign(a->grad_peer_ptrs, a->grad_peer_ptrs + a->world);
   c->flag_peers.assign(a->flag_peer_ptrs, a->flag_peer_ptrs + a->world);
   c->grad_bytes = a->grad_bytes; c->flag_bytes = a->flag_bytes;
@@ -432,8 +438,12 @@ dc_status ctx_post_consumed(dc_ctx* c, int layer, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? DC_OK : fail(c, DC_ECUDA, "post consumed: launch failed");
 }
 
-dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, const std::vector<int>& params, cudaStream_t st) {
+dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, const std::vector<int>& params,
+                                cudaStream_t st) {
   if (dc_status e = check_sticky(c)) return e;
+  if (micro < 0 || micro >= c->micro_steps) return fail(c, DC_EINVAL, "dc_reduce_scatter_step: micro out of range");
+  const int n = c->micro_steps;
+  const int mode = n == 1 ? RS_UPDATE : micro == 0 ? RS_FIRST : micro < n - 1 ? RS_ADD : RS_FINAL;
   const int s = layer & 1;
   const int u = c->layer_use[layer];
   if (u == 0) return fail(c, DC_ESTATE, "dc_reduce_scatter_step: grad slot of layer never acquired");
@@ -453,21 +463,21 @@ dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, const std::vec
   c->rs_done_total += (uint32_t)ctas;
   dc_status r = k_rs_adam(mem, c->world, c->rank, slots.data(), c->myflag(c->L.f_gready + (int64_t)s * c->world),
                           (uint32_t)u, peers_at(c, c->L.f_gcons + (int64_t)s * c->world + c->rank), (uint32_t)u,
-                          c->myflag(c->L.f_rsdone), c->rs_done_total, c->master, c->m, c->v, c->shard, sc, cc,
+                          c->myflag(c->L.f_rsdone), c->rs_done_total, c->master, c->m, c->v, c->shard, c->grad_acc,
+                          mode, n, sc, cc,
                           c->beta1, c->beta2, c->eps, ctas, c->timeout_ns, c->err_dev, st);
   if (r != DC_OK) return fail(c, r, "dc_reduce_scatter_step: launch failed");
   return DC_OK;
 }
 }  // namespace dc
 
-extern "C" dc_status dc_reduce_scatter_step(dc_ctx* c, int32_t layer, int32_t step_t, int32_t apply_update,
+extern "C" dc_status dc_reduce_scatter_step(dc_ctx* c, int32_t layer, int32_t step_t, int32_t micro,
                                             cudaStream_t st) {
   if (!c || layer < 0 || layer >= c->L.n_layers) return fail(c, DC_EINVAL, "dc_reduce_scatter_step: bad layer");
-  if (!apply_update) return fail(c, DC_EINVAL, "dc_reduce_scatter_step: accumulate-only is not implemented");
   if (step_t < 1) return fail(c, DC_EINVAL, "dc_reduce_scatter_step: step_t is 1-based");
   std::vector<int> params;
   for (int i = c->L.layer_first[layer]; i < c->L.layer_first[layer] + c->L.layer_count[layer]; ++i) params.push_back(i);
-  return reduce_scatter_params(c, layer, step_t, params, st);
+  return reduce_scatter_params(c, layer, step_t, micro, params, st);
 }
 
 // ------------------------------------------------------------------ offload
@@ -541,4 +551,5 @@ int ctx_world(const dc_ctx* c) { return c->world; }
 int ctx_rank(const dc_ctx* c) { return c->rank; }
 const dc_schedule* ctx_sched(const dc_ctx* c) { return c->sched; }
 int64_t ctx_numel(const dc_ctx* c, int p) { return c->numel[p]; }
+int ctx_micro_steps(const dc_ctx* c) { return c->micro_steps; }
 }  // namespace dc

@@ -18,6 +18,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "adam.cuh"
 #include "dc_internal.h"
 #include "ptx.cuh"
@@ -145,6 +147,7 @@ struct RsParams {
   uint32_t* done_ctr;
   uint32_t done_target;
   float* master; float* m; float* v; bf16* shard;
+  float* acc;                 // fp32 accumulated grad shard (gradient accumulation)
   float w1, w2, b2, neg_s, c, eps, invN;
   uint64_t timeout_ns;
   uint32_t* err;
@@ -152,7 +155,12 @@ struct RsParams {
 
 constexpr int RS_UNR = 2;   // groups of 8 elements per thread per iteration (loads hoisted)
 
-template <int MAXQ>
+// MODE (gradient accumulation; dc.h dc_reduce_scatter_step):
+//   RS_UPDATE  g = sum * 1/N, Adam                      (n = 1)
+//   RS_FIRST   acc = sum                                (micro-step 0 of n > 1)
+//   RS_ADD     acc = acc + sum                          (micro-steps 1 .. n-2)
+//   RS_FINAL   g = (acc + sum) * 1/(N n), Adam          (micro-step n-1)
+template <int MAXQ, int MODE>
 __global__ void __launch_bounds__(256) rs_adam_kernel(const RsParams p) {
   {   // grad-ready of every rank was awaited by the preceding wait kernel
     const uint64_t pol = policy_evict_first();
@@ -165,23 +173,60 @@ __global__ void __launch_bounds__(256) rs_adam_kernel(const RsParams p) {
       float* mst = p.master + p.store_off[mi];
       float* mm = p.m + p.store_off[mi];
       float* vv = p.v + p.store_off[mi];
+      float* acc = p.acc + p.store_off[mi];
       bf16* sh = p.shard + p.store_off[mi];
-      for (int64_t i0 = tid; i0 < n8; i0 += nthr * RS_UNR) {
-        Group8<MAXQ> x[RS_UNR];
+      if constexpr (MODE == RS_FIRST || MODE == RS_ADD) {
+        for (int64_t i0 = tid; i0 < n8; i0 += nthr * RS_UNR) {
+          uint4 G[RS_UNR][MAXQ], A[RS_UNR][2];
 #pragma unroll
-        for (int u = 0; u < RS_UNR; ++u) {     // every load of RS_UNR groups before any math
-          const int64_t i = i0 + u * nthr;
-          if (i < n8) {
-            const uint8_t* gp[MAXQ];
+          for (int u = 0; u < RS_UNR; ++u) {
+            const int64_t i = i0 + u * nthr;
+            if (i < n8) {
 #pragma unroll
-            for (int q = 0; q < MAXQ; ++q) gp[q] = q < p.world ? p.slot[q] + gbase + i * 16 : nullptr;
-            load_group8<MAXQ>(x[u], gp, p.world, mst + 8 * i, mm + 8 * i, vv + 8 * i, pol);
+              for (int q = 0; q < MAXQ; ++q)
+                if (q < p.world) G[u][q] = ld_stream(p.slot[q] + gbase + i * 16, pol);
+              if constexpr (MODE == RS_ADD) {
+                A[u][0] = ld_stream(acc + 8 * i, pol);
+                A[u][1] = ld_stream(acc + 8 * i + 4, pol);
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < RS_UNR; ++u) {
+            const int64_t i = i0 + u * nthr;
+            if (i < n8) {
+              float g[8];
+              sum_ranks8<MAXQ>(G[u], p.world, g);
+              if constexpr (MODE == RS_ADD) {
+                const float* af = reinterpret_cast<const float*>(&A[u][0]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) g[j] = __fadd_rn(af[j], g[j]);
+              }
+              st_stream(acc + 8 * i, *reinterpret_cast<const uint4*>(&g[0]), pol);
+              st_stream(acc + 8 * i + 4, *reinterpret_cast<const uint4*>(&g[4]), pol);
+            }
           }
         }
+      } else {
+        constexpr bool ACC = MODE == RS_FINAL;
+        for (int64_t i0 = tid; i0 < n8; i0 += nthr * RS_UNR) {
+          Group8<MAXQ> x[RS_UNR];
 #pragma unroll
-        for (int u = 0; u < RS_UNR; ++u) {
-          const int64_t i = i0 + u * nthr;
-          if (i < n8) finish_group8<MAXQ>(x[u], p.world, mst + 8 * i, mm + 8 * i, vv + 8 * i, sh + 8 * i, a, pol);
+          for (int u = 0; u < RS_UNR; ++u) {     // every load of RS_UNR groups before any math
+            const int64_t i = i0 + u * nthr;
+            if (i < n8) {
+              const uint8_t* gp[MAXQ];
+#pragma unroll
+              for (int q = 0; q < MAXQ; ++q) gp[q] = q < p.world ? p.slot[q] + gbase + i * 16 : nullptr;
+              load_group8<MAXQ, ACC>(x[u], gp, p.world, mst + 8 * i, mm + 8 * i, vv + 8 * i, pol, acc + 8 * i);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < RS_UNR; ++u) {
+            const int64_t i = i0 + u * nthr;
+            if (i < n8)
+              finish_group8<MAXQ, ACC>(x[u], p.world, mst + 8 * i, mm + 8 * i, vv + 8 * i, sh + 8 * i, a, pol);
+          }
         }
       }
     }
@@ -200,8 +245,9 @@ __global__ void __launch_bounds__(256) rs_adam_kernel(const RsParams p) {
 dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const uint64_t* slot_peers,
                     const uint32_t* ready_local, uint32_t ready_target, PeerFlags consumed_peers,
                     uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master, float* m,
-                    float* v, void* shard, float s, float c, double beta1, double beta2, double eps, int ctas,
-                    uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st) {
+                    float* v, void* shard, float* acc, int mode, int micro_steps, float s, float c, double beta1,
+                    double beta2, double eps, int ctas, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st) {
+  if (mode < RS_UPDATE || mode > RS_FINAL || (mode != RS_UPDATE && !acc) || micro_steps < 1) return DC_EINVAL;
   if (mem.size() > (size_t)RS_MAXM) return DC_EINVAL;
   RsParams p{};
   p.nm = (int)mem.size();
@@ -219,21 +265,31 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
   p.consumed_value = consumed_value;
   p.done_ctr = done_ctr; p.done_target = done_target;
   p.master = master; p.m = m; p.v = v; p.shard = reinterpret_cast<bf16*>(shard);
+  p.acc = acc;
   p.w1 = (float)(1.0 - beta1);          // fp32(1 - b1) rounded once from double
   p.w2 = (float)(1.0 - beta2);
   p.b2 = (float)beta2;
   p.neg_s = -s;
   p.c = c;
   p.eps = (float)eps;
-  p.invN = (float)(1.0 / (double)world);
+  p.invN = (float)(1.0 / ((double)world * micro_steps));   // fp32(1/(N n)), one rounding
   p.timeout_ns = timeout_ns;
   p.err = err_flag;
   wait_flags_kernel<<<1, 1, 0, st>>>(ready_local, world, ready_target, timeout_ns, err_flag, 0x300u);
   count_launch();
-  if (world == 1) rs_adam_kernel<1><<<ctas, 256, 0, st>>>(p);
-  else if (world == 2) rs_adam_kernel<2><<<ctas, 256, 0, st>>>(p);
-  else if (world <= 4) rs_adam_kernel<4><<<ctas, 256, 0, st>>>(p);
-  else rs_adam_kernel<MAXW><<<ctas, 256, 0, st>>>(p);
+  auto launch = [&](auto mode_c) {
+    constexpr int MODE = decltype(mode_c)::value;
+    if (world == 1) rs_adam_kernel<1, MODE><<<ctas, 256, 0, st>>>(p);
+    else if (world == 2) rs_adam_kernel<2, MODE><<<ctas, 256, 0, st>>>(p);
+    else if (world <= 4) rs_adam_kernel<4, MODE><<<ctas, 256, 0, st>>>(p);
+    else rs_adam_kernel<MAXW, MODE><<<ctas, 256, 0, st>>>(p);
+  };
+  switch (mode) {
+    case RS_UPDATE: launch(std::integral_constant<int, RS_UPDATE>{}); break;
+    case RS_FIRST: launch(std::integral_constant<int, RS_FIRST>{}); break;
+    case RS_ADD: launch(std::integral_constant<int, RS_ADD>{}); break;
+    default: launch(std::integral_constant<int, RS_FINAL>{}); break;
+  }
   if (cudaGetLastError() != cudaSuccess) return DC_ECUDA;
   count_launch();
   return DC_OK;
@@ -270,10 +326,17 @@ cudaError_t preload_comm_kernels() {
   cudaFuncAttributes a;
   cudaError_t e = cudaFuncGetAttributes(&a, ag_push_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, wait_flags_kernel);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel<1>);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel<2>);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel<4>);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel<MAXW>);
+  auto pre = [&](auto mode_c) {
+    constexpr int MODE = decltype(mode_c)::value;
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel<1, MODE>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel<2, MODE>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel<4, MODE>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel<MAXW, MODE>);
+  };
+  pre(std::integral_constant<int, RS_UPDATE>{});
+  pre(std::integral_constant<int, RS_FIRST>{});
+  pre(std::integral_constant<int, RS_ADD>{});
+  pre(std::integral_constant<int, RS_FINAL>{});
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, post_flags_kernel);
   return e;
 }

@@ -40,6 +40,7 @@ int ctx_world(const dc_ctx* c);
 int ctx_rank(const dc_ctx* c);
 const dc_schedule* ctx_sched(const dc_ctx* c);
 int64_t ctx_numel(const dc_ctx* c, int p);
+int ctx_micro_steps(const dc_ctx* c);
 int sched_num_ops(const dc_schedule* s);
 void sched_op(const dc_schedule* s, int i, int* kind, int* id, const int64_t** members, int* nmem,
               int64_t* arena_off, int64_t* bytes, const int** posts, int* nposts, const int** waits, int* nwaits);
@@ -80,7 +81,7 @@ void ctx_adam_scalars(const dc_ctx* c, int step_t, EpiAdam* out);
 // shard-store pointers of a param (fp32 master/m/v, bf16 shard) on this rank
 void ctx_param_state(const dc_ctx* c, int param, float** master, float** m, float** v, void** shard);
 // dc_reduce_scatter_step restricted to a subset of the layer's params
-dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, const std::vector<int>& params,
+dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, const std::vector<int>& params,
                                 cudaStream_t st);
 
 // ------------------------------------------------------------------ kernels
@@ -120,8 +121,11 @@ dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const
 dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const uint64_t* slot_peers,
                     const uint32_t* ready_local, uint32_t ready_target, PeerFlags consumed_peers,
                     uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master,
-                    float* m, float* v, void* shard, float s, float c, double beta1, double beta2,
-                    double eps, int ctas, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st);
+                    float* m, float* v, void* shard, float* acc, int mode, int micro_steps, float s, float c,
+                    double beta1, double beta2, double eps, int ctas, uint64_t timeout_ns, uint32_t* err_flag,
+                    cudaStream_t st);
+// reduce-scatter modes (gradient accumulation)
+enum { RS_UPDATE = 0, RS_FIRST = 1, RS_ADD = 2, RS_FINAL = 3 };
 void k_post_flags(PeerFlags dst, uint32_t value, cudaStream_t st);
 void k_wait_flags(const uint32_t* flags, int n, uint32_t target, uint64_t timeout_ns,
                   uint32_t* err_flag, cudaStream_t st);

@@ -77,6 +77,7 @@ struct dc_model {
   __int128 pending_mnk = 0;          // sum of M*N*K of the hosting GEMMs so far
   int64_t bwd_mnk = 0;               // sum of M*N*K of one layer's backward GEMMs
   int step_t = 0;
+  int n_micro = 1;                   // gradient-accumulation micro-steps (ctx)
   std::string err;
 
   int pid(int layer, int slot) const { return ctx_layout(ctx).layer_first[layer] + slot; }
@@ -110,12 +111,16 @@ static void build_s0(dc_model* m) {
       default: return {};
     }
   };
-  for (int l = 0; l < L; ++l)
-    for (int c : fwd_codes) comp.push_back({K_COMPUTE, c, true, 0, l, params_of(c, l)});
-  comp.push_back({K_COMPUTE, F_LOSS, true, 0, L - 1, {}});
-  for (int l = L - 1; l >= 0; --l) {
-    for (int c : bwd_codes) comp.push_back({K_COMPUTE, c, false, 0, l, params_of(c, l)});
-    comp.push_back({K_RS, RS_OP, false, 0, l, {}});
+  // n micro-steps; every micro-step reduce-scatters its gradients
+  // into the partitioned accumulator, the last one also updates
+  for (int mu = 0; mu < m->n_micro; ++mu) {
+    for (int l = 0; l < L; ++l)
+      for (int c : fwd_codes) comp.push_back({K_COMPUTE, c, true, mu, l, params_of(c, l)});
+    comp.push_back({K_COMPUTE, F_LOSS, true, mu, L - 1, {}});
+    for (int l = L - 1; l >= 0; --l) {
+      for (int c : bwd_codes) comp.push_back({K_COMPUTE, c, false, mu, l, params_of(c, l)});
+      comp.push_back({K_RS, RS_OP, false, mu, l, {}});
+    }
   }
   // S_0: gather before first use, release after last use, per region
   m->s0.clear();
@@ -145,6 +150,7 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   auto m = std::make_unique<dc_model>();
   m->ctx = ctx;
   m->d = *d;
+  m->n_micro = ctx_micro_steps(ctx);
   const Layout& L = ctx_layout(ctx);
   if (d->layers != L.n_layers) return mfail(nullptr, DC_EINVAL, "dc_model_create: layer count mismatch");
   if (d->n_heads % d->n_kv) return mfail(nullptr, DC_EINVAL, "dc_model_create: n_heads % n_kv != 0");
@@ -178,7 +184,7 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   m->ws_dA = take(T * h * 2); m->ws_dB = take(T * h * 2); m->ws_dact = take(T * f * 2);
   m->ws_dgu = take(T * 2 * f * 2); m->ws_dh = take(T * h * 2); m->ws_dx2 = take(T * h * 2);
   m->ws_dqkv = take(T * m->qkvd * 2); m->ws_dgp = take((int64_t)rmsnorm_bwd_blocks((int)T) * h * 4);
-  m->ws_lossp = take(1024 * 4); m->ws_loss = take(256);
+  m->ws_lossp = take(1024 * 4); m->ws_loss = take(4 * (int64_t)m->n_micro);
   m->ws_bytes = off - ws0;
   m->act_bytes = off;
   build_s0(m.get());
@@ -277,7 +283,13 @@ static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t l
   return DC_OK;
 }
 
-static const void* layer_in(const dc_model* m, int l) { return l == 0 ? m->x : m->A(m->la[l - 1].y); }
+// micro-batch mu of the bound [n][T][H] inputs
+static const void* micro_in(const dc_model* m, const void* base, int mu) {
+  return reinterpret_cast<const uint8_t*>(base) + (int64_t)mu * m->d.tokens * m->d.hidden * 2;
+}
+static const void* layer_in(const dc_model* m, int l, int mu) {
+  return l == 0 ? micro_in(m, m->x, mu) : m->A(m->la[l - 1].y);
+}
 
 static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
   const int T = m->d.tokens, H = m->d.hidden, F = m->d.ffn, qd = m->qd, kvd = m->kvd, qkvd = m->qkvd;
@@ -304,7 +316,7 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
   dc_status s = DC_OK;
   switch (o.code) {
     case F_ATTN_NORM:
-      k_rmsnorm_fwd(layer_in(m, l), m->W(l, P_G1), m->A(a.h1), (float*)m->A(a.rstd1), T, H, st);
+      k_rmsnorm_fwd(layer_in(m, l, o.micro), m->W(l, P_G1), m->A(a.h1), (float*)m->A(a.rstd1), T, H, st);
       break;
     case F_QKV:
       s = gemm(m, T, qkvd, H, m->A(a.h1), H, 0, {m->W(l, P_Q), m->W(l, P_K), m->W(l, P_V)}, {H, H, H},
@@ -315,7 +327,7 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       break;
     case F_O:
       s = gemm(m, T, H, qd, m->A(a.a), qd, 0, {m->W(l, P_O)}, {qd}, {H / 256}, 0, 0, m->A(a.x2), H,
-               layer_in(m, l), H, st);
+               layer_in(m, l, o.micro), H, st);
       break;
     case F_MLP_NORM:
       k_rmsnorm_fwd(m->A(a.x2), m->W(l, P_G2), m->A(a.h2), (float*)m->A(a.rstd2), T, H, st);
@@ -333,7 +345,8 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       break;
     case F_LOSS:
       m->cur_d = 0;
-      k_loss(m->A(a.y), m->target, m->A(m->ws_dA), (float*)m->A(m->ws_lossp), (float*)m->A(m->ws_loss),
+      k_loss(m->A(a.y), micro_in(m, m->target, o.micro), m->A(m->ws_dA), (float*)m->A(m->ws_lossp),
+             (float*)m->A(m->ws_loss) + o.micro,
              (int64_t)T * H, st);
       break;
     case B_DOWN:
@@ -387,7 +400,7 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       break;
     case B_ATTN_NORM: {
       const int nb = rmsnorm_bwd_blocks(T);
-      k_rmsnorm_bwd(m->A(m->ws_dh), layer_in(m, l), m->W(l, P_G1), (float*)m->A(a.rstd1), m->A(m->ws_dx2), dnext,
+      k_rmsnorm_bwd(m->A(m->ws_dh), layer_in(m, l, o.micro), m->W(l, P_G1), (float*)m->A(a.rstd1), m->A(m->ws_dx2), dnext,
                     (float*)m->A(m->ws_dgp), T, H, st);
       k_colsum_to_bf16((float*)m->A(m->ws_dgp), nb, H, G(P_G1), st);
       if ((s = dc_grad_slot_publish(m->ctx, l, st)) != DC_OK) return s;
@@ -415,7 +428,8 @@ static void compute_pmem(dc_model* m) {
   const Layout& L = ctx_layout(m->ctx);
   const int N = ctx_world(m->ctx);
   const int64_t T = m->d.tokens, h = m->d.hidden;
-  int64_t stat = L.shard_elems * 6 + 2 * L.grad_slot_bytes + (int64_t)m->ws_bytes + 2 * T * h * 2;
+  int64_t stat = L.shard_elems * 6 + 2 * L.grad_slot_bytes + (int64_t)m->ws_bytes + 2 * m->n_micro * T * h * 2 +
+                 (m->n_micro > 1 ? L.shard_elems * 4 : 0);   // fp32 grad accumulator
   int64_t live_ag = 0, act = 0;
   const LayerAct& a0 = m->la[0];
   auto piece = [&](int code) -> int64_t {
@@ -513,8 +527,9 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
   m->step_t = step_t;
   // an offloaded fragment is reloaded before its layer's RS op (reading D17),
   // i.e. after the dW GEMMs: the fused update needs every state resident
-  m->fused_active = m->fused_adam;
-  m->side_active = m->side_adam && !m->fused_adam;
+  // (both also assume one micro-step: the update consumes the slot directly)
+  m->fused_active = m->fused_adam && m->n_micro == 1;
+  m->side_active = m->side_adam && !m->fused_adam && m->n_micro == 1;
   m->pending_layer = -1;
   for (int i = 0, n = sched_num_ops(sc); i < n && (m->fused_active || m->side_active); ++i) {
     int kind, id, nm, np, nw;
@@ -571,14 +586,15 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
         cudaStreamWaitEvent(rss, m->ev_pos[id], 0);
         if (profile) cudaEventRecord(m->ev_t0[id], rss);
         if (m->fused_active)   // the weights were updated in their dW epilogues; the norm gains remain
-          s = reduce_scatter_params(m->ctx, o.layer, step_t, {m->pid(o.layer, P_G1), m->pid(o.layer, P_G2)}, rss);
+          s = reduce_scatter_params(m->ctx, o.layer, step_t, o.micro, {m->pid(o.layer, P_G1), m->pid(o.layer, P_G2)},
+                                    rss);
         else if (m->side_active && o.layer > 0) {   // rides on layer l-1's backward GEMMs
           s = ctx_side_job(m->ctx, o.layer, step_t, &m->pending);
           m->pending_layer = o.layer;
           m->pending_assigned = 0;
           m->pending_mnk = 0;
         } else
-          s = dc_reduce_scatter_step(m->ctx, o.layer, step_t, 1, rss);
+          s = dc_reduce_scatter_step(m->ctx, o.layer, step_t, o.micro, rss);
         if (profile) cudaEventRecord(m->ev_t1[id], rss);
         break;
       }

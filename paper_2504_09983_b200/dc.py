@@ -53,7 +53,8 @@ class InitArgs(C.Structure):
                 ("flag_peer_ptrs", p_u64), ("flag_bytes", C.c_uint64),
                 ("host_pinned", vp), ("host_pinned_bytes", C.c_uint64),
                 ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
-                ("seed", C.c_uint64), ("flags", C.c_uint32), ("spin_limit", C.c_uint32)]
+                ("seed", C.c_uint64), ("flags", C.c_uint32), ("spin_limit", C.c_uint32),
+                ("micro_steps", C.c_int32), ("grad_acc", vp)]
 
 
 class PlanOpts(C.Structure):

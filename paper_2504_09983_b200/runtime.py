@@ -42,6 +42,7 @@ class RankState:
         self.tensors = {}
         self.streams = None
         self.sched = None
+        self.micro_steps = 1
 
     def stream_handles(self):
         return [s.cuda_stream for s in self.streams]
@@ -86,12 +87,14 @@ def _alloc_symmetric(nbytes, group, device):
 
 
 def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr=1e-3, beta1=0.9,
-                 beta2=0.999, eps=1e-8, seed=0, init=True, host_pinned_bytes=0, spin_ms=20000, extra_flags=0):
+                 beta2=0.999, eps=1e-8, seed=0, init=True, host_pinned_bytes=0, spin_ms=20000, extra_flags=0,
+                 micro_steps=1):
     """Allocate and dc_init the ranks this process drives: all N virtual ranks,
-    or this process's rank when `virtual` is False."""
+    or this process's rank when `virtual` is False.  micro_steps > 1: gradient
+    accumulation (an fp32 grad-accumulation shard is allocated)."""
     dev = torch.device("cuda", device)
     numel, layer_of, init_k = table_arrays(table)
-    mops = max_s0_ops(table)
+    mops = max_s0_ops(table, micro_steps)
     la = dc.LayoutArgs(world, len(table), dc.i64_array(numel), dc.i32_array(layer_of), mops)
     lay = dc.Layout()
     dc.check(dc.lib.dc_layout_query(C.byref(la), C.byref(lay)))
@@ -115,6 +118,8 @@ def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr
         t["master"] = torch.empty(lay.shard_elems, dtype=torch.float32, device=dev)
         t["m"] = torch.empty(lay.shard_elems, dtype=torch.float32, device=dev)
         t["v"] = torch.empty(lay.shard_elems, dtype=torch.float32, device=dev)
+        if micro_steps > 1:
+            t["acc"] = torch.empty(lay.shard_elems, dtype=torch.float32, device=dev)
         if host_pinned_bytes:
             t["host"] = torch.empty(host_pinned_bytes, dtype=torch.uint8, pin_memory=True)
         a = dc.InitArgs()
@@ -134,6 +139,9 @@ def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr
         a.seed = seed
         a.flags = (dc.DC_INIT_WEIGHTS if init else 0) | (dc.DC_VIRTUAL_RANKS if virtual else 0) | extra_flags
         a.spin_limit = spin_ms
+        a.micro_steps = micro_steps
+        a.grad_acc = t["acc"].data_ptr() if micro_steps > 1 else None
+        st.micro_steps = micro_steps
         out = C.c_void_p()
         dc.check(dc.lib.dc_init(C.byref(a), C.byref(out)))
         st.ctx = out
@@ -162,7 +170,8 @@ def grad_offset(st, p):
 
 
 def attach_model(ranks, cfg, xs, targets):
-    """dc_model_create + bind per rank; xs/targets: dict rank -> bf16 device [T, H]."""
+    """dc_model_create + bind per rank; xs/targets: dict rank -> bf16 device
+    [n, T, H] (n = micro_steps micro-batches; [T, H] when n = 1)."""
     d = dc.ModelDims(cfg.hidden, cfg.ffn, cfg.n_heads, cfg.n_kv, cfg.head_dim, cfg.layers, cfg.tokens)
     for r, st in ranks.items():
         m = C.c_void_p()

@@ -98,8 +98,9 @@ def mlp_param_table(cfg: ModelConfig) -> List[ParamSpec]:
 
 # --- compute-op graph -------------------------------------------------------
 # Each op: dict(name, kind in {"compute","rs"}, phase in {"fwd","bwd"}, micro,
-# layer, params=[param ids consumed]).  RS(l) is the reduce-scatter + Adam of
-# layer l, placed after the layer's last backward op.
+# layer, params=[param ids consumed]).  RS(l) is the reduce-scatter (+ Adam on
+# the last micro-step) of layer l, placed after the layer's last backward op
+# of every micro-step.
 
 LLAMA_FWD = (("attn_norm", ("attn_norm",)), ("qkv", ("wq", "wk", "wv")),
              ("attn_mix", ()), ("o_proj", ("wo",)), ("mlp_norm", ("mlp_norm",)),
@@ -124,9 +125,9 @@ def llama_compute_ops(cfg: ModelConfig, micro_steps: int = 1):
             for nm, ps in LLAMA_BWD:
                 ops.append(dict(name=nm, kind="compute", phase="bwd", micro=mu, layer=l,
                                 params=[pid(l, p) for p in ps]))
-            if mu == micro_steps - 1:
-                ops.append(dict(name="rs", kind="rs", phase="bwd", micro=mu, layer=l,
-                                params=[]))
+            # every micro-step reduce-scatters into the partitioned fp32
+            # accumulator; the last one also applies Adam
+            ops.append(dict(name="rs", kind="rs", phase="bwd", micro=mu, layer=l, params=[]))
     return ops
 
 

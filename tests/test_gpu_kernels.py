@@ -141,62 +141,89 @@ def test_gemm_rejects_bad_shapes():
 
 
 # ------------------------------------------------------------------ RS + Adam
-def _grads(world, table, S, q, step):
+def _grads(world, table, S, q, step, micro=0):
     out = []
     for i, p in enumerate(table):
-        g = nx.rne_bf16(seeded(500 + 10 * step + q, i, p.numel, std=0.01))
+        g = nx.rne_bf16(seeded(500 + 10 * step + q + 4096 * micro, i, p.numel, std=0.01))
         out.append(np.concatenate([g, np.zeros(world * S[i] - p.numel, np.float32)]))
     return out
 
 
-@pytest.mark.parametrize("world", [1, 2, 4])
-def test_rs_adam_virtual_ranks(world):
+def _bits_equal(got, ref, what):
+    rel = np.abs(got.astype(np.float64) - ref) / np.maximum(np.abs(ref), 1e-30)
+    assert rel.max() <= 1e-5, (what, rel.max())
+    assert got.tobytes() == ref.tobytes(), (what, "not bit-exact")
+
+
+@pytest.mark.parametrize("world,n", [(1, 1), (2, 1), (4, 1), (1, 2), (2, 3), (4, 2)])
+def test_rs_adam_virtual_ranks(world, n):
+    """rs_adam (n = 1) and its gradient-accumulation modes (n > 1: acc = rs,
+    acc += rs, then Adam on (acc + rs) / (N n)) vs the oracle, bit-exact,
+    two optimizer steps, the accumulator checked after every micro-step."""
     cfg = synth.small_llama(layers=2)
     table = synth.llama_param_table(cfg)
     lr = 1e-3
-    ranks = rt.create_ranks(table, world, lr=lr)
+    ranks = rt.create_ranks(table, world, lr=lr, micro_steps=n)
     S = [nx.shard_len(p.numel, world) for p in table]
     full = ost.init_full_params(table)
     o_master = [[nx.shard_of(full[i], world, r) for i in range(len(table))] for r in range(world)]
     o_m = [[np.zeros(S[i], np.float32) for i in range(len(table))] for r in range(world)]
     o_v = [[np.zeros(S[i], np.float32) for i in range(len(table))] for r in range(world)]
     for step in (1, 2):
-        grads = {q: _grads(world, table, S, q, step) for q in range(world)}
+        o_acc = [[None] * len(table) for _ in range(world)]
+        for mu in range(n):
+            grads = {q: _grads(world, table, S, q, step, mu) for q in range(world)}
 
-        def work(st):
-            cs, rs = st.streams[0], st.streams[2]
-            for layer in (1, 0):
-                dc.check(dc.lib.dc_grad_slot_acquire(st.ctx, layer, cs.cuda_stream), st.ctx)
-                slot = C.c_void_p()
-                dc.check(dc.lib.dc_grad_slot(st.ctx, layer, C.byref(slot)), st.ctx)
-                with torch.cuda.stream(cs):
-                    for i, p in enumerate(table):
-                        if p.layer != layer:
-                            continue
-                        v = rt.view(slot.value + rt.grad_offset(st, i), world * S[i], torch.bfloat16)
-                        v.copy_(bf16_tensor(grads[st.rank][i]))
-                dc.check(dc.lib.dc_grad_slot_publish(st.ctx, layer, cs.cuda_stream), st.ctx)
-                ev = torch.cuda.Event()
-                ev.record(cs)
-                rs.wait_event(ev)                    # local order, as the executor does
-                dc.check(dc.lib.dc_reduce_scatter_step(st.ctx, layer, step, 1, rs.cuda_stream), st.ctx)
-            torch.cuda.synchronize()
+            def work(st):
+                cs, rs = st.streams[0], st.streams[2]
+                for layer in (1, 0):
+                    dc.check(dc.lib.dc_grad_slot_acquire(st.ctx, layer, cs.cuda_stream), st.ctx)
+                    slot = C.c_void_p()
+                    dc.check(dc.lib.dc_grad_slot(st.ctx, layer, C.byref(slot)), st.ctx)
+                    with torch.cuda.stream(cs):
+                        for i, p in enumerate(table):
+                            if p.layer != layer:
+                                continue
+                            v = rt.view(slot.value + rt.grad_offset(st, i), world * S[i], torch.bfloat16)
+                            v.copy_(bf16_tensor(grads[st.rank][i]))
+                    dc.check(dc.lib.dc_grad_slot_publish(st.ctx, layer, cs.cuda_stream), st.ctx)
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                    rs.wait_event(ev)                    # local order, as the executor does
+                    dc.check(dc.lib.dc_reduce_scatter_step(st.ctx, layer, step, mu, rs.cuda_stream), st.ctx)
+                torch.cuda.synchronize()
 
-        rt.run_parallel(ranks, work)
-        rt.poll(ranks)
+            rt.run_parallel(ranks, work)
+            rt.poll(ranks)
+            for r, st in ranks.items():
+                for i, p in enumerate(table):
+                    gq = [grads[q][i] for q in range(world)]
+                    off, sz = rt.shard_range(st, i)
+                    if mu < n - 1:
+                        o_acc[r][i] = nx.accumulate(o_acc[r][i], nx.reduce_scatter(gq, world, r))
+                        _bits_equal(st.tensors["acc"][off:off + sz].cpu().numpy(), o_acc[r][i], (r, p.name, mu))
+                        continue
+                    mst, m1, v1, shb = nx.rs_adam_shard(gq, o_master[r][i], o_m[r][i], o_v[r][i], world, r,
+                                                        step, lr, acc=o_acc[r][i], micro_steps=n)
+                    o_master[r][i], o_m[r][i], o_v[r][i] = mst, m1, v1
         for r, st in ranks.items():
             ms, mm, vv = (st.tensors[k].cpu().numpy() for k in ("master", "m", "v"))
             sh = st.tensors["shard"].view(torch.int16).cpu().numpy().view(np.uint16)
             for i, p in enumerate(table):
-                mst, m1, v1, shb = nx.rs_adam_shard([grads[q][i] for q in range(world)], o_master[r][i],
-                                                    o_m[r][i], o_v[r][i], world, r, step, lr)
-                o_master[r][i], o_m[r][i], o_v[r][i] = mst, m1, v1
-                off, n = rt.shard_range(st, i)
-                for got, ref in ((ms[off:off + n], mst), (mm[off:off + n], m1), (vv[off:off + n], v1)):
-                    rel = np.abs(got - ref) / np.maximum(np.abs(ref), 1e-30)
-                    assert rel.max() <= 1e-5, (r, p.name, rel.max())
-                    assert got.tobytes() == ref.tobytes(), (r, p.name, "not bit-exact")
-                assert np.array_equal(sh[off:off + n], nx.bf16_bits(mst))
+                off, sz = rt.shard_range(st, i)
+                for k, got, ref in (("master", ms, o_master), ("m", mm, o_m), ("v", vv, o_v)):
+                    _bits_equal(got[off:off + sz], ref[r][i], (r, p.name, k, step))
+                assert np.array_equal(sh[off:off + sz], nx.bf16_bits(o_master[r][i]))
+
+
+def test_rs_micro_out_of_range():
+    cfg = synth.small_llama(layers=1)
+    table = synth.llama_param_table(cfg)
+    st = rt.create_ranks(table, 1, micro_steps=2)[0]
+    cs = st.streams[0]
+    dc.check(dc.lib.dc_grad_slot_acquire(st.ctx, 0, cs.cuda_stream), st.ctx)
+    assert dc.lib.dc_reduce_scatter_step(st.ctx, 0, 1, 2, cs.cuda_stream) == dc.DC_EINVAL
+    assert dc.lib.dc_reduce_scatter_step(st.ctx, 0, 1, -1, cs.cuda_stream) == dc.DC_EINVAL
 
 
 # ------------------------------------------------------------------ all-gather
