@@ -244,6 +244,10 @@ typedef struct {
   int32_t kernel;                /* 0 auto (CTA pairs), 1 one-CTA tiles, 2 pairs */
 } dc_gemm_args;
 dc_status dc_gemm(const dc_gemm_args* g, cudaStream_t stream);
+/* CTA pairs the default pair kernel keeps co-resident on this device
+ * (cudaOccupancyMaxActiveClusters; the persistent grid never exceeds it);
+ * -1 on a CUDA error. */
+int32_t dc_gemm_pair_slots(void);
 
 dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_model** out);
 dc_status dc_model_destroy(dc_model* m);

@@ -98,7 +98,7 @@ struct dc_ctx {
   int slot_use[2] = {0, 0};
   std::vector<int> layer_use;
   uint32_t rs_done_total = 0;
-  int rs_ctas = 0;
+  int rs_ctas = 0, rs_threads = 256;
   // error word: host-mapped pinned (device writes on a flag-wait timeout)
   uint32_t* err_host = nullptr;
   uint32_t* err_dev = nullptr;
@@ -176,6 +176,7 @@ extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
   c->layer_use.assign(c->L.n_layers, 0);
   c->rs_ctas = 296;                     // rs_adam grid, two CTAs per SM (DC_RS_CTAS overrides)
   if (const char* e = getenv("DC_RS_CTAS")) c->rs_ctas = std::max(1, atoi(e));
+  if (const char* e = getenv("DC_RS_THREADS")) c->rs_threads = atoi(e) == 128 ? 128 : 256;
   DC_CUDA_TRY(cudaSetDevice(a->device), &c->err);
   DC_CUDA_TRY(preload_glue_kernels(), &c->err);
   DC_CUDA_TRY(preload_comm_kernels(), &c->err);
@@ -459,13 +460,13 @@ dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, con
   const double bc2 = 1.0 - std::pow(c->beta2, step_t);
   const float sc = (float)(c->lr / bc1);
   const float cc = (float)std::sqrt(bc2);
-  int ctas = (int)std::min<int64_t>(c->rs_ctas, std::max<int64_t>(1, elems / 8 / 256));
+  int ctas = (int)std::min<int64_t>(c->rs_ctas, std::max<int64_t>(1, elems / 8 / c->rs_threads));
   c->rs_done_total += (uint32_t)ctas;
   dc_status r = k_rs_adam(mem, c->world, c->rank, slots.data(), c->myflag(c->L.f_gready + (int64_t)s * c->world),
                           (uint32_t)u, peers_at(c, c->L.f_gcons + (int64_t)s * c->world + c->rank), (uint32_t)u,
                           c->myflag(c->L.f_rsdone), c->rs_done_total, c->master, c->m, c->v, c->shard, c->grad_acc,
                           mode, n, sc, cc,
-                          c->beta1, c->beta2, c->eps, ctas, c->timeout_ns, c->err_dev, st);
+                          c->beta1, c->beta2, c->eps, ctas, c->rs_threads, c->timeout_ns, c->err_dev, st);
   if (r != DC_OK) return fail(c, r, "dc_reduce_scatter_step: launch failed");
   return DC_OK;
 }

@@ -246,7 +246,9 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
                     const uint32_t* ready_local, uint32_t ready_target, PeerFlags consumed_peers,
                     uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master, float* m,
                     float* v, void* shard, float* acc, int mode, int micro_steps, float s, float c, double beta1,
-                    double beta2, double eps, int ctas, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st) {
+                    double beta2, double eps, int ctas, int threads, uint64_t timeout_ns, uint32_t* err_flag,
+                    cudaStream_t st) {
+  if (threads != 128 && threads != 256) return DC_EINVAL;
   if (mode < RS_UPDATE || mode > RS_FINAL || (mode != RS_UPDATE && !acc) || micro_steps < 1) return DC_EINVAL;
   if (mem.size() > (size_t)RS_MAXM) return DC_EINVAL;
   RsParams p{};
@@ -279,10 +281,10 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
   count_launch();
   auto launch = [&](auto mode_c) {
     constexpr int MODE = decltype(mode_c)::value;
-    if (world == 1) rs_adam_kernel<1, MODE><<<ctas, 256, 0, st>>>(p);
-    else if (world == 2) rs_adam_kernel<2, MODE><<<ctas, 256, 0, st>>>(p);
-    else if (world <= 4) rs_adam_kernel<4, MODE><<<ctas, 256, 0, st>>>(p);
-    else rs_adam_kernel<MAXW, MODE><<<ctas, 256, 0, st>>>(p);
+    if (world == 1) rs_adam_kernel<1, MODE><<<ctas, threads, 0, st>>>(p);
+    else if (world == 2) rs_adam_kernel<2, MODE><<<ctas, threads, 0, st>>>(p);
+    else if (world <= 4) rs_adam_kernel<4, MODE><<<ctas, threads, 0, st>>>(p);
+    else rs_adam_kernel<MAXW, MODE><<<ctas, threads, 0, st>>>(p);
   };
   switch (mode) {
     case RS_UPDATE: launch(std::integral_constant<int, RS_UPDATE>{}); break;

@@ -122,8 +122,8 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
                     const uint32_t* ready_local, uint32_t ready_target, PeerFlags consumed_peers,
                     uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master,
                     float* m, float* v, void* shard, float* acc, int mode, int micro_steps, float s, float c,
-                    double beta1, double beta2, double eps, int ctas, uint64_t timeout_ns, uint32_t* err_flag,
-                    cudaStream_t st);
+                    double beta1, double beta2, double eps, int ctas, int threads, uint64_t timeout_ns,
+                    uint32_t* err_flag, cudaStream_t st);
 // reduce-scatter modes (gradient accumulation)
 enum { RS_UPDATE = 0, RS_FIRST = 1, RS_ADD = 2, RS_FINAL = 3 };
 void k_post_flags(PeerFlags dst, uint32_t value, cudaStream_t st);

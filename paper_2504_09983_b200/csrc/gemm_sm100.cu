@@ -246,34 +246,38 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ----------------------------------------------------------- MMA issuer
-      int stage = 0; uint32_t phase = 0;
-      int acc = 0; uint32_t aphase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+    // ------------------------------------------------------------- MMA issuer
+    // The whole warp walks the loop (warp-uniform descriptors stay in uniform
+    // registers); one elected lane issues each tcgen05 instruction.
+    const uint64_t a_d0 = p.a_mn ? ptx::umma_desc_sw128(ptx::smem_u32(smA), 8192, 1024)
+                                 : ptx::umma_desc_sw128(ptx::smem_u32(smA), 16, 1024);
+    const uint64_t b_d0 = p.b_mn ? ptx::umma_desc_sw128(ptx::smem_u32(smB), 8192, 1024)
+                                 : ptx::umma_desc_sw128(ptx::smem_u32(smB), 16, 1024);
+    const uint32_t a_ks = p.a_mn ? 2048 >> 4 : 32 >> 4;     // descriptor step per UMMA_K
+    const uint32_t b_ks = p.b_mn ? 2048 >> 4 : 32 >> 4;
+    int stage = 0; uint32_t phase = 0;
+    int acc = 0; uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d = tmem_base + acc * BN;
+      for (int kb = 0; kb < p.k_blocks; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
-        const uint32_t d = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
-          ptx::tc_fence_after();
-          const uint32_t a_addr = ptx::smem_u32(smA + stage * A_STAGE);
-          const uint32_t b_addr = ptx::smem_u32(smB + stage * B_STAGE);
+        const uint64_t ad = a_d0 + (uint32_t)(stage * (A_STAGE >> 4));
+        const uint64_t bd = b_d0 + (uint32_t)(stage * (B_STAGE >> 4));
+        if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            uint64_t ad, bd;
-            if (!p.a_mn) ad = ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
-            else         ad = ptx::umma_desc_sw128(a_addr + k * 2048, 8192, 1024);
-            if (!p.b_mn) bd = ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
-            else         bd = ptx::umma_desc_sw128(b_addr + k * 2048, 8192, 1024);
-            ptx::umma_f16(d, ad, bd, p.idesc, (kb | k) != 0);
-          }
+          for (int k = 0; k < BK / UMMA_K; ++k)
+            ptx::umma_f16(d, ad + k * a_ks, bd + k * b_ks, p.idesc, (kb | k) != 0);
           ptx::umma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        ptx::umma_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; aphase ^= 1; }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (ptx::elect_one()) ptx::umma_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------- epilogue
@@ -483,8 +487,15 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
-      // ----------------------------------------------------------- MMA issuer (leader)
+    if (rank == 0) {
+      // ----------------------------------------------------------- MMA issuer (leader CTA)
+      // whole warp walks the loop (uniform descriptors); one elected lane issues
+      const uint64_t a_d0 = p.a_mn ? ptx::umma_desc_sw128(ptx::smem_u32(smA), 8192, 1024)
+                                   : ptx::umma_desc_sw128(ptx::smem_u32(smA), 16, 1024);
+      const uint64_t b_d0 = p.b_mn ? ptx::umma_desc_sw128(ptx::smem_u32(smB), 8192, 1024)
+                                   : ptx::umma_desc_sw128(ptx::smem_u32(smB), 16, 1024);
+      const uint32_t a_ks = p.a_mn ? 2048 >> 4 : 32 >> 4;
+      const uint32_t b_ks = p.b_mn ? 2048 >> 4 : 32 >> 4;
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t aphase = 0;
       for (int tile = pair; tile < num_tiles; tile += npairs) {
@@ -494,21 +505,19 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a_addr = ptx::smem_u32(smA + stage * A2_STAGE);
-          const uint32_t b_addr = ptx::smem_u32(smB + stage * Pair<BNT, ST>::B_STAGE);
+          const uint64_t ad = a_d0 + (uint32_t)(stage * (A2_STAGE >> 4));
+          const uint64_t bd = b_d0 + (uint32_t)(stage * (Pair<BNT, ST>::B_STAGE >> 4));
+          if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            uint64_t ad, bd;
-            if (!p.a_mn) ad = ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
-            else         ad = ptx::umma_desc_sw128(a_addr + k * 2048, 8192, 1024);
-            if (!p.b_mn) bd = ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
-            else         bd = ptx::umma_desc_sw128(b_addr + k * 2048, 8192, 1024);
-            ptx::umma_f16_2sm(d, ad, bd, p.idesc, (kb | k) != 0);
+            for (int k = 0; k < BK / UMMA_K; ++k)
+              ptx::umma_f16_2sm(d, ad + k * a_ks, bd + k * b_ks, p.idesc, (kb | k) != 0);
+            ptx::umma_commit_2sm_mc(&empty[stage], 0x3);
           }
-          ptx::umma_commit_2sm_mc(&empty[stage], 0x3);
+          __syncwarp();
           if (++stage == Pair<BNT, ST>::STAGES) { stage = 0; phase ^= 1; }
         }
-        ptx::umma_commit_2sm_mc(&tfull[acc], 0x3);
+        if (ptx::elect_one()) ptx::umma_commit_2sm_mc(&tfull[acc], 0x3);
+        __syncwarp();
         if (++acc == 2) { acc = 0; aphase ^= 1; }
       }
     }
@@ -630,6 +639,31 @@ static int num_sms_cached() {
   return n;
 }
 
+// 0: 256-wide 6 stages (default), 2: 256-wide 7 stages (DC_GEMM_STAGES=7)
+static int env_st_pick() {
+  static const int v = (getenv("DC_GEMM_STAGES") && atoi(getenv("DC_GEMM_STAGES")) == 7) ? 2 : 0;
+  return v;
+}
+
+// co-resident 2-CTA clusters of a pair-kernel configuration (0: 256/6, 1: 128/9,
+// 2: 256/7), from cudaOccupancyMaxActiveClusters; filled by preload
+static int g_pair_slots[3] = {0, 0, 0};
+static int pair_slots(int cfg) { return g_pair_slots[cfg]; }
+
+template <int BN_, int ST_>
+static cudaError_t query_pair_slots(int* out) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * 148, 1, 1);
+  cfg.blockDim = dim3(GEMM2_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = Pair<BN_, ST_>::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaOccupancyMaxActiveClusters(out, gemm2_bf16_sm100<BN_, ST_, 0>, &cfg);
+}
+
 dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* err, const EpiAdam* adam,
                       const SideJob* side) {
   if (g->M <= 0 || g->N <= 0 || g->K <= 0 || (g->N % 8) || (g->K % 8) || g->n_bseg < 1 || g->n_bseg > 4) {
@@ -713,8 +747,12 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
   }
   const int tiles = p.m_tiles * p.n_tiles;
   if (pair) {
-    const int pairs = std::min(tiles, sms / 2);
-    static const int env_st = getenv("DC_GEMM_STAGES") ? atoi(getenv("DC_GEMM_STAGES")) : 6;
+    // persistent grid: never more pairs than can be co-resident (an odd SM
+    // count in a GPC leaves an SM without a partner; a non-resident pair
+    // would run as a second wave after the others finished)
+    const int slots = pair_slots(bnt == 128 ? 1 : env_st_pick());
+    const int pairs = std::min(tiles, std::min(sms / 2, slots > 0 ? slots : sms / 2));
+    const int env_st = env_st_pick() == 2 ? 7 : 6;
     const int g2 = 2 * pairs;
 #define DC_PAIR_LAUNCH(BN_, ST_)                                                                   \
     (p.epi ? gemm2_bf16_sm100<BN_, ST_, 1><<<g2, GEMM2_THREADS, Pair<BN_, ST_>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p) \
@@ -735,6 +773,13 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
 }
 
 }  // namespace dc
+
+extern "C" int32_t dc_gemm_pair_slots(void) {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] { err = dc::preload_gemm_kernels(); });
+  return err == cudaSuccess ? dc::pair_slots(0) : -1;
+}
 
 extern "C" dc_status dc_gemm(const dc_gemm_args* g, cudaStream_t stream) {
   std::string err;
@@ -766,6 +811,9 @@ cudaError_t preload_gemm_kernels() {
   DC_PAIR_ATTR(128, 9, 0)
   DC_PAIR_ATTR(128, 9, 1)
 #undef DC_PAIR_ATTR
+  if (e == cudaSuccess) e = query_pair_slots<256, 6>(&g_pair_slots[0]);
+  if (e == cudaSuccess) e = query_pair_slots<128, 9>(&g_pair_slots[1]);
+  if (e == cudaSuccess) e = query_pair_slots<256, 7>(&g_pair_slots[2]);
   return e;
 }
 }  // namespace dc

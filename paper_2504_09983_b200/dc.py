@@ -10,6 +10,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdc_b200.so")
+if os.environ.get("DC_LIB_AB"):      # A/B experiments: another in-tree build of the same library
+    LIB_PATH = os.path.join(os.path.dirname(_HERE), os.environ["DC_LIB_AB"])
 
 if not os.path.exists(LIB_PATH):
     raise ImportError("libdc_b200.so not built: run `python -m paper_2504_09983_b200.build` "
@@ -106,6 +108,7 @@ _sig = {
     "dc_offload_fragments": (C.c_int, [vp, C.c_int64, C.POINTER(Fragment), p_i32]),
     "dc_offload": (C.c_int, [vp, C.c_int32, C.c_int32, vp]),
     "dc_gemm": (C.c_int, [C.POINTER(GemmArgs), vp]),
+    "dc_gemm_pair_slots": (C.c_int32, []),
     "dc_model_create": (C.c_int, [vp, C.POINTER(ModelDims), C.POINTER(vp)]),
     "dc_model_destroy": (C.c_int, [vp]),
     "dc_model_act_bytes": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
