@@ -242,6 +242,11 @@ typedef struct {
   const void* R; int64_t ldr;
   int32_t num_sms;               /* 0 = all SMs                                 */
   int32_t kernel;                /* 0 auto (CTA pairs), 1 one-CTA tiles, 2 pairs */
+  int32_t stream_k;              /* 1: split the last waves' k-blocks evenly over */
+                                 /* the pairs (fp32 partials through a per-stream */
+                                 /* workspace, deterministic). Only when no other */
+                                 /* persistent GEMM can run concurrently on the  */
+                                 /* device (it spins on another pair's partial). */
 } dc_gemm_args;
 dc_status dc_gemm(const dc_gemm_args* g, cudaStream_t stream);
 /* CTA pairs the default pair kernel keeps co-resident on this device
@@ -284,7 +289,11 @@ dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t which, void
  * rs_adam arithmetic, bit-identical) is sliced across layer l-1's backward
  * GEMM launches and streamed by idle warps of the CTA-pair GEMM, so the
  * HBM-bound update overlaps tensor-bound work instead of competing for SMs;
- * layer 0's update stays an rs_adam launch.  Same offload exclusion. */
+ * layer 0's update stays an rs_adam launch.  Same offload exclusion.
+ * "stream_k" (default 1 unless N > 1 virtual ranks share the GPU): the layer
+ * GEMMs split their last waves with stream-K (dc_gemm_args.stream_k).
+ * "rs_overlap" (default 1): reduce-scatter + Adam on the rs stream beside the
+ * backward GEMMs; 0 runs it in compute-stream order. */
 dc_status dc_model_set_option(dc_model* m, const char* key, int64_t value);
 /* Number of kernels the last dc_model_step launched. */
 dc_status dc_model_launch_count(const dc_model* m, int64_t* n);

@@ -553,4 +553,5 @@ int ctx_rank(const dc_ctx* c) { return c->rank; }
 const dc_schedule* ctx_sched(const dc_ctx* c) { return c->sched; }
 int64_t ctx_numel(const dc_ctx* c, int p) { return c->numel[p]; }
 int ctx_micro_steps(const dc_ctx* c) { return c->micro_steps; }
+uint32_t ctx_flags(const dc_ctx* c) { return c->flags; }
 }  // namespace dc

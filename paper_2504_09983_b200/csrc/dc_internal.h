@@ -41,6 +41,7 @@ int ctx_rank(const dc_ctx* c);
 const dc_schedule* ctx_sched(const dc_ctx* c);
 int64_t ctx_numel(const dc_ctx* c, int p);
 int ctx_micro_steps(const dc_ctx* c);
+uint32_t ctx_flags(const dc_ctx* c);
 int sched_num_ops(const dc_schedule* s);
 void sched_op(const dc_schedule* s, int i, int* kind, int* id, const int64_t** members, int* nmem,
               int64_t* arena_off, int64_t* bytes, const int** posts, int* nposts, const int** waits, int* nwaits);

@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 
 #include "adam.cuh"
@@ -60,7 +61,63 @@ struct GemmParams {
   // previous layer's reduce-scatter + Adam, streamed by 6 otherwise idle warps
   // while the tensor cores run this GEMM (same arithmetic as rs_adam)
   SideJob side;
+  // stream-K tail (pair kernel): tiles [0, sk_dp) are data-parallel (tile t on
+  // pair t % npairs); the remaining tiles' k-blocks [0, sk_total) are split into
+  // npairs contiguous ranges.  A tile cut by a range boundary is computed in two
+  // parts: the head's fp32 partial goes through sk_ws (flag sk_flags = sk_epoch),
+  // the pair holding the tail adds it in its epilogue, which it runs last.
+  int sk_on, sk_dp;
+  int64_t sk_total;
+  float* sk_ws;
+  uint32_t* sk_flags;
+  uint32_t sk_epoch;
 };
+
+// One unit of a pair's work list: k-blocks [kb0, kb1) of `tile`;
+// mode 0 full tile, 1 head of a split tile (write fp32 partial), 2 tail (add it)
+struct Unit { int tile, kb0, kb1, mode; };
+
+struct WorkList {
+  int n_dp, n_rest, finish;     // DP tiles, SK units without a wait, trailing tail unit
+  int ta, ka, tb;               // first SK tile / its start k-block, first non-tail SK tile
+  int64_t s1;                   // end of this pair's SK range (k-block index)
+  __device__ __forceinline__ int count() const { return n_dp + n_rest + finish; }
+};
+
+__device__ __forceinline__ WorkList work_list(const GemmParams& p, int pair, int npairs) {
+  WorkList w{};
+  const int tiles = p.m_tiles * p.n_tiles;
+  const int dp = p.sk_on ? p.sk_dp : tiles;
+  w.n_dp = pair < dp ? (dp - 1 - pair) / npairs + 1 : 0;
+  if (!p.sk_on) return w;
+  const int KB = p.k_blocks;
+  const int64_t s0 = (int64_t)pair * p.sk_total / npairs;
+  w.s1 = (int64_t)(pair + 1) * p.sk_total / npairs;
+  w.ta = dp + (int)(s0 / KB);
+  w.ka = (int)(s0 % KB);
+  w.finish = w.ka != 0;                         // ranges are >= KB long: the tail ends its tile
+  w.tb = w.ta + w.finish;
+  const int64_t first = (int64_t)(w.tb - dp) * KB;
+  w.n_rest = w.s1 > first ? (int)((w.s1 - first + KB - 1) / KB) : 0;
+  return w;
+}
+
+__device__ __forceinline__ Unit unit_at(const GemmParams& p, const WorkList& w, int pair, int npairs, int i) {
+  Unit u;
+  if (i < w.n_dp) { u.tile = pair + i * npairs; u.kb0 = 0; u.kb1 = p.k_blocks; u.mode = 0; return u; }
+  i -= w.n_dp;
+  const int KB = p.k_blocks;
+  if (i < w.n_rest) {
+    u.tile = w.tb + i;
+    u.kb0 = 0;
+    const int64_t end = w.s1 - (int64_t)(u.tile - p.sk_dp) * KB;
+    u.kb1 = end < KB ? (int)end : KB;
+    u.mode = u.kb1 < KB ? 1 : 0;
+    return u;
+  }
+  u.tile = w.ta; u.kb0 = w.ka; u.kb1 = KB; u.mode = 2;
+  return u;
+}
 
 __device__ __forceinline__ int seg_of(const GemmParams& p, int idx) {
   int s = 0;
@@ -426,7 +483,8 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_ctarank();
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
-  const int num_tiles = p.m_tiles * p.n_tiles;      // 256 x 256 tiles
+  const WorkList wl = work_list(p, pair, npairs);
+  const int nunits = wl.count();
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&mapA);
@@ -448,7 +506,9 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     if (lane == 0) {
       // ----------------------------------------------------------- producer (both CTAs)
       int stage = 0; uint32_t phase = 0;
-      for (int tile = pair; tile < num_tiles; tile += npairs) {
+      for (int ui = 0; ui < nunits; ++ui) {
+        const Unit un = unit_at(p, wl, pair, npairs, ui);
+        const int tile = un.tile;
         const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
         const int m0 = mt * BM2 + (int)rank * 128;
         int bseg = 0, n0 = nt * BNT;
@@ -457,7 +517,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           n0 = (nt - (bseg ? p.seg_end[bseg - 1] : 0)) * BNT;
         }
         n0 += (int)rank * (BNT / 2);
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (A2_STAGE + Pair<BNT, ST>::B_STAGE));
           const uint32_t lbar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
@@ -498,11 +558,12 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       const uint32_t b_ks = p.b_mn ? 2048 >> 4 : 32 >> 4;
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t aphase = 0;
-      for (int tile = pair; tile < num_tiles; tile += npairs) {
+      for (int ui = 0; ui < nunits; ++ui) {
+        const Unit un = unit_at(p, wl, pair, npairs, ui);
         ptx::mbar_wait(&tempty[acc], aphase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + acc * BNT;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint64_t ad = a_d0 + (uint32_t)(stage * (A2_STAGE >> 4));
@@ -510,7 +571,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           if (ptx::elect_one()) {
 #pragma unroll
             for (int k = 0; k < BK / UMMA_K; ++k)
-              ptx::umma_f16_2sm(d, ad + k * a_ks, bd + k * b_ks, p.idesc, (kb | k) != 0);
+              ptx::umma_f16_2sm(d, ad + k * a_ks, bd + k * b_ks, p.idesc, (kb != un.kb0) | (k != 0));
             ptx::umma_commit_2sm_mc(&empty[stage], 0x3);
           }
           __syncwarp();
@@ -524,12 +585,23 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   } else if (warp >= 4 && warp < 8) {
     // ------------------------------------------------------------- epilogue (both CTAs)
     const int q = warp & 3;
+    const int rl = q * 32 + lane;                 // this thread's row inside the CTA's 128
     int acc = 0; uint32_t aphase = 0;
-    for (int tile = pair; tile < num_tiles; tile += npairs) {
+    for (int ui = 0; ui < nunits; ++ui) {
+      const Unit un = unit_at(p, wl, pair, npairs, ui);
+      const int tile = un.tile;
       const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      // split tile: fp32 partial of this CTA's 128 rows, [chunk][j/4][row][4]
+      float* ws = un.mode ? p.sk_ws + ((int64_t)(tile - p.sk_dp) * 2 + rank) * (128 * BNT) : nullptr;
+      uint32_t* flag = un.mode ? p.sk_flags + (tile - p.sk_dp) * 2 + rank : nullptr;
+      if (un.mode == 2) {                          // the head's partial must have landed
+        const uint64_t t0 = ptx::globaltimer();
+        while (ptx::ld_acquire_gpu(flag) != p.sk_epoch)
+          if (ptx::globaltimer() - t0 > 4000000000ull) __trap();
+      }
       ptx::mbar_wait(&tfull[acc], aphase);
       ptx::tc_fence_after();
-      const int row = mt * BM2 + (int)rank * 128 + q * 32 + lane;
+      const int row = mt * BM2 + (int)rank * 128 + rl;
       const bool row_ok = row < p.M;
       __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
       const __nv_bfloat16* rrow = p.R ? p.R + (int64_t)row * p.ldr : nullptr;
@@ -539,6 +611,25 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BNT + c * 32, v);
         ptx::tmem_ld_wait();
         const int col0 = nt * BNT + c * 32;
+        if (un.mode == 1) {                        // head: store the raw fp32 partial
+          float4* w4 = reinterpret_cast<float4*>(ws) + (int64_t)c * 8 * 128 + rl;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            __stcg(w4 + j * 128, make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                             __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
+          continue;
+        }
+        if (un.mode == 2) {                        // tail: partial(head) + this part, fp32
+          const float4* w4 = reinterpret_cast<const float4*>(ws) + (int64_t)c * 8 * 128 + rl;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 h = __ldcg(w4 + j * 128);
+            v[4 * j] = __float_as_uint(__fadd_rn(h.x, __uint_as_float(v[4 * j])));
+            v[4 * j + 1] = __float_as_uint(__fadd_rn(h.y, __uint_as_float(v[4 * j + 1])));
+            v[4 * j + 2] = __float_as_uint(__fadd_rn(h.z, __uint_as_float(v[4 * j + 2])));
+            v[4 * j + 3] = __float_as_uint(__fadd_rn(h.w, __uint_as_float(v[4 * j + 3])));
+          }
+        }
         if (row_ok && col0 < p.N) {
           if constexpr (EPI == 1) {
             epilogue_chunk<1>(p, row, col0, v);
@@ -585,6 +676,11 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+      if (un.mode == 1) {                          // publish the partial (all 128 rows written)
+        __threadfence();
+        ptx::named_bar_sync(1, 128);
+        if (rl == 0) ptx::st_release_gpu(flag, p.sk_epoch);
+      }
       if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
   } else if (p.side.nm > 0) {
@@ -637,6 +733,25 @@ static int num_sms_cached() {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   }
   return n;
+}
+
+// stream-K workspace, one per stream (launches on one stream are ordered, so
+// they may share it; the epoch makes stale flags of earlier launches harmless)
+struct SkWorkspace { float* buf = nullptr; uint32_t* flags = nullptr; uint32_t epoch = 0; };
+static SkWorkspace* sk_workspace(cudaStream_t st, int max_tiles, int bnt) {
+  static std::mutex mu;
+  static std::map<cudaStream_t, SkWorkspace> ws;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = ws.find(st);
+  if (it != ws.end()) return &it->second;
+  // capacity: 2 * 74 split tiles of 2 CTAs x 128 rows x 256 fp32 columns
+  (void)bnt; (void)max_tiles;
+  const size_t tiles_cap = 2 * 74 + 2, per = 2ull * 128 * 256 * 4;
+  SkWorkspace w;
+  if (cudaMalloc(&w.buf, tiles_cap * per) != cudaSuccess) return nullptr;
+  if (cudaMalloc(&w.flags, tiles_cap * 2 * 4) != cudaSuccess) return nullptr;
+  if (cudaMemsetAsync(w.flags, 0, tiles_cap * 2 * 4, st) != cudaSuccess) return nullptr;   // ordered before use
+  return &(ws[st] = w);
 }
 
 // 0: 256-wide 6 stages (default), 2: 256-wide 7 stages (DC_GEMM_STAGES=7)
@@ -752,6 +867,21 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
     // would run as a second wave after the others finished)
     const int slots = pair_slots(bnt == 128 ? 1 : env_st_pick());
     const int pairs = std::min(tiles, std::min(sms / 2, slots > 0 ? slots : sms / 2));
+    static const bool sk_env = !(getenv("DC_GEMM_SK") && atoi(getenv("DC_GEMM_SK")) == 0);
+    // stream-K pays only when the k-loop is long (measured on the layer shapes,
+    // profiles/r01d: +3-4 % at K >= 14336, -2 % at K = 4096, where the idle
+    // pairs of the last partial wave let the others clock higher)
+    if (g->stream_k && sk_env && !p.epi && tiles > pairs && tiles % pairs && p.k_blocks >= 128 &&
+        tiles - (tiles / pairs - 1) * pairs <= 150) {
+      p.sk_on = 1;
+      p.sk_dp = (tiles / pairs - 1) * pairs;            // leaves [pairs, 2 pairs) tiles to split
+      p.sk_total = (int64_t)(tiles - p.sk_dp) * p.k_blocks;
+      SkWorkspace* w = sk_workspace(stream, 2 * pairs, bnt);
+      if (!w) { *err = "dc_gemm: stream-K workspace allocation failed"; return DC_EOOM; }
+      p.sk_ws = w->buf;
+      p.sk_flags = w->flags;
+      p.sk_epoch = ++w->epoch;
+    }
     const int env_st = env_st_pick() == 2 ? 7 : 6;
     const int g2 = 2 * pairs;
 #define DC_PAIR_LAUNCH(BN_, ST_)                                                                   \

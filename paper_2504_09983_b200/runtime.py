@@ -45,10 +45,7 @@ class RankState:
         self.micro_steps = 1
 
     def stream_handles(self):
-        h = [s.cuda_stream for s in self.streams]
-        if os.environ.get("DC_RS_ON_COMPUTE") == "1":   # experiment: RS + Adam serialised with compute
-            h[2] = h[0]
-        return h
+        return [s.cuda_stream for s in self.streams]
 
 
 _IPC_KEEP = []   # imported peer storages must outlive every use of their pointers

@@ -48,7 +48,7 @@ def test_init_bitexact():
 
 
 # ------------------------------------------------------------------ GEMM
-def _gemm(M, N, K, A, lda, a_mn, Bs, ldbs, ends, b_mn, split_k, Cm, ldc, R=None, ldr=0, sms=0, kernel=0):
+def _gemm(M, N, K, A, lda, a_mn, Bs, ldbs, ends, b_mn, split_k, Cm, ldc, R=None, ldr=0, sms=0, kernel=0, sk=0):
     g = dc.GemmArgs()
     g.M, g.N, g.K = M, N, K
     g.A, g.lda, g.a_mn_major = A.data_ptr(), lda, a_mn
@@ -62,6 +62,7 @@ def _gemm(M, N, K, A, lda, a_mn, Bs, ldbs, ends, b_mn, split_k, Cm, ldc, R=None,
     # kernel 1: one-CTA tiles; 2: CTA pairs 256 x 256; 3: CTA pairs 256 x 128
     os.environ["DC_GEMM_BN"] = "128" if kernel == 3 else "256"
     g.kernel = 2 if kernel == 3 else kernel
+    g.stream_k = sk
     dc.check(dc.lib.dc_gemm(C.byref(g), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
 
@@ -138,6 +139,48 @@ def test_gemm_rejects_bad_shapes():
     g.M, g.N, g.K, g.n_bseg = 8, 7, 8, 1
     g.A = g.B[0] = g.C = A.data_ptr()
     assert dc.lib.dc_gemm(C.byref(g), None) == dc.DC_EINVAL
+
+
+# stream-K tails: with `sms` pairs' worth of SMs and a tile count that is not a
+# multiple of the pair count, the last [P, 2P) tiles are split into P equal
+# k-ranges; split tiles add the head's fp32 partial in the tail's epilogue.
+# (stream-K needs k_blocks >= 128, i.e. K > 8128)
+SK_CASES = pytest.mark.parametrize("M,N,K,sms", [(768, 1280, 8192, 8), (640, 1024, 8200, 6), (2048, 2560, 8192, 0)])
+
+
+@pytest.mark.parametrize("kernel", [2, 3], ids=["pair256", "pair128"])
+@SK_CASES
+def test_gemm_stream_k_forward_residual(M, N, K, sms, kernel):
+    a, A = _mat(61, M, K)
+    b, B = _mat(62, N, K)
+    r, R = _mat(63, M, N)
+    outs = []
+    for sk in (1, 1, 0):
+        Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        _gemm(M, N, K, A, K, 0, [B], [K], [0], 0, 0, Cm, N, R=R, ldr=N, sms=sms, kernel=kernel, sk=sk)
+        outs.append(Cm)
+    _check(outs[0], a @ b.T + r, np.abs(a) @ np.abs(b).T + np.abs(r), "sk fwd")
+    assert torch.equal(outs[0], outs[1])                  # deterministic split and sum order
+    _check(outs[2], a @ b.T + r, np.abs(a) @ np.abs(b).T + np.abs(r), "dp fwd")
+
+
+@SK_CASES
+def test_gemm_stream_k_dx_dw(M, N, K, sms):
+    # dX layout with B split along K into two segments
+    a, A = _mat(71, M, K)
+    k1 = (K // 2) // 64 * 64
+    w1, W1 = _mat(72, k1, N)
+    w2, W2 = _mat(73, K - k1, N)
+    Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    _gemm(M, N, K, A, K, 0, [W1, W2], [N, N], [k1 // 64, -(-K // 64)], 1, 1, Cm, N, sms=sms, kernel=2, sk=1)
+    wcat = np.concatenate([w1, w2])
+    _check(Cm, a @ wcat, np.abs(a) @ np.abs(wcat), "sk dx")
+    # dW layout: A stored [K][M], B stored [K][N]
+    dy, DY = _mat(74, K, M)
+    x, X = _mat(75, K, N)
+    Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    _gemm(M, N, K, DY, M, 1, [X], [N], [0], 1, 0, Cm, N, sms=sms, kernel=2, sk=1)
+    _check(Cm, dy.T @ x, np.abs(dy).T @ np.abs(x), "sk dw")
 
 
 # ------------------------------------------------------------------ RS + Adam
