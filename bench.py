@@ -251,7 +251,7 @@ def main():
     x_dev = x_host.to(dev).view(n_micro, T, cfg.hidden)
     t_dev = t_host.to(dev).view(n_micro, T, cfg.hidden)
     rt.attach_model(ranks, cfg, {rank: x_dev}, {rank: t_dev})
-    for key in ("rs_overlap", "stream_k"):                      # A/B knobs (DC_RS_OVERLAP=0/1 ...)
+    for key in ("rs_overlap", "stream_k", "comm_sms"):          # A/B knobs (DC_RS_OVERLAP=0/1 ...)
         if os.environ.get("DC_" + key.upper()) is not None:
             dc.check(dc.lib.dc_model_set_option(st.model, key.encode(), int(os.environ["DC_" + key.upper()])))
     cs = st.streams[0]

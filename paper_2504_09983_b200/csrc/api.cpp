@@ -554,4 +554,8 @@ const dc_schedule* ctx_sched(const dc_ctx* c) { return c->sched; }
 int64_t ctx_numel(const dc_ctx* c, int p) { return c->numel[p]; }
 int ctx_micro_steps(const dc_ctx* c) { return c->micro_steps; }
 uint32_t ctx_flags(const dc_ctx* c) { return c->flags; }
+void ctx_set_rs_ctas(dc_ctx* c, int ctas) {
+  c->rs_ctas = ctas > 0 ? ctas : 296;
+  if (const char* e = getenv("DC_RS_CTAS")) c->rs_ctas = std::max(1, atoi(e));
+}
 }  // namespace dc

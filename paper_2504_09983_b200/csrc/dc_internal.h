@@ -41,6 +41,17 @@ int ctx_rank(const dc_ctx* c);
 const dc_schedule* ctx_sched(const dc_ctx* c);
 int64_t ctx_numel(const dc_ctx* c, int p);
 int ctx_micro_steps(const dc_ctx* c);
+void ctx_set_rs_ctas(dc_ctx* c, int ctas);   // 0 = default (2 per SM of the device)
+
+// spatial SM partition (green contexts, sm_partition.cpp)
+struct SmPartition {
+  int gemm_sms = 0, comm_sms = 0;
+  cudaStream_t compute = nullptr, rs = nullptr, ag = nullptr;
+  void* ctx_gemm = nullptr;
+  void* ctx_comm = nullptr;
+};
+dc_status sm_partition_create(int device, int comm_sms, SmPartition* out, std::string* err);
+void sm_partition_destroy(SmPartition* p);
 uint32_t ctx_flags(const dc_ctx* c);
 int sched_num_ops(const dc_schedule* s);
 void sched_op(const dc_schedule* s, int i, int* kind, int* id, const int64_t** members, int* nmem,

@@ -60,7 +60,7 @@ struct dc_model {
   const void* x = nullptr;
   const void* target = nullptr;
   std::vector<cudaEvent_t> ev_pos, ev_done, ev_t0, ev_t1;
-  cudaEvent_t ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_join[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   std::vector<int64_t> dur_us;       // per S_0 op
   std::vector<int64_t> p_mem;        // per S_0 op
   int32_t epoch = 0;
@@ -79,7 +79,10 @@ struct dc_model {
   int step_t = 0;
   int n_micro = 1;                   // gradient-accumulation micro-steps (ctx)
   int stream_k = 1;                  // stream-K GEMM tails (off when ranks share a GPU)
-  int rs_overlap = 1;                // RS + Adam on its own stream (N > 1 default)
+  int rs_overlap = 1;                // RS + Adam on its own stream
+  int comm_sms = 0;                  // > 0: SM partition (GEMMs | comm + Adam), green contexts
+  SmPartition part{};
+  int gemm_sms = 0;                  // SMs the layer GEMMs may use (0 = all)
   std::string err;
 
   int pid(int layer, int slot) const { return ctx_layout(ctx).layer_first[layer] + slot; }
@@ -232,6 +235,7 @@ extern "C" dc_status dc_model_destroy(dc_model* m) {
     cudaEventDestroy(m->ev_t0[i]); cudaEventDestroy(m->ev_t1[i]);
   }
   for (auto& e : m->ev_join) if (e) cudaEventDestroy(e);
+  sm_partition_destroy(&m->part);
   delete m;
   return DC_OK;
 }
@@ -287,6 +291,7 @@ static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t l
   g.b_mn_major = b_mn; g.b_split_k = split_k;
   g.C = C; g.ldc = ldc; g.R = R; g.ldr = ldr;
   g.stream_k = m->stream_k;
+  g.num_sms = m->gemm_sms;
   std::string err;
   dc_status s = launch_gemm(&g, st, &err, adam, side);
   if (s != DC_OK) return mfail(m, s, err);
@@ -526,7 +531,7 @@ extern "C" dc_status dc_model_profile_json(const dc_model* mc, char* buf, size_t
   return DC_OK;
 }
 
-extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile, cudaStream_t cs, cudaStream_t ags,
+extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile, cudaStream_t ucs, cudaStream_t ags,
                                    cudaStream_t rss, cudaStream_t cps) {
   if (!m || !m->act) return mfail(m, DC_ESTATE, "dc_model_step: model not bound");
   const dc_schedule* sc = ctx_sched(m->ctx);
@@ -535,6 +540,26 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
   const int N = ctx_world(m->ctx);
   if (step_t < 1) return mfail(m, DC_EINVAL, "dc_model_step: step_t is 1-based");
   m->step_t = step_t;
+  // the caller's compute stream orders the step; with an SM partition the work
+  // runs on the partition's streams (GEMM side / communication + Adam side)
+  cudaStream_t cs = ucs;
+  if (m->comm_sms > 0) {
+    if (!m->part.ctx_gemm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      std::string err;
+      dc_status ps = sm_partition_create(dev, m->comm_sms, &m->part, &err);
+      if (ps != DC_OK) return mfail(m, ps, "dc_model_step: " + err);
+    }
+    cs = m->part.compute;
+    rss = m->part.rs;
+    ags = m->part.ag;
+    m->gemm_sms = m->part.gemm_sms;
+    ctx_set_rs_ctas(m->ctx, 2 * m->part.comm_sms);
+  } else {
+    m->gemm_sms = 0;
+    ctx_set_rs_ctas(m->ctx, 0);
+  }
   if (!m->rs_overlap) rss = cs;
   // an offloaded fragment is reloaded before its layer's RS op (reading D17),
   // i.e. after the dW GEMMs: the fused update needs every state resident
@@ -549,10 +574,11 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
     sched_op(sc, i, &kind, &id, &mem, &nm, &off, &bytes, &posts, &np, &waits, &nw);
     if (kind >= K_OFF) m->fused_active = m->side_active = false;
   }
-  dc_status s = dc_step_begin(m->ctx, ++m->epoch, cs);
+  dc_status s = dc_step_begin(m->ctx, ++m->epoch, ucs);
   if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
   // streams must not run ahead of the previous step's tail on the compute stream
-  cudaEventRecord(m->ev_join[0], cs);
+  cudaEventRecord(m->ev_join[0], ucs);
+  if (cs != ucs) cudaStreamWaitEvent(cs, m->ev_join[0], 0);
   cudaStreamWaitEvent(ags, m->ev_join[0], 0);
   cudaStreamWaitEvent(rss, m->ev_join[0], 0);
   cudaStreamWaitEvent(cps, m->ev_join[0], 0);
@@ -628,13 +654,17 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
     }
     if (s != DC_OK) return mfail(m, s, std::string("dc_model_step: ") + dc_last_error(m->ctx) + " / " + m->err);
   }
-  // join every stream into the compute stream (step end)
+  // join every stream into the caller's compute stream (step end)
   cudaEventRecord(m->ev_join[1], ags);
   cudaEventRecord(m->ev_join[2], rss);
   cudaEventRecord(m->ev_join[3], cps);
-  cudaStreamWaitEvent(cs, m->ev_join[1], 0);
-  cudaStreamWaitEvent(cs, m->ev_join[2], 0);
-  cudaStreamWaitEvent(cs, m->ev_join[3], 0);
+  cudaStreamWaitEvent(ucs, m->ev_join[1], 0);
+  cudaStreamWaitEvent(ucs, m->ev_join[2], 0);
+  cudaStreamWaitEvent(ucs, m->ev_join[3], 0);
+  if (cs != ucs) {
+    cudaEventRecord(m->ev_join[4], cs);
+    cudaStreamWaitEvent(ucs, m->ev_join[4], 0);
+  }
   if (cudaGetLastError() != cudaSuccess) return mfail(m, DC_ECUDA, "dc_model_step: CUDA error");
   m->launches = launch_count() - l0;
   if (profile) {
@@ -664,6 +694,14 @@ extern "C" dc_status dc_model_set_option(dc_model* m, const char* key, int64_t v
   if (!strcmp(key, "side_adam")) {
     if (value && ctx_world(m->ctx) != 1) return mfail(m, DC_EINVAL, "side_adam needs N == 1");
     m->side_adam = value != 0;
+    return DC_OK;
+  }
+  if (!strcmp(key, "comm_sms")) {
+    if (value < 0 || value > 64) return mfail(m, DC_EINVAL, "comm_sms in [0, 64]");
+    if (value && (ctx_flags(m->ctx) & DC_VIRTUAL_RANKS) && ctx_world(m->ctx) > 1)
+      return mfail(m, DC_EINVAL, "comm_sms needs one rank per GPU");
+    if (m->part.ctx_gemm && value != m->comm_sms) sm_partition_destroy(&m->part);
+    m->comm_sms = (int)value;
     return DC_OK;
   }
   if (!strcmp(key, "rs_overlap")) {
