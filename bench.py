@@ -39,6 +39,7 @@ def parse():
     ap.add_argument("--seq", type=int, default=2048)
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--micro", type=int, default=1, help="gradient-accumulation micro-steps per step (P:362)")
+    ap.add_argument("--checkpoint", action="store_true", help="layer-level activation checkpointing (P:440)")
     ap.add_argument("--passes", default="PS", help="S0 | P | S | PS")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default="", help="write the rank-0 profile / plan here")
@@ -170,7 +171,8 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
-GEMM_OPS = ("qkv", "o_proj", "gate_up", "down", "down_bwd", "gate_up_bwd", "o_bwd", "qkv_bwd")
+GEMM_OPS = ("qkv", "o_proj", "gate_up", "down", "down_bwd", "gate_up_bwd", "o_bwd", "qkv_bwd",
+            "re_qkv", "re_o_proj", "re_gate_up")
 
 
 def gemm_flops(name, cfg, T):
@@ -179,7 +181,8 @@ def gemm_flops(name, cfg, T):
     fwd = {"qkv": 2 * T * h * qkvd, "o_proj": 2 * T * qd * h, "gate_up": 2 * T * h * 2 * f, "down": 2 * T * f * h}
     bwd = {"down_bwd": 2 * fwd["down"], "gate_up_bwd": 2 * fwd["gate_up"], "o_bwd": 2 * fwd["o_proj"],
            "qkv_bwd": 2 * fwd["qkv"]}
-    return {**fwd, **bwd}[name]
+    re = {"re_" + k: v for k, v in fwd.items()}          # checkpoint recompute
+    return {**fwd, **bwd, **re}[name]
 
 
 def measure_tc(group, world, dev, torch, dist):
@@ -250,7 +253,7 @@ def main():
     t_host = torch.from_numpy(nx.bf16_bits(t_np).view(np.int16)).view(torch.bfloat16).pin_memory()
     x_dev = x_host.to(dev).view(n_micro, T, cfg.hidden)
     t_dev = t_host.to(dev).view(n_micro, T, cfg.hidden)
-    rt.attach_model(ranks, cfg, {rank: x_dev}, {rank: t_dev})
+    rt.attach_model(ranks, cfg, {rank: x_dev}, {rank: t_dev}, checkpoint=args.checkpoint)
     for key in ("rs_overlap", "stream_k", "comm_sms"):          # A/B knobs (DC_RS_OVERLAP=0/1 ...)
         if os.environ.get("DC_" + key.upper()) is not None:
             dc.check(dc.lib.dc_model_set_option(st.model, key.encode(), int(os.environ["DC_" + key.upper()])))
@@ -417,9 +420,11 @@ def main():
                                        "seq %d, b=%d per GPU, ZeRO-3 + proactive prefetch%s%s" %
                                        (cfg.layers, args.seq, args.batch,
                                         " + selective unshard" if "S" in args.passes else "",
-                                        ", grad accumulation %d" % n_micro if n_micro > 1 else ""),
+                                        (", grad accumulation %d" % n_micro if n_micro > 1 else "") +
+                                        (", layer activation checkpointing" if args.checkpoint else "")),
                            "model": "llama3-8b-shaped synthetic stack (random init)",
                            "global_batch": world * args.batch * n_micro, "micro_steps": n_micro,
+                           "checkpoint": bool(args.checkpoint),
                            "seq_len": args.seq, "parallelism": "fsdp%d" % world, "passes": args.passes,
                            "mem_budget_M": M, "plan_ms": round(t_plan * 1e3, 2),
                            "unshard_params": len(plan["unshard"]),

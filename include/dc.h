@@ -224,6 +224,10 @@ dc_status dc_offload(dc_ctx* ctx, int32_t fragment, int32_t op, cudaStream_t str
  * ------------------------------------------------------------------------ */
 typedef struct {
   int32_t hidden, ffn, n_heads, n_kv, head_dim, layers, tokens;
+  int32_t checkpoint;            /* 1: layer-level activation checkpointing (*/
+                                 /* "recomputing each layer as a block"): only each */
+                                 /* layer's output is kept; the backward of a layer */
+                                 /* re-runs its forward ops (all but down) first    */
 } dc_model_dims;
 
 /* Plain GEMM entry (tests, comparators): C[M,N] (bf16, row-major, ldc) =

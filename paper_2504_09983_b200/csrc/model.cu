@@ -41,6 +41,7 @@ struct S0 {
   bool fwd;
   int micro, layer;
   std::vector<int> params;
+  bool re = false;  // forward op re-run in the backward (activation checkpointing)
 };
 
 struct LayerAct { int64_t h1, rstd1, qkv, a, x2, h2, rstd2, gu, act, y; };
@@ -105,6 +106,8 @@ static void build_s0(dc_model* m) {
   std::vector<S0> comp;
   static const int fwd_codes[] = {F_ATTN_NORM, F_QKV, F_ATTN_MIX, F_O, F_MLP_NORM, F_GATE_UP, F_ACT, F_DOWN};
   static const int bwd_codes[] = {B_DOWN, B_ACT, B_GATE_UP, B_MLP_NORM, B_O, B_ATTN_MIX, B_QKV, B_ATTN_NORM};
+  // layer checkpointing: the forward ops the layer's gradients need
+  static const int re_codes[] = {F_ATTN_NORM, F_QKV, F_ATTN_MIX, F_O, F_MLP_NORM, F_GATE_UP, F_ACT};
   auto params_of = [&](int code, int l) -> std::vector<int> {
     switch (code) {
       case F_ATTN_NORM: case B_ATTN_NORM: return {m->pid(l, P_G1)};
@@ -123,6 +126,8 @@ static void build_s0(dc_model* m) {
       for (int c : fwd_codes) comp.push_back({K_COMPUTE, c, true, mu, l, params_of(c, l)});
     comp.push_back({K_COMPUTE, F_LOSS, true, mu, L - 1, {}});
     for (int l = L - 1; l >= 0; --l) {
+      if (m->d.checkpoint)
+        for (int c : re_codes) comp.push_back({K_COMPUTE, c, false, mu, l, params_of(c, l), true});
       for (int c : bwd_codes) comp.push_back({K_COMPUTE, c, false, mu, l, params_of(c, l)});
       comp.push_back({K_RS, RS_OP, false, mu, l, {}});
     }
@@ -185,8 +190,14 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   uint64_t off = 0;
   auto take = [&](int64_t bytes) { int64_t o = (int64_t)off; off += (bytes + 255) / 256 * 256; return o; };
   m->la.resize(d->layers);
+  if (d->checkpoint != 0 && d->checkpoint != 1) return mfail(nullptr, DC_EINVAL, "dc_model_create: checkpoint is 0 or 1");
   for (int l = 0; l < d->layers; ++l) {
     LayerAct& a = m->la[l];
+    if (l > 0 && d->checkpoint) {          // one shared set of layer activations,
+      a = m->la[0];                        // each layer keeps only its output y
+      a.y = take(T * h * 2);
+      continue;
+    }
     a.h1 = take(T * h * 2); a.rstd1 = take(T * 4); a.qkv = take(T * m->qkvd * 2); a.a = take(T * m->qd * 2);
     a.x2 = take(T * h * 2); a.h2 = take(T * h * 2); a.rstd2 = take(T * 4); a.gu = take(T * 2 * f * 2);
     a.act = take(T * f * 2); a.y = take(T * h * 2);
@@ -462,12 +473,17 @@ static void compute_pmem(dc_model* m) {
     }
   };
   (void)a0;
+  // checkpointing: one shared layer activation set (static) + each layer's y
+  if (m->d.checkpoint) stat += (int64_t)m->layer_act_bytes - T * h * 2;
   for (size_t i = 0; i < m->s0.size(); ++i) {
     const S0& o = m->s0[i];
     m->p_mem[i] = stat + live_ag + act;
     if (o.kind == K_AG) live_ag += L.S[o.params[0]] * N * 2;
     else if (o.kind == K_REL) live_ag -= L.S[o.params[0]] * N * 2;
-    else if (o.kind == K_COMPUTE) {
+    else if (o.kind == K_COMPUTE && m->d.checkpoint) {
+      if (o.fwd && o.code == F_DOWN) act += piece(F_DOWN);
+      else if (!o.fwd && o.code == B_ATTN_NORM) act -= piece(F_DOWN);
+    } else if (o.kind == K_COMPUTE) {
       if (o.fwd) act += piece(o.code);
       else if (o.code == B_ATTN_NORM) {
         int64_t layer_total = 0;
@@ -508,7 +524,8 @@ extern "C" dc_status dc_model_profile_json(const dc_model* mc, char* buf, size_t
     const char* kind = o.kind == K_AG ? "ag" : o.kind == K_REL ? "rel" : o.kind == K_RS ? "rs" : "compute";
     s += "{\"dur_us\":" + std::to_string(m->dur_us[i]) + ",\"id\":" + std::to_string(i) + ",\"kind\":\"" + kind +
          "\",\"layer\":" + std::to_string(o.layer) + ",\"micro\":" + std::to_string(o.micro) + ",\"name\":\"" +
-         (o.kind == K_AG ? "ag" : o.kind == K_REL ? "rel" : op_name(o.code)) + "\",\"p_mem\":" +
+         (o.kind == K_AG ? "ag" : o.kind == K_REL ? "rel" : (o.re ? "re_" : "") + std::string(op_name(o.code))) +
+         "\",\"p_mem\":" +
          std::to_string(m->p_mem[i]) + ",\"params\":[";
     for (size_t j = 0; j < o.params.size(); ++j) s += (j ? "," : "") + std::to_string(o.params[j]);
     s += "],\"phase\":\"" + std::string(o.fwd ? "fwd" : "bwd") + "\",\"transient\":0}";

@@ -169,10 +169,11 @@ def grad_offset(st, p):
     return b.value
 
 
-def attach_model(ranks, cfg, xs, targets):
+def attach_model(ranks, cfg, xs, targets, checkpoint=False):
     """dc_model_create + bind per rank; xs/targets: dict rank -> bf16 device
     [n, T, H] (n = micro_steps micro-batches; [T, H] when n = 1)."""
-    d = dc.ModelDims(cfg.hidden, cfg.ffn, cfg.n_heads, cfg.n_kv, cfg.head_dim, cfg.layers, cfg.tokens)
+    d = dc.ModelDims(cfg.hidden, cfg.ffn, cfg.n_heads, cfg.n_kv, cfg.head_dim, cfg.layers, cfg.tokens,
+                     int(checkpoint))
     for r, st in ranks.items():
         m = C.c_void_p()
         dc.check(dc.lib.dc_model_create(st.ctx, C.byref(d), C.byref(m)))

@@ -110,7 +110,13 @@ LLAMA_BWD = (("down_bwd", ("wdown",)), ("act_bwd", ()), ("gate_up_bwd", ("wgate"
              ("qkv_bwd", ("wq", "wk", "wv")), ("attn_norm_bwd", ("attn_norm",)))
 
 
-def llama_compute_ops(cfg: ModelConfig, micro_steps: int = 1):
+# Layer-level activation checkpointing ("recomputing each
+# layer as a block"): the forward keeps only each layer's output; the backward
+# of layer l first re-runs the forward ops its gradients need (all but `down`).
+LLAMA_RECOMPUTE = tuple(("re_" + nm, ps) for nm, ps in LLAMA_FWD if nm != "down")
+
+
+def llama_compute_ops(cfg: ModelConfig, micro_steps: int = 1, checkpoint: bool = False):
     P = len(LLAMA_NAMES)
     pid = lambda l, nm: l * P + LLAMA_NAMES.index(nm)
     ops = []
@@ -122,7 +128,7 @@ def llama_compute_ops(cfg: ModelConfig, micro_steps: int = 1):
         ops.append(dict(name="loss", kind="compute", phase="fwd", micro=mu,
                         layer=cfg.layers - 1, params=[]))
         for l in reversed(range(cfg.layers)):
-            for nm, ps in LLAMA_BWD:
+            for nm, ps in (LLAMA_RECOMPUTE if checkpoint else ()) + LLAMA_BWD:
                 ops.append(dict(name=nm, kind="compute", phase="bwd", micro=mu, layer=l,
                                 params=[pid(l, p) for p in ps]))
             # every micro-step reduce-scatters into the partitioned fp32

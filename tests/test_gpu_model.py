@@ -157,3 +157,42 @@ def test_side_job_adam_bitexact_vs_rs_adam():
             assert torch.equal(x.view(torch.int16) if k == "shard" else x.view(torch.int32),
                                y.view(torch.int16) if k == "shard" else y.view(torch.int32)), (t, k)
     assert not torch.isnan(a[0].tensors["master"]).any()
+
+
+@pytest.mark.parametrize("world,passes", [(1, dc.DC_PASS_SHARD),
+                                          (2, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD)])
+def test_activation_checkpointing_bitexact(world, passes):
+    """Layer-level activation checkpointing: the backward
+    re-runs each layer's forward ops from the saved layer input, with the same
+    kernels on the same inputs, so the step is bit-identical to keeping every
+    activation; the activation buffer shrinks to one layer's set + L outputs."""
+    cfg = synth.small_llama(layers=3, seq=128)
+    table = synth.llama_param_table(cfg)
+    runs = {}
+    for ck in (0, 1):
+        ranks = rt.create_ranks(table, world, lr=LR)
+        xs, ts = {}, {}
+        for r in ranks:
+            x, t = ost.rank_batch(cfg, r)
+            xs[r], ts[r] = bf16_tensor(x), bf16_tensor(t)
+        rt.attach_model(ranks, cfg, xs, ts, checkpoint=bool(ck))
+        prof = rt.profile_json(ranks[0], tc=[[4096, 10], [1 << 20, 20], [1 << 26, 400]])
+        names = [o["name"] for o in prof["ops"]]
+        assert ("re_gate_up" in names) == bool(ck)
+        sched = dc.plan(json.dumps(prof), 1 << 40, M_prefetch=1 << 22, passes=passes, strict=True)
+        rt.bind(ranks, {r: sched for r in ranks})
+        for t in (1, 2):
+            rt.step(ranks, t, profile=(t == 2))
+            torch.cuda.synchronize()
+            rt.poll(ranks)
+        runs[ck] = ranks
+    a, b = runs[0], runs[1]
+    assert b[0].tensors["act"].numel() < a[0].tensors["act"].numel()
+    for r in a:
+        for k in ("master", "m", "v", "shard"):
+            x, y = a[r].tensors[k], b[r].tensors[k]
+            assert torch.equal(x.view(torch.int16) if k == "shard" else x.view(torch.int32),
+                               y.view(torch.int16) if k == "shard" else y.view(torch.int32)), (r, k)
+        assert _loss(a[r]) == _loss(b[r])
+    prof = json.loads(dc.model_profile_json(b[0].model))
+    assert all(o["dur_us"] > 0 for o in prof["ops"] if o["kind"] == "compute")

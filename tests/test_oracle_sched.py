@@ -88,6 +88,18 @@ def test_s0_counts_and_adjacency():
     s0 = osd.build_s0(synth.models.llama_compute_ops(synth.LLAMA3_8B))
     assert sum(o["kind"] == "ag" for o in s0) == 576
     assert sum(o["kind"] == "rs" for o in s0) == 32
+    # layer checkpointing: same gathers, but the backward gather of every
+    # param except the down projection now lands before its recompute op
+    s0c = osd.build_s0(synth.models.llama_compute_ops(synth.LLAMA3_8B, checkpoint=True))
+    assert sum(o["kind"] == "ag" for o in s0c) == 576
+    for i, o in enumerate(s0c):
+        if o["kind"] == "ag" and o["phase"] == "bwd":
+            nxt = next(x for x in s0c[i + 1:] if x["kind"] == "compute")
+            assert nxt["name"].startswith("re_") or nxt["name"] == "down_bwd"
+    # gradient accumulation: one RS per layer per micro-step
+    s0g = osd.build_s0(synth.models.llama_compute_ops(synth.small_llama(layers=3), micro_steps=4))
+    assert sum(o["kind"] == "rs" for o in s0g) == 12
+    assert sum(o["kind"] == "ag" for o in s0g) == 9 * 3 * 2 * 4
 
 
 # ---------------------------------------------------------------- Algorithm 1
