@@ -89,8 +89,9 @@ def dsilu(z):
 # ---------------------------------------------------------------------------
 # Llama-shaped synthetic layer
 # ---------------------------------------------------------------------------
-def llama_layer_fwd(x, W, cfg, rnd):
-    """W: dict name -> float array (bf16-valued for the bf16 regime)."""
+def attn_fwd(x, W, cfg, rnd):
+    """Attention half of the synthetic layer (shared by the Llama and Mixtral
+    shapes): returns x2, h2 and the cache."""
     f = lambda k: np.asarray(W[k], np.float64)
     x = np.asarray(x, np.float64)
     h1, rstd1 = rmsnorm_fwd(x, f("attn_norm"), rnd)
@@ -100,29 +101,14 @@ def llama_layer_fwd(x, W, cfg, rnd):
     a = r64(rnd, q + rep_kv(k, cfg) * rep_kv(v, cfg))
     x2 = r64(rnd, x + a @ f("wo").T)
     h2, rstd2 = rmsnorm_fwd(x2, f("mlp_norm"), rnd)
-    gt = r64(rnd, h2 @ f("wgate").T)
-    up = r64(rnd, h2 @ f("wup").T)
-    act = r64(rnd, silu(gt) * up)
-    y = r64(rnd, x2 + act @ f("wdown").T)
-    cache = dict(x=x, h1=h1, rstd1=rstd1, q=q, k=k, v=v, a=a, x2=x2, h2=h2,
-                 rstd2=rstd2, gt=gt, up=up, act=act)
-    return y, cache
+    return dict(x=x, h1=h1, rstd1=rstd1, q=q, k=k, v=v, a=a, x2=x2, h2=h2, rstd2=rstd2)
 
 
-def llama_layer_bwd(dy, c, W, cfg, rnd):
-    """Returns dx and the parameter grads (rounded with rnd), manual backward."""
+def attn_bwd(dy, dh2, c, W, cfg, rnd, G):
+    """Backward of the attention half given dL/dy (through the residual) and
+    dL/dh2 (through the MLP); fills G, returns dx."""
     f = lambda k: np.asarray(W[k], np.float64)
     dy = np.asarray(dy, np.float64)
-    G = {}
-    # y = x2 + act Wd^T
-    dact = r64(rnd, dy @ f("wdown"))
-    G["wdown"] = r64(rnd, dy.T @ c["act"])
-    # act = silu(gt) * up
-    dgt = r64(rnd, dact * c["up"] * dsilu(c["gt"]))
-    dup = r64(rnd, dact * silu(c["gt"]))
-    dh2 = r64(rnd, dgt @ f("wgate") + dup @ f("wup"))
-    G["wgate"] = r64(rnd, dgt.T @ c["h2"])
-    G["wup"] = r64(rnd, dup.T @ c["h2"])
     # h2 = RMSNorm(x2) * g2 ; x2 also feeds y directly
     dxn, dg2 = rmsnorm_bwd(dh2, c["x2"], f("mlp_norm"), c["rstd2"])
     G["mlp_norm"] = r64(rnd, dg2)
@@ -140,8 +126,132 @@ def llama_layer_bwd(dy, c, W, cfg, rnd):
     G["wv"] = r64(rnd, dv.T @ c["h1"])
     dxa, dg1 = rmsnorm_bwd(dh1, c["x"], f("attn_norm"), c["rstd1"])
     G["attn_norm"] = r64(rnd, dg1)
-    dx = r64(rnd, dx2 + dxa)
-    return dx, G
+    return r64(rnd, dx2 + dxa)
+
+
+def llama_layer_fwd(x, W, cfg, rnd):
+    """W: dict name -> float array (bf16-valued for the bf16 regime)."""
+    f = lambda k: np.asarray(W[k], np.float64)
+    c = attn_fwd(x, W, cfg, rnd)
+    h2 = c["h2"]
+    gt = r64(rnd, h2 @ f("wgate").T)
+    up = r64(rnd, h2 @ f("wup").T)
+    act = r64(rnd, silu(gt) * up)
+    y = r64(rnd, c["x2"] + act @ f("wdown").T)
+    c.update(gt=gt, up=up, act=act)
+    return y, c
+
+
+def llama_layer_bwd(dy, c, W, cfg, rnd):
+    """Returns dx and the parameter grads (rounded with rnd), manual backward."""
+    f = lambda k: np.asarray(W[k], np.float64)
+    dy = np.asarray(dy, np.float64)
+    G = {}
+    # y = x2 + act Wd^T
+    dact = r64(rnd, dy @ f("wdown"))
+    G["wdown"] = r64(rnd, dy.T @ c["act"])
+    # act = silu(gt) * up
+    dgt = r64(rnd, dact * c["up"] * dsilu(c["gt"]))
+    dup = r64(rnd, dact * silu(c["gt"]))
+    dh2 = r64(rnd, dgt @ f("wgate") + dup @ f("wup"))
+    G["wgate"] = r64(rnd, dgt.T @ c["h2"])
+    G["wup"] = r64(rnd, dup.T @ c["h2"])
+    return attn_bwd(dy, dh2, c, W, cfg, rnd, G), G
+
+
+# ---------------------------------------------------------------------------
+# Mixtral-shaped layer (SURVEY.md §8(d) config 4; PAPER.md line 440): the MLP
+# is replaced by E experts with fixed balanced top-2 routing.
+#   logits = h2 Wr^T (fp32);  token t -> experts e0 = t mod E, e1 = (t+1) mod E
+#   (g0, g1) = softmax(logits[t, e0], logits[t, e1])
+#   expert e on its rows X_e = h2[tokens routed to e, ascending t]:
+#     O_e = (SiLU(X_e W1_e^T) * (X_e W3_e^T)) W2_e^T
+#   y[t] = x2[t] + g0[t] O_e0[t] + g1[t] O_e1[t]
+# ---------------------------------------------------------------------------
+def moe_route(T, E):
+    """(e0, e1) per token of the fixed balanced top-2 routing."""
+    e0 = np.arange(T) % E
+    return e0, (e0 + 1) % E
+
+
+def expert_tokens(T, E, e):
+    """Tokens routed to expert e, ascending (every expert gets 2 T / E)."""
+    e0, e1 = moe_route(T, E)
+    return np.nonzero((e0 == e) | (e1 == e))[0]
+
+
+def r32(x):
+    """fp32 storage (router logits and gates are kept in fp32)."""
+    return np.asarray(np.asarray(x, np.float64).astype(np.float32), np.float64)
+
+
+def _gate_rnd(rnd):
+    """fp32 rounding of router logits / gates in the storage-rounded regime;
+    none in the fp64 pin mode (rnd = ident)."""
+    return ident if rnd is ident else r32
+
+
+def moe_layer_fwd(x, W, cfg, rnd):
+    f = lambda k: np.asarray(W[k], np.float64)
+    c = attn_fwd(x, W, cfg, rnd)
+    h2, T, E, F = c["h2"], c["h2"].shape[0], cfg.n_experts, cfg.ffn
+    r32 = _gate_rnd(rnd)
+    logits = r32(h2 @ f("router").T)
+    e0, e1 = moe_route(T, E)
+    t = np.arange(T)
+    l0, l1 = logits[t, e0], logits[t, e1]
+    g0 = r32(1.0 / (1.0 + np.exp(l1 - l0)))
+    g1 = r32(1.0 / (1.0 + np.exp(l0 - l1)))
+    O = np.zeros((E, T, cfg.hidden))        # expert outputs scattered back to token rows
+    exp_cache = []
+    for e in range(E):
+        rows = expert_tokens(T, E, e)
+        X = h2[rows]
+        gu = r64(rnd, X @ np.concatenate([f("w1_%d" % e), f("w3_%d" % e)]).T)
+        a, b = gu[:, :F], gu[:, F:]
+        H = r64(rnd, silu(a) * b)
+        O[e, rows] = r64(rnd, H @ f("w2_%d" % e).T)
+        exp_cache.append(dict(rows=rows, X=X, a=a, b=b, H=H))
+    y = r64(rnd, c["x2"] + g0[:, None] * O[e0, t] + g1[:, None] * O[e1, t])
+    c.update(logits=logits, g0=g0, g1=g1, O=O, exp=exp_cache)
+    return y, c
+
+
+def moe_layer_bwd(dy, c, W, cfg, rnd):
+    f = lambda k: np.asarray(W[k], np.float64)
+    dy = np.asarray(dy, np.float64)
+    G = {}
+    h2, T, E, F = c["h2"], dy.shape[0], cfg.n_experts, cfg.ffn
+    r32 = _gate_rnd(rnd)
+    e0, e1 = moe_route(T, E)
+    t = np.arange(T)
+    g0, g1, O = c["g0"], c["g1"], c["O"]
+    # combine: dO_e[t] = g_k[t] dy[t] for the pair (t, e = e_k); dg_k = <dy, O_e_k>
+    dO = np.zeros_like(O)
+    dO[e0, t] = r64(rnd, g0[:, None] * dy)
+    dO[e1, t] = r64(rnd, g1[:, None] * dy)
+    dg0 = r32(np.sum(dy * O[e0, t], axis=1))
+    dg1 = r32(np.sum(dy * O[e1, t], axis=1))
+    dX = np.zeros((E, T, cfg.hidden))
+    for e in range(E):
+        ec = c["exp"][e]
+        rows = ec["rows"]
+        dOe = dO[e, rows]
+        dH = r64(rnd, dOe @ f("w2_%d" % e))
+        G["w2_%d" % e] = r64(rnd, dOe.T @ ec["H"])
+        da = r64(rnd, dH * ec["b"] * dsilu(ec["a"]))
+        db = r64(rnd, dH * silu(ec["a"]))
+        dX[e, rows] = r64(rnd, da @ f("w1_%d" % e) + db @ f("w3_%d" % e))
+        G["w1_%d" % e] = r64(rnd, da.T @ ec["X"])
+        G["w3_%d" % e] = r64(rnd, db.T @ ec["X"])
+    # gates: g0 = sigma(l0 - l1), g1 = 1 - g0  ->  dl0 = g0 g1 (dg0 - dg1), dl1 = -dl0
+    dl0 = r32(g0 * g1 * (dg0 - dg1))
+    dlog = np.zeros((T, E))
+    dlog[t, e0] = dl0
+    dlog[t, e1] = -dl0
+    G["router"] = r64(rnd, dlog.T @ h2)
+    dh2 = r64(rnd, dX[e0, t] + dX[e1, t] + dlog @ f("router"))
+    return attn_bwd(dy, dh2, c, W, cfg, rnd, G), G
 
 
 def mse_loss(y, t):
@@ -153,18 +263,19 @@ def mse_loss(y, t):
 
 def llama_stack_fwd_bwd(x, t, Ws, cfg, rnd):
     """Ws: list over layers of weight dicts.  Returns (loss, grads per layer,
-    layer outputs)."""
+    layer outputs).  Mixtral-shaped layers when cfg.n_experts > 0."""
+    layer_fwd, layer_bwd = (moe_layer_fwd, moe_layer_bwd) if cfg.n_experts else (llama_layer_fwd, llama_layer_bwd)
     h = r64(rnd, x)
     caches, outs = [], []
     for W in Ws:
-        h, c = llama_layer_fwd(h, W, cfg, rnd)
+        h, c = layer_fwd(h, W, cfg, rnd)
         caches.append(c)
         outs.append(h)
     loss, dy = mse_loss(h, t)
     d = r64(rnd, dy)
     grads = [None] * len(Ws)
     for l in reversed(range(len(Ws))):
-        d, grads[l] = llama_layer_bwd(d, caches[l], Ws[l], cfg, rnd)
+        d, grads[l] = layer_bwd(d, caches[l], Ws[l], cfg, rnd)
     return loss, grads, outs
 
 

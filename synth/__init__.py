@@ -11,12 +11,14 @@ layer math or scheduling).  It only defines:
 """
 from .gen import (splitmix64, uniform_u24, values, std_to_k, K_MLP, K_UNIT,
                   SEED_WEIGHTS, seed_inputs, seed_targets)
-from .models import (ModelConfig, ParamSpec, llama_param_table, mlp_param_table,
-                     LLAMA3_8B, LLAMA3_70B, MIXTRAL_8X7B, small_llama, MLP_CONFIG1)
+from .models import (ModelConfig, ParamSpec, llama_param_table, mlp_param_table, moe_param_table,
+                     param_table, compute_ops, LLAMA3_8B, LLAMA3_70B, MIXTRAL_8X7B, small_llama,
+                     small_mixtral, MLP_CONFIG1)
 
 __all__ = [
     "splitmix64", "uniform_u24", "values", "std_to_k", "K_MLP", "K_UNIT",
     "SEED_WEIGHTS", "seed_inputs", "seed_targets",
-    "ModelConfig", "ParamSpec", "llama_param_table", "mlp_param_table",
-    "LLAMA3_8B", "LLAMA3_70B", "MIXTRAL_8X7B", "small_llama", "MLP_CONFIG1",
+    "ModelConfig", "ParamSpec", "llama_param_table", "mlp_param_table", "moe_param_table",
+    "param_table", "compute_ops", "LLAMA3_8B", "LLAMA3_70B", "MIXTRAL_8X7B", "small_llama",
+    "small_mixtral", "MLP_CONFIG1",
 ]

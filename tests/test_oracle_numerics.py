@@ -323,3 +323,107 @@ def test_sharded_equals_replicated_with_accumulation(kind):
     for i, p in enumerate(table):
         got = nx.all_gather([sh.master[r][i] for r in range(N)], p.numel)
         assert got.tobytes() == rp.master[i].tobytes()
+
+
+# ---------------------------------------------------------------- Mixtral-shaped layer (config 4)
+def test_moe_routing_is_balanced_top2():
+    """Fixed balanced top-2: every token goes to two distinct
+    experts and every expert receives exactly 2 T / E tokens, ascending."""
+    T, E = 96, 8
+    e0, e1 = om.moe_route(T, E)
+    assert np.all(e0 != e1)
+    seen = np.zeros(T, int)
+    for e in range(E):
+        rows = om.expert_tokens(T, E, e)
+        assert len(rows) == 2 * T // E and np.all(np.diff(rows) > 0)
+        assert np.all((e0[rows] == e) | (e1[rows] == e))
+        seen[rows] += 1
+    assert np.all(seen == 2)
+
+
+def _moe_weights(cfg, seed=7):
+    table = synth.moe_param_table(cfg)
+    full = ost.init_full_params(table)
+    P = len(table) // cfg.layers
+    Ws = []
+    for l in range(cfg.layers):
+        W = {}
+        for j, p in enumerate(table[l * P:(l + 1) * P]):
+            w = full[l * P + j].reshape(p.shape)
+            if p.k == 0.0:
+                w = w + synth.values(seed, p.id, 0, p.numel, 0.2)
+            if p.name == "router":          # spread the gates away from 1/2
+                w = w * 20.0
+            W[p.name] = nx.rne_bf16(w)
+        Ws.append(W)
+    return Ws
+
+
+def _torch_moe_stack(x, t, Ws, cfg):
+    x = torch.tensor(x, dtype=torch.float64)
+    TW = [{k: torch.tensor(v, dtype=torch.float64, requires_grad=True) for k, v in W.items()} for W in Ws]
+
+    def rms(z, g):
+        return z * torch.rsqrt((z * z).mean(1, keepdim=True) + om.RMS_EPS) * g
+
+    grp = cfg.n_heads // cfg.n_kv
+    E = cfg.n_experts
+    h = x
+    for W in TW:
+        T = h.shape[0]
+        h1 = rms(h, W["attn_norm"])
+        q, k, v = h1 @ W["wq"].T, h1 @ W["wk"].T, h1 @ W["wv"].T
+        kk = k.reshape(T, cfg.n_kv, 1, cfg.head_dim).expand(T, cfg.n_kv, grp, cfg.head_dim).reshape(T, -1)
+        vv = v.reshape(T, cfg.n_kv, 1, cfg.head_dim).expand(T, cfg.n_kv, grp, cfg.head_dim).reshape(T, -1)
+        x2 = h + (q + kk * vv) @ W["wo"].T
+        h2 = rms(x2, W["mlp_norm"])
+        logits = h2 @ W["router"].T
+        tok = torch.arange(T)
+        sel = torch.stack([tok % E, (tok + 1) % E], 1)            # [T, 2]
+        gates = torch.softmax(torch.gather(logits, 1, sel), dim=1)
+        out = torch.zeros_like(x2)
+        for e in range(E):
+            for kslot in range(2):
+                m = sel[:, kslot] == e
+                xe = h2[m]
+                oe = (torch.nn.functional.silu(xe @ W["w1_%d" % e].T) * (xe @ W["w3_%d" % e].T)) @ W["w2_%d" % e].T
+                out = out.index_add(0, tok[m], gates[m, kslot:kslot + 1] * oe)
+        h = x2 + out
+    loss = (0.5 * (h - torch.tensor(t, dtype=torch.float64)) ** 2).mean()
+    loss.backward()
+    return loss.item(), [{k: v.grad.numpy() for k, v in W.items()} for W in TW]
+
+
+def test_moe_layer_fp64_vs_torch_autograd():
+    """fp64 mode of the manual Mixtral-shaped backward (gates, router, experts,
+    scatter of dX) == torch.autograd fp64; a dropped term or wrong sign fails."""
+    cfg = synth.small_mixtral(layers=2, seq=64)
+    Ws = _moe_weights(cfg)
+    x, t = ost.rank_batch(cfg, 0)
+    loss, G, _ = om.llama_stack_fwd_bwd(x, t, Ws, cfg, om.ident)
+    tl, TG = _torch_moe_stack(x, t, Ws, cfg)
+    assert abs(loss - tl) <= 1e-12 * abs(tl)
+    for l in range(cfg.layers):
+        for k in G[l]:
+            ref = TG[l][k]
+            assert np.max(np.abs(G[l][k] - ref)) <= 1e-10 * np.max(np.abs(ref)), (l, k)
+
+
+def test_moe_bf16_close_to_fp64_and_sharded_equals_replicated():
+    cfg = synth.small_mixtral(layers=1, seq=64)
+    Ws = _moe_weights(cfg)
+    x, t = ost.rank_batch(cfg, 0)
+    xb = nx.rne_bf16(x)
+    l64, G64, _ = om.llama_stack_fwd_bwd(xb, t, Ws, cfg, om.ident)
+    l16, G16, _ = om.llama_stack_fwd_bwd(xb, t, Ws, cfg, nx.rne_bf16)
+    assert abs(l16 - l64) <= 2e-2 * abs(l64)
+    for k in G64[0]:
+        assert np.linalg.norm(G16[0][k] - G64[0][k]) <= 3e-2 * np.linalg.norm(G64[0][k]), k
+    table = synth.moe_param_table(cfg)
+    sh = ost.ShardedState(table, 2, bf16=True)
+    rp = ost.ReplicatedState(table, 2, bf16=True)
+    l1, _ = ost.sharded_step(sh, cfg, lr=1.5e-5)
+    l2 = ost.replicated_step(rp, cfg, lr=1.5e-5)
+    assert l1 == l2
+    for i, p in enumerate(table):
+        assert nx.all_gather([sh.master[r][i] for r in range(2)], p.numel).tobytes() == rp.master[i].tobytes()
