@@ -27,6 +27,14 @@ sys.path.insert(0, ROOT)
 
 METRIC = "tokens/sec/box (device-timed, max over ranks) at 1/2/4/8 B200; AG/RS GB/s vs 900 GB/s"
 GiB = 1 << 30
+# model -> (synth config name, default layers on one GPU, BASELINE config it stands for)
+MODELS = {
+    "llama3-8b": ("LLAMA3_8B", 32, "BASELINE configs[1]"),
+    # 14 B of state per parameter: 70B L=8 (96 GB) and Mixtral L=4 (81 GB) fit
+    # one 180 GB B200; the full stacks are the 8-GPU configs[2] / configs[3]
+    "llama3-70b": ("LLAMA3_70B", 8, "BASELINE configs[2] layer shapes"),
+    "mixtral-8x7b": ("MIXTRAL_8X7B", 4, "BASELINE configs[3] layer shapes"),
+}
 
 
 def parse():
@@ -37,7 +45,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=2)
     ap.add_argument("--seq", type=int, default=2048)
-    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--model", default="llama3-8b", choices=sorted(MODELS),
+                    help="layer shapes (PAPER.md line 440 / BASELINE configs)")
+    ap.add_argument("--layers", type=int, default=0, help="0: the model's default for one GPU")
     ap.add_argument("--micro", type=int, default=1, help="gradient-accumulation micro-steps per step (P:362)")
     ap.add_argument("--checkpoint", action="store_true", help="layer-level activation checkpointing (P:440)")
     ap.add_argument("--passes", default="PS", help="S0 | P | S | PS")
@@ -145,8 +155,11 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import dataclasses
-    cfg = dataclasses.replace(synth.LLAMA3_8B, layers=args.layers, seq=args.seq, batch=args.batch)
+    if args.model != "llama3-8b":
+        print(json.dumps({"impl": "reference", "unavailable": "the oracle sample is defined for the default "
+                          "llama3-8b workload only (a 70B / Mixtral layer's states exceed a bounded CPU sample)"}))
+        return
+    cfg = model_config(args)
     T = 32
     sample_run = OracleSample(cfg, T)
     secs = []
@@ -171,18 +184,23 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
-GEMM_OPS = ("qkv", "o_proj", "gate_up", "down", "down_bwd", "gate_up_bwd", "o_bwd", "qkv_bwd",
-            "re_qkv", "re_o_proj", "re_gate_up")
+def _base_op(name):
+    """exp_gu_3 -> exp_gu (per-expert MoE ops carry the expert index)."""
+    head, _, tail = name.rpartition("_")
+    return head if tail.isdigit() else name
 
 
 def gemm_flops(name, cfg, T):
+    """2 M N K of the op's GEMMs (dX and dW in the backward); None for non-GEMM ops."""
     h, f, qd = cfg.hidden, cfg.ffn, cfg.q_dim
     qkvd = qd + 2 * cfg.kv_dim
-    fwd = {"qkv": 2 * T * h * qkvd, "o_proj": 2 * T * qd * h, "gate_up": 2 * T * h * 2 * f, "down": 2 * T * f * h}
-    bwd = {"down_bwd": 2 * fwd["down"], "gate_up_bwd": 2 * fwd["gate_up"], "o_bwd": 2 * fwd["o_proj"],
-           "qkv_bwd": 2 * fwd["qkv"]}
+    R = 2 * T // cfg.n_experts if cfg.n_experts else 0      # rows per expert (top-2, balanced)
+    fwd = {"qkv": 2 * T * h * qkvd, "o_proj": 2 * T * qd * h, "gate_up": 2 * T * h * 2 * f, "down": 2 * T * f * h,
+           "exp_gu": 2 * R * h * 2 * f, "exp_down": 2 * R * f * h}
+    bwd = {k + "_bwd": 2 * v for k, v in fwd.items()}
+    bwd["o_bwd"] = bwd.pop("o_proj_bwd")
     re = {"re_" + k: v for k, v in fwd.items()}          # checkpoint recompute
-    return {**fwd, **bwd, **re}[name]
+    return {**fwd, **bwd, **re}.get(_base_op(name))
 
 
 def measure_tc(group, world, dev, torch, dist):
@@ -211,6 +229,15 @@ def measure_tc(group, world, dev, torch, dist):
     return pts
 
 
+def model_config(args):
+    import dataclasses
+
+    import synth
+    name, default_layers, _ = MODELS[args.model]
+    return dataclasses.replace(getattr(synth, name), layers=args.layers or default_layers, seq=args.seq,
+                               batch=args.batch)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -231,11 +258,9 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
-    base = synth.LLAMA3_8B
-    cfg = synth.ModelConfig(base.name, base.kind, base.hidden, base.ffn, base.n_heads, base.n_kv, base.head_dim,
-                            args.layers, seq=args.seq, batch=args.batch)
+    cfg = model_config(args)
     T = cfg.tokens
-    table = synth.llama_param_table(cfg)
+    table = synth.param_table(cfg)
     lr = 1.5e-5
     n_micro = max(1, args.micro)
     if world == 1:
@@ -342,9 +367,10 @@ def main():
         if o["kind"] in ("compute", "rs"):
             by.setdefault(o["name"], 0)
             by[o["name"]] += o["dur_us"]
-            if o["name"] in GEMM_OPS:
+            fl = gemm_flops(o["name"], cfg, T)
+            if fl:
                 gemm_us += o["dur_us"]
-                gemm_fl += gemm_flops(o["name"], cfg, T)
+                gemm_fl += fl
     pk = peaks()
     achieved = gemm_fl / (gemm_us * 1e-6) / 1e12 if gemm_us else None
     traffic = None
@@ -398,7 +424,7 @@ def main():
 
     # ---- CPU oracle timed on host cores (rank 0, N = 1 only)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.model == "llama3-8b":
         Ts = 128
         sample_run = OracleSample(cfg, Ts)
         sec = min(sample_run.step() for _ in range(2))
@@ -416,13 +442,16 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": {"workload": "llama3-8b-stack (BASELINE configs[1]): L=%d h=4096 f=14336 32/8 heads, "
+                "config": {"workload": "%s-stack (%s): L=%d h=%d f=%d %d/%d heads%s, "
                                        "seq %d, b=%d per GPU, ZeRO-3 + proactive prefetch%s%s" %
-                                       (cfg.layers, args.seq, args.batch,
+                                       (args.model, MODELS[args.model][2], cfg.layers, cfg.hidden, cfg.ffn,
+                                        cfg.n_heads, cfg.n_kv,
+                                        ", %d experts top-2 (fixed balanced)" % cfg.n_experts if cfg.n_experts else "",
+                                        args.seq, args.batch,
                                         " + selective unshard" if "S" in args.passes else "",
                                         (", grad accumulation %d" % n_micro if n_micro > 1 else "") +
                                         (", layer activation checkpointing" if args.checkpoint else "")),
-                           "model": "llama3-8b-shaped synthetic stack (random init)",
+                           "model": "%s-shaped synthetic stack (random init)" % args.model,
                            "global_batch": world * args.batch * n_micro, "micro_steps": n_micro,
                            "checkpoint": bool(args.checkpoint),
                            "seq_len": args.seq, "parallelism": "fsdp%d" % world, "passes": args.passes,

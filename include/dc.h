@@ -228,6 +228,13 @@ typedef struct {
                                  /* "recomputing each layer as a block"): only each */
                                  /* layer's output is kept; the backward of a layer */
                                  /* re-runs its forward ops (all but down) first    */
+  int32_t n_experts;             /* 0: Llama-shaped MLP; 2..8: Mixtral-shaped MoE  */
+                                 /* MLP: router [E, hidden], */
+                                 /* fixed balanced top-2 routing t -> t mod E,       */
+                                 /* (t+1) mod E, gates = softmax of the two logits;  */
+                                 /* per layer 7 + 3E params in the order attn_norm,  */
+                                 /* wq, wk, wv, wo, mlp_norm, router, then w1_e,     */
+                                 /* w3_e, w2_e per expert.  tokens % (4E) == 0.      */
 } dc_model_dims;
 
 /* Plain GEMM entry (tests, comparators): C[M,N] (bf16, row-major, ldc) =

@@ -16,7 +16,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "--expt-relaxed-constexpr"]
 
-SOURCES = ["api.cpp", "planner.cpp", "gemm_sm100.cu", "glue.cu", "comm.cu", "model.cu", "sm_partition.cpp"]
+SOURCES = ["api.cpp", "planner.cpp", "gemm_sm100.cu", "glue.cu", "comm.cu", "model.cu", "moe.cu", "sm_partition.cpp"]
 
 
 def _newer(src, dst, deps=()):

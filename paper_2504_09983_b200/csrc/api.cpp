@@ -181,6 +181,7 @@ extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
   DC_CUDA_TRY(preload_glue_kernels(), &c->err);
   DC_CUDA_TRY(preload_comm_kernels(), &c->err);
   DC_CUDA_TRY(preload_gemm_kernels(), &c->err);
+  DC_CUDA_TRY(preload_moe_kernels(), &c->err);
   DC_CUDA_TRY(cudaHostAlloc(&c->err_host, 4, cudaHostAllocMapped), &c->err);
   *c->err_host = 0;
   DC_CUDA_TRY(cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0), &c->err);

@@ -111,6 +111,16 @@ void k_act_fwd(const void* gu, void* act, int T, int F, cudaStream_t st);
 void k_act_bwd(const void* dact, const void* gu, void* dgu, int T, int F, cudaStream_t st);
 void k_loss(const void* y, const void* t, void* dy, float* partial, float* loss, int64_t n, cudaStream_t st);
 void k_zero(void* p, int64_t bytes, cudaStream_t st);
+// moe.cu: Mixtral-shaped MoE MLP glue (fixed balanced top-2 routing)
+void k_moe_router_fwd(const void* h2, const void* wr, float* g01, int T, int H, int E, cudaStream_t st);
+void k_moe_gather(const void* h2, void* X, int T, int H, int E, cudaStream_t st);
+void k_moe_combine(const void* x2, const void* O, const float* g01, void* y, int T, int H, int E, cudaStream_t st);
+void k_moe_combine_bwd(const void* dy, const void* O, const float* g01, void* dO, float* dl0, int T, int H, int E,
+                       cudaStream_t st);
+void k_moe_router_bwd(const void* dX, const float* dl0, const void* wr, const void* h2, void* dh2, float* part,
+                      int T, int H, int E, cudaStream_t st);
+int moe_router_dw_blocks(int T);
+cudaError_t preload_moe_kernels();
 // force-load every kernel of the library (lazy module loading at first launch
 // can block behind another rank's spinning flag wait on the same GPU)
 cudaError_t preload_glue_kernels();

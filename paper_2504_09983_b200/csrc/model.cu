@@ -24,16 +24,27 @@ namespace {
 
 enum OpCode {
   F_ATTN_NORM, F_QKV, F_ATTN_MIX, F_O, F_MLP_NORM, F_GATE_UP, F_ACT, F_DOWN, F_LOSS,
-  B_DOWN, B_ACT, B_GATE_UP, B_MLP_NORM, B_O, B_ATTN_MIX, B_QKV, B_ATTN_NORM, RS_OP
+  B_DOWN, B_ACT, B_GATE_UP, B_MLP_NORM, B_O, B_ATTN_MIX, B_QKV, B_ATTN_NORM, RS_OP,
+  // Mixtral-shaped MoE MLP (per-expert ops carry the expert index)
+  F_ROUTER, F_MOE_GATHER, F_EXP_GU, F_EXP_ACT, F_EXP_DOWN, F_MOE_COMBINE,
+  B_MOE_COMBINE, B_EXP_DOWN, B_EXP_ACT, B_EXP_GU, B_ROUTER
 };
 const char* op_name(int c) {
   static const char* n[] = {"attn_norm", "qkv", "attn_mix", "o_proj", "mlp_norm", "gate_up", "act", "down", "loss",
                             "down_bwd", "act_bwd", "gate_up_bwd", "mlp_norm_bwd", "o_bwd", "attn_mix_bwd",
-                            "qkv_bwd", "attn_norm_bwd", "rs"};
+                            "qkv_bwd", "attn_norm_bwd", "rs",
+                            "router", "moe_gather", "exp_gu", "exp_act", "exp_down", "moe_combine",
+                            "moe_combine_bwd", "exp_down_bwd", "exp_act_bwd", "exp_gu_bwd", "router_bwd"};
   return n[c];
 }
 // param slots inside a layer (llama order of synth/models.py)
 enum { P_G1, P_Q, P_K, P_V, P_O, P_G2, P_GATE, P_UP, P_DOWN, P_N };
+// MoE layer (synth/models.py moe_names): attention slots, router, then
+// per expert e: w1 (gate) 7 + 3e, w3 (up) 8 + 3e, w2 (down) 9 + 3e
+enum { P_ROUTER = 6, P_EXP0 = 7 };
+inline int p_w1(int e) { return P_EXP0 + 3 * e; }
+inline int p_w3(int e) { return P_EXP0 + 3 * e + 1; }
+inline int p_w2(int e) { return P_EXP0 + 3 * e + 2; }
 
 struct S0 {
   int kind;       // K_COMPUTE / K_AG / K_REL / K_RS
@@ -42,9 +53,17 @@ struct S0 {
   int micro, layer;
   std::vector<int> params;
   bool re = false;  // forward op re-run in the backward (activation checkpointing)
+  int e = -1;       // expert of a per-expert MoE op
 };
 
-struct LayerAct { int64_t h1, rstd1, qkv, a, x2, h2, rstd2, gu, act, y; };
+std::string op_label(const S0& o) {
+  std::string s = (o.re ? "re_" : "") + std::string(op_name(o.code));
+  if (o.e >= 0) s += "_" + std::to_string(o.e);
+  return s;
+}
+
+// MoE: gu / act / X / O hold all experts' rows, expert-major ([E][R][.])
+struct LayerAct { int64_t h1, rstd1, qkv, a, x2, h2, rstd2, gu, act, y, g01, X, O; };
 
 }  // namespace
 
@@ -56,6 +75,8 @@ struct dc_model {
   std::vector<LayerAct> la;
   int64_t ws_dA = 0, ws_dB = 0, ws_dact = 0, ws_dgu = 0, ws_dh = 0, ws_dx2 = 0, ws_dqkv = 0, ws_dgp = 0,
           ws_lossp = 0, ws_loss = 0;
+  int64_t ws_dO = 0, ws_dX = 0, ws_dl0 = 0, ws_rgp = 0;   // MoE backward
+  int E = 0, R = 0;                                      // experts, rows per expert (2T/E)
   uint64_t act_bytes = 0, layer_act_bytes = 0, ws_bytes = 0;
   uint8_t* act = nullptr;
   const void* x = nullptr;
@@ -104,11 +125,29 @@ static dc_status mfail(dc_model* m, dc_status s, const std::string& e) {
 static void build_s0(dc_model* m) {
   const int L = m->d.layers;
   std::vector<S0> comp;
-  static const int fwd_codes[] = {F_ATTN_NORM, F_QKV, F_ATTN_MIX, F_O, F_MLP_NORM, F_GATE_UP, F_ACT, F_DOWN};
-  static const int bwd_codes[] = {B_DOWN, B_ACT, B_GATE_UP, B_MLP_NORM, B_O, B_ATTN_MIX, B_QKV, B_ATTN_NORM};
+  using CE = std::pair<int, int>;   // (code, expert)
+  std::vector<CE> fwd_codes, bwd_codes, re_codes;
+  for (int c : {F_ATTN_NORM, F_QKV, F_ATTN_MIX, F_O, F_MLP_NORM}) fwd_codes.push_back({c, -1});
+  if (m->E == 0) {
+    for (int c : {F_GATE_UP, F_ACT, F_DOWN}) fwd_codes.push_back({c, -1});
+    for (int c : {B_DOWN, B_ACT, B_GATE_UP}) bwd_codes.push_back({c, -1});
+  } else {   // synth/models.py moe_compute_ops
+    fwd_codes.push_back({F_ROUTER, -1});
+    fwd_codes.push_back({F_MOE_GATHER, -1});
+    for (int e = 0; e < m->E; ++e)
+      for (int c : {F_EXP_GU, F_EXP_ACT, F_EXP_DOWN}) fwd_codes.push_back({c, e});
+    fwd_codes.push_back({F_MOE_COMBINE, -1});
+    bwd_codes.push_back({B_MOE_COMBINE, -1});
+    for (int e = 0; e < m->E; ++e)
+      for (int c : {B_EXP_DOWN, B_EXP_ACT, B_EXP_GU}) bwd_codes.push_back({c, e});
+    bwd_codes.push_back({B_ROUTER, -1});
+  }
+  for (int c : {B_MLP_NORM, B_O, B_ATTN_MIX, B_QKV, B_ATTN_NORM}) bwd_codes.push_back({c, -1});
   // layer checkpointing: the forward ops the layer's gradients need
-  static const int re_codes[] = {F_ATTN_NORM, F_QKV, F_ATTN_MIX, F_O, F_MLP_NORM, F_GATE_UP, F_ACT};
-  auto params_of = [&](int code, int l) -> std::vector<int> {
+  // (all but the op that forms the layer output from the saved pieces)
+  for (const CE& ce : fwd_codes)
+    if (ce.first != F_DOWN && ce.first != F_MOE_COMBINE) re_codes.push_back(ce);
+  auto params_of = [&](int code, int e, int l) -> std::vector<int> {
     switch (code) {
       case F_ATTN_NORM: case B_ATTN_NORM: return {m->pid(l, P_G1)};
       case F_QKV: case B_QKV: return {m->pid(l, P_Q), m->pid(l, P_K), m->pid(l, P_V)};
@@ -116,19 +155,28 @@ static void build_s0(dc_model* m) {
       case F_MLP_NORM: case B_MLP_NORM: return {m->pid(l, P_G2)};
       case F_GATE_UP: case B_GATE_UP: return {m->pid(l, P_GATE), m->pid(l, P_UP)};
       case F_DOWN: case B_DOWN: return {m->pid(l, P_DOWN)};
+      case F_ROUTER: case B_ROUTER: return {m->pid(l, P_ROUTER)};
+      case F_EXP_GU: case B_EXP_GU: return {m->pid(l, p_w1(e)), m->pid(l, p_w3(e))};
+      case F_EXP_DOWN: case B_EXP_DOWN: return {m->pid(l, p_w2(e))};
       default: return {};
     }
+  };
+  auto op = [&](const CE& ce, bool fwd, int mu, int l, bool re) {
+    S0 o{K_COMPUTE, ce.first, fwd, mu, l, params_of(ce.first, ce.second, l)};
+    o.re = re;
+    o.e = ce.second;
+    return o;
   };
   // n micro-steps; every micro-step reduce-scatters its gradients
   // into the partitioned accumulator, the last one also updates
   for (int mu = 0; mu < m->n_micro; ++mu) {
     for (int l = 0; l < L; ++l)
-      for (int c : fwd_codes) comp.push_back({K_COMPUTE, c, true, mu, l, params_of(c, l)});
+      for (const CE& c : fwd_codes) comp.push_back(op(c, true, mu, l, false));
     comp.push_back({K_COMPUTE, F_LOSS, true, mu, L - 1, {}});
     for (int l = L - 1; l >= 0; --l) {
       if (m->d.checkpoint)
-        for (int c : re_codes) comp.push_back({K_COMPUTE, c, false, mu, l, params_of(c, l), true});
-      for (int c : bwd_codes) comp.push_back({K_COMPUTE, c, false, mu, l, params_of(c, l)});
+        for (const CE& c : re_codes) comp.push_back(op(c, false, mu, l, true));
+      for (const CE& c : bwd_codes) comp.push_back(op(c, false, mu, l, false));
       comp.push_back({K_RS, RS_OP, false, mu, l, {}});
     }
   }
@@ -178,10 +226,22 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   if (d->hidden % 256 || d->ffn % 256 || m->qd % 256 || m->kvd % 256 || d->hidden > 8192 || d->tokens % 8)
     return mfail(nullptr, DC_EINVAL, "dc_model_create: hidden/ffn/q/kv dims must be multiples of 256, hidden <= 8192");
   const int64_t h = d->hidden, f = d->ffn;
-  const int64_t want[P_N] = {h, m->qd * h, m->kvd * h, m->kvd * h, h * m->qd, h, f * h, f * h, h * f};
+  m->E = d->n_experts;
+  if (m->E != 0 && (m->E < 2 || m->E > 8 || d->tokens % (4 * m->E)))
+    return mfail(nullptr, DC_EINVAL, "dc_model_create: n_experts is 0 or 2..8, tokens % (4 n_experts) == 0");
+  m->R = m->E ? 2 * d->tokens / m->E : 0;
+  std::vector<int64_t> want = {h, m->qd * h, m->kvd * h, m->kvd * h, h * m->qd, h};
+  if (m->E == 0) {
+    for (int64_t n : {f * h, f * h, h * f}) want.push_back(n);
+  } else {
+    want.push_back(m->E * h);
+    for (int e = 0; e < m->E; ++e)
+      for (int64_t n : {f * h, f * h, h * f}) want.push_back(n);
+  }
   for (int l = 0; l < d->layers; ++l) {
-    if (L.layer_count[l] != P_N) return mfail(nullptr, DC_EINVAL, "dc_model_create: 9 params per layer expected");
-    for (int s = 0; s < P_N; ++s)
+    if (L.layer_count[l] != (int)want.size())
+      return mfail(nullptr, DC_EINVAL, "dc_model_create: params per layer: 9 (Llama) or 7 + 3E (MoE) expected");
+    for (int s = 0; s < (int)want.size(); ++s)
       if (ctx_numel(ctx, L.layer_first[l] + s) != want[s])
         return mfail(nullptr, DC_EINVAL, "dc_model_create: param shape mismatch");
   }
@@ -199,8 +259,13 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
       continue;
     }
     a.h1 = take(T * h * 2); a.rstd1 = take(T * 4); a.qkv = take(T * m->qkvd * 2); a.a = take(T * m->qd * 2);
-    a.x2 = take(T * h * 2); a.h2 = take(T * h * 2); a.rstd2 = take(T * 4); a.gu = take(T * 2 * f * 2);
-    a.act = take(T * f * 2); a.y = take(T * h * 2);
+    a.x2 = take(T * h * 2); a.h2 = take(T * h * 2); a.rstd2 = take(T * 4);
+    const int64_t rows = m->E ? 2 * T : T;          // top-2: every token in two experts
+    if (m->E) { a.g01 = take(T * 2 * 4); a.X = take(rows * h * 2); }
+    a.gu = take(rows * 2 * f * 2);
+    a.act = take(rows * f * 2);
+    if (m->E) a.O = take(rows * h * 2);
+    a.y = take(T * h * 2);
     if (l == 0) m->layer_act_bytes = off;
   }
   const uint64_t ws0 = off;
@@ -208,6 +273,10 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   m->ws_dgu = take(T * 2 * f * 2); m->ws_dh = take(T * h * 2); m->ws_dx2 = take(T * h * 2);
   m->ws_dqkv = take(T * m->qkvd * 2); m->ws_dgp = take((int64_t)rmsnorm_bwd_blocks((int)T) * h * 4);
   m->ws_lossp = take(1024 * 4); m->ws_loss = take(4 * (int64_t)m->n_micro);
+  if (m->E) {
+    m->ws_dO = take(2 * T * h * 2); m->ws_dX = take(2 * T * h * 2); m->ws_dl0 = take(T * 4);
+    m->ws_rgp = take((int64_t)moe_router_dw_blocks((int)T) * m->E * h * 4);
+  }
   m->ws_bytes = off - ws0;
   m->act_bytes = off;
   build_s0(m.get());
@@ -438,6 +507,69 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       m->cur_d ^= 1;
       break;
     }
+    // ---- Mixtral-shaped MoE MLP; expert e's R rows
+    // sit at row e R of X / gu / act / O and of the dO / dX workspaces
+    case F_ROUTER:
+      k_moe_router_fwd(m->A(a.h2), m->W(l, P_ROUTER), (float*)m->A(a.g01), T, H, m->E, st);
+      break;
+    case F_MOE_GATHER:
+      k_moe_gather(m->A(a.h2), m->A(a.X), T, H, m->E, st);
+      break;
+    case F_EXP_GU: {
+      const int e = o.e, R = m->R;
+      s = gemm(m, R, 2 * F, H, m->A(a.X) + (int64_t)e * R * H * 2, H, 0, {m->W(l, p_w1(e)), m->W(l, p_w3(e))},
+               {H, H}, {F / 256, 2 * F / 256}, 0, 0, m->A(a.gu) + (int64_t)e * R * 2 * F * 2, 2 * F, nullptr, 0, st);
+      break;
+    }
+    case F_EXP_ACT:
+      k_act_fwd(m->A(a.gu) + (int64_t)o.e * m->R * 2 * F * 2, m->A(a.act) + (int64_t)o.e * m->R * F * 2, m->R, F, st);
+      break;
+    case F_EXP_DOWN: {
+      const int e = o.e, R = m->R;
+      s = gemm(m, R, H, F, m->A(a.act) + (int64_t)e * R * F * 2, F, 0, {m->W(l, p_w2(e))}, {F}, {H / 256}, 0, 0,
+               m->A(a.O) + (int64_t)e * R * H * 2, H, nullptr, 0, st);
+      break;
+    }
+    case F_MOE_COMBINE:
+      k_moe_combine(m->A(a.x2), m->A(a.O), (const float*)m->A(a.g01), m->A(a.y), T, H, m->E, st);
+      break;
+    case B_MOE_COMBINE:
+      // (the executor has enqueued dc_grad_slot_acquire for this layer)
+      k_moe_combine_bwd(dcur, m->A(a.O), (const float*)m->A(a.g01), m->A(m->ws_dO), (float*)m->A(m->ws_dl0), T, H,
+                        m->E, st);
+      break;
+    case B_EXP_DOWN: {
+      const int e = o.e, R = m->R;
+      uint8_t* dOe = m->A(m->ws_dO) + (int64_t)e * R * H * 2;
+      // dact_e = dO_e W2_e ; dW2_e = dO_e^T act_e
+      s = gemm(m, R, F, H, dOe, H, 0, {m->W(l, p_w2(e))}, {F}, {F / 256}, 1, 0, m->A(m->ws_dact), F, nullptr, 0, st);
+      if (s == DC_OK)
+        s = gemm(m, H, F, R, dOe, H, 1, {m->A(a.act) + (int64_t)e * R * F * 2}, {F}, {F / 256}, 1, 0, G(p_w2(e)), F,
+                 nullptr, 0, st);
+      break;
+    }
+    case B_EXP_ACT:
+      k_act_bwd(m->A(m->ws_dact), m->A(a.gu) + (int64_t)o.e * m->R * 2 * F * 2, m->A(m->ws_dgu), m->R, F, st);
+      break;
+    case B_EXP_GU: {
+      const int e = o.e, R = m->R;
+      const uint8_t* Xe = m->A(a.X) + (int64_t)e * R * H * 2;
+      // dX_e = d(gate|up)_e [W1_e; W3_e] (B split along K) ; dW1_e, dW3_e = d(gate), d(up)^T X_e
+      s = gemm(m, R, H, 2 * F, m->A(m->ws_dgu), 2 * F, 0, {m->W(l, p_w1(e)), m->W(l, p_w3(e))}, {H, H},
+               {F / 64, 2 * F / 64}, 1, 1, m->A(m->ws_dX) + (int64_t)e * R * H * 2, H, nullptr, 0, st);
+      if (s == DC_OK)
+        s = gemm(m, F, H, R, m->A(m->ws_dgu), 2 * F, 1, {Xe}, {H}, {H / 256}, 1, 0, G(p_w1(e)), H, nullptr, 0, st);
+      if (s == DC_OK)
+        s = gemm(m, F, H, R, m->A(m->ws_dgu) + (int64_t)F * 2, 2 * F, 1, {Xe}, {H}, {H / 256}, 1, 0, G(p_w3(e)), H,
+                 nullptr, 0, st);
+      break;
+    }
+    case B_ROUTER:
+      // dh2 = dX_e0 + dX_e1 + dlogits Wr ; dWr = dlogits^T h2 (block partials, fixed-order column sum)
+      k_moe_router_bwd(m->A(m->ws_dX), (const float*)m->A(m->ws_dl0), m->W(l, P_ROUTER), m->A(a.h2), m->A(m->ws_dh),
+                       (float*)m->A(m->ws_rgp), T, H, m->E, st);
+      k_colsum_to_bf16((float*)m->A(m->ws_rgp), moe_router_dw_blocks(T), m->E * H, G(P_ROUTER), st);
+      break;
     default:
       return mfail(m, DC_EINVAL, "run_op: bad op");
   }
@@ -457,9 +589,9 @@ static void compute_pmem(dc_model* m) {
   int64_t stat = L.shard_elems * 6 + 2 * L.grad_slot_bytes + (int64_t)m->ws_bytes + 2 * m->n_micro * T * h * 2 +
                  (m->n_micro > 1 ? L.shard_elems * 4 : 0);   // fp32 grad accumulator
   int64_t live_ag = 0, act = 0;
-  const LayerAct& a0 = m->la[0];
+  const int64_t f = m->d.ffn, R = m->R;
+  // bytes of saved activation a forward op produces
   auto piece = [&](int code) -> int64_t {
-    const int64_t f = m->d.ffn;
     switch (code) {
       case F_ATTN_NORM: return T * h * 2 + T * 4;
       case F_QKV: return T * m->qkvd * 2;
@@ -469,10 +601,19 @@ static void compute_pmem(dc_model* m) {
       case F_GATE_UP: return T * 2 * f * 2;
       case F_ACT: return T * f * 2;
       case F_DOWN: return T * h * 2;
+      case F_ROUTER: return T * 2 * 4;
+      case F_MOE_GATHER: return 2 * T * h * 2;
+      case F_EXP_GU: return R * 2 * f * 2;
+      case F_EXP_ACT: return R * f * 2;
+      case F_EXP_DOWN: return R * h * 2;
+      case F_MOE_COMBINE: return T * h * 2;
       default: return 0;
     }
   };
-  (void)a0;
+  const int out_code = m->E ? F_MOE_COMBINE : F_DOWN;   // forms the layer output y
+  int64_t layer_total = 0;
+  for (const S0& o : m->s0)
+    if (o.kind == K_COMPUTE && o.fwd && o.layer == 0 && o.micro == 0) layer_total += piece(o.code);
   // checkpointing: one shared layer activation set (static) + each layer's y
   if (m->d.checkpoint) stat += (int64_t)m->layer_act_bytes - T * h * 2;
   for (size_t i = 0; i < m->s0.size(); ++i) {
@@ -481,15 +622,11 @@ static void compute_pmem(dc_model* m) {
     if (o.kind == K_AG) live_ag += L.S[o.params[0]] * N * 2;
     else if (o.kind == K_REL) live_ag -= L.S[o.params[0]] * N * 2;
     else if (o.kind == K_COMPUTE && m->d.checkpoint) {
-      if (o.fwd && o.code == F_DOWN) act += piece(F_DOWN);
-      else if (!o.fwd && o.code == B_ATTN_NORM) act -= piece(F_DOWN);
+      if (o.fwd && o.code == out_code) act += piece(out_code);
+      else if (!o.fwd && o.code == B_ATTN_NORM) act -= piece(out_code);
     } else if (o.kind == K_COMPUTE) {
       if (o.fwd) act += piece(o.code);
-      else if (o.code == B_ATTN_NORM) {
-        int64_t layer_total = 0;
-        for (int c = F_ATTN_NORM; c <= F_DOWN; ++c) layer_total += piece(c);
-        act -= layer_total;
-      }
+      else if (o.code == B_ATTN_NORM) act -= layer_total;
     }
   }
 }
@@ -524,7 +661,7 @@ extern "C" dc_status dc_model_profile_json(const dc_model* mc, char* buf, size_t
     const char* kind = o.kind == K_AG ? "ag" : o.kind == K_REL ? "rel" : o.kind == K_RS ? "rs" : "compute";
     s += "{\"dur_us\":" + std::to_string(m->dur_us[i]) + ",\"id\":" + std::to_string(i) + ",\"kind\":\"" + kind +
          "\",\"layer\":" + std::to_string(o.layer) + ",\"micro\":" + std::to_string(o.micro) + ",\"name\":\"" +
-         (o.kind == K_AG ? "ag" : o.kind == K_REL ? "rel" : (o.re ? "re_" : "") + std::string(op_name(o.code))) +
+         (o.kind == K_AG ? "ag" : o.kind == K_REL ? "rel" : op_label(o)) +
          "\",\"p_mem\":" +
          std::to_string(m->p_mem[i]) + ",\"params\":[";
     for (size_t j = 0; j < o.params.size(); ++j) s += (j ? "," : "") + std::to_string(o.params[j]);
@@ -625,7 +762,7 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
         if (N > 1)
           for (int p : o.params)
             if (gather_ev[p]) cudaStreamWaitEvent(cs, gather_ev[p], 0);
-        if (o.code == B_DOWN) {   // first grad-slot write of the layer's backward
+        if (o.code == B_DOWN || o.code == B_MOE_COMBINE) {   // first non-recompute backward op of the layer
           s = dc_grad_slot_acquire(m->ctx, o.layer, cs);
           if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
         }
@@ -700,8 +837,9 @@ extern "C" dc_status dc_model_loss_ptr(const dc_model* m, float** loss) {
 extern "C" dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t which, void** p) {
   if (!m || !p || !m->act || layer < 0 || layer >= m->d.layers) return mfail(nullptr, DC_EINVAL, "dc_model_act_ptr: bad args");
   const LayerAct& a = m->la[layer];
-  const int64_t offs[] = {a.h1, a.qkv, a.a, a.x2, a.h2, a.gu, a.act, a.y, m->ws_dA, m->ws_dB};
-  if (which < 0 || which >= 10) return mfail(nullptr, DC_EINVAL, "dc_model_act_ptr: which in [0, 10)");
+  const int64_t offs[] = {a.h1, a.qkv, a.a, a.x2, a.h2, a.gu, a.act, a.y, m->ws_dA, m->ws_dB, a.g01, a.X, a.O};
+  const int nw = m->E ? 13 : 10;
+  if (which < 0 || which >= nw) return mfail(nullptr, DC_EINVAL, "dc_model_act_ptr: which in [0, 10) (MoE: [0, 13))");
   *p = m->A(offs[which]);
   return DC_OK;
 }
@@ -710,6 +848,7 @@ extern "C" dc_status dc_model_set_option(dc_model* m, const char* key, int64_t v
   if (!m || !key) return mfail(nullptr, DC_EINVAL, "dc_model_set_option: null argument");
   if (!strcmp(key, "side_adam")) {
     if (value && ctx_world(m->ctx) != 1) return mfail(m, DC_EINVAL, "side_adam needs N == 1");
+    if (value && m->E) return mfail(m, DC_EINVAL, "side_adam: Llama-shaped layers only");
     m->side_adam = value != 0;
     return DC_OK;
   }
@@ -733,6 +872,7 @@ extern "C" dc_status dc_model_set_option(dc_model* m, const char* key, int64_t v
   }
   if (!strcmp(key, "fused_adam")) {
     if (value && ctx_world(m->ctx) != 1) return mfail(m, DC_EINVAL, "fused_adam needs N == 1");
+    if (value && m->E) return mfail(m, DC_EINVAL, "fused_adam: Llama-shaped layers only");
     m->fused_adam = value != 0;
     return DC_OK;
   }

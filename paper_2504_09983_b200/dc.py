@@ -71,7 +71,7 @@ class Fragment(C.Structure):
 class ModelDims(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("ffn", C.c_int32), ("n_heads", C.c_int32), ("n_kv", C.c_int32),
                 ("head_dim", C.c_int32), ("layers", C.c_int32), ("tokens", C.c_int32),
-                ("checkpoint", C.c_int32)]
+                ("checkpoint", C.c_int32), ("n_experts", C.c_int32)]
 
 
 class GemmArgs(C.Structure):

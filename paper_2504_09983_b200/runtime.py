@@ -28,9 +28,10 @@ def table_arrays(table):
 
 
 def max_s0_ops(table, micro_steps=1):
-    # compute ops (<= 9 fwd + 9 bwd per layer + loss) + one gather and one
-    # release per param per phase per micro-step, rounded up generously
-    return (2 * 3 * len(table) + 20 * (max(p.layer for p in table) + 1) + 16) * micro_steps
+    # one gather and one release per param per phase, the compute ops (at most
+    # 3 per param and 20 per layer, incl. recompute) + RS per layer, per
+    # micro-step, rounded up generously
+    return (8 * len(table) + 24 * (max(p.layer for p in table) + 1) + 16) * micro_steps
 
 
 class RankState:
@@ -173,7 +174,7 @@ def attach_model(ranks, cfg, xs, targets, checkpoint=False):
     """dc_model_create + bind per rank; xs/targets: dict rank -> bf16 device
     [n, T, H] (n = micro_steps micro-batches; [T, H] when n = 1)."""
     d = dc.ModelDims(cfg.hidden, cfg.ffn, cfg.n_heads, cfg.n_kv, cfg.head_dim, cfg.layers, cfg.tokens,
-                     int(checkpoint))
+                     int(checkpoint), int(getattr(cfg, "n_experts", 0)))
     for r, st in ranks.items():
         m = C.c_void_p()
         dc.check(dc.lib.dc_model_create(st.ctx, C.byref(d), C.byref(m)))

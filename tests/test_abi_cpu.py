@@ -86,10 +86,13 @@ def test_plan_parity_pins():
         assert o == c
 
 
-def test_plan_parity_llama_s0():
-    comp = synth.models.llama_compute_ops(synth.small_llama(layers=4))
+@pytest.mark.parametrize("cfg", [synth.small_llama(layers=4), synth.small_mixtral(layers=3)], ids=["llama", "mixtral"])
+def test_plan_parity_layer_stack_s0(cfg):
+    """dc_plan == oracle on the S_0 of a Llama- and a Mixtral-shaped stack
+    (31 tensors per MoE layer: many small gathers for Fuse)."""
+    comp = synth.compute_ops(cfg)
     s0 = osd.build_s0(comp)
-    B = {p.id: nx.shard_len(p.numel, 8) * 8 * 2 for p in synth.llama_param_table(synth.small_llama(layers=4))}
+    B = {p.id: nx.shard_len(p.numel, 8) * 8 * 2 for p in synth.param_table(cfg)}
     live = osd.live_before_s0(s0, B)
     rng = random.Random(3)
     act, pm = 0, {}

@@ -1,0 +1,169 @@
+"""Mixtral-shaped MoE layers (PAPER.md line 440:
+Mixtral 8x7B) through the sharded step on the GPU, against the oracle's
+moe_layer_fwd/bwd (oracle/model.py) and its N-rank simulated sharded step.
+
+31 tensors per layer at E = 8 (many medium shards: the small-message gather
+regime of P:471).  Tolerances as for the Llama-shaped stack (BASELINE north
+star): bf16 layer outputs, loss and grads <= 2e-2 relative (norm-wise); the
+updated fp32 master within 2.02 lr everywhere and <= 1e-6 on >= 95 % of the
+elements (Adam's step-1 update is -lr g / (|g| + eps)).
+"""
+import ctypes as C
+import json
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import model as om
+from oracle import numerics as nx
+from oracle import step as ost
+from tests.gpu_util import bf16_tensor, rel_norm, to_np
+
+pytestmark = pytest.mark.gpu
+
+dc = pytest.importorskip("paper_2504_09983_b200.dc")
+from paper_2504_09983_b200 import runtime as rt  # noqa: E402
+
+LR = 1e-3
+PS = dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD
+
+
+def _setup(cfg, world, passes, checkpoint=False, M=1 << 40, prefetch=1 << 22):
+    table = synth.param_table(cfg)
+    ranks = rt.create_ranks(table, world, lr=LR)
+    xs, ts = {}, {}
+    for r in ranks:
+        x, t = ost.rank_batch(cfg, r)
+        xs[r], ts[r] = bf16_tensor(x), bf16_tensor(t)
+    rt.attach_model(ranks, cfg, xs, ts, checkpoint=checkpoint)
+    prof = rt.profile_json(ranks[0], tc=[[4096, 10], [1 << 20, 20], [1 << 26, 400]])
+    sched = dc.plan(json.dumps(prof), M, M_prefetch=prefetch, passes=passes, strict=True)
+    rt.bind(ranks, {r: sched for r in ranks})
+    return table, ranks, prof
+
+
+def _loss(st):
+    return rt.view(rt.loss_ptr(st), 1, torch.float32).item()
+
+
+def test_moe_s0_matches_workload_graph():
+    """The executor's compute ops (profile skeleton) are synth's MoE op graph,
+    in order, with the same consumed params; gathers/releases follow S_0."""
+    cfg = synth.small_mixtral(layers=2, seq=128)
+    for ck in (False, True):
+        _, ranks, prof = _setup(cfg, 1, dc.DC_PASS_SHARD, checkpoint=ck)
+        got = [(o["name"], o["phase"], o["layer"], o["params"]) for o in prof["ops"] if o["kind"] in ("compute", "rs")]
+        want = [(o["name"], o["phase"], o["layer"], o["params"]) for o in synth.compute_ops(cfg, checkpoint=ck)]
+        assert got == want
+        n_ag = sum(o["kind"] == "ag" for o in prof["ops"])
+        assert n_ag == 2 * len(synth.param_table(cfg))        # one per param per phase (S_0)
+
+
+@pytest.mark.parametrize("world,passes", [(1, dc.DC_PASS_SHARD), (2, PS)])
+def test_moe_step_matches_oracle(world, passes):
+    cfg = synth.small_mixtral(layers=2, seq=128)
+    table, ranks, _ = _setup(cfg, world, passes)
+    oracle = ost.ShardedState(table, world, bf16=True)
+    o_losses, o_grads = ost.sharded_step(oracle, cfg, lr=LR)
+    rt.step(ranks, 1)
+    torch.cuda.synchronize()
+    rt.poll(ranks)
+    for r, st in ranks.items():
+        assert abs(_loss(st) - o_losses[r]) <= 2e-2 * abs(o_losses[r])
+        for layer in (0, 1):
+            slot = C.c_void_p()
+            dc.check(dc.lib.dc_grad_slot(st.ctx, layer, C.byref(slot)), st.ctx)
+            for i, p in enumerate(table):
+                if p.layer != layer:
+                    continue
+                S = nx.shard_len(p.numel, world)
+                got = to_np(rt.view(slot.value + rt.grad_offset(st, i), world * S, torch.bfloat16))
+                ref = o_grads[r][i]
+                assert rel_norm(got[:p.numel], ref[:p.numel]) <= 2e-2, (r, p.name, rel_norm(got, ref))
+                assert not got[p.numel:].any()
+        ms = st.tensors["master"].cpu().numpy()
+        close, tot = 0, 0
+        for i, p in enumerate(table):
+            off, n = rt.shard_range(st, i)
+            d = np.abs(ms[off:off + n].astype(np.float64) - oracle.master[r][i])
+            assert d.max() <= 2.02 * LR, (r, p.name, d.max())
+            close += int((d <= 1e-6).sum())
+            tot += n
+        assert close >= 0.95 * tot, close / tot
+
+
+def test_moe_layer_outputs_gates_and_routing():
+    """Per layer: the gates (fp32), the expert-major token gather X (exact: a
+    permutation of h2) and the layer output y against the oracle's layer."""
+    cfg = synth.small_mixtral(layers=2, seq=128)
+    table, ranks, _ = _setup(cfg, 1, dc.DC_PASS_SHARD)
+    st = ranks[0]
+    ref = ost.ShardedState(table, 1, bf16=True)
+    full = ref.gathered(0)
+    P = len(table) // cfg.layers
+    Ws = [{p.name: full[l * P + j].reshape(p.shape) for j, p in enumerate(table[l * P:(l + 1) * P])}
+          for l in range(cfg.layers)]
+    x, t = ost.rank_batch(cfg, 0)
+    h = nx.rne_bf16(x)
+    rt.step(ranks, 1)
+    torch.cuda.synchronize()
+    T, H, E = cfg.tokens, cfg.hidden, cfg.n_experts
+
+    def act(l, which, n, dt):
+        p = C.c_void_p()
+        dc.check(dc.lib.dc_model_act_ptr(st.model, l, which, C.byref(p)))
+        return to_np(rt.view(p.value, n, dt))
+
+    for l in range(cfg.layers):
+        y_ref, c = om.moe_layer_fwd(h, Ws[l], cfg, nx.rne_bf16)
+        g01 = act(l, 10, 2 * T, torch.float32).reshape(T, 2)
+        assert rel_norm(g01[:, 0], c["g0"]) <= 1e-3 and rel_norm(g01[:, 1], c["g1"]) <= 1e-3
+        assert np.all(np.abs(g01.sum(axis=1) - 1.0) <= 1e-6)
+        h2 = act(l, 4, T * H, torch.bfloat16).reshape(T, H)
+        X = act(l, 11, 2 * T * H, torch.bfloat16).reshape(E, 2 * T // E, H)
+        for e in range(E):
+            assert np.array_equal(X[e], h2[om.expert_tokens(T, E, e)])
+        y = act(l, 7, T * H, torch.bfloat16).reshape(T, H)
+        assert rel_norm(y, y_ref) <= 2e-2, (l, rel_norm(y, y_ref))
+        h = y_ref
+
+
+@pytest.mark.parametrize("world,passes", [(1, dc.DC_PASS_SHARD), (2, PS)])
+def test_moe_checkpointing_bitexact(world, passes):
+    """Layer activation checkpointing on MoE layers: recompute re-runs the
+    router, gather and every expert's forward from the saved layer input;
+    bit-identical states and loss after two steps."""
+    cfg = synth.small_mixtral(layers=2, seq=128)
+    runs = {}
+    for ck in (False, True):
+        _, ranks, _ = _setup(cfg, world, passes, checkpoint=ck)
+        for t in (1, 2):
+            rt.step(ranks, t)
+            torch.cuda.synchronize()
+            rt.poll(ranks)
+        runs[ck] = ranks
+    a, b = runs[False], runs[True]
+    assert b[0].tensors["act"].numel() < a[0].tensors["act"].numel()
+    for r in a:
+        for k in ("master", "m", "v", "shard"):
+            x, y = a[r].tensors[k], b[r].tensors[k]
+            assert torch.equal(x.view(torch.int16) if k == "shard" else x.view(torch.int32),
+                               y.view(torch.int16) if k == "shard" else y.view(torch.int32)), (r, k)
+        assert _loss(a[r]) == _loss(b[r])
+
+
+def test_moe_options_and_shape_errors():
+    cfg = synth.small_mixtral(layers=1, seq=128)
+    _, ranks, _ = _setup(cfg, 1, dc.DC_PASS_SHARD)
+    st = ranks[0]
+    assert dc.lib.dc_model_set_option(st.model, b"fused_adam", 1) == dc.DC_EINVAL
+    assert dc.lib.dc_model_set_option(st.model, b"side_adam", 1) == dc.DC_EINVAL
+    # a Llama-shaped model on a MoE param table is refused
+    d = dc.ModelDims(cfg.hidden, cfg.ffn, cfg.n_heads, cfg.n_kv, cfg.head_dim, cfg.layers, cfg.tokens, 0, 0)
+    m = C.c_void_p()
+    assert dc.lib.dc_model_create(st.ctx, C.byref(d), C.byref(m)) == dc.DC_EINVAL
+    # tokens must split evenly into 2T/E rows per expert with R % 8 == 0
+    d = dc.ModelDims(cfg.hidden, cfg.ffn, cfg.n_heads, cfg.n_kv, cfg.head_dim, cfg.layers, 136, 0, 8)
+    assert dc.lib.dc_model_create(st.ctx, C.byref(d), C.byref(m)) == dc.DC_EINVAL
