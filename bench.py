@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--checkpoint", action="store_true", help="layer-level activation checkpointing (P:440)")
     ap.add_argument("--passes", default="PS", help="S0 | P | S | PS")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="test mode: every rank on cuda:0 (gloo host collectives, CUDA-IPC peer maps, fixed T_c); "
+                         "exercises the N > 1 launch on a one-GPU box, numbers are not a bench value")
     ap.add_argument("--profile-json", default="", help="write the rank-0 profile / plan here")
     return ap.parse_args()
 
@@ -252,11 +255,19 @@ def main():
     world = args.gpus
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.share_gpu:
+        local = 0
+        os.environ["DC_SYMM"] = "ipc"         # symmetric memory refuses two ranks on one device
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # host-side collectives (barrier, MAX of timings / profiles) run on `cdev`
+    cdev = torch.device("cpu") if args.share_gpu else dev
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
     cfg = model_config(args)
     T = cfg.tokens
@@ -298,10 +309,15 @@ def main():
         step_no += 1
         rt.step(ranks, step_no, profile=(i == 4))
     barrier()
-    tc = measure_tc(group, world, dev, torch, dist) if world > 1 else [[0, 0], [1 << 40, 0]]
+    if world > 1 and not args.share_gpu:
+        tc = measure_tc(group, world, dev, torch, dist)
+    elif world > 1:       # shared GPU: no link to measure; 20 us + 100 GB/s
+        tc = [[0, 20], [1 << 30, 20 + (1 << 30) // 100000]]
+    else:
+        tc = [[0, 0], [1 << 40, 0]]
     prof = rt.profile_json(st, tc=tc)
     if world > 1:   # element-wise MAX over ranks (reading D12)
-        prof = rt.max_reduce_profile(prof, group, device=dev)
+        prof = rt.max_reduce_profile(prof, group, device=cdev)
     total = torch.cuda.get_device_properties(dev).total_memory
     M = int(0.9 * (total - 7 * GiB))
     passes = dc.DC_PASS_SHARD | (dc.DC_PASS_PREFETCH if "P" in args.passes else 0) | \
@@ -347,7 +363,7 @@ def main():
         barrier()
         clocks = clk.stop()
         rt.poll(ranks)
-        ms = torch.tensor([e0.elapsed_time(e1) / k], device=dev)
+        ms = torch.tensor([e0.elapsed_time(e1) / k], device=cdev)
         if world > 1:
             dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=group)
         return ms.item(), clocks, launches
@@ -415,7 +431,7 @@ def main():
         _ = loss_host.tolist()
     e1.record(cs)
     barrier()
-    ems = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    ems = torch.tensor([e0.elapsed_time(e1) / args.steps], device=cdev)
     if world > 1:
         dist.all_reduce(ems, op=dist.ReduceOp.MAX, group=group)
     e2e = {"value": tokens_box / (ems.item() / 1e3), "unit": "tokens/s",
