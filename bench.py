@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--micro", type=int, default=1, help="gradient-accumulation micro-steps per step (P:362)")
     ap.add_argument("--checkpoint", action="store_true", help="layer-level activation checkpointing (P:440)")
     ap.add_argument("--passes", default="PS", help="S0 | P | S | PS")
+    ap.add_argument("--offload", action="store_true",
+                    help="adaptive offload of optimizer states (Alg. 2, P:370-408) with host-resident fragments "
+                         "(reading D28): BASELINE configs[4], e.g. --model llama3-70b --layers 16 --batch 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--share-gpu", action="store_true",
                     help="test mode: every rank on cuda:0 (gloo host collectives, CUDA-IPC peer maps, fixed T_c); "
@@ -206,6 +209,35 @@ def gemm_flops(name, cfg, T):
     return {**fwd, **bwd, **re}.get(_base_op(name))
 
 
+def pcie_peaks(dev, torch, nbytes=1 << 30):
+    """Pinned-host copy bandwidth (GB/s): H2D alone, D2H alone, and both at
+    once on two streams (PCIe is full duplex) — the roofline of the offload
+    path (BASELINE configs[4]).  Outside any timed region."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def run(h2d, d2h):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            if h2d:
+                with torch.cuda.stream(s1):
+                    d.copy_(h, non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    h2.copy_(d2, non_blocking=True)
+        torch.cuda.synchronize()
+        return 3 * nbytes * (h2d + d2h) / (time.perf_counter() - t0) / 1e9
+
+    run(True, True)
+    out = {"h2d": run(True, False), "d2h": run(False, True), "duplex": run(True, True)}
+    del h, h2, d, d2
+    return {k: round(v, 1) for k, v in out.items()}
+
+
 def measure_tc(group, world, dev, torch, dist):
     """T_c(V) table for the planner at N > 1: all-gather time vs full bytes,
     MAX over ranks (reading D12).  Measured with the NCCL comparator (same
@@ -275,10 +307,11 @@ def main():
     lr = 1.5e-5
     n_micro = max(1, args.micro)
     if world == 1:
-        ranks = rt.create_ranks(table, 1, local, virtual=True, lr=lr, micro_steps=n_micro)
+        ranks = rt.create_ranks(table, 1, local, virtual=True, lr=lr, micro_steps=n_micro,
+                                defer_states=args.offload)
     else:
         ranks = rt.create_ranks(table, world, local, virtual=False, group=group, rank=rank, lr=lr,
-                                micro_steps=n_micro)
+                                micro_steps=n_micro, defer_states=args.offload)
     st = ranks[rank]
     from oracle import numerics as nx          # bf16 rounding of the synthetic inputs only
     x_np = np.concatenate([synth.values(synth.seed_inputs(rank, mu), 0, 0, T * cfg.hidden, synth.K_UNIT)
@@ -301,13 +334,20 @@ def main():
             dist.barrier(group=group)
 
     # ---- S_0 warm-up + profile (five warm-up iterations, then profile)
-    prof0 = rt.profile_json(st)
-    s0 = dc.plan(json.dumps(prof0), 1 << 50, passes=dc.DC_PASS_SHARD)
-    rt.bind(ranks, {rank: s0}, group=group)
     step_no = 0
-    for i in range(5):
-        step_no += 1
-        rt.step(ranks, step_no, profile=(i == 4))
+    frags = None
+    if args.offload:
+        # the states do not fit beside the step, so S_0 cannot run: plan from
+        # the executor's exact analytic P_mem (durations are not used by the
+        # P / S / offload passes); whole (layer, m|v) fragments
+        frags = rt.offload_fragments(st, rt.layer_state_bytes(table, world))
+    else:
+        prof0 = rt.profile_json(st)
+        s0 = dc.plan(json.dumps(prof0), 1 << 50, passes=dc.DC_PASS_SHARD)
+        rt.bind(ranks, {rank: s0}, group=group)
+        for i in range(5):
+            step_no += 1
+            rt.step(ranks, step_no, profile=(i == 4))
     barrier()
     if world > 1 and not args.share_gpu:
         tc = measure_tc(group, world, dev, torch, dist)
@@ -315,13 +355,14 @@ def main():
         tc = [[0, 20], [1 << 30, 20 + (1 << 30) // 100000]]
     else:
         tc = [[0, 0], [1 << 40, 0]]
-    prof = rt.profile_json(st, tc=tc)
+    prof = rt.profile_json(st, tc=tc, frags=frags)
     if world > 1:   # element-wise MAX over ranks (reading D12)
         prof = rt.max_reduce_profile(prof, group, device=cdev)
     total = torch.cuda.get_device_properties(dev).total_memory
     M = int(0.9 * (total - 7 * GiB))
     passes = dc.DC_PASS_SHARD | (dc.DC_PASS_PREFETCH if "P" in args.passes else 0) | \
-        (dc.DC_PASS_UNSHARD if "S" in args.passes and args.passes != "S0" else 0)
+        (dc.DC_PASS_UNSHARD if "S" in args.passes and args.passes != "S0" else 0) | \
+        (dc.DC_PASS_OFFLOAD if args.offload else 0)
     t_plan = time.perf_counter()
     sched = dc.plan(json.dumps(prof), M, passes=passes, strict=True)
     t_plan = time.perf_counter() - t_plan
@@ -330,6 +371,22 @@ def main():
     if world > 1:
         dist.barrier(group=group)
     rt.bind(ranks, {rank: sched}, group=group)
+    offload_info = None
+    if args.offload:
+        # extra ring slots (round-robin: a reload need not wait for the write-back
+        # just issued) where the device has room beyond the plan, 6 GiB kept free
+        fb = max(f["bytes"] for f in frags)
+        off_bytes = sum(frags[i]["bytes"] for i in plan["offload"])
+        free_b = torch.cuda.mem_get_info(dev)[0]
+        dev_states = 2 * st.layout.shard_elems * 4 - off_bytes
+        extra = int(max(0, min(2, (free_b - 6 * GiB - dev_states - 4 * fb) // fb)))
+        mf, vf, pool, hb = rt.bind_host_states(ranks, alloc_host=True, extra_slots=extra)[rank]
+        offload_info = {"pcie_peak_gbs": pcie_peaks(dev, torch),
+                        "offloaded_bytes": off_bytes, "fragments": len(plan["offload"]),
+                        "fragment_bytes": max(f["bytes"] for f in frags), "pool_bytes": pool,
+                        "device_state_bytes": 4 * (2 * st.layout.shard_elems - mf - vf),
+                        "pcie_bytes_per_step": 2 * off_bytes, "warnings": plan["warnings"][:4],
+                        "n_warnings": len(plan["warnings"])}
     if world > 1:
         dist.barrier(group=group)
     if args.profile_json and rank == 0:
@@ -374,6 +431,9 @@ def main():
         clocks["remeasured"] = True
     tokens_box = world * T * n_micro
     value = tokens_box / (ms / 1e3)
+    if offload_info:
+        offload_info["pcie_gbs"] = offload_info["pcie_bytes_per_step"] / (ms / 1e3) / 1e9
+        offload_info["pcie_frac_of_duplex"] = offload_info["pcie_gbs"] / offload_info["pcie_peak_gbs"]["duplex"]
 
     # ---- per-op breakdown of the last timed step (events recorded in-region)
     last = rt.profile_json(st)
@@ -472,7 +532,7 @@ def main():
                            "checkpoint": bool(args.checkpoint),
                            "seq_len": args.seq, "parallelism": "fsdp%d" % world, "passes": args.passes,
                            "mem_budget_M": M, "plan_ms": round(t_plan * 1e3, 2),
-                           "unshard_params": len(plan["unshard"]),
+                           "unshard_params": len(plan["unshard"]), "offload": offload_info,
                            "l2": "working set (~120 GB/GPU of weights, states, activations) >> 126 MB L2; no flush"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clocks, "kernels": kernels, "collectives": coll}

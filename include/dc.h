@@ -46,9 +46,11 @@ typedef enum {
 } dc_status;
 
 enum { DC_BF16 = 0, DC_FP32 = 1 };
-enum { DC_INIT_WEIGHTS = 1u, DC_VIRTUAL_RANKS = 2u, DC_DEBUG_POISON = 4u };
+enum { DC_INIT_WEIGHTS = 1u, DC_VIRTUAL_RANKS = 2u, DC_DEBUG_POISON = 4u,
+       DC_DEFER_STATES = 8u   /* exp_avg/exp_avg_sq may be NULL: bound later (dc_model_bind_host_states) */ };
 enum { DC_PASS_SHARD = 1u, DC_PASS_PREFETCH = 2u, DC_PASS_UNSHARD = 4u, DC_PASS_OFFLOAD = 8u };
-enum { DC_D2H_START = 0, DC_D2H_SYNC_FREE = 1, DC_H2D_START = 2, DC_H2D_SYNC = 3 };
+enum { DC_D2H_START = 0, DC_D2H_SYNC_FREE = 1, DC_H2D_START = 2, DC_H2D_SYNC = 3,
+       DC_WRITEBACK = 4       /* host-resident states: D2H of the updated fragment */ };
 
 typedef struct dc_ctx dc_ctx;
 typedef struct dc_schedule dc_schedule;
@@ -211,6 +213,16 @@ dc_status dc_reduce_scatter_step(dc_ctx* ctx, int32_t layer, int32_t step_t, int
  * the pinned host slot on copy_stream), DC_D2H_SYNC_FREE (compute stream waits
  * for that copy; the device slice may then be reused), DC_H2D_START,
  * DC_H2D_SYNC (the stream passed waits for the reload).
+ *
+ * Host-resident states (reading D28, dc_model_bind_host_states): the device
+ * copy of an offloaded fragment exists only in a ring slot of a device pool,
+ * from its reload (DC_H2D_START: host -> slot) through its layer's update
+ * (rs_adam reads and writes the slot) to DC_WRITEBACK (slot -> host, issued
+ * by the executor right after that update); DC_D2H_START / DC_D2H_SYNC_FREE
+ * are then no-ops because the host copy is already current.  The device m / v
+ * arrays hold only the fragments the plan keeps resident, so the offloaded
+ * bytes are really free for activations.  DC_WRITEBACK outside host-state mode
+ * is DC_ESTATE.
  * ------------------------------------------------------------------------ */
 typedef struct { int32_t layer; int32_t state; /* 0 = m, 1 = v */ int64_t offset_elems, elems; } dc_fragment;
 dc_status dc_offload_fragments(dc_ctx* ctx, int64_t max_fragment_bytes, dc_fragment* out,
@@ -306,6 +318,29 @@ dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t which, void
  * "rs_overlap" (default 1): reduce-scatter + Adam on the rs stream beside the
  * backward GEMMs; 0 runs it in compute-stream order. */
 dc_status dc_model_set_option(dc_model* m, const char* key, int64_t value);
+/* Host-resident optimizer states (reading D28; §4.4 P:370-408 with
+ * the update fused per layer, D17).  After dc_bind_schedule of a plan whose
+ * offloaded fragments (dc_offload_fragments) are whole (layer, m|v) slices
+ * forming a prefix of the fragment order:
+ *   query: m_first / v_first = first element of m / v that stays device
+ *     resident (every element below is offloaded; shard_elems when all are,
+ *     0 without offload); pool_bytes = ring of slots the reloads land in
+ *     (slots * the largest offloaded fragment; a slot is reused once the
+ *     fragment in it was written back, in schedule order on the copy stream).
+ *   bind: m_dev / v_dev = fp32 device arrays of shard_elems - m_first /
+ *     v_first elements (NULL if 0), pool = at least the queried pool_bytes of
+ *     device memory (NULL if 0); whole extra slots are used round-robin so
+ *     a reload need not wait for the write-back just issued.  host_bytes (query) = pinned host bytes the offloaded fragments'
+ *     slots span (fragments are packed in id order); host_pinned (bind), if
+ *     not NULL, replaces dc_init's host_pinned buffer.  Caller-owned.  States
+ *     are reset to zero (device arrays and the offloaded fragments' pinned
+ *     host slots): bind before the first step.
+ * DC_EINVAL if the plan's offload set is not such a prefix, DC_ESTATE without
+ * a bound schedule or with micro_steps > 1. */
+dc_status dc_model_host_states_query(dc_model* m, int64_t* m_first, int64_t* v_first, uint64_t* pool_bytes,
+                                     uint64_t* host_bytes);
+dc_status dc_model_bind_host_states(dc_model* m, float* m_dev, float* v_dev, void* pool, uint64_t pool_bytes,
+                                    void* host_pinned, uint64_t host_bytes);
 /* Number of kernels the last dc_model_step launched. */
 dc_status dc_model_launch_count(const dc_model* m, int64_t* n);
 

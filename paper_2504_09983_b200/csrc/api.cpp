@@ -65,7 +65,12 @@ static dc_status make_layout(int world, int n, const int64_t* numel, const int32
 
 using namespace dc;
 
-struct FragInfo { int layer, state; int64_t off, elems, host_off; cudaEvent_t d2h, h2d; };
+struct FragInfo {
+  int layer, state;
+  int64_t off, elems, host_off;
+  cudaEvent_t d2h, h2d;
+  float* slot = nullptr;      // host-resident mode: device ring slot of an offloaded fragment
+};
 
 struct dc_ctx {
   int rank = 0, world = 1, device = 0;
@@ -103,6 +108,10 @@ struct dc_ctx {
   uint32_t* err_host = nullptr;
   uint32_t* err_dev = nullptr;
   std::vector<FragInfo> frags;
+  // host-resident optimizer states (reading D28)
+  bool states_bound = true;             // false from dc_init(DC_DEFER_STATES) until the bind
+  bool host_states = false;
+  std::vector<float*> lay_m, lay_v;     // per layer: m / v base for rs_adam (ring slot) or null
   std::string err;
 
   uint32_t* flag(int q, int64_t word) const { return reinterpret_cast<uint32_t*>(flag_peers[q]) + word; }
@@ -148,7 +157,9 @@ extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
   dc_status s = make_layout(a->world, a->n_params, a->numel, a->layer_of, a->max_s0_ops, &c->L, &err);
   if (s != DC_OK) return fail(nullptr, s, "dc_init: " + err);
   if (a->rank < 0 || a->rank >= a->world) return fail(nullptr, DC_EINVAL, "dc_init: rank out of range");
-  if (!a->shard_param || !a->master || !a->exp_avg || !a->exp_avg_sq || !a->grad_peer_ptrs || !a->flag_peer_ptrs)
+  const bool defer = (a->flags & DC_DEFER_STATES) != 0;
+  if (!a->shard_param || !a->master || (!defer && (!a->exp_avg || !a->exp_avg_sq)) || !a->grad_peer_ptrs ||
+      !a->flag_peer_ptrs)
     return fail(nullptr, DC_EINVAL, "dc_init: null buffer");
   if (a->grad_bytes < (uint64_t)(2 * c->L.grad_slot_bytes)) return fail(nullptr, DC_EOOM, "dc_init: grad buffer < 2 slots");
   if (a->flag_bytes < (uint64_t)(c->L.flag_words * 4)) return fail(nullptr, DC_EOOM, "dc_init: flag table too small");
@@ -186,8 +197,11 @@ extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
   *c->err_host = 0;
   DC_CUDA_TRY(cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0), &c->err);
   cudaStream_t st = 0;
-  DC_CUDA_TRY(cudaMemsetAsync(c->m, 0, c->L.shard_elems * 4, st), &c->err);
-  DC_CUDA_TRY(cudaMemsetAsync(c->v, 0, c->L.shard_elems * 4, st), &c->err);
+  c->states_bound = !defer;
+  if (!defer) {
+    DC_CUDA_TRY(cudaMemsetAsync(c->m, 0, c->L.shard_elems * 4, st), &c->err);
+    DC_CUDA_TRY(cudaMemsetAsync(c->v, 0, c->L.shard_elems * 4, st), &c->err);
+  }
   DC_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<void*>(c->grad_peers[c->rank]), 0, 2 * c->L.grad_slot_bytes, st), &c->err);
   DC_CUDA_TRY(cudaMemsetAsync(c->myflag(0), 0, c->L.flag_words * 4, st), &c->err);
   if (a->flags & DC_INIT_WEIGHTS) {
@@ -449,6 +463,11 @@ dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, con
   const int s = layer & 1;
   const int u = c->layer_use[layer];
   if (u == 0) return fail(c, DC_ESTATE, "dc_reduce_scatter_step: grad slot of layer never acquired");
+  if (!c->states_bound) return fail(c, DC_ESTATE, "dc_reduce_scatter_step: optimizer states not bound (DC_DEFER_STATES)");
+  // host-resident fragments are updated in their ring slot (base shifted so
+  // that base + store_off lands at the slot)
+  float* mb = (c->host_states && c->lay_m[layer]) ? c->lay_m[layer] : c->m;
+  float* vb = (c->host_states && c->lay_v[layer]) ? c->lay_v[layer] : c->v;
   std::vector<RsMember> mem;
   int64_t elems = 0;
   for (int i : params) {
@@ -465,7 +484,7 @@ dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, con
   c->rs_done_total += (uint32_t)ctas;
   dc_status r = k_rs_adam(mem, c->world, c->rank, slots.data(), c->myflag(c->L.f_gready + (int64_t)s * c->world),
                           (uint32_t)u, peers_at(c, c->L.f_gcons + (int64_t)s * c->world + c->rank), (uint32_t)u,
-                          c->myflag(c->L.f_rsdone), c->rs_done_total, c->master, c->m, c->v, c->shard, c->grad_acc,
+                          c->myflag(c->L.f_rsdone), c->rs_done_total, c->master, mb, vb, c->shard, c->grad_acc,
                           mode, n, sc, cc,
                           c->beta1, c->beta2, c->eps, ctas, c->rs_threads, c->timeout_ns, c->err_dev, st);
   if (r != DC_OK) return fail(c, r, "dc_reduce_scatter_step: launch failed");
@@ -517,10 +536,31 @@ extern "C" dc_status dc_offload_fragments(dc_ctx* c, int64_t max_bytes, dc_fragm
 extern "C" dc_status dc_offload(dc_ctx* c, int32_t fi, int32_t op, cudaStream_t st) {
   if (!c || fi < 0 || fi >= (int)c->frags.size()) return fail(c, DC_EINVAL, "dc_offload: bad fragment");
   FragInfo& f = c->frags[fi];
-  float* dev = (f.state == 0 ? c->m : c->v) + f.off;
   if ((uint64_t)(f.host_off + f.elems * 4) > c->host_pinned_bytes || !c->host_pinned)
     return fail(c, DC_EOOM, "dc_offload: pinned host buffer too small");
   char* host = reinterpret_cast<char*>(c->host_pinned) + f.host_off;
+  if (c->host_states && f.slot) {   // reading D28: the host copy is authoritative
+    switch (op) {
+      case DC_D2H_START:
+      case DC_D2H_SYNC_FREE:
+        return DC_OK;                 // already written back after the last update
+      case DC_H2D_START:
+        DC_CUDA_TRY(cudaMemcpyAsync(f.slot, host, f.elems * 4, cudaMemcpyHostToDevice, st), &c->err);
+        DC_CUDA_TRY(cudaEventRecord(f.h2d, st), &c->err);
+        return DC_OK;
+      case DC_H2D_SYNC:
+        DC_CUDA_TRY(cudaStreamWaitEvent(st, f.h2d, 0), &c->err);
+        return DC_OK;
+      case DC_WRITEBACK:
+        DC_CUDA_TRY(cudaMemcpyAsync(host, f.slot, f.elems * 4, cudaMemcpyDeviceToHost, st), &c->err);
+        return DC_OK;
+      default:
+        return fail(c, DC_EINVAL, "dc_offload: bad op");
+    }
+  }
+  if (op == DC_WRITEBACK) return fail(c, DC_ESTATE, "dc_offload: DC_WRITEBACK needs host-resident states");
+  if (!c->states_bound) return fail(c, DC_ESTATE, "dc_offload: optimizer states not bound");
+  float* dev = (f.state == 0 ? c->m : c->v) + f.off;
   switch (op) {
     case DC_D2H_START:
       DC_CUDA_TRY(cudaMemcpyAsync(host, dev, f.elems * 4, cudaMemcpyDeviceToHost, st), &c->err);
@@ -548,6 +588,44 @@ extern "C" dc_status dc_offload(dc_ctx* c, int32_t fi, int32_t op, cudaStream_t 
 
 // internal accessors for model.cu
 namespace dc {
+int ctx_num_frags(const dc_ctx* c) { return (int)c->frags.size(); }
+void ctx_frag(const dc_ctx* c, int i, int* layer, int* state, int64_t* off, int64_t* elems) {
+  const FragInfo& f = c->frags[i];
+  *layer = f.layer; *state = f.state; *off = f.off; *elems = f.elems;
+}
+uint64_t ctx_frag_host_end(const dc_ctx* c, int i) { return (uint64_t)(c->frags[i].host_off + c->frags[i].elems * 4); }
+dc_status ctx_bind_host_states(dc_ctx* c, float* m_dev, int64_t m_first, float* v_dev, int64_t v_first,
+                               const std::vector<float*>& frag_slot, void* host_pinned, uint64_t host_bytes) {
+  if (frag_slot.size() != c->frags.size()) return fail(c, DC_EINVAL, "host states: fragment table changed");
+  if (host_pinned) {
+    c->host_pinned = host_pinned;
+    c->host_pinned_bytes = host_bytes;
+  }
+  if (!c->host_pinned) return fail(c, DC_EINVAL, "host states: no pinned host buffer (dc_init_args.host_pinned)");
+  const int64_t E = c->L.shard_elems;
+  // base pointers: element i of m lives at m_dev[i - m_first] (never read below m_first)
+  c->m = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(m_dev) - (uintptr_t)(m_first * 4));
+  c->v = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(v_dev) - (uintptr_t)(v_first * 4));
+  c->lay_m.assign(c->L.n_layers, nullptr);
+  c->lay_v.assign(c->L.n_layers, nullptr);
+  c->host_states = false;
+  for (size_t i = 0; i < c->frags.size(); ++i) {
+    FragInfo& f = c->frags[i];
+    f.slot = frag_slot[i];
+    if (!f.slot) continue;
+    c->host_states = true;
+    float* base = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(f.slot) - (uintptr_t)(f.off * 4));
+    (f.state == 0 ? c->lay_m : c->lay_v)[f.layer] = base;
+    if ((uint64_t)(f.host_off + f.elems * 4) > c->host_pinned_bytes)
+      return fail(c, DC_EOOM, "host states: pinned host buffer too small");
+    memset(reinterpret_cast<char*>(c->host_pinned) + f.host_off, 0, f.elems * 4);   // states start at zero
+  }
+  if (m_first < E) DC_CUDA_TRY(cudaMemset(m_dev, 0, (E - m_first) * 4), &c->err);
+  if (v_first < E) DC_CUDA_TRY(cudaMemset(v_dev, 0, (E - v_first) * 4), &c->err);
+  DC_CUDA_TRY(cudaDeviceSynchronize(), &c->err);
+  c->states_bound = true;
+  return DC_OK;
+}
 const Layout& ctx_layout(const dc_ctx* c) { return c->L; }
 int ctx_world(const dc_ctx* c) { return c->world; }
 int ctx_rank(const dc_ctx* c) { return c->rank; }

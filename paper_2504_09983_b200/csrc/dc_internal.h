@@ -92,6 +92,13 @@ dc_status ctx_post_consumed(dc_ctx* c, int layer, cudaStream_t st);
 void ctx_adam_scalars(const dc_ctx* c, int step_t, EpiAdam* out);
 // shard-store pointers of a param (fp32 master/m/v, bf16 shard) on this rank
 void ctx_param_state(const dc_ctx* c, int param, float** master, float** m, float** v, void** shard);
+// offload fragments (dc_offload_fragments) and the host-resident state bind
+// (reading D28): frag_slot[i] = device ring slot of offloaded fragment i, or null
+int ctx_num_frags(const dc_ctx* c);
+void ctx_frag(const dc_ctx* c, int i, int* layer, int* state, int64_t* off, int64_t* elems);
+dc_status ctx_bind_host_states(dc_ctx* c, float* m_dev, int64_t m_first, float* v_dev, int64_t v_first,
+                               const std::vector<float*>& frag_slot, void* host_pinned, uint64_t host_bytes);
+uint64_t ctx_frag_host_end(const dc_ctx* c, int i);   // pinned host byte offset after fragment i
 // dc_reduce_scatter_step restricted to a subset of the layer's params
 dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, const std::vector<int>& params,
                                 cudaStream_t st);

@@ -105,6 +105,15 @@ struct dc_model {
   int comm_sms = 0;                  // > 0: SM partition (GEMMs | comm + Adam), green contexts
   SmPartition part{};
   int gemm_sms = 0;                  // SMs the layer GEMMs may use (0 = all)
+  // host-resident optimizer states (reading D28): fragments written back after RS(layer)
+  bool host_states = false;
+  std::vector<std::vector<int>> wb_frags;   // per layer
+  // write-backs (D2H) run on their own stream so they overlap the reloads
+  // (H2D, copy stream): PCIe is full duplex.  wb_ev[f] = f's last write-back;
+  // a reload waits for every write-back of its ring slot (and of itself)
+  cudaStream_t wb_stream = nullptr;
+  std::vector<cudaEvent_t> wb_ev;
+  std::vector<int> frag_slot;
   std::string err;
 
   int pid(int layer, int slot) const { return ctx_layout(ctx).layer_first[layer] + slot; }
@@ -315,6 +324,8 @@ extern "C" dc_status dc_model_destroy(dc_model* m) {
     cudaEventDestroy(m->ev_t0[i]); cudaEventDestroy(m->ev_t1[i]);
   }
   for (auto& e : m->ev_join) if (e) cudaEventDestroy(e);
+  for (auto& e : m->wb_ev) cudaEventDestroy(e);
+  if (m->wb_stream) cudaStreamDestroy(m->wb_stream);
   sm_partition_destroy(&m->part);
   delete m;
   return DC_OK;
@@ -736,6 +747,7 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
   cudaStreamWaitEvent(ags, m->ev_join[0], 0);
   cudaStreamWaitEvent(rss, m->ev_join[0], 0);
   cudaStreamWaitEvent(cps, m->ev_join[0], 0);
+  if (m->host_states) cudaStreamWaitEvent(m->wb_stream, m->ev_join[0], 0);
   std::vector<cudaEvent_t> gather_ev(ctx_layout(m->ctx).S.size(), nullptr);
   const int nops = sched_num_ops(sc);
   for (int i = 0; i < nops; ++i) {
@@ -787,6 +799,15 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
         } else
           s = dc_reduce_scatter_step(m->ctx, o.layer, step_t, o.micro, rss);
         if (profile) cudaEventRecord(m->ev_t1[id], rss);
+        if (s == DC_OK && m->host_states && !m->wb_frags[o.layer].empty()) {
+          // reading D28: the updated host-resident fragments go straight back
+          cudaEventRecord(m->ev_done[id], rss);
+          cudaStreamWaitEvent(m->wb_stream, m->ev_done[id], 0);
+          for (int f : m->wb_frags[o.layer]) {
+            if ((s = dc_offload(m->ctx, f, DC_WRITEBACK, m->wb_stream)) != DC_OK) break;
+            cudaEventRecord(m->wb_ev[f], m->wb_stream);
+          }
+        }
         break;
       }
       case K_OFF:
@@ -798,6 +819,9 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
       case K_RELOAD:
         cudaEventRecord(m->ev_join[1], cs);
         cudaStreamWaitEvent(cps, m->ev_join[1], 0);
+        if (m->host_states && mem[0] < (int64_t)m->frag_slot.size() && m->frag_slot[mem[0]] >= 0)
+          for (size_t g = 0; g < m->frag_slot.size(); ++g)      // the slot's earlier occupants are written back
+            if (m->frag_slot[g] == m->frag_slot[mem[0]]) cudaStreamWaitEvent(cps, m->wb_ev[g], 0);
         s = dc_offload(m->ctx, (int)mem[0], DC_H2D_START, cps);
         break;
       case K_RELOADSYNC:
@@ -815,6 +839,10 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
   cudaStreamWaitEvent(ucs, m->ev_join[1], 0);
   cudaStreamWaitEvent(ucs, m->ev_join[2], 0);
   cudaStreamWaitEvent(ucs, m->ev_join[3], 0);
+  if (m->host_states) {
+    cudaEventRecord(m->ev_join[3], m->wb_stream);
+    cudaStreamWaitEvent(ucs, m->ev_join[3], 0);
+  }
   if (cs != ucs) {
     cudaEventRecord(m->ev_join[4], cs);
     cudaStreamWaitEvent(ucs, m->ev_join[4], 0);
@@ -877,6 +905,172 @@ extern "C" dc_status dc_model_set_option(dc_model* m, const char* key, int64_t v
     return DC_OK;
   }
   return mfail(m, DC_EINVAL, std::string("dc_model_set_option: unknown key ") + key);
+}
+
+// ------------------------------------------------------------------ host-resident states (D28)
+namespace {
+struct HostPlan {
+  std::vector<int> slot_of;      // per fragment: ring slot, -1 = resident on the device
+  int n_slots = 0;
+  int64_t slot_elems = 0, m_first = 0, v_first = 0;
+};
+}  // namespace
+
+static dc_status host_plan(dc_model* m, HostPlan* hp, int avail_slots = 0) {
+  const dc_schedule* sc = ctx_sched(m->ctx);
+  if (!sc) return mfail(m, DC_ESTATE, "host states: no schedule bound");
+  if (m->n_micro != 1) return mfail(m, DC_ESTATE, "host states: gradient accumulation (micro_steps > 1) unsupported");
+  const Layout& L = ctx_layout(m->ctx);
+  const int nf = ctx_num_frags(m->ctx);
+  hp->slot_of.assign(nf, -1);
+  std::vector<char> off(nf, 0);
+  const int nops = sched_num_ops(sc);
+  for (int i = 0; i < nops; ++i) {
+    int kind, id, nm, np, nw;
+    const int64_t* mem; const int* posts; const int* waits;
+    int64_t ao, bytes;
+    sched_op(sc, i, &kind, &id, &mem, &nm, &ao, &bytes, &posts, &np, &waits, &nw);
+    if (kind == K_OFF) {
+      if (mem[0] < 0 || mem[0] >= nf) return mfail(m, DC_EINVAL, "host states: plan fragment id out of range");
+      off[mem[0]] = 1;
+    }
+  }
+  // whole (layer, state) fragments forming a prefix per state
+  auto lay_lo = [&](int l) { return L.store_off[L.layer_first[l]]; };
+  auto lay_n = [&](int l) {
+    int64_t e = 0;
+    for (int p = L.layer_first[l]; p < L.layer_first[l] + L.layer_count[l]; ++p) e += L.S[p];
+    return e;
+  };
+  std::vector<int> n_off(2, 0);
+  std::vector<std::vector<char>> lay_off(2, std::vector<char>(L.n_layers, 0));
+  for (int f = 0; f < nf; ++f) {
+    if (!off[f]) continue;
+    int layer, state;
+    int64_t o, elems;
+    ctx_frag(m->ctx, f, &layer, &state, &o, &elems);
+    if (o != lay_lo(layer) || elems != lay_n(layer))
+      return mfail(m, DC_EINVAL, "host states: offloaded fragments must be whole (layer, state) slices "
+                                 "(dc_offload_fragments with max bytes >= a layer's state)");
+    lay_off[state][layer] = 1;
+    hp->slot_elems = std::max(hp->slot_elems, (elems + 63) / 64 * 64);
+  }
+  for (int st = 0; st < 2; ++st) {
+    int a = 0;
+    while (a < L.n_layers && lay_off[st][a]) ++a;
+    for (int l = a; l < L.n_layers; ++l)
+      if (lay_off[st][l]) return mfail(m, DC_EINVAL, "host states: offloaded layers must be a prefix per state");
+    n_off[st] = a;
+  }
+  hp->m_first = n_off[0] < L.n_layers ? lay_lo(n_off[0]) : L.shard_elems;
+  hp->v_first = n_off[1] < L.n_layers ? lay_lo(n_off[1]) : L.shard_elems;
+  // ring slots in schedule order: a reload takes a free slot, the write-back
+  // after its layer's RS returns it.  Minimal pool: the lowest free slot.
+  // With more slots than the minimum: the least recently freed one, so a
+  // reload does not wait for the write-back just issued (PCIe full duplex)
+  auto assign = [&](int n_fifo) -> dc_status {
+    std::vector<char> busy;
+    std::vector<int> fifo;
+    for (int q = 0; q < n_fifo; ++q) fifo.push_back(q);
+    hp->slot_of.assign(nf, -1);
+    for (int i = 0; i < nops; ++i) {
+      int kind, id, nm, np, nw;
+      const int64_t* mem; const int* posts; const int* waits;
+      int64_t ao, bytes;
+      sched_op(sc, i, &kind, &id, &mem, &nm, &ao, &bytes, &posts, &np, &waits, &nw);
+      if (kind == K_RELOAD && off[mem[0]]) {
+        int sl = 0;
+        if (n_fifo) {
+          if (fifo.empty()) return mfail(m, DC_EOOM, "host states: pool slots exhausted");
+          sl = fifo.front();
+          fifo.erase(fifo.begin());
+        } else {
+          while (sl < (int)busy.size() && busy[sl]) ++sl;
+          if (sl == (int)busy.size()) busy.push_back(0);
+          busy[sl] = 1;
+        }
+        hp->slot_of[mem[0]] = sl;
+      } else if (kind == K_RS) {
+        const int layer = m->s0[id].layer;
+        for (int f = 0; f < nf; ++f) {
+          int fl, fs;
+          int64_t o, e;
+          ctx_frag(m->ctx, f, &fl, &fs, &o, &e);
+          if (off[f] && fl == layer) {
+            if (hp->slot_of[f] < 0) return mfail(m, DC_EINVAL, "host states: fragment updated before its reload");
+            if (n_fifo) fifo.push_back(hp->slot_of[f]);
+            else busy[hp->slot_of[f]] = 0;
+          }
+        }
+      }
+    }
+    for (int f = 0; f < nf; ++f)
+      if (off[f] && hp->slot_of[f] < 0) return mfail(m, DC_EINVAL, "host states: offloaded fragment never reloaded");
+    hp->n_slots = n_fifo ? n_fifo : (int)busy.size();
+    return DC_OK;
+  };
+  dc_status s = assign(0);
+  if (s == DC_OK && avail_slots > hp->n_slots) s = assign(avail_slots);
+  return s;
+}
+
+extern "C" dc_status dc_model_host_states_query(dc_model* m, int64_t* m_first, int64_t* v_first, uint64_t* pool_bytes,
+                                                uint64_t* host_bytes) {
+  if (!m || !m_first || !v_first || !pool_bytes || !host_bytes)
+    return mfail(nullptr, DC_EINVAL, "dc_model_host_states_query: null");
+  HostPlan hp;
+  dc_status s = host_plan(m, &hp);
+  if (s != DC_OK) return s;
+  *host_bytes = 0;
+  for (int f = 0; f < (int)hp.slot_of.size(); ++f)
+    if (hp.slot_of[f] >= 0) *host_bytes = std::max<uint64_t>(*host_bytes, ctx_frag_host_end(m->ctx, f));
+  *m_first = hp.m_first;
+  *v_first = hp.v_first;
+  *pool_bytes = (uint64_t)hp.n_slots * hp.slot_elems * 4;
+  return DC_OK;
+}
+
+extern "C" dc_status dc_model_bind_host_states(dc_model* m, float* m_dev, float* v_dev, void* pool, uint64_t pool_bytes,
+                                               void* host_pinned, uint64_t host_bytes) {
+  if (!m) return mfail(nullptr, DC_EINVAL, "dc_model_bind_host_states: null model");
+  HostPlan hp;
+  dc_status s = host_plan(m, &hp);
+  if (s != DC_OK) return s;
+  const Layout& L = ctx_layout(m->ctx);
+  uint64_t need = (uint64_t)hp.n_slots * hp.slot_elems * 4;
+  if (need && pool_bytes / (hp.slot_elems * 4) > (uint64_t)hp.n_slots) {   // extra slots given: use them
+    s = host_plan(m, &hp, (int)std::min<uint64_t>(pool_bytes / (hp.slot_elems * 4), 1 << 20));
+    if (s != DC_OK) return s;
+    need = (uint64_t)hp.n_slots * hp.slot_elems * 4;
+  }
+  if (pool_bytes < need || (need && !pool)) return mfail(m, DC_EOOM, "dc_model_bind_host_states: pool too small");
+  if ((hp.m_first < L.shard_elems && !m_dev) || (hp.v_first < L.shard_elems && !v_dev))
+    return mfail(m, DC_EINVAL, "dc_model_bind_host_states: null state array");
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al16(m_dev) || !al16(v_dev) || !al16(pool)) return mfail(m, DC_EINVAL, "dc_model_bind_host_states: alignment");
+  const int nf = ctx_num_frags(m->ctx);
+  std::vector<float*> slot(nf, nullptr);
+  m->wb_frags.assign(L.n_layers, {});
+  if (!m->wb_stream && cudaStreamCreateWithFlags(&m->wb_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return mfail(m, DC_ECUDA, "dc_model_bind_host_states: stream creation failed");
+  for (auto& e : m->wb_ev) cudaEventDestroy(e);
+  m->wb_ev.assign(nf, nullptr);
+  for (auto& e : m->wb_ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return mfail(m, DC_ECUDA, "dc_model_bind_host_states: event creation failed");
+  m->frag_slot = hp.slot_of;
+  for (int f = 0; f < nf; ++f) {
+    if (hp.slot_of[f] < 0) continue;
+    slot[f] = reinterpret_cast<float*>(pool) + (int64_t)hp.slot_of[f] * hp.slot_elems;
+    int layer, state;
+    int64_t o, e;
+    ctx_frag(m->ctx, f, &layer, &state, &o, &e);
+    m->wb_frags[layer].push_back(f);
+  }
+  s = ctx_bind_host_states(m->ctx, m_dev, hp.m_first, v_dev, hp.v_first, slot, host_pinned, host_bytes);
+  if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
+  m->host_states = need > 0;
+  return DC_OK;
 }
 
 extern "C" dc_status dc_model_launch_count(const dc_model* m, int64_t* n) {

@@ -22,9 +22,9 @@ DC_OK, DC_EINVAL, DC_EOOM, DC_EINFEASIBLE, DC_ECUDA, DC_ESTATE, DC_EPROFILE, DC_
 STATUS = {0: "DC_OK", 1: "DC_EINVAL", 2: "DC_EOOM", 3: "DC_EINFEASIBLE", 4: "DC_ECUDA",
           5: "DC_ESTATE", 6: "DC_EPROFILE", 7: "DC_ETIMEOUT"}
 DC_BF16, DC_FP32 = 0, 1
-DC_INIT_WEIGHTS, DC_VIRTUAL_RANKS, DC_DEBUG_POISON = 1, 2, 4
+DC_INIT_WEIGHTS, DC_VIRTUAL_RANKS, DC_DEBUG_POISON, DC_DEFER_STATES = 1, 2, 4, 8
 DC_PASS_SHARD, DC_PASS_PREFETCH, DC_PASS_UNSHARD, DC_PASS_OFFLOAD = 1, 2, 4, 8
-DC_D2H_START, DC_D2H_SYNC_FREE, DC_H2D_START, DC_H2D_SYNC = 0, 1, 2, 3
+DC_D2H_START, DC_D2H_SYNC_FREE, DC_H2D_START, DC_H2D_SYNC, DC_WRITEBACK = 0, 1, 2, 3, 4
 
 
 class DCError(RuntimeError):
@@ -120,6 +120,8 @@ _sig = {
     "dc_model_act_ptr": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(vp)]),
     "dc_model_launch_count": (C.c_int, [vp, p_i64]),
     "dc_model_set_option": (C.c_int, [vp, C.c_char_p, C.c_int64]),
+    "dc_model_host_states_query": (C.c_int, [vp, p_i64, p_i64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "dc_model_bind_host_states": (C.c_int, [vp, vp, vp, vp, C.c_uint64, vp, C.c_uint64]),
 }
 EXPORTS = tuple(_sig)
 for _name, (_res, _args) in _sig.items():

@@ -89,10 +89,12 @@ def _alloc_symmetric(nbytes, group, device):
 
 def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr=1e-3, beta1=0.9,
                  beta2=0.999, eps=1e-8, seed=0, init=True, host_pinned_bytes=0, spin_ms=20000, extra_flags=0,
-                 micro_steps=1):
+                 micro_steps=1, defer_states=False):
     """Allocate and dc_init the ranks this process drives: all N virtual ranks,
     or this process's rank when `virtual` is False.  micro_steps > 1: gradient
-    accumulation (an fp32 grad-accumulation shard is allocated)."""
+    accumulation (an fp32 grad-accumulation shard is allocated).  defer_states:
+    m / v are not allocated here; bind_host_states() sizes them from the plan
+    (host-resident offload, reading D28)."""
     dev = torch.device("cuda", device)
     numel, layer_of, init_k = table_arrays(table)
     mops = max_s0_ops(table, micro_steps)
@@ -117,8 +119,9 @@ def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr
         t = st.tensors
         t["shard"] = torch.empty(lay.shard_elems, dtype=torch.bfloat16, device=dev)
         t["master"] = torch.empty(lay.shard_elems, dtype=torch.float32, device=dev)
-        t["m"] = torch.empty(lay.shard_elems, dtype=torch.float32, device=dev)
-        t["v"] = torch.empty(lay.shard_elems, dtype=torch.float32, device=dev)
+        if not defer_states:
+            t["m"] = torch.empty(lay.shard_elems, dtype=torch.float32, device=dev)
+            t["v"] = torch.empty(lay.shard_elems, dtype=torch.float32, device=dev)
         if micro_steps > 1:
             t["acc"] = torch.empty(lay.shard_elems, dtype=torch.float32, device=dev)
         if host_pinned_bytes:
@@ -131,14 +134,15 @@ def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr
                                          C.cast(st._keep[2], dc.p_f32))
         a.max_s0_ops = mops
         a.shard_param, a.master = t["shard"].data_ptr(), t["master"].data_ptr()
-        a.exp_avg, a.exp_avg_sq = t["m"].data_ptr(), t["v"].data_ptr()
+        a.exp_avg, a.exp_avg_sq = (None, None) if defer_states else (t["m"].data_ptr(), t["v"].data_ptr())
         a.grad_peer_ptrs, a.grad_bytes = C.cast(st._keep[3], dc.p_u64), grad_bytes
         a.flag_peer_ptrs, a.flag_bytes = C.cast(st._keep[4], dc.p_u64), lay.flag_bytes
         a.host_pinned = t["host"].data_ptr() if host_pinned_bytes else None
         a.host_pinned_bytes = host_pinned_bytes
         a.lr, a.beta1, a.beta2, a.eps = lr, beta1, beta2, eps
         a.seed = seed
-        a.flags = (dc.DC_INIT_WEIGHTS if init else 0) | (dc.DC_VIRTUAL_RANKS if virtual else 0) | extra_flags
+        a.flags = (dc.DC_INIT_WEIGHTS if init else 0) | (dc.DC_VIRTUAL_RANKS if virtual else 0) | extra_flags | \
+            (dc.DC_DEFER_STATES if defer_states else 0)
         a.spin_limit = spin_ms
         a.micro_steps = micro_steps
         a.grad_acc = t["acc"].data_ptr() if micro_steps > 1 else None
@@ -238,12 +242,79 @@ def plan_digest(sched_json):
 
 
 def offload_fragments(st, max_fragment_bytes):
-    """dc_offload_fragments -> planner fragment records {id, layer, bytes}."""
+    """dc_offload_fragments -> planner fragment records {id, layer, bytes}.
+    The full records (state, element offset and count, pinned host byte
+    offset: fragments are packed in id order) are kept on the rank state."""
     n = C.c_int32(0)
     dc.check(dc.lib.dc_offload_fragments(st.ctx, max_fragment_bytes, None, C.byref(n)), st.ctx)
     arr = (dc.Fragment * n.value)()
     dc.check(dc.lib.dc_offload_fragments(st.ctx, max_fragment_bytes, arr, C.byref(n)), st.ctx)
+    st.frags, host_off = [], 0
+    for f in arr:
+        st.frags.append(dict(layer=f.layer, state=f.state, off=f.offset_elems, elems=f.elems, host_off=host_off))
+        host_off += f.elems * 4
     return [dict(id=i, layer=f.layer, bytes=f.elems * 4) for i, f in enumerate(arr)]
+
+
+def layer_state_bytes(table, world):
+    """Bytes of the largest layer's m (or v) shard: dc_offload_fragments with
+    this maximum gives whole (layer, state) fragments (host-resident mode)."""
+    per = {}
+    for p in table:
+        per[p.layer] = per.get(p.layer, 0) + -(-p.numel // (8 * world)) * 8
+    return 4 * max(per.values())
+
+
+def bind_host_states(ranks, alloc_host=False, extra_slots=0):
+    """After bind(): size m / v to the elements the plan keeps on the device,
+    allocate the reload ring pool and dc_model_bind_host_states (states reset
+    to zero; reading D28).  alloc_host: allocate the pinned host slots now, at
+    the size the offloaded fragments need (else dc_init's host_pinned buffer
+    is used).  Returns {rank: (m_first, v_first, pool_bytes, host_bytes)}."""
+    out = {}
+    for r, st in ranks.items():
+        mf, vf, pb, hb = C.c_int64(), C.c_int64(), C.c_uint64(), C.c_uint64()
+        dc.check(dc.lib.dc_model_host_states_query(st.model, C.byref(mf), C.byref(vf), C.byref(pb), C.byref(hb)),
+                 st.ctx)
+        E = st.layout.shard_elems
+        t = st.tensors
+        t["m"] = torch.empty(max(E - mf.value, 4), dtype=torch.float32, device=st.device)
+        t["v"] = torch.empty(max(E - vf.value, 4), dtype=torch.float32, device=st.device)
+        extra = 0
+        if pb.value and extra_slots:      # slot = the largest offloaded fragment, 256 B aligned
+            offl = [f for f in st.frags if f["off"] < (mf.value if f["state"] == 0 else vf.value)]
+            extra = extra_slots * max(-(-f["elems"] // 64) * 64 * 4 for f in offl)
+        pbytes = pb.value + extra
+        t["pool"] = torch.empty(max(pbytes, 256), dtype=torch.uint8, device=st.device)
+        host, hbytes = None, 0
+        if alloc_host:
+            t["host"] = torch.empty(max(hb.value, 256), dtype=torch.uint8, pin_memory=True)
+            host, hbytes = t["host"].data_ptr(), t["host"].numel()
+        dc.check(dc.lib.dc_model_bind_host_states(st.model, t["m"].data_ptr(), t["v"].data_ptr(),
+                                                  t["pool"].data_ptr(), pbytes, host, hbytes), st.ctx)
+        st.host_states = (mf.value, vf.value, pbytes, hb.value)
+        out[r] = st.host_states
+    return out
+
+
+def full_states(st):
+    """(m, v) fp32 on the CPU over all shard elements: the device-resident part
+    plus the offloaded fragments' pinned host copies (tests / diagnostics)."""
+    if not getattr(st, "host_states", None):
+        return st.tensors["m"].cpu(), st.tensors["v"].cpu()
+    mf, vf = st.host_states[:2]
+    E = st.layout.shard_elems
+    host = st.tensors["host"].view(torch.float32)
+    out = []
+    for state, first, dev in ((0, mf, st.tensors["m"]), (1, vf, st.tensors["v"])):
+        full = torch.empty(E, dtype=torch.float32)
+        full[first:] = dev[:E - first].cpu()
+        for f in st.frags:
+            if f["state"] == state and f["off"] < first:
+                h = f["host_off"] // 4
+                full[f["off"]:f["off"] + f["elems"]] = host[h:h + f["elems"]]
+        out.append(full)
+    return tuple(out)
 
 
 def profile_json(st, tc=None, frags=None):

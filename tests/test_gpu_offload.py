@@ -92,3 +92,66 @@ def test_offload_step_bitexact_vs_resident(world):
                 b = off[r].tensors[k].view(torch.int32)
                 assert torch.equal(a, b), (t, r, k)
             assert torch.equal(ref[r].tensors["shard"].view(torch.int16), off[r].tensors["shard"].view(torch.int16))
+
+
+@pytest.mark.parametrize("world,moe", [(1, False), (2, False), (1, True)])
+def test_host_resident_states_bitexact_vs_resident(world, moe):
+    """Reading D28 (host-resident offload): the offloaded (layer, m|v)
+    fragments have no device array at all — each is reloaded into a ring slot
+    of a small pool, updated there and written back right after its layer's
+    update.  Three steps bit-identical to the all-resident step; the device m /
+    v arrays shrink by the offloaded prefix and the pool is smaller than what
+    it stands in for."""
+    cfg = synth.small_mixtral(layers=3, seq=128) if moe else synth.small_llama(layers=3, seq=128)
+    table = synth.param_table(cfg)
+    n = sum(-(-p.numel // (8 * world)) * 8 for p in table)
+
+    def make(defer):
+        ranks = rt.create_ranks(table, world, lr=LR, host_pinned_bytes=8 * n + 4096, defer_states=defer)
+        xs, ts = {}, {}
+        for r in ranks:
+            x, t = ost.rank_batch(cfg, r)
+            xs[r], ts[r] = bf16_tensor(x), bf16_tensor(t)
+        rt.attach_model(ranks, cfg, xs, ts)
+        return ranks
+
+    ref = make(False)
+    prof = rt.profile_json(ref[0])
+    rt.bind(ref, {r: dc.plan(json.dumps(prof), 1 << 40, passes=dc.DC_PASS_SHARD) for r in ref})
+    off = make(True)
+    for st in off.values():
+        frags = rt.offload_fragments(st, rt.layer_state_bytes(table, world))
+    assert len(frags) == 2 * cfg.layers                       # one per (layer, state)
+    prof = rt.profile_json(off[0], frags=frags)
+    peak = max(o["p_mem"] + o["transient"] for o in prof["ops"])
+    m_opt = sum(f["bytes"] for f in frags)
+    sched = dc.plan(json.dumps(prof), peak + m_opt - frags[0]["bytes"] - frags[1]["bytes"] - frags[2]["bytes"],
+                    passes=dc.DC_PASS_SHARD | dc.DC_PASS_OFFLOAD, strict=True)
+    plan = json.loads(dc.schedule_json(sched))
+    assert plan["offload"] == [0, 1, 2]                       # layer 0 m, v and layer 1 m
+    rt.bind(off, {r: sched for r in off})
+    # MoE case: pinned slots sized from the plan; N=2: two extra ring slots (round-robin reuse)
+    info = rt.bind_host_states(off, alloc_host=moe, extra_slots=2 if world == 2 else 0)
+    E = off[0].layout.shard_elems
+    for r, (mf, vf, pool, hb) in info.items():
+        assert hb == sum(frags[i]["bytes"] for i in plan["offload"])
+        assert mf > vf > 0                                     # m: layers 0-1 offloaded, v: layer 0
+        assert off[r].tensors["m"].numel() == E - mf and off[r].tensors["v"].numel() == E - vf
+        assert 0 < pool <= sum(frags[i]["bytes"] for i in plan["offload"]) + (2 * frags[0]["bytes"] if world == 2 else 0)
+    # a DC_WRITEBACK outside host-state mode is refused
+    rt.offload_fragments(ref[0], rt.layer_state_bytes(table, world))
+    assert dc.lib.dc_offload(ref[0].ctx, 0, dc.DC_WRITEBACK, ref[0].streams[3].cuda_stream) == dc.DC_ESTATE
+    for t in (1, 2, 3):
+        rt.step(ref, t)
+        rt.step(off, t)
+        torch.cuda.synchronize()
+        rt.poll(ref)
+        rt.poll(off)
+        for r in ref:
+            for k in ("master", "shard"):
+                dt = torch.int16 if k == "shard" else torch.int32
+                assert torch.equal(ref[r].tensors[k].view(dt), off[r].tensors[k].view(dt)), (t, r, k)
+            m_ref, v_ref = ref[r].tensors["m"].cpu(), ref[r].tensors["v"].cpu()
+            m_off, v_off = rt.full_states(off[r])
+            assert torch.equal(m_ref.view(torch.int32), m_off.view(torch.int32)), (t, r, "m")
+            assert torch.equal(v_ref.view(torch.int32), v_off.view(torch.int32)), (t, r, "v")
