@@ -342,6 +342,9 @@ def main():
         # P / S / offload passes); whole (layer, m|v) fragments
         frags = rt.offload_fragments(st, rt.layer_state_bytes(table, world))
     else:
+        # the fp32 m / v fragments define M_opt, which passes P and S add to the
+        # profile's P_mem (reading D14); 256 MiB chunks (D15)
+        frags = rt.offload_fragments(st, 256 << 20)
         prof0 = rt.profile_json(st)
         s0 = dc.plan(json.dumps(prof0), 1 << 50, passes=dc.DC_PASS_SHARD)
         rt.bind(ranks, {rank: s0}, group=group)
