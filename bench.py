@@ -365,7 +365,7 @@ def main():
     M = int(0.9 * (total - 7 * GiB))
     passes = dc.DC_PASS_SHARD | (dc.DC_PASS_PREFETCH if "P" in args.passes else 0) | \
         (dc.DC_PASS_UNSHARD if "S" in args.passes and args.passes != "S0" else 0) | \
-        (dc.DC_PASS_OFFLOAD if args.offload else 0)
+        (dc.DC_PASS_OFFLOAD | dc.DC_PASS_HOST_STATES if args.offload else 0)
     t_plan = time.perf_counter()
     sched = dc.plan(json.dumps(prof), M, passes=passes, strict=True)
     t_plan = time.perf_counter() - t_plan
@@ -432,6 +432,14 @@ def main():
     if clocks["reasons"] and BAD_REASONS & set(clocks["reasons"]):
         ms, clocks, launches = timed(args.steps)          # re-measure once
         clocks["remeasured"] = True
+    # host cost of enqueueing one step (diagnostic, outside the timed region):
+    # if it approaches ms_per_step the step is launch-bound
+    barrier()
+    t_h = time.perf_counter()
+    step_no += 1
+    rt.step(ranks, step_no)
+    host_enqueue_ms = (time.perf_counter() - t_h) * 1e3
+    barrier()
     tokens_box = world * T * n_micro
     value = tokens_box / (ms / 1e3)
     if offload_info:
@@ -538,7 +546,8 @@ def main():
                            "unshard_params": len(plan["unshard"]), "offload": offload_info,
                            "l2": "working set (~120 GB/GPU of weights, states, activations) >> 126 MB L2; no flush"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clocks, "kernels": kernels, "collectives": coll}
+                "clocks": clocks, "kernels": kernels, "collectives": coll,
+                "host_enqueue_ms_per_step": round(host_enqueue_ms, 2)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

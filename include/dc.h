@@ -48,7 +48,8 @@ typedef enum {
 enum { DC_BF16 = 0, DC_FP32 = 1 };
 enum { DC_INIT_WEIGHTS = 1u, DC_VIRTUAL_RANKS = 2u, DC_DEBUG_POISON = 4u,
        DC_DEFER_STATES = 8u   /* exp_avg/exp_avg_sq may be NULL: bound later (dc_model_bind_host_states) */ };
-enum { DC_PASS_SHARD = 1u, DC_PASS_PREFETCH = 2u, DC_PASS_UNSHARD = 4u, DC_PASS_OFFLOAD = 8u };
+enum { DC_PASS_SHARD = 1u, DC_PASS_PREFETCH = 2u, DC_PASS_UNSHARD = 4u, DC_PASS_OFFLOAD = 8u,
+       DC_PASS_HOST_STATES = 16u  /* with OFFLOAD: reload rule for host-resident fragments (reading D28) */ };
 enum { DC_D2H_START = 0, DC_D2H_SYNC_FREE = 1, DC_H2D_START = 2, DC_H2D_SYNC = 3,
        DC_WRITEBACK = 4       /* host-resident states: D2H of the updated fragment */ };
 

@@ -22,6 +22,7 @@ import json
 from fractions import Fraction
 
 PASS_SHARD, PASS_PREFETCH, PASS_UNSHARD, PASS_OFFLOAD = 1, 2, 4, 8
+PASS_HOST_STATES = 16     # reload rule for host-resident fragments (reading D28)
 PASSES_PS = PASS_SHARD | PASS_PREFETCH | PASS_UNSHARD
 GiB = 1 << 30
 
@@ -297,7 +298,7 @@ def apply_unshard(S, sel):
 # ---------------------------------------------------------------------------
 # §4.4 — Algorithm 2 (forward offload) and the backward reload rule
 # ---------------------------------------------------------------------------
-def alg2_and_reload(S, P_other, tr, B, frags, M, s0):
+def alg2_and_reload(S, P_other, tr, B, frags, M, s0, host_states=False):
     """Returns (S with offload entries, offloaded frag ids, warnings).
 
     Algorithm 2: M_peak = max mem(o); M_opt = sum B_os; offload fragments in
@@ -309,7 +310,15 @@ def alg2_and_reload(S, P_other, tr, B, frags, M, s0):
     free) such that every backward o' >= o satisfies
     mem(o') + (M_opt - M^-) + R + B_os <= M; TransferSync before the RS of the
     fragment's layer (D17).  No such o by that deadline -> synchronous reload
-    there and a warning."""
+    there and a warning.
+
+    host_states (reading D28): an offloaded fragment is on the device only from
+    its reload to its layer's update (written back right after), so during the
+    backward the resident state is M_opt - sum(offloaded) and a placed reload
+    occupies only [its reload op, its RS op].  The earliest o (same lower
+    bounds) such that every backward o' in [o, RS] satisfies
+    mem(o') + resident + live(o') + B_os <= M, live(o') = bytes of the reloads
+    already placed that span o'."""
     mem, trans = replay(S, P_other, tr, B)
     need = [m + t for m, t in zip(mem, trans)]
     M_opt = sum(f["bytes"] for f in frags)
@@ -352,6 +361,35 @@ def alg2_and_reload(S, P_other, tr, B, frags, M, s0):
     suffix = [0] * (len(bwd) + 1)
     for k in range(len(bwd) - 1, -1, -1):
         suffix[k] = max(suffix[k + 1], need[bwd[k]])
+    if host_states:
+        resident = M_opt - tot
+        live = [0] * len(bwd)
+        prev = 0
+        for f in reversed(offl):
+            dead_j = rs_pos.get(f["layer"], bwd[-1])
+            dead_k = bwd.index(dead_j) if dead_j in bwd else len(bwd) - 1
+            lo = prev
+            fj = freed_at.get(f["id"], -1)
+            while lo < len(bwd) and bwd[lo] < fj:
+                lo += 1
+            k_sel = None
+            for k in range(lo, dead_k + 1):
+                if all(need[bwd[q]] + resident + live[q] + f["bytes"] <= M for q in range(k, dead_k + 1)):
+                    k_sel = k
+                    break
+            if k_sel is None:
+                warnings.append("reload_sync_fallback frag=%d" % f["id"])
+                k_sel = dead_k
+            for q in range(k_sel, dead_k + 1):
+                live[q] += f["bytes"]
+            pre[bwd[k_sel]].append(dict(kind="reload", frag=f["id"], fbytes=f["bytes"]))
+            pre[dead_j].append(dict(kind="reload_sync", frag=f["id"], fbytes=f["bytes"]))
+            prev = k_sel
+        out = [dict(kind="offload", frag=f["id"], fbytes=f["bytes"]) for f in offl]
+        for j, e in enumerate(S):
+            out.extend(pre[j])
+            out.append(e)
+        return out, [f["id"] for f in offl], warnings
     resident = M_opt - Mminus
     R, prev = 0, 0
     for f in reversed(offl):
@@ -505,7 +543,8 @@ def plan(prof, M, M_prefetch=2 * GiB, alpha=(3, 2), passes=PASSES_PS, strict=Fal
         S = apply_unshard(S, unshard)
     offload, warnings = [], []
     if passes & PASS_OFFLOAD:
-        S, offload, warnings = alg2_and_reload(S, P_other, tr, B, frags, M, s0)
+        S, offload, warnings = alg2_and_reload(S, P_other, tr, B, frags, M, s0,
+                                               host_states=bool(passes & PASS_HOST_STATES))
     core = [e for e in S if e["kind"] in ("compute", "rs", "ag", "rel")]
     peak_no_opt = peak_of(core, P_other, tr, B)
     cap, ag_off, rel_off, rel_iv = assign_arena(S, B)

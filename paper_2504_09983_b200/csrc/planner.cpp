@@ -448,7 +448,7 @@ struct Planner {
   const S0Op& s0_of(const Entry& e) const { return e.kind == K_AG ? s0[e.members[0].second] : s0[e.ref]; }
 
   std::vector<Entry> alg2(const std::vector<Entry>& S, std::vector<int64_t>& offload_ids,
-                          std::vector<std::string>& warnings) const {
+                          std::vector<std::string>& warnings, bool host_states = false) const {
     std::vector<int64_t> mem, trans;
     replay(S, mem, trans);
     std::vector<int64_t> need(S.size());
@@ -495,6 +495,42 @@ struct Planner {
     if (bwd.empty()) throw InfeasibleErr("offloaded fragments need a backward region to reload in");
     std::vector<int64_t> suffix(bwd.size() + 1, 0);
     for (int k = (int)bwd.size() - 1; k >= 0; --k) suffix[k] = std::max(suffix[k + 1], need[bwd[k]]);
+    // host-resident fragments (reading D28): resident state M_opt - offloaded,
+    // a reload lives on [reload op, RS op]; earliest k with every backward op
+    // in [k, dead] fitting.  The valid k form a suffix of [lo, dead] (the max
+    // only grows as k moves earlier), so scan down from the deadline
+    if (host_states) {
+      const int64_t res_h = M_opt - tot;
+      std::vector<int64_t> live(bwd.size(), 0);
+      int prev_h = 0;
+      for (auto it = offl.rbegin(); it != offl.rend(); ++it) {
+        const Frag& f = *it;
+        int dead_j = rs_pos.count(f.layer) ? rs_pos[f.layer] : bwd.back();
+        int dead_k = (int)bwd.size() - 1;
+        for (size_t k = 0; k < bwd.size(); ++k)
+          if (bwd[k] == dead_j) { dead_k = (int)k; break; }
+        int lo = prev_h;
+        int fj = freed_at.count(f.id) ? freed_at[f.id] : -1;
+        while (lo < (int)bwd.size() && bwd[lo] < fj) ++lo;
+        int ksel = -1;
+        int64_t run = INT64_MIN;
+        for (int k = dead_k; k >= lo; --k) {
+          run = std::max(run, need[bwd[k]] + live[k]);
+          if (run + res_h + f.bytes > M) break;
+          ksel = k;
+        }
+        if (ksel < 0) {
+          warnings.push_back("reload_sync_fallback frag=" + std::to_string(f.id));
+          ksel = dead_k;
+        }
+        for (int q = ksel; q <= dead_k; ++q) live[q] += f.bytes;
+        Entry r; r.kind = K_RELOAD; r.frag = f.id; r.fbytes = f.bytes;
+        pre[bwd[ksel]].push_back(r);
+        Entry rsy; rsy.kind = K_RELOADSYNC; rsy.frag = f.id; rsy.fbytes = f.bytes;
+        pre[dead_j].push_back(rsy);
+        prev_h = ksel;
+      }
+    } else {
     const int64_t resident = M_opt - Mminus;
     int64_t R = 0;
     int prev = 0;
@@ -520,6 +556,7 @@ struct Planner {
       pre[dead_j].push_back(rsy);
       R += f.bytes;
       prev = ksel;
+    }
     }
     std::vector<Entry> out;
     for (auto& f : offl) {
@@ -687,7 +724,7 @@ extern "C" dc_status dc_plan(const char* profile_json, uint64_t mem_budget, cons
       sched->unshard = P.select_unshard(S, pk);
       S = P.apply_unshard(S, sched->unshard);
     }
-    if (o.passes & DC_PASS_OFFLOAD) S = P.alg2(S, sched->offload, sched->warnings);
+    if (o.passes & DC_PASS_OFFLOAD) S = P.alg2(S, sched->offload, sched->warnings, (o.passes & DC_PASS_HOST_STATES) != 0);
     std::vector<Entry> core;
     for (auto& e : S)
       if (e.kind == K_COMPUTE || e.kind == K_RS || e.kind == K_AG || e.kind == K_REL) core.push_back(e);

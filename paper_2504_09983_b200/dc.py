@@ -23,7 +23,7 @@ STATUS = {0: "DC_OK", 1: "DC_EINVAL", 2: "DC_EOOM", 3: "DC_EINFEASIBLE", 4: "DC_
           5: "DC_ESTATE", 6: "DC_EPROFILE", 7: "DC_ETIMEOUT"}
 DC_BF16, DC_FP32 = 0, 1
 DC_INIT_WEIGHTS, DC_VIRTUAL_RANKS, DC_DEBUG_POISON, DC_DEFER_STATES = 1, 2, 4, 8
-DC_PASS_SHARD, DC_PASS_PREFETCH, DC_PASS_UNSHARD, DC_PASS_OFFLOAD = 1, 2, 4, 8
+DC_PASS_SHARD, DC_PASS_PREFETCH, DC_PASS_UNSHARD, DC_PASS_OFFLOAD, DC_PASS_HOST_STATES = 1, 2, 4, 8, 16
 DC_D2H_START, DC_D2H_SYNC_FREE, DC_H2D_START, DC_H2D_SYNC, DC_WRITEBACK = 0, 1, 2, 3, 4
 
 

@@ -120,7 +120,7 @@ def test_plan_parity_random():
         M_pf = rng.choice([2048, 8192, 1 << 30])
         alpha = rng.choice([(3, 2), (1, 1), (2, 1), (5, 4)])
         passes = rng.choice([osd.PASSES_PS, osd.PASSES_PS | osd.PASS_OFFLOAD, osd.PASS_SHARD | osd.PASS_PREFETCH,
-                             osd.PASS_SHARD])
+                             osd.PASS_SHARD, osd.PASSES_PS | osd.PASS_OFFLOAD | osd.PASS_HOST_STATES])
         o, c = _both(prof, M, M_pf, alpha, passes, strict=rng.random() < 0.5)
         assert o == c, (it, o if isinstance(o, int) else o[:200], c if isinstance(c, int) else c[:200])
         n += isinstance(c, str)

@@ -282,6 +282,32 @@ def test_reload_flat_profile_sync_fallback():
     assert s[rs - 1][0] == "reload_sync" and ("reload", 0) in s[rs - 4:rs]
 
 
+def test_reload_host_states_frees_after_update():
+    """Reading D28 (host-resident fragments), hand trace.  Layers 1 then 0 in the
+    backward; P_mem: a0 20, a1 80 | c1 80, rs1 60, c0 60, d0 40, rs0 40; frags
+    f0 (layer 0), f1 (layer 1), 20 B each; M = 90 -> both offloaded (80 + 40 -
+    40 <= 90), resident 0.  f1 (deadline rs1): c1 gives 80 + 20 > 90, rs1 gives
+    60 + 20 -> reload before rs1.  f0 (deadline rs0): the paper's rule keeps f1
+    counted (R = 20) after rs1, so f0 fits only from d0 (40 + 20 + 20 <= 90);
+    host-resident f1 is written back after rs1, so f0 fits from c0 (60 + 20),
+    not from rs1 (60 + 20 + 20 > 90)."""
+    comp = [("a0", "compute", "fwd", 0, 0, []), ("a1", "compute", "fwd", 0, 1, []),
+            ("c1", "compute", "bwd", 0, 1, []), ("rs1", "rs", "bwd", 0, 1, []),
+            ("c0", "compute", "bwd", 0, 0, []), ("d0", "compute", "bwd", 0, 0, []), ("rs0", "rs", "bwd", 0, 0, [])]
+    pm = dict(enumerate([20, 80, 80, 60, 60, 40, 40]))
+    frags = [dict(id=0, layer=0, bytes=20), dict(id=1, layer=1, bytes=20)]
+    prof = make_profile(comp, {}, pm, frags=frags)
+    paper = seq(osd.plan(prof, 90, passes=PSO))
+    host = seq(osd.plan(prof, 90, passes=PSO | osd.PASS_HOST_STATES))
+    def before(s, f):       # the compute-like op a reload is issued in front of
+        return next(e for e in s[s.index(("reload", f)):] if e[0] in ("compute", "rs"))
+    for s in (paper, host):
+        assert before(s, 1) == ("rs", 3)
+    assert before(paper, 0) == ("compute", 5)
+    assert before(host, 0) == ("compute", 4)
+    assert osd.plan(prof, 90, passes=PSO | osd.PASS_HOST_STATES)["warnings"] == []
+
+
 def test_alg2_infeasible():
     with pytest.raises(osd.Infeasible):
         osd.plan(_offload_profile([20, 120], [30], 2, 10), 100, passes=PSO)
