@@ -24,6 +24,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")   # streams of one rank never share a HW queue
 
 METRIC = "tokens/sec/box (device-timed, max over ranks) at 1/2/4/8 B200; AG/RS GB/s vs 900 GB/s"
 GiB = 1 << 30

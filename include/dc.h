@@ -271,6 +271,16 @@ typedef struct {
                                  /* workspace, deterministic). Only when no other */
                                  /* persistent GEMM can run concurrently on the  */
                                  /* device (it spins on another pair's partial). */
+  int32_t epilogue;              /* 0 plain; CTA pairs only, N = F (SwiGLU width): */
+                                 /* 2 GLU forward: B = {W_gate, W_up} (2 K-major  */
+                                 /*   segments, bseg_end ignored), C = gate half  */
+                                 /*   of gu, C + glu_off = up half (ldc = 2F),    */
+                                 /*   aux[row * ld_aux + j] = SiLU(g) * u (bf16)  */
+                                 /* 3 GLU backward: acc = dact, aux = gu (ld_aux  */
+                                 /*   = 2F, up half at + glu_off), C = d(gate),   */
+                                 /*   C + glu_off = d(up); same values as the     */
+                                 /*   separate act / act_bwd kernels, bit for bit */
+  void* aux; int64_t ld_aux, glu_off;
 } dc_gemm_args;
 dc_status dc_gemm(const dc_gemm_args* g, cudaStream_t stream);
 /* CTA pairs the default pair kernel keeps co-resident on this device

@@ -24,6 +24,7 @@
 #include <map>
 #include <mutex>
 
+#include "act.cuh"
 #include "adam.cuh"
 #include "dc_internal.h"
 #include "ptx.cuh"
@@ -61,6 +62,12 @@ struct GemmParams {
   // previous layer's reduce-scatter + Adam, streamed by 6 otherwise idle warps
   // while the tensor cores run this GEMM (same arithmetic as rs_adam)
   SideJob side;
+  // epilogue modes 2 / 3 (pair kernel): SiLU(gate) * up fused into the gate|up
+  // GEMM (2: C = gu gate half, C + glu_off = up half, aux = act) and its
+  // backward into the down-projection dX GEMM (3: acc = dact, aux = gu,
+  // C = d(gate), C + glu_off = d(up)); N = F there
+  __nv_bfloat16* aux;
+  int64_t ld_aux, glu_off;
   // stream-K tail (pair kernel): tiles [0, sk_dp) are data-parallel (tile t on
   // pair t % npairs); the remaining tiles' k-blocks [0, sk_total) are split into
   // npairs contiguous ranges.  A tile cut by a range boundary is computed in two
@@ -224,6 +231,71 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
 #pragma unroll
     for (int j = 0; j < 32; ++j)
       if (col0 + j < p.N) crow[col0 + j] = __float2bfloat16_rn(f[j]);
+  }
+}
+
+// GLU forward (mode 2), one 32-column chunk of a row: gate / up accumulators
+// -> bf16 gu (as the unfused GEMM stores them) and act = SiLU(g) * u from the
+// rounded values (as the unfused act kernel computes it)
+__device__ __forceinline__ void glu_fwd_chunk(const GemmParams& p, int row, int col0, const uint32_t (&vg)[32],
+                                              const uint32_t (&vu)[32]) {
+  __nv_bfloat16* grow = p.C + (int64_t)row * p.ldc + col0;
+  __nv_bfloat16* urow = grow + p.glu_off;
+  __nv_bfloat16* arow = p.aux + (int64_t)row * p.ld_aux + col0;
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    uint4 og, ou, oa;
+    __nv_bfloat162* g2 = reinterpret_cast<__nv_bfloat162*>(&og);
+    __nv_bfloat162* u2 = reinterpret_cast<__nv_bfloat162*>(&ou);
+    __nv_bfloat162* a2 = reinterpret_cast<__nv_bfloat162*>(&oa);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      g2[t] = __floats2bfloat162_rn(__uint_as_float(vg[j + 2 * t]), __uint_as_float(vg[j + 2 * t + 1]));
+      u2[t] = __floats2bfloat162_rn(__uint_as_float(vu[j + 2 * t]), __uint_as_float(vu[j + 2 * t + 1]));
+      const float2 g = __bfloat1622float2(g2[t]), u = __bfloat1622float2(u2[t]);
+      a2[t] = __floats2bfloat162_rn(silu_mul(g.x, u.x), silu_mul(g.y, u.y));
+    }
+    *reinterpret_cast<uint4*>(grow + j) = og;
+    *reinterpret_cast<uint4*>(urow + j) = ou;
+    *reinterpret_cast<uint4*>(arow + j) = oa;
+  }
+}
+
+// GLU backward (mode 3): acc = dact (rounded to bf16 as the unfused GEMM
+// stores it), g / u from gu -> d(gate), d(up) as the unfused act_bwd kernel
+__device__ __forceinline__ void glu_bwd_chunk(const GemmParams& p, int row, int col0, const uint32_t (&v)[32]) {
+  const __nv_bfloat16* gr = p.aux + (int64_t)row * p.ld_aux + col0;
+  const __nv_bfloat16* ur = gr + p.glu_off;
+  __nv_bfloat16* dgr = p.C + (int64_t)row * p.ldc + col0;
+  __nv_bfloat16* dur = dgr + p.glu_off;
+  // all eight 16-byte loads in flight before the first store (the stores could
+  // alias them as far as the compiler knows, which would serialise the latency)
+  uint4 gvs[4], uvs[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    gvs[t] = __ldg(reinterpret_cast<const uint4*>(gr) + t);
+    uvs[t] = __ldg(reinterpret_cast<const uint4*>(ur) + t);
+  }
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gvs[j / 8]);
+    const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uvs[j / 8]);
+    uint4 og, ou;
+    __nv_bfloat162* dg2 = reinterpret_cast<__nv_bfloat162*>(&og);
+    __nv_bfloat162* du2 = reinterpret_cast<__nv_bfloat162*>(&ou);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float2 g = __bfloat1622float2(g2[t]), u = __bfloat1622float2(u2[t]);
+      const float da0 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(v[j + 2 * t])));
+      const float da1 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(v[j + 2 * t + 1])));
+      float dg0, du0, dg1, du1;
+      silu_mul_bwd(da0, g.x, u.x, dg0, du0);
+      silu_mul_bwd(da1, g.y, u.y, dg1, du1);
+      dg2[t] = __floats2bfloat162_rn(dg0, dg1);
+      du2[t] = __floats2bfloat162_rn(du0, du1);
+    }
+    *reinterpret_cast<uint4*>(dgr + j) = og;
+    *reinterpret_cast<uint4*>(dur + j) = ou;
   }
 }
 
@@ -512,11 +584,16 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
         const int m0 = mt * BM2 + (int)rank * 128;
         int bseg = 0, n0 = nt * BNT;
-        if (!p.split_k) {
-          bseg = seg_of(p, nt);
-          n0 = (nt - (bseg ? p.seg_end[bseg - 1] : 0)) * BNT;
+        if constexpr (EPI == 2) {            // GLU: CTA r stages segment r (gate | up), same columns
+          bseg = (int)rank;
+          n0 = nt * (BNT / 2);
+        } else {
+          if (!p.split_k) {
+            bseg = seg_of(p, nt);
+            n0 = (nt - (bseg ? p.seg_end[bseg - 1] : 0)) * BNT;
+          }
+          n0 += (int)rank * (BNT / 2);
         }
-        n0 += (int)rank * (BNT / 2);
         for (int kb = un.kb0; kb < un.kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (A2_STAGE + Pair<BNT, ST>::B_STAGE));
@@ -605,8 +682,20 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       const bool row_ok = row < p.M;
       __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
       const __nv_bfloat16* rrow = p.R ? p.R + (int64_t)row * p.ldr : nullptr;
+      if constexpr (EPI == 2) {
+        // GLU forward: accumulator columns [0, BNT/2) = gate, [BNT/2, BNT) = up
 #pragma unroll 1
-      for (int c = 0; c < BNT / 32; ++c) {
+        for (int c = 0; c < BNT / 64; ++c) {
+          uint32_t vg[32], vu[32];
+          ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BNT + c * 32, vg);
+          ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BNT + BNT / 2 + c * 32, vu);
+          ptx::tmem_ld_wait();
+          const int col0 = nt * (BNT / 2) + c * 32;
+          if (row_ok && col0 < p.N) glu_fwd_chunk(p, row, col0, vg, vu);
+        }
+      }
+#pragma unroll 1
+      for (int c = 0; c < (EPI == 2 ? 0 : BNT / 32); ++c) {
         uint32_t v[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BNT + c * 32, v);
         ptx::tmem_ld_wait();
@@ -633,6 +722,8 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         if (row_ok && col0 < p.N) {
           if constexpr (EPI == 1) {
             epilogue_chunk<1>(p, row, col0, v);
+          } else if constexpr (EPI == 3) {
+            glu_bwd_chunk(p, row, col0, v);
           } else {
             float f[32];
 #pragma unroll
@@ -826,13 +917,29 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
     if (!pair) { *err = "dc_gemm: a side job needs the CTA-pair kernel"; return DC_EINVAL; }
     p.side = *side;
   }
+  const int glu = g->epilogue;
+  if (glu) {
+    if (glu != 2 && glu != 3) { *err = "dc_gemm: epilogue is 0, 2 or 3"; return DC_EINVAL; }
+    if (!pair || bnt != 256 || adam || (side && side->nm > 0) || g->R || !g->aux || (g->N % 128) ||
+        (g->ld_aux % 8) || (g->glu_off % 8) || (g->ldc % 8))
+      { *err = "dc_gemm: GLU epilogue needs the 256-wide pair kernel, N % 128 == 0, aux, 16 B aligned rows, no R"; return DC_EINVAL; }
+    if (glu == 2 && (g->n_bseg != 2 || g->b_split_k || g->b_mn_major))
+      { *err = "dc_gemm: GLU forward needs B = {gate, up}, K-major, split along N"; return DC_EINVAL; }
+    p.epi = glu;
+    p.aux = reinterpret_cast<__nv_bfloat16*>(g->aux);
+    p.ld_aux = g->ld_aux;
+    p.glu_off = g->glu_off;
+    if (glu == 2) p.n_tiles = (g->N + 127) / 128;     // a tile = 128 gate + the same 128 up columns
+  }
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a_mn << 15) | ((uint32_t)p.b_mn << 16) |
             ((uint32_t)(bnt >> 3) << 17) | ((uint32_t)(tm >> 4) << 24);
   CUtensorMap mA, mB[4];
   bool ok = p.a_mn ? make_map(&mA, g->A, g->M, g->K, g->lda, 64)
                    : make_map(&mA, g->A, g->K, g->M, g->lda, rows_per_cta);
   int prev = 0;
-  for (int s = 0; s < g->n_bseg; ++s) {
+  for (int s = 0; s < g->n_bseg && glu == 2; ++s)   // GLU: two [N][K] K-major tensors, CTA r reads segment r
+    ok = ok && make_map(&mB[s], g->B[s], g->K, g->N, g->ldb[s], bnt / 2);
+  for (int s = 0; s < g->n_bseg && glu != 2; ++s) {
     p.seg_end[s] = g->bseg_end[s];
     const int unit = g->b_split_k ? BK : BN;
     const int64_t lo = (int64_t)prev * unit;
@@ -848,7 +955,7 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
                               : make_map(&mB[s], g->B[s], kdim, ndim, g->ldb[s], pair ? bnt / 2 : BN));
     prev = g->bseg_end[s];
   }
-  if (!g->b_split_k)      // caller's N segment ends are in units of 256 columns
+  if (!g->b_split_k && glu != 2)   // caller's N segment ends are in units of 256 columns
     for (int s = 0; s < g->n_bseg; ++s) p.seg_end[s] *= 256 / bnt;
   if (g->n_bseg == 1) p.seg_end[0] = g->b_split_k ? p.k_blocks : p.n_tiles;
   for (int s = g->n_bseg; s < 4; ++s) { mB[s] = mB[0]; p.seg_end[s] = p.seg_end[g->n_bseg - 1]; }
@@ -882,12 +989,14 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
       p.sk_flags = w->flags;
       p.sk_epoch = ++w->epoch;
     }
-    const int env_st = env_st_pick() == 2 ? 7 : 6;
+    const int env_st = glu ? 6 : (env_st_pick() == 2 ? 7 : 6);
     const int g2 = 2 * pairs;
 #define DC_PAIR_LAUNCH(BN_, ST_)                                                                   \
     (p.epi ? gemm2_bf16_sm100<BN_, ST_, 1><<<g2, GEMM2_THREADS, Pair<BN_, ST_>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p) \
            : gemm2_bf16_sm100<BN_, ST_, 0><<<g2, GEMM2_THREADS, Pair<BN_, ST_>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p))
-    if (bnt == 128) DC_PAIR_LAUNCH(128, 9);
+    if (glu == 2) gemm2_bf16_sm100<256, 6, 2><<<g2, GEMM2_THREADS, Pair<256, 6>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+    else if (glu == 3) gemm2_bf16_sm100<256, 6, 3><<<g2, GEMM2_THREADS, Pair<256, 6>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+    else if (bnt == 128) DC_PAIR_LAUNCH(128, 9);
     else if (env_st == 6) DC_PAIR_LAUNCH(256, 6);
     else DC_PAIR_LAUNCH(256, 7);
 #undef DC_PAIR_LAUNCH
@@ -938,6 +1047,8 @@ cudaError_t preload_gemm_kernels() {
   DC_PAIR_ATTR(256, 7, 1)
   DC_PAIR_ATTR(256, 6, 0)
   DC_PAIR_ATTR(256, 6, 1)
+  DC_PAIR_ATTR(256, 6, 2)
+  DC_PAIR_ATTR(256, 6, 3)
   DC_PAIR_ATTR(128, 9, 0)
   DC_PAIR_ATTR(128, 9, 1)
 #undef DC_PAIR_ATTR

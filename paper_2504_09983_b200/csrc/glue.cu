@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "act.cuh"
 #include "dc_internal.h"
 
 namespace dc {
@@ -294,8 +295,6 @@ void k_attn_mix_bwd(void* dqkv, const void* qkv, int T, int qd, int kvd, int hd,
 }
 
 // ------------------------------------------------------------------ SiLU * up
-__device__ __forceinline__ float sigmoidf_(float z) { return 1.0f / (1.0f + expf(-z)); }
-
 __global__ void act_fwd_kernel(const bf16* __restrict__ gu, bf16* __restrict__ act, int T, int F) {
   const int64_t n8 = (int64_t)T * F / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
@@ -306,7 +305,7 @@ __global__ void act_fwd_kernel(const bf16* __restrict__ gu, bf16* __restrict__ a
     load8(row + c, g);
     load8(row + F + c, u);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = g[j] * sigmoidf_(g[j]) * u[j];
+    for (int j = 0; j < 8; ++j) o[j] = silu_mul(g[j], u[j]);
     store8(act + e, o);
   }
 }
@@ -329,11 +328,7 @@ __global__ void act_bwd_kernel(const bf16* __restrict__ dact, const bf16* __rest
     load8(row + F + c, u);
     load8(dact + e, da);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float s = sigmoidf_(g[j]);
-      du[j] = da[j] * (g[j] * s);
-      dg[j] = da[j] * u[j] * (s * (1.0f + g[j] * (1.0f - s)));
-    }
+    for (int j = 0; j < 8; ++j) silu_mul_bwd(da[j], g[j], u[j], dg[j], du[j]);
     store8(dgu + (int64_t)t * 2 * F + c, dg);
     store8(dgu + (int64_t)t * 2 * F + F + c, du);
   }

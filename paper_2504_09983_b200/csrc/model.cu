@@ -105,6 +105,9 @@ struct dc_model {
   int comm_sms = 0;                  // > 0: SM partition (GEMMs | comm + Adam), green contexts
   SmPartition part{};
   int gemm_sms = 0;                  // SMs the layer GEMMs may use (0 = all)
+  int fuse_act = 0;                  // bit 0: SiLU*up in the gate|up GEMM epilogue; bit 1: its backward
+                                     // in the down dX epilogue.  Bit-identical; measured no faster in
+                                     // the power-capped N = 1 step (profiles/r01g/fuse_act_ab.md): off
   // host-resident optimizer states (reading D28): fragments written back after RS(layer)
   bool host_states = false;
   std::vector<std::vector<int>> wb_frags;   // per layer
@@ -295,6 +298,7 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   // opt-in: bit-identical and relieves the SM contention, but the 1 kW power
   // cap lowers the clock by as much as the overlap gains (profiles/r01)
   m->side_adam = false;
+  if (const char* e = getenv("DC_FUSE_ACT")) m->fuse_act = atoi(e) & 3;   // A/B knob
   {
     const int64_t T_ = d->tokens, H_ = d->hidden, F_ = d->ffn, qd_ = m->qd, kvd_ = m->kvd, qkvd_ = m->qkvd;
     m->bwd_mnk = T_ * F_ * H_ + H_ * F_ * T_ +                       // down_bwd: dX, dW
@@ -350,14 +354,20 @@ extern "C" dc_status dc_model_bind(dc_model* m, void* buf, uint64_t bytes, const
 }
 
 // ------------------------------------------------------------------ layer ops
+struct Glu { int mode; void* aux; int64_t ld_aux, off; };   // dc_gemm_args.epilogue 2 / 3
+
 static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t lda, int a_mn,
                       std::initializer_list<const void*> Bs, std::initializer_list<int64_t> ldbs,
                       std::initializer_list<int> ends, int b_mn, int split_k, void* C, int64_t ldc,
-                      const void* R, int64_t ldr, cudaStream_t st, const EpiAdam* adam = nullptr) {
-  // a backward GEMM carries its share of the pending layer's RS + Adam
+                      const void* R, int64_t ldr, cudaStream_t st, const EpiAdam* adam = nullptr,
+                      const Glu* glu = nullptr) {
+  // a backward GEMM carries its share of the pending layer's RS + Adam (not a
+  // GLU-epilogue GEMM: its share moves to the next one)
   SideJob sj{};
   const SideJob* side = nullptr;
-  if (m->pending_layer >= 0) {
+  if (m->pending_layer >= 0 && glu) {
+    m->pending_mnk += (__int128)M * N * K;
+  } else if (m->pending_layer >= 0) {
     m->pending_mnk += (__int128)M * N * K;
     const int64_t G = m->pending.g1;
     int64_t target = (int64_t)((__int128)G * m->pending_mnk / m->bwd_mnk);
@@ -383,6 +393,12 @@ static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t l
   g.C = C; g.ldc = ldc; g.R = R; g.ldr = ldr;
   g.stream_k = m->stream_k;
   g.num_sms = m->gemm_sms;
+  if (glu) {
+    g.epilogue = glu->mode;
+    g.aux = glu->aux;
+    g.ld_aux = glu->ld_aux;
+    g.glu_off = glu->off;
+  }
   std::string err;
   dc_status s = launch_gemm(&g, st, &err, adam, side);
   if (s != DC_OK) return mfail(m, s, err);
@@ -439,11 +455,17 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       k_rmsnorm_fwd(m->A(a.x2), m->W(l, P_G2), m->A(a.h2), (float*)m->A(a.rstd2), T, H, st);
       break;
     case F_GATE_UP:
-      s = gemm(m, T, 2 * F, H, m->A(a.h2), H, 0, {m->W(l, P_GATE), m->W(l, P_UP)}, {H, H},
-               {F / 256, 2 * F / 256}, 0, 0, m->A(a.gu), 2 * F, nullptr, 0, st);
+      if (m->fuse_act & 1) {   // gu and act = SiLU(gate) * up from one GEMM (epilogue 2)
+        const Glu glu{2, m->A(a.act), F, F};
+        s = gemm(m, T, F, H, m->A(a.h2), H, 0, {m->W(l, P_GATE), m->W(l, P_UP)}, {H, H}, {0, 0}, 0, 0,
+                 m->A(a.gu), 2 * F, nullptr, 0, st, nullptr, &glu);
+      } else {
+        s = gemm(m, T, 2 * F, H, m->A(a.h2), H, 0, {m->W(l, P_GATE), m->W(l, P_UP)}, {H, H},
+                 {F / 256, 2 * F / 256}, 0, 0, m->A(a.gu), 2 * F, nullptr, 0, st);
+      }
       break;
     case F_ACT:
-      k_act_fwd(m->A(a.gu), m->A(a.act), T, F, st);
+      if (!(m->fuse_act & 1)) k_act_fwd(m->A(a.gu), m->A(a.act), T, F, st);
       break;
     case F_DOWN:
       s = gemm(m, T, H, F, m->A(a.act), F, 0, {m->W(l, P_DOWN)}, {F}, {H / 256}, 0, 0, m->A(a.y), H,
@@ -457,13 +479,20 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       break;
     case B_DOWN:
       // (the executor has enqueued dc_grad_slot_acquire for this layer)
-      // dact = dy Wd  (A K-major [T,H]; B = Wd [H rows = K][F] MN-major)
-      s = gemm(m, T, F, H, dcur, H, 0, {m->W(l, P_DOWN)}, {F}, {F / 256}, 1, 0, m->A(m->ws_dact), F, nullptr, 0, st);
+      // dact = dy Wd  (A K-major [T,H]; B = Wd [H rows = K][F] MN-major); fused:
+      // the epilogue turns dact into d(gate | up) with gu (epilogue 3)
+      if (m->fuse_act & 2) {
+        const Glu glu{3, m->A(a.gu), 2 * F, F};
+        s = gemm(m, T, F, H, dcur, H, 0, {m->W(l, P_DOWN)}, {F}, {F / 256}, 1, 0, m->A(m->ws_dgu), 2 * F, nullptr, 0,
+                 st, nullptr, &glu);
+      } else {
+        s = gemm(m, T, F, H, dcur, H, 0, {m->W(l, P_DOWN)}, {F}, {F / 256}, 1, 0, m->A(m->ws_dact), F, nullptr, 0, st);
+      }
       if (s == DC_OK)  // dWd = dy^T act : A = dy stored [T][H] (MN-major), B = act [T][F] (MN-major)
         s = gemm(m, H, F, T, dcur, H, 1, {m->A(a.act)}, {F}, {F / 256}, 1, 0, G(P_DOWN), F, nullptr, 0, st, ADAM(P_DOWN));
       break;
     case B_ACT:
-      k_act_bwd(m->A(m->ws_dact), m->A(a.gu), m->A(m->ws_dgu), T, F, st);
+      if (!(m->fuse_act & 2)) k_act_bwd(m->A(m->ws_dact), m->A(a.gu), m->A(m->ws_dgu), T, F, st);
       break;
     case B_GATE_UP:
       // dh2 = dgate Wg + dup Wu : A = dgu [T, 2F] K-major, B split along K
@@ -528,12 +557,20 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       break;
     case F_EXP_GU: {
       const int e = o.e, R = m->R;
-      s = gemm(m, R, 2 * F, H, m->A(a.X) + (int64_t)e * R * H * 2, H, 0, {m->W(l, p_w1(e)), m->W(l, p_w3(e))},
-               {H, H}, {F / 256, 2 * F / 256}, 0, 0, m->A(a.gu) + (int64_t)e * R * 2 * F * 2, 2 * F, nullptr, 0, st);
+      if (m->fuse_act & 1) {
+        const Glu glu{2, m->A(a.act) + (int64_t)e * R * F * 2, F, F};
+        s = gemm(m, R, F, H, m->A(a.X) + (int64_t)e * R * H * 2, H, 0, {m->W(l, p_w1(e)), m->W(l, p_w3(e))},
+                 {H, H}, {0, 0}, 0, 0, m->A(a.gu) + (int64_t)e * R * 2 * F * 2, 2 * F, nullptr, 0, st, nullptr, &glu);
+      } else {
+        s = gemm(m, R, 2 * F, H, m->A(a.X) + (int64_t)e * R * H * 2, H, 0, {m->W(l, p_w1(e)), m->W(l, p_w3(e))},
+                 {H, H}, {F / 256, 2 * F / 256}, 0, 0, m->A(a.gu) + (int64_t)e * R * 2 * F * 2, 2 * F, nullptr, 0, st);
+      }
       break;
     }
     case F_EXP_ACT:
-      k_act_fwd(m->A(a.gu) + (int64_t)o.e * m->R * 2 * F * 2, m->A(a.act) + (int64_t)o.e * m->R * F * 2, m->R, F, st);
+      if (!(m->fuse_act & 1))
+        k_act_fwd(m->A(a.gu) + (int64_t)o.e * m->R * 2 * F * 2, m->A(a.act) + (int64_t)o.e * m->R * F * 2, m->R, F,
+                  st);
       break;
     case F_EXP_DOWN: {
       const int e = o.e, R = m->R;
@@ -552,15 +589,22 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
     case B_EXP_DOWN: {
       const int e = o.e, R = m->R;
       uint8_t* dOe = m->A(m->ws_dO) + (int64_t)e * R * H * 2;
-      // dact_e = dO_e W2_e ; dW2_e = dO_e^T act_e
-      s = gemm(m, R, F, H, dOe, H, 0, {m->W(l, p_w2(e))}, {F}, {F / 256}, 1, 0, m->A(m->ws_dact), F, nullptr, 0, st);
+      // dact_e = dO_e W2_e (fused: -> d(gate | up)_e with gu_e) ; dW2_e = dO_e^T act_e
+      if (m->fuse_act & 2) {
+        const Glu glu{3, m->A(a.gu) + (int64_t)e * R * 2 * F * 2, 2 * F, F};
+        s = gemm(m, R, F, H, dOe, H, 0, {m->W(l, p_w2(e))}, {F}, {F / 256}, 1, 0, m->A(m->ws_dgu), 2 * F, nullptr, 0,
+                 st, nullptr, &glu);
+      } else {
+        s = gemm(m, R, F, H, dOe, H, 0, {m->W(l, p_w2(e))}, {F}, {F / 256}, 1, 0, m->A(m->ws_dact), F, nullptr, 0, st);
+      }
       if (s == DC_OK)
         s = gemm(m, H, F, R, dOe, H, 1, {m->A(a.act) + (int64_t)e * R * F * 2}, {F}, {F / 256}, 1, 0, G(p_w2(e)), F,
                  nullptr, 0, st);
       break;
     }
     case B_EXP_ACT:
-      k_act_bwd(m->A(m->ws_dact), m->A(a.gu) + (int64_t)o.e * m->R * 2 * F * 2, m->A(m->ws_dgu), m->R, F, st);
+      if (!(m->fuse_act & 2))
+        k_act_bwd(m->A(m->ws_dact), m->A(a.gu) + (int64_t)o.e * m->R * 2 * F * 2, m->A(m->ws_dgu), m->R, F, st);
       break;
     case B_EXP_GU: {
       const int e = o.e, R = m->R;
@@ -886,6 +930,11 @@ extern "C" dc_status dc_model_set_option(dc_model* m, const char* key, int64_t v
       return mfail(m, DC_EINVAL, "comm_sms needs one rank per GPU");
     if (m->part.ctx_gemm && value != m->comm_sms) sm_partition_destroy(&m->part);
     m->comm_sms = (int)value;
+    return DC_OK;
+  }
+  if (!strcmp(key, "fuse_act")) {
+    if (value < 0 || value > 3) return mfail(m, DC_EINVAL, "fuse_act in [0, 3] (bit 0 forward, bit 1 backward)");
+    m->fuse_act = (int)value;
     return DC_OK;
   }
   if (!strcmp(key, "rs_overlap")) {

@@ -80,7 +80,8 @@ class GemmArgs(C.Structure):
                 ("n_bseg", C.c_int32), ("B", vp * 4), ("ldb", C.c_int64 * 4), ("bseg_end", C.c_int32 * 4),
                 ("b_mn_major", C.c_int32), ("b_split_k", C.c_int32),
                 ("C", vp), ("ldc", C.c_int64), ("R", vp), ("ldr", C.c_int64), ("num_sms", C.c_int32),
-                ("kernel", C.c_int32), ("stream_k", C.c_int32)]
+                ("kernel", C.c_int32), ("stream_k", C.c_int32),
+                ("epilogue", C.c_int32), ("aux", vp), ("ld_aux", C.c_int64), ("glu_off", C.c_int64)]
 
 
 ctx_p, sched_p, model_p = vp, vp, vp

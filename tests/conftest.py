@@ -11,6 +11,10 @@ if ROOT not in sys.path:
 os.environ.setdefault("OMP_NUM_THREADS", "1")
 os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
 os.environ.setdefault("MKL_NUM_THREADS", "1")
+# virtual ranks put several ranks' streams (5 each) in one CUDA context; with
+# the default 8 hardware connections a stream-wait or spinning flag kernel of
+# one rank can stall another rank's stream that shares its connection
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 
 def pytest_configure(config):

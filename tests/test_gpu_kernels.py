@@ -121,6 +121,67 @@ def test_gemm_ksplit_mn_major_b(kernel):
     _check(Cm, a @ wcat, np.abs(a) @ np.abs(wcat), "ksplit")
 
 
+def _silu(z):
+    return z / (1.0 + np.exp(-z))
+
+
+@pytest.mark.parametrize("M,F,K", [(256, 256, 192), (200, 384, 136), (600, 512, 64)])
+def test_gemm_glu_epilogues(M, F, K):
+    """Epilogue 2 (gate|up GEMM -> gu + SiLU(g) * u) and 3 (dact GEMM ->
+    d(gate | up) from gu): gu bit-identical to the plain segmented GEMM, act /
+    d(gate) / d(up) vs fp64 of the same bf16 operands; ragged M."""
+    x, X = _mat(81, M, K)
+    wg, WG = _mat(82, F, K)
+    wu, WU = _mat(83, F, K)
+    plain = torch.empty(M, 2 * F, dtype=torch.bfloat16, device="cuda")
+    _gemm(M, 2 * F, K, X, K, 0, [WG, WU], [K, K], [F // 256 if F % 256 == 0 else 0, 2 * F // 256], 0, 0, plain, 2 * F,
+          kernel=2) if F % 256 == 0 else None
+    gu = torch.full((M, 2 * F), float("nan"), dtype=torch.bfloat16, device="cuda")
+    act = torch.full((M, F), float("nan"), dtype=torch.bfloat16, device="cuda")
+    g = dc.GemmArgs()
+    g.M, g.N, g.K = M, F, K
+    g.A, g.lda, g.a_mn_major = X.data_ptr(), K, 0
+    g.n_bseg = 2
+    g.B[0], g.B[1], g.ldb[0], g.ldb[1] = WG.data_ptr(), WU.data_ptr(), K, K
+    g.C, g.ldc, g.kernel = gu.data_ptr(), 2 * F, 2
+    g.epilogue, g.aux, g.ld_aux, g.glu_off = 2, act.data_ptr(), F, F
+    os.environ["DC_GEMM_BN"] = "256"
+    dc.check(dc.lib.dc_gemm(C.byref(g), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    ref = np.concatenate([x @ wg.T, x @ wu.T], axis=1)
+    _check(gu, ref, np.abs(x) @ np.abs(np.concatenate([wg, wu]).T), "glu fwd gu")
+    if F % 256 == 0:
+        assert torch.equal(gu.view(torch.int16), plain.view(torch.int16))
+    gun = to_np(gu)
+    a_ref = _silu(gun[:, :F]) * gun[:, F:]
+    _check(act, a_ref, np.abs(a_ref), "glu fwd act")
+    # backward: dact = dY Wd (Wd stored [K rows][F], MN-major), epilogue 3
+    dy, DY = _mat(84, M, K)
+    wd, WD = _mat(85, K, F)
+    dgu = torch.full((M, 2 * F), float("nan"), dtype=torch.bfloat16, device="cuda")
+    g = dc.GemmArgs()
+    g.M, g.N, g.K = M, F, K
+    g.A, g.lda, g.a_mn_major = DY.data_ptr(), K, 0
+    g.n_bseg = 1
+    g.B[0], g.ldb[0], g.bseg_end[0] = WD.data_ptr(), F, F // 256 if F >= 256 else 1
+    g.b_mn_major = 1
+    g.C, g.ldc, g.kernel = dgu.data_ptr(), 2 * F, 2
+    g.epilogue, g.aux, g.ld_aux, g.glu_off = 3, gu.data_ptr(), 2 * F, F
+    dc.check(dc.lib.dc_gemm(C.byref(g), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    da = nx.rne_bf16(dy @ wd)
+    gg, uu = gun[:, :F], gun[:, F:]
+    s = 1.0 / (1.0 + np.exp(-gg))
+    dg_ref, du_ref = da * uu * s * (1 + gg * (1 - s)), da * gg * s
+    got = to_np(dgu)
+    for name, gv, rv in (("d(gate)", got[:, :F], dg_ref), ("d(up)", got[:, F:], du_ref)):
+        err = np.abs(gv - rv)
+        assert (err <= 2.0 ** -7 * np.abs(rv) + 1e-6 * np.abs(rv).max()).all(), (name, err.max())
+    # refused combinations
+    g.R = gu.data_ptr()
+    assert dc.lib.dc_gemm(C.byref(g), torch.cuda.current_stream().cuda_stream) == dc.DC_EINVAL
+
+
 @KERNELS
 @pytest.mark.parametrize("M,N,K,sms", [(384, 512, 296, 0), (512, 256, 1024, 4), (256, 256, 64, 0)])
 def test_gemm_dw_both_mn_major(M, N, K, sms, kernel):

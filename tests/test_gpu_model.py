@@ -196,3 +196,30 @@ def test_activation_checkpointing_bitexact(world, passes):
         assert _loss(a[r]) == _loss(b[r])
     prof = json.loads(dc.model_profile_json(b[0].model))
     assert all(o["dur_us"] > 0 for o in prof["ops"] if o["kind"] == "compute")
+
+
+@pytest.mark.parametrize("moe,checkpoint", [(False, False), (False, True), (True, False)])
+def test_fused_act_epilogues_bitexact(moe, checkpoint):
+    """SiLU(gate) * up in the gate|up GEMM epilogue and its backward in the
+    down-projection dX epilogue (option fuse_act = 3; default 1: forward only) == the separate
+    act / act_bwd kernels, bit for bit (shared act.cuh arithmetic), over two
+    steps; Llama- and Mixtral-shaped layers, with layer recompute."""
+    cfg = synth.small_mixtral(layers=2, seq=128) if moe else synth.small_llama(layers=2, seq=128)
+    table = synth.param_table(cfg)
+    runs = []
+    for fuse in (3, 0):
+        ranks = rt.create_ranks(table, 1, lr=LR)
+        x, t = ost.rank_batch(cfg, 0)
+        rt.attach_model(ranks, cfg, {0: bf16_tensor(x)}, {0: bf16_tensor(t)}, checkpoint=checkpoint)
+        dc.check(dc.lib.dc_model_set_option(ranks[0].model, b"fuse_act", fuse))
+        prof = rt.profile_json(ranks[0])
+        rt.bind(ranks, {0: dc.plan(json.dumps(prof), 1 << 40, passes=dc.DC_PASS_SHARD)})
+        for s in (1, 2):
+            rt.step(ranks, s)
+        torch.cuda.synchronize()
+        runs.append(ranks[0])
+    a, b = runs
+    for k in ("master", "m", "v", "shard"):
+        dt = torch.int16 if k == "shard" else torch.int32
+        assert torch.equal(a.tensors[k].view(dt), b.tensors[k].view(dt)), k
+    assert _loss(a) == _loss(b)
