@@ -522,10 +522,27 @@ def main():
 
     coll = None
     if world > 1:
-        ag_us = sum(o["dur_us"] for o in last["ops"] if o["kind"] == "ag")
-        coll = {"note": "AG busbw = (N-1)/N x gathered bytes / gather time (incl. flag waits)",
-                "ag_busbw_gbs": (world - 1) / world * sum(p["bytes"] for p in last["params"]) * 2 / (ag_us * 1e-6) / 1e9
-                if ag_us else None, "nvlink_peak_gbs": 900}
+        # per issued gather of the last timed step: transfer time (every receiver
+        # ready -> every sender's stores landed here, CUDA events on the AG stream)
+        dur = {o["id"]: o["dur_us"] for o in last["ops"] if o["kind"] == "ag"}
+        ags = [(o["bytes"], dur.get(o["id"], 0)) for o in plan["ops"] if o["kind"] == "ag"]
+        ags = [(b, us) for b, us in ags if us > 0]
+        f = (world - 1) / world
+        tot_b, tot_us = sum(b for b, _ in ags), sum(us for _, us in ags)
+        big = [(b, us) for b, us in ags if b >= (64 << 20)]
+        rs_per_layer_b = {}
+        for p in last["params"]:
+            rs_per_layer_b[p.get("layer", 0)] = rs_per_layer_b.get(p.get("layer", 0), 0) + p["bytes"]
+        rs_us = [o["dur_us"] for o in last["ops"] if o["kind"] == "rs"]
+        rs_b = sum(rs_per_layer_b.values())
+        coll = {"note": "busbw = (N-1)/N x bytes / time; AG time from every receiver ready to all stores landed; "
+                        "RS time = the fused reduce-scatter + Adam kernel (bf16 grads in over NVLink)",
+                "gathers_per_step": len(ags), "ag_bytes_per_step": tot_b,
+                "ag_busbw_gbs": f * tot_b / (tot_us * 1e-6) / 1e9 if tot_us else None,
+                "ag_busbw_gbs_ge_64MiB": (f * sum(b for b, _ in big) / (sum(us for _, us in big) * 1e-6) / 1e9
+                                          if big else None),
+                "rs_busbw_gbs": f * rs_b / (sum(rs_us) * 1e-6) / 1e9 if rs_us and sum(rs_us) else None,
+                "nvlink_peak_gbs": 900}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

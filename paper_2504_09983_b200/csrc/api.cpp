@@ -112,6 +112,7 @@ struct dc_ctx {
   bool states_bound = true;             // false from dc_init(DC_DEFER_STATES) until the bind
   bool host_states = false;
   std::vector<float*> lay_m, lay_v;     // per layer: m / v base for rs_adam (ring slot) or null
+  cudaEvent_t gt_start = nullptr, gt_end = nullptr;   // one-shot gather timing (profiling)
   std::string err;
 
   uint32_t* flag(int q, int64_t word) const { return reinterpret_cast<uint32_t*>(flag_peers[q]) + word; }
@@ -341,9 +342,11 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
     const uint32_t target = c->fepoch * (uint32_t)(c->world * ctas * c->ag_launches[gid]);
     dc_status s = k_ag_push(am, c->world, c->rank, c->arena_peers.data(), c->myflag(c->L.f_ready + (int64_t)gid * c->world),
                             c->fepoch, peers_at(c, c->L.f_done + gid), c->myflag(c->L.f_done + gid), target, ctas,
-                            c->timeout_ns, c->err_dev, st);
+                            c->timeout_ns, c->err_dev, st, c->gt_start);
     if (s != DC_OK) return fail(c, s, "dc_gather: launch failed");
+    if (c->gt_end) DC_CUDA_TRY(cudaEventRecord(c->gt_end, st), &c->err);
   }
+  c->gt_start = c->gt_end = nullptr;
   if (done_evt) DC_CUDA_TRY(cudaEventRecord(done_evt, st), &c->err);
   return DC_OK;
 }
@@ -589,6 +592,7 @@ extern "C" dc_status dc_offload(dc_ctx* c, int32_t fi, int32_t op, cudaStream_t 
 // internal accessors for model.cu
 namespace dc {
 int ctx_num_frags(const dc_ctx* c) { return (int)c->frags.size(); }
+void ctx_set_gather_timing(dc_ctx* c, cudaEvent_t start, cudaEvent_t end) { c->gt_start = start; c->gt_end = end; }
 void ctx_frag(const dc_ctx* c, int i, int* layer, int* state, int64_t* off, int64_t* elems) {
   const FragInfo& f = c->frags[i];
   *layer = f.layer; *state = f.state; *off = f.off; *elems = f.elems;

@@ -99,6 +99,10 @@ void ctx_frag(const dc_ctx* c, int i, int* layer, int* state, int64_t* off, int6
 dc_status ctx_bind_host_states(dc_ctx* c, float* m_dev, int64_t m_first, float* v_dev, int64_t v_first,
                                const std::vector<float*>& frag_slot, void* host_pinned, uint64_t host_bytes);
 uint64_t ctx_frag_host_end(const dc_ctx* c, int i);   // pinned host byte offset after fragment i
+// one-shot timing of the next dc_gather (profiling): `start` is recorded once
+// every receiver is ready (after the ready-flag wait), `end` once every
+// sender's stores have landed here (after the done-counter wait)
+void ctx_set_gather_timing(dc_ctx* c, cudaEvent_t start, cudaEvent_t end);
 // dc_reduce_scatter_step restricted to a subset of the layer's params
 dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, const std::vector<int>& params,
                                 cudaStream_t st);
@@ -146,7 +150,7 @@ struct RsMember {
 dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const uint64_t* arena_peers,
                     const uint32_t* ready_local, uint32_t epoch, PeerFlags done_peers,
                     const uint32_t* done_local, uint32_t done_target, int ctas, uint64_t timeout_ns,
-                    uint32_t* err_flag, cudaStream_t st);
+                    uint32_t* err_flag, cudaStream_t st, cudaEvent_t ev_after_ready = nullptr);
 dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const uint64_t* slot_peers,
                     const uint32_t* ready_local, uint32_t ready_target, PeerFlags consumed_peers,
                     uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master,

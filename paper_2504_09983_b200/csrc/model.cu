@@ -688,7 +688,28 @@ static void compute_pmem(dc_model* m) {
 
 // Read the per-op CUDA-event durations of the last profiled step (µs).
 static dc_status collect_profile(dc_model* m) {
+  const bool timed_ag = ctx_world(m->ctx) > 1;
+  std::vector<char> gathered(m->s0.size(), 0);   // gathers issued by the bound schedule
+  if (timed_ag) {
+    const dc_schedule* sc = ctx_sched(m->ctx);
+    for (int i = 0, n = sc ? sched_num_ops(sc) : 0; i < n; ++i) {
+      int kind, id, nm, np, nw;
+      const int64_t* mem; const int* posts; const int* waits;
+      int64_t off, bytes;
+      sched_op(sc, i, &kind, &id, &mem, &nm, &off, &bytes, &posts, &np, &waits, &nw);
+      if (kind == K_AG && id >= 0 && id < (int)gathered.size()) gathered[id] = 1;
+    }
+  }
   for (size_t i = 0; i < m->s0.size(); ++i) {
+    if (m->s0[i].kind == K_AG) {     // N > 1: the gather's transfer time (0 if unsharded / fused away)
+      m->dur_us[i] = 0;
+      if (!gathered[i]) continue;
+      if (cudaEventSynchronize(m->ev_t1[i]) != cudaSuccess) return mfail(m, DC_ECUDA, "profile: event sync failed");
+      float ms = 0.0f;
+      if (cudaEventElapsedTime(&ms, m->ev_t0[i], m->ev_t1[i]) == cudaSuccess)
+        m->dur_us[i] = std::max<int64_t>(1, (int64_t)std::llround(ms * 1000.0));
+      continue;
+    }
     if (m->s0[i].kind != K_COMPUTE && m->s0[i].kind != K_RS) continue;
     if (cudaEventSynchronize(m->ev_t1[i]) != cudaSuccess) return mfail(m, DC_ECUDA, "profile: event sync failed");
     float ms = 0.0f;
@@ -804,6 +825,7 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
         if (N > 1) {
           cudaEventRecord(m->ev_pos[id], cs);
           cudaStreamWaitEvent(ags, m->ev_pos[id], 0);
+          if (profile) ctx_set_gather_timing(m->ctx, m->ev_t0[id], m->ev_t1[id]);   // transfer time
           s = dc_gather(m->ctx, id, ags, m->ev_done[id]);
           for (int j = 0; j < nm; ++j) gather_ev[mem[j]] = m->ev_done[id];
         } else {
