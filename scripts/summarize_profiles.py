@@ -1,6 +1,6 @@
 """Summarise a round's ncu artifacts (scripts/profile_round.sh) into markdown:
 launch-list shares per kernel, and per-launch key metrics of the --set full
-captures.  Usage: summarize_profiles.py <prof_dir> > summary.md"""
+captures.  Usage: summarize_profiles.py <prof_dir> [launch csv] [capture names...] > summary.md"""
 import collections
 import csv
 import io
@@ -25,7 +25,7 @@ def launches(path):
     return rows
 
 
-rows = launches(d + "/launches.csv")
+rows = launches(d + "/" + (sys.argv[2] if len(sys.argv) > 2 else "launches.csv"))
 tot = collections.defaultdict(float)
 cnt = collections.Counter()
 for k, v in rows:
@@ -49,7 +49,7 @@ KEYS = [("gpu__time_duration.sum", "time"), ("sm__pipe_tensor_op_tcgen05_cycles_
         ("dram__bytes_read.sum", "DRAM rd"), ("dram__bytes_write.sum", "DRAM wr"),
         ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM %"),
         ("sm__cycles_elapsed.avg.per_second", "SM clk"), ("launch__registers_per_thread", "regs")]
-for name in ("gemm2", "rs_adam"):
+for name in (sys.argv[3:] or ["gemm2", "rs_adam"]):
     try:
         h, units, rows = raw("%s/%s.ncu-rep" % (d, name))
     except Exception as e:
