@@ -314,6 +314,8 @@ def main():
         ranks = rt.create_ranks(table, world, local, virtual=False, group=group, rank=rank, lr=lr,
                                 micro_steps=n_micro, defer_states=args.offload)
     st = ranks[rank]
+    if os.environ.get("DC_AG_COPY_ENGINE") is not None:       # gathers on the copy engines (f-3)
+        dc.check(dc.lib.dc_set_option(st.ctx, b"ag_copy_engine", int(os.environ["DC_AG_COPY_ENGINE"])), st.ctx)
     from oracle import numerics as nx          # bf16 rounding of the synthetic inputs only
     x_np = np.concatenate([synth.values(synth.seed_inputs(rank, mu), 0, 0, T * cfg.hidden, synth.K_UNIT)
                            for mu in range(n_micro)])

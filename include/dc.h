@@ -178,6 +178,11 @@ dc_status dc_step_begin(dc_ctx* ctx, int32_t epoch, cudaStream_t compute_stream)
  * ------------------------------------------------------------------------ */
 dc_status dc_gather(dc_ctx* ctx, int32_t gather_id, cudaStream_t ag_stream, cudaEvent_t done_evt);
 /* Unsharded tensor of param (row-major, numel elements; padding follows). */
+/* Context options.  "ag_copy_engine" (default 0): 1 issues every gather's
+ * stores as cudaMemcpyAsync peer copies (copy engines; no SM time beside the
+ * GEMMs) under the same ready / done flag protocol; bit-identical
+ * gathered buffers.  Set before dc_bind_schedule (DC_ESTATE after). */
+dc_status dc_set_option(dc_ctx* ctx, const char* key, int64_t value);
 dc_status dc_tensor_ptr(const dc_ctx* ctx, int32_t param, void** full_ptr);
 /* Release op `release_id` (schedule op id): posts the ready flags listed in
  * its posts_ready_for to every peer, on compute_stream.  */

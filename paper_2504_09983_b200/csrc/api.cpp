@@ -113,6 +113,7 @@ struct dc_ctx {
   bool host_states = false;
   std::vector<float*> lay_m, lay_v;     // per layer: m / v base for rs_adam (ring slot) or null
   cudaEvent_t gt_start = nullptr, gt_end = nullptr;   // one-shot gather timing (profiling)
+  int ag_ce = 0;                        // 1: gathers as copy-engine peer copies (no SM time)
   std::string err;
 
   uint32_t* flag(int q, int64_t word) const { return reinterpret_cast<uint32_t*>(flag_peers[q]) + word; }
@@ -270,8 +271,8 @@ extern "C" dc_status dc_bind_schedule(dc_ctx* c, const dc_schedule* s, const uin
       int64_t shard_bytes = 0;
       for (int j = 0; j < nm; ++j) shard_bytes += c->L.S[mem[j]] * 2;
       int ctas = (int)std::min<int64_t>(32, std::max<int64_t>(1, shard_bytes / (64 * 1024)));
-      c->ag_ctas[id] = ctas;
-      c->ag_launches[id] = (nm + 47) / 48;
+      c->ag_ctas[id] = c->ag_ce ? 1 : ctas;             // done bumps per sender per gather
+      c->ag_launches[id] = c->ag_ce ? 1 : (nm + 47) / 48;
     }
   }
   c->sched = s;
@@ -340,15 +341,29 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
     }
     const int ctas = c->ag_ctas[gid];
     const uint32_t target = c->fepoch * (uint32_t)(c->world * ctas * c->ag_launches[gid]);
-    dc_status s = k_ag_push(am, c->world, c->rank, c->arena_peers.data(), c->myflag(c->L.f_ready + (int64_t)gid * c->world),
-                            c->fepoch, peers_at(c, c->L.f_done + gid), c->myflag(c->L.f_done + gid), target, ctas,
-                            c->timeout_ns, c->err_dev, st, c->gt_start);
+    dc_status s = c->ag_ce
+        ? k_ag_copy(am, c->world, c->arena_peers.data(), c->myflag(c->L.f_ready + (int64_t)gid * c->world), c->fepoch,
+                    peers_at(c, c->L.f_done + gid), c->myflag(c->L.f_done + gid), target, c->timeout_ns, c->err_dev,
+                    st, c->gt_start)
+        : k_ag_push(am, c->world, c->rank, c->arena_peers.data(), c->myflag(c->L.f_ready + (int64_t)gid * c->world),
+                    c->fepoch, peers_at(c, c->L.f_done + gid), c->myflag(c->L.f_done + gid), target, ctas,
+                    c->timeout_ns, c->err_dev, st, c->gt_start);
     if (s != DC_OK) return fail(c, s, "dc_gather: launch failed");
     if (c->gt_end) DC_CUDA_TRY(cudaEventRecord(c->gt_end, st), &c->err);
   }
   c->gt_start = c->gt_end = nullptr;
   if (done_evt) DC_CUDA_TRY(cudaEventRecord(done_evt, st), &c->err);
   return DC_OK;
+}
+
+extern "C" dc_status dc_set_option(dc_ctx* c, const char* key, int64_t value) {
+  if (!c || !key) return fail(c, DC_EINVAL, "dc_set_option: null argument");
+  if (!strcmp(key, "ag_copy_engine")) {
+    if (c->sched) return fail(c, DC_ESTATE, "dc_set_option: ag_copy_engine must be set before dc_bind_schedule");
+    c->ag_ce = value != 0;
+    return DC_OK;
+  }
+  return fail(c, DC_EINVAL, std::string("dc_set_option: unknown key ") + key);
 }
 
 extern "C" dc_status dc_tensor_ptr(const dc_ctx* c, int32_t p, void** ptr) {

@@ -301,6 +301,40 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
 
 // ------------------------------------------------------------------ flags
 struct PostParams { uint32_t* p[MAXW]; int n; uint32_t value; };
+// +value on every listed counter (release, system scope) after the stream's
+// earlier copies completed: the copy-engine gather's "my stores landed"
+__global__ void add_flags_kernel(const PostParams p) {
+  __threadfence_system();
+  for (int i = 0; i < p.n; ++i) ptx::red_add_release_sys(p.p[i], p.value);
+}
+
+// Copy-engine all-gather: the same protocol as ag_push (wait
+// every receiver's ready flag, then every sender bumps every receiver's done
+// counter by one, then wait for N bumps per epoch) with the stores issued as
+// cudaMemcpyAsync peer copies on the stream — no SM time for the data.
+dc_status k_ag_copy(const std::vector<AgMember>& mem, int world, const uint64_t* arena_peers,
+                    const uint32_t* ready_local, uint32_t epoch, PeerFlags done_peers, const uint32_t* done_local,
+                    uint32_t done_target, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st,
+                    cudaEvent_t ev_after_ready) {
+  wait_flags_kernel<<<1, 1, 0, st>>>(ready_local, world, epoch, timeout_ns, err_flag, 0x100u);
+  count_launch();
+  if (ev_after_ready) cudaEventRecord(ev_after_ready, st);
+  for (const AgMember& a : mem)
+    for (int q = 0; q < world; ++q)
+      if (cudaMemcpyAsync(reinterpret_cast<uint8_t*>(arena_peers[q]) + a.dst_off_bytes, a.src, a.bytes,
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return DC_ECUDA;
+  PostParams p{};
+  p.n = world;
+  for (int q = 0; q < world; ++q) p.p[q] = done_peers.p[q];
+  p.value = 1;
+  add_flags_kernel<<<1, 1, 0, st>>>(p);
+  count_launch();
+  wait_flags_kernel<<<1, 1, 0, st>>>(done_local, 1, done_target, timeout_ns, err_flag, 0x200u);
+  count_launch();
+  return cudaGetLastError() == cudaSuccess ? DC_OK : DC_ECUDA;
+}
+
 __global__ void post_flags_kernel(const PostParams p) {
   __threadfence_system();
   for (int i = 0; i < p.n; ++i) ptx::st_release_sys(p.p[i], p.value);
@@ -342,6 +376,7 @@ cudaError_t preload_comm_kernels() {
   pre(std::integral_constant<int, RS_ADD>{});
   pre(std::integral_constant<int, RS_FINAL>{});
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, post_flags_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, add_flags_kernel);
   return e;
 }
 }  // namespace dc

@@ -159,6 +159,10 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
                     uint32_t* err_flag, cudaStream_t st);
 // reduce-scatter modes (gradient accumulation)
 enum { RS_UPDATE = 0, RS_FIRST = 1, RS_ADD = 2, RS_FINAL = 3 };
+dc_status k_ag_copy(const std::vector<AgMember>& mem, int world, const uint64_t* arena_peers,
+                    const uint32_t* ready_local, uint32_t epoch, PeerFlags done_peers, const uint32_t* done_local,
+                    uint32_t done_target, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st,
+                    cudaEvent_t ev_after_ready);
 void k_post_flags(PeerFlags dst, uint32_t value, cudaStream_t st);
 void k_wait_flags(const uint32_t* flags, int n, uint32_t target, uint64_t timeout_ns,
                   uint32_t* err_flag, cudaStream_t st);
