@@ -176,14 +176,14 @@ def run_reference(args):
         secs.append(sample_run.step())
     per_step = float(np.mean(secs))
     # tokens/s of the whole L-layer stack: T tokens need L layer-samples
-    val = T / (per_step * args.layers)
-    sample = "1 Llama-3-8B-shaped layer, %d tokens, N=1: oracle fwd+bwd+RS+Adam; scaled x%d layers" % (T, args.layers)
+    val = T / (per_step * cfg.layers)
+    sample = "1 Llama-3-8B-shaped layer, %d tokens, N=1: oracle fwd+bwd+RS+Adam; scaled x%d layers" % (T, cfg.layers)
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * args.layers * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * cfg.layers * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (oracle)",
             "data": "synthetic",
             "config": {"workload": "llama3-8b-stack (BASELINE configs[1]), oracle sample", "seq_len": args.seq,
-                       "global_batch": args.batch, "layers": args.layers},
+                       "global_batch": args.batch, "layers": cfg.layers},
             "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
