@@ -15,6 +15,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "--expt-relaxed-constexpr"]
+FLAGS += os.environ.get("DC_NVCC_EXTRA", "").split()        # A/B experiments only (e.g. -DDC_RS_UNR=4)
 
 SOURCES = ["api.cpp", "planner.cpp", "gemm_sm100.cu", "glue.cu", "comm.cu", "model.cu", "moe.cu", "sm_partition.cpp"]
 

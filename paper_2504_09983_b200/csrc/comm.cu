@@ -155,7 +155,10 @@ struct RsParams {
   uint32_t* err;
 };
 
-constexpr int RS_UNR = 2;   // groups of 8 elements per thread per iteration (loads hoisted)
+#ifndef DC_RS_UNR
+#define DC_RS_UNR 2
+#endif
+constexpr int RS_UNR = DC_RS_UNR;   // groups of 8 elements per thread per iteration (loads hoisted)
 
 // MODE (gradient accumulation; dc.h dc_reduce_scatter_step):
 //   RS_UPDATE  g = sum * 1/N, Adam                      (n = 1)

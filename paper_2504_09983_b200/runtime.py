@@ -83,7 +83,7 @@ def _alloc_symmetric(nbytes, group, device):
         t = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
         h = symm_mem.rendezvous(t, group.group_name)
         return t, [int(p) for p in h.buffer_ptrs]
-    except RuntimeError:
+    except Exception:     # no symmetric-memory backend for this group / build: CUDA IPC
         return _alloc_symmetric_ipc(nbytes, group, device)
 
 
