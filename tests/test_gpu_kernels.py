@@ -20,6 +20,7 @@ import torch
 import synth
 from oracle import numerics as nx
 from oracle import step as ost
+from tests import sched_util as su
 from tests.gpu_util import bf16_tensor, seeded, to_np
 
 pytestmark = pytest.mark.gpu
@@ -259,13 +260,24 @@ def _bits_equal(got, ref, what):
     assert got.tobytes() == ref.tobytes(), (what, "not bit-exact")
 
 
-@pytest.mark.parametrize("world,n", [(1, 1), (2, 1), (4, 1), (1, 2), (2, 3), (4, 2)])
-def test_rs_adam_virtual_ranks(world, n):
+def _ragged_table():
+    """Edge-case parameter sizes: smaller than one 16 B shard vector per rank
+    (1, 7), odd (13, 4099, 65537) and a 1 MiB tensor; two layers."""
+    sizes = [(0, 1), (0, 7), (0, 4099), (0, 1 << 19), (1, 13), (1, 65537), (1, 24)]
+    k = float(synth.std_to_k(0.02))
+    return [synth.ParamSpec(id=i, layer=l, name="p%d" % i, shape=(n,), k=(0.0 if i == 0 else k), dtype="bf16")
+            for i, (l, n) in enumerate(sizes)]
+
+
+@pytest.mark.parametrize("world,n,ragged", [(1, 1, False), (2, 1, False), (4, 1, False), (1, 2, False),
+                                            (2, 3, False), (4, 2, False), (3, 1, True), (8, 2, True)])
+def test_rs_adam_virtual_ranks(world, n, ragged):
     """rs_adam (n = 1) and its gradient-accumulation modes (n > 1: acc = rs,
     acc += rs, then Adam on (acc + rs) / (N n)) vs the oracle, bit-exact,
-    two optimizer steps, the accumulator checked after every micro-step."""
+    two optimizer steps, the accumulator checked after every micro-step.
+    Ragged: tiny / odd tensors (mostly padding at N = 8) and N = 3 (1/N inexact)."""
     cfg = synth.small_llama(layers=2)
-    table = synth.llama_param_table(cfg)
+    table = _ragged_table() if ragged else synth.llama_param_table(cfg)
     lr = 1e-3
     ranks = rt.create_ranks(table, world, lr=lr, micro_steps=n)
     S = [nx.shard_len(p.numel, world) for p in table]
@@ -333,6 +345,49 @@ def test_rs_micro_out_of_range():
 # ------------------------------------------------------------------ all-gather
 def _ops(sched):
     return json.loads(dc.schedule_json(sched))["ops"]
+
+
+@pytest.mark.parametrize("world,ce", [(3, 0), (8, 0), (8, 1)])
+def test_ag_ragged_virtual_ranks(world, ce):
+    """Gathers of ragged tensors (1 .. 2^19 elements, padded shards) through a
+    planned schedule without a model: every gathered buffer == the padded
+    concatenation of the shards, bit for bit; SM push and copy-engine modes."""
+    table = _ragged_table()
+    ranks = rt.create_ranks(table, world)
+    for st in ranks.values():
+        dc.check(dc.lib.dc_set_option(st.ctx, b"ag_copy_engine", ce), st.ctx)
+    B = {p.id: nx.shard_len(p.numel, world) * world * 2 for p in table}
+    comp = [("f%d" % p.id, "compute", "fwd", 0, p.layer, [p.id]) for p in table]
+    comp += [("b%d" % p.id, "compute", "bwd", 0, p.layer, [p.id]) for p in reversed(table)]
+    comp += [("end", "compute", "bwd", 0, 0, [])]              # a profile ends with a compute-like op
+    prof = su.make_profile(comp, B, lambda o: 0, tc=[[4096, 10], [1 << 20, 20], [1 << 26, 400]])
+    sched = dc.plan(json.dumps(prof), 1 << 40, M_prefetch=1 << 22,
+                    passes=dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH, strict=True)
+    rt.bind(ranks, {r: sched for r in ranks})
+    full = ost.init_full_params(table)
+    for st in ranks.values():
+        dc.check(dc.lib.dc_step_begin(st.ctx, 1, st.streams[0].cuda_stream), st.ctx)
+    checked = []
+    for o in _ops(sched):
+        if o["kind"] == "ag":
+            for st in ranks.values():
+                dc.check(dc.lib.dc_gather(st.ctx, o["id"], st.streams[1].cuda_stream, None), st.ctx)
+            torch.cuda.synchronize()
+            for st in ranks.values():
+                for p in o["members"]:
+                    ptr = C.c_void_p()
+                    dc.check(dc.lib.dc_tensor_ptr(st.ctx, p, C.byref(ptr)), st.ctx)
+                    S = nx.shard_len(table[p].numel, world)
+                    got = rt.view(ptr.value, world * S, torch.bfloat16).view(torch.int16).cpu().numpy()
+                    ref = nx.all_gather_padded([nx.bf16_bits(nx.shard_of(full[p], world, q)) for q in range(world)])
+                    assert np.array_equal(got.view(np.uint16), ref), (st.rank, p)
+                    checked.append(p)
+        elif o["kind"] == "rel":
+            for st in ranks.values():
+                dc.check(dc.lib.dc_release(st.ctx, o["id"], st.streams[0].cuda_stream), st.ctx)
+    torch.cuda.synchronize()
+    rt.poll(ranks)
+    assert sorted(set(checked)) == list(range(len(table)))
 
 
 @pytest.mark.parametrize("world,passes", [(2, dc.DC_PASS_SHARD), (4, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH),
