@@ -435,6 +435,7 @@ def main():
     if clocks["reasons"] and BAD_REASONS & set(clocks["reasons"]):
         ms, clocks, launches = timed(args.steps)          # re-measure once
         clocks["remeasured"] = True
+    last = rt.profile_json(st)        # per-op events of the last timed step (read before any other step)
     # host cost of enqueueing one step (diagnostic, outside the timed region):
     # if it approaches ms_per_step the step is launch-bound
     barrier()
@@ -443,6 +444,17 @@ def main():
     rt.step(ranks, step_no)
     host_enqueue_ms = (time.perf_counter() - t_h) * 1e3
     barrier()
+    # one more step (outside the timed region) with the reduce-scatter + Adam in
+    # compute-stream order: the GEMMs' own throughput without rs_adam holding
+    # SMs (in the overlapped timed step a GEMM launched while rs_adam runs waits
+    # for its CTAs, and that wait is inside the GEMM op's events)
+    ov = int(os.environ.get("DC_RS_OVERLAP", "1"))
+    dc.check(dc.lib.dc_model_set_option(st.model, b"rs_overlap", 0))
+    step_no += 1
+    rt.step(ranks, step_no, profile=1)
+    dc.check(dc.lib.dc_model_set_option(st.model, b"rs_overlap", ov))
+    ordered = rt.profile_json(st)
+    barrier()
     tokens_box = world * T * n_micro
     value = tokens_box / (ms / 1e3)
     if offload_info:
@@ -450,7 +462,6 @@ def main():
         offload_info["pcie_frac_of_duplex"] = offload_info["pcie_gbs"] / offload_info["pcie_peak_gbs"]["duplex"]
 
     # ---- per-op breakdown of the last timed step (events recorded in-region)
-    last = rt.profile_json(st)
     by = {}
     gemm_us, gemm_fl = 0, 0
     for o in last["ops"]:
@@ -463,6 +474,7 @@ def main():
                 gemm_fl += fl
     pk = peaks()
     achieved = gemm_fl / (gemm_us * 1e-6) / 1e12 if gemm_us else None
+    ord_us = sum(o["dur_us"] for o in ordered["ops"] if o["kind"] == "compute" and gemm_flops(o["name"], cfg, T))
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
@@ -473,7 +485,11 @@ def main():
                 "achieved": achieved, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
                 "frac": achieved / pk["bf16_tflops_sustained"] if achieved else None, "traffic": traffic,
                 "peak_source": pk["source"] + ", sustained bf16 (kernel inside a long step)",
-                "flops_per_step": gemm_fl, "gemm_ms_per_step": gemm_us / 1e3}
+                "flops_per_step": gemm_fl, "gemm_ms_per_step": gemm_us / 1e3,
+                "achieved_stream_ordered": gemm_fl / (ord_us * 1e-6) / 1e12 if ord_us else None,
+                "note": "achieved: GEMM op events of the last timed step (RS + Adam overlapped on its own stream: "
+                        "a GEMM launched while rs_adam holds the SMs waits inside its events); "
+                        "achieved_stream_ordered: one extra step with RS + Adam in compute-stream order"}
     shard_elems = st.layout.shard_elems
     rs_us = by.get("rs", 0)
     # per shard element: bf16 grads of N ranks + fp32 master/m/v r+w + bf16 shard w
