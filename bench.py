@@ -538,6 +538,13 @@ def main():
                "sample": "1 Llama-3-8B-shaped layer, %d tokens, N=1: oracle fwd+bwd+RS+Adam (best of 2, %.1f s); "
                          "tokens/s scaled to the %d-layer stack" % (Ts, sec, cfg.layers)}
 
+    # exposed communication (SURVEY §8 d): the compute stream's idle time in the
+    # last timed step = step time - sum of compute-op events (each op's start
+    # event is recorded after its waits on gathers / grad-slot flags)
+    busy_ms = sum(o["dur_us"] for o in last["ops"] if o["kind"] == "compute") / 1e3
+    exposed = {"ms": max(0.0, ms - busy_ms), "frac": max(0.0, ms - busy_ms) / ms,
+               "note": "step time - compute-stream busy time of the last timed step (waits on gathers, "
+                       "grad-slot / reduce-scatter flags and launch gaps); target < 10 % at N > 1"}
     coll = None
     if world > 1:
         # per issued gather of the last timed step: transfer time (every receiver
@@ -582,6 +589,7 @@ def main():
                            "unshard_params": len(plan["unshard"]), "offload": offload_info,
                            "l2": "working set (~120 GB/GPU of weights, states, activations) >> 126 MB L2; no flush"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "exposed_comm": exposed,
                 "clocks": clocks, "kernels": kernels, "collectives": coll,
                 "host_enqueue_ms_per_step": round(host_enqueue_ms, 2)}
         print(json.dumps(line), flush=True)
