@@ -24,7 +24,6 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")   # streams of one rank never share a HW queue
 
 METRIC = "tokens/sec/box (device-timed, max over ranks) at 1/2/4/8 B200; AG/RS GB/s vs 900 GB/s"
 GiB = 1 << 30
@@ -239,6 +238,25 @@ def pcie_peaks(dev, torch, nbytes=1 << 30):
     return {k: round(v, 1) for k, v in out.items()}
 
 
+def tc_from_profile(prof):
+    """T_c(V) of our own gather: in the profiled S_0 step every
+    gather is one parameter, issued after its predecessor compute op finished
+    (D23), and timed from "every receiver ready" to "every sender's stores
+    landed".  Median per size, sizes ascending, made non-decreasing; integer us.
+    None when the step timed no gathers (N = 1)."""
+    B = {p["id"]: p["bytes"] for p in prof["params"]}
+    by = {}
+    for o in prof["ops"]:
+        if o["kind"] == "ag" and o["dur_us"] > 0:
+            by.setdefault(B[o["params"][0]], []).append(o["dur_us"])
+    if not by:
+        return None
+    pts = [[b, int(statistics.median(v))] for b, v in sorted(by.items())]
+    for i in range(1, len(pts)):
+        pts[i][1] = max(pts[i][1], pts[i - 1][1])
+    return pts
+
+
 def measure_tc(group, world, dev, torch, dist):
     """T_c(V) table for the planner at N > 1: all-gather time vs full bytes,
     MAX over ranks (reading D12).  Measured with the NCCL comparator (same
@@ -355,12 +373,16 @@ def main():
             step_no += 1
             rt.step(ranks, step_no, profile=(i == 4))
     barrier()
+    tc_nccl = None
+    tc = tc_from_profile(rt.profile_json(st)) if world > 1 and not args.offload else None
     if world > 1 and not args.share_gpu:
-        tc = measure_tc(group, world, dev, torch, dist)
-    elif world > 1:       # shared GPU: no link to measure; 20 us + 100 GB/s
-        tc = [[0, 20], [1 << 30, 20 + (1 << 30) // 100000]]
-    else:
+        tc_nccl = measure_tc(group, world, dev, torch, dist)   # comparator (NCCL all-gather), reported
+    if tc is None and world > 1:
+        tc = tc_nccl or [[0, 20], [1 << 30, 20 + (1 << 30) // 100000]]
+    elif tc is None:
         tc = [[0, 0], [1 << 40, 0]]
+    if world > 1 and len(tc) < 2:
+        tc = [[0, tc[0][1]], tc[0]]
     prof = rt.profile_json(st, tc=tc, frags=frags)
     if world > 1:   # element-wise MAX over ranks (reading D12)
         prof = rt.max_reduce_profile(prof, group, device=cdev)
@@ -587,6 +609,7 @@ def main():
                            "seq_len": args.seq, "parallelism": "fsdp%d" % world, "passes": args.passes,
                            "mem_budget_M": M, "plan_ms": round(t_plan * 1e3, 2),
                            "unshard_params": len(plan["unshard"]), "offload": offload_info,
+                           "tc_table": prof["tc"], "tc_nccl_comparator": tc_nccl,
                            "l2": "working set (~120 GB/GPU of weights, states, activations) >> 126 MB L2; no flush"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "exposed_comm": exposed,

@@ -13,7 +13,9 @@ os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
 os.environ.setdefault("MKL_NUM_THREADS", "1")
 # virtual ranks put several ranks' streams (5 each) in one CUDA context; with
 # the default 8 hardware connections a stream-wait or spinning flag kernel of
-# one rank can stall another rank's stream that shares its connection
+# one rank can stall another rank's stream that shares its connection.  (Not
+# for several processes sharing one GPU: tests/test_gpu_multiprocess.py and
+# bench.py --share-gpu keep 8 — 32 per context stalled their handshake.)
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 

@@ -26,7 +26,9 @@ def _free_port():
 
 def _worker(rank, world, port, out_dir):
     # torch symmetric memory rejects two ranks on one device: peer-map via CUDA IPC
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), DC_SYMM="ipc")
+    # two processes time-slice one GPU: keep the default 8 hardware connections
+    # per context (measured: 32 per context can stall the pair's flag handshake)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), DC_SYMM="ipc", CUDA_DEVICE_MAX_CONNECTIONS="8")
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import synth
