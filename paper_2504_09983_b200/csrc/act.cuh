@@ -1,13 +1,16 @@
-// SiLU(gate) * up and its backward, fp32 with explicit IEEE roundings (no FMA
-// contraction), shared by the stand-alone glue kernels (glue.cu) and the GEMM
-// epilogues that fuse them (gemm_sm100.cu), so the fused and unfused paths are
-// bit-identical.  Inputs are the bf16-stored values (as fp32).
+// SiLU(gate) * up and its backward in fp32, shared by the stand-alone glue
+// kernels (glue.cu) and the GEMM epilogues that fuse them (gemm_sm100.cu), so
+// the fused and unfused paths are bit-identical.  Inputs are the bf16-stored
+// values (as fp32), outputs are rounded to bf16: the sigmoid uses the hardware
+// exp2 / reciprocal approximations (relative error ~1e-6, 2^-8 is the bf16 step),
+// the products explicit IEEE roundings (no FMA contraction).  These kernels are
+// ALU-bound as much as HBM-bound with the IEEE expf / division.
 #pragma once
 #include <cuda_runtime.h>
 
 namespace dc {
 
-__device__ __forceinline__ float sigmoid_rn(float z) { return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-z))); }
+__device__ __forceinline__ float sigmoid_rn(float z) { return __fdividef(1.0f, __fadd_rn(1.0f, __expf(-z))); }
 
 // act = (g * sigmoid(g)) * u
 __device__ __forceinline__ float silu_mul(float g, float u) { return __fmul_rn(__fmul_rn(g, sigmoid_rn(g)), u); }

@@ -5,6 +5,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "act.cuh"
 #include "dc_internal.h"
 
@@ -196,8 +198,84 @@ __global__ void __launch_bounds__(RN_T) rmsnorm_bwd_kernel(const bf16* __restric
   }
 }
 
+// Two-pass form (default): (1) one warp per row: dot[row] = sum_c dh g n
+// (fixed lane order + shuffle tree); (2) a thread owns 8 columns of a 16-row
+// chunk: dx = dres + rstd (dh g - n dot / H) and the dg partial of its columns,
+// rows in order.  Every access is a coalesced 16-byte vector and nothing waits
+// on a CTA-wide reduction, so the HBM pipe stays busy (the one-pass kernel
+// above serialises a block reduction per row).
+constexpr int RD_WARPS = 8;
+__global__ void __launch_bounds__(RD_WARPS * 32) rmsnorm_bwd_dot_kernel(const bf16* __restrict__ dh,
+                                                                      const bf16* __restrict__ x,
+                                                                      const bf16* __restrict__ g,
+                                                                      const float* __restrict__ rstd,
+                                                                      float* __restrict__ dot, int T, int H) {
+  const int row = blockIdx.x * RD_WARPS + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (row >= T) return;
+  const float rs = rstd[row];
+  const bf16* dhr = dh + (int64_t)row * H;
+  const bf16* xr = x + (int64_t)row * H;
+  float s = 0.0f;
+  for (int c = lane * 8; c < H; c += 256) {
+    float a[8], n[8], gg[8];
+    load8(dhr + c, a);
+    load8(xr + c, n);
+    load8(g + c, gg);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s = fmaf(a[i] * gg[i], n[i] * rs, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) dot[row] = s / (float)H;
+}
+
+__global__ void __launch_bounds__(256) rmsnorm_bwd_dx_kernel(const bf16* __restrict__ dh, const bf16* __restrict__ x,
+                                                             const bf16* __restrict__ g,
+                                                             const float* __restrict__ rstd,
+                                                             const float* __restrict__ dot,
+                                                             const bf16* __restrict__ dres, bf16* __restrict__ dx,
+                                                             float* __restrict__ dgp, int T, int H) {
+  const int c = (blockIdx.y * 256 + threadIdx.x) * 8;
+  if (c >= H) return;
+  float gg[8], acc[8];
+  load8(g + c, gg);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+  const int r0 = blockIdx.x * RB_ROWS;
+  const int r1 = min(T, r0 + RB_ROWS);
+#pragma unroll 4
+  for (int row = r0; row < r1; ++row) {
+    const float rs = rstd[row], dm = dot[row];
+    float a[8], n[8], d[8];
+    load8(dh + (int64_t)row * H + c, a);
+    load8(x + (int64_t)row * H + c, n);
+    if (dres) load8(dres + (int64_t)row * H + c, d);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      n[i] = n[i] * rs;
+      acc[i] += a[i] * n[i];
+      d[i] = (dres ? d[i] : 0.0f) + rs * (a[i] * gg[i] - n[i] * dm);
+    }
+    store8(dx + (int64_t)row * H + c, d);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dgp[(int64_t)blockIdx.x * H + c + i] = acc[i];
+}
+
 void k_rmsnorm_bwd(const void* dh, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
                    float* dg_partial, int T, int H, cudaStream_t st) {
+  static const bool one_pass = getenv("DC_RMSNORM_BWD_1PASS") && atoi(getenv("DC_RMSNORM_BWD_1PASS"));
+  if (!one_pass) {
+    float* dot = dg_partial + (int64_t)rmsnorm_bwd_blocks(T) * H;    // T floats of scratch after the partials
+    rmsnorm_bwd_dot_kernel<<<(T + RD_WARPS - 1) / RD_WARPS, RD_WARPS * 32, 0, st>>>(
+        (const bf16*)dh, (const bf16*)x, (const bf16*)g, rstd, dot, T, H);
+    dim3 grid(rmsnorm_bwd_blocks(T), (H / 8 + 255) / 256);
+    rmsnorm_bwd_dx_kernel<<<grid, 256, 0, st>>>((const bf16*)dh, (const bf16*)x, (const bf16*)g, rstd, dot,
+                                                 (const bf16*)dres, (bf16*)dx, dg_partial, T, H);
+    count_launch();
+    count_launch();
+    return;
+  }
   const int ch = (H + RN_T * 8 - 1) / (RN_T * 8);
 #define DC_RB(CH_)                                                                                  \
   rmsnorm_bwd_kernel<CH_><<<rmsnorm_bwd_blocks(T), RN_T, 0, st>>>((const bf16*)dh, (const bf16*)x,     \
@@ -390,6 +468,7 @@ cudaError_t preload_glue_kernels() {
   const void* fns[] = {(const void*)init_param_kernel, (const void*)rmsnorm_fwd_kernel,
                        (const void*)rmsnorm_bwd_kernel<1>, (const void*)rmsnorm_bwd_kernel<2>,
                        (const void*)rmsnorm_bwd_kernel<3>, (const void*)rmsnorm_bwd_kernel<4>, (const void*)colsum_kernel,
+                       (const void*)rmsnorm_bwd_dot_kernel, (const void*)rmsnorm_bwd_dx_kernel,
                        (const void*)attn_mix_fwd_kernel, (const void*)attn_mix_bwd_kernel,
                        (const void*)act_fwd_kernel, (const void*)act_bwd_kernel,
                        (const void*)loss_kernel, (const void*)loss_final_kernel};

@@ -283,7 +283,7 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   const uint64_t ws0 = off;
   m->ws_dA = take(T * h * 2); m->ws_dB = take(T * h * 2); m->ws_dact = take(T * f * 2);
   m->ws_dgu = take(T * 2 * f * 2); m->ws_dh = take(T * h * 2); m->ws_dx2 = take(T * h * 2);
-  m->ws_dqkv = take(T * m->qkvd * 2); m->ws_dgp = take((int64_t)rmsnorm_bwd_blocks((int)T) * h * 4);
+  m->ws_dqkv = take(T * m->qkvd * 2); m->ws_dgp = take(((int64_t)rmsnorm_bwd_blocks((int)T) * h + T) * 4);   // partials + row dots
   m->ws_lossp = take(1024 * 4); m->ws_loss = take(4 * (int64_t)m->n_micro);
   if (m->E) {
     m->ws_dO = take(2 * T * h * 2); m->ws_dX = take(2 * T * h * 2); m->ws_dl0 = take(T * 4);
