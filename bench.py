@@ -564,6 +564,12 @@ def main():
     # last timed step = step time - sum of compute-op events (each op's start
     # event is recorded after its waits on gathers / grad-slot flags)
     busy_ms = sum(o["dur_us"] for o in last["ops"] if o["kind"] == "compute") / 1e3
+    # peak memory (SURVEY §8 d): every device buffer of the run is a torch
+    # allocation (states, grad slots, flags, arena, activations, pool), so the
+    # allocator's peak is the device total; the plan's own bound beside it
+    mem = {"device_peak_allocated": torch.cuda.max_memory_allocated(dev),
+           "device_peak_reserved": torch.cuda.max_memory_reserved(dev),
+           "plan_peak": plan["peak_no_opt"] + plan.get("m_opt", 0), "M": M}
     exposed = {"ms": max(0.0, ms - busy_ms), "frac": max(0.0, ms - busy_ms) / ms,
                "note": "step time - compute-stream busy time of the last timed step (waits on gathers, "
                        "grad-slot / reduce-scatter flags and launch gaps); target < 10 % at N > 1"}
@@ -612,7 +618,7 @@ def main():
                            "tc_table": prof["tc"], "tc_nccl_comparator": tc_nccl,
                            "l2": "working set (~120 GB/GPU of weights, states, activations) >> 126 MB L2; no flush"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "exposed_comm": exposed,
+                "exposed_comm": exposed, "memory": mem,
                 "clocks": clocks, "kernels": kernels, "collectives": coll,
                 "host_enqueue_ms_per_step": round(host_enqueue_ms, 2)}
         print(json.dumps(line), flush=True)
