@@ -71,7 +71,10 @@ __global__ void __launch_bounds__(512) ag_push_kernel(const AgParams p) {
       uint4 v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) v[u] = __ldg(src + i + u * nthr);
-      for (int q = 0; q < p.world; ++q) {
+      // destinations rotated by rank: the N senders start on N different
+      // receivers instead of all on rank 0 (spreads NVSwitch ingress)
+      for (int qq = 0; qq < p.world; ++qq) {
+        const int q = (qq + p.rank) % p.world;
         uint4* dst = reinterpret_cast<uint4*>(p.arena[q] + off);
 #pragma unroll
         for (int u = 0; u < 4; ++u) dst[i + u * nthr] = v[u];
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(512) ag_push_kernel(const AgParams p) {
     }
     for (; i < n; i += nthr) {
       const uint4 v = __ldg(src + i);
-      for (int q = 0; q < p.world; ++q) reinterpret_cast<uint4*>(p.arena[q] + off)[i] = v;
+      for (int qq = 0; qq < p.world; ++qq) reinterpret_cast<uint4*>(p.arena[(qq + p.rank) % p.world] + off)[i] = v;
     }
   }
   __syncthreads();
