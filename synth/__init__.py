@@ -4,7 +4,8 @@ This package holds NO arithmetic of the method (no gather, reduce-scatter, Adam,
 layer math or scheduling).  It only defines:
 
 * the counter-based value generator (splitmix64 -> uniform with a given std),
-  which the CUDA init kernel re-implements independently (csrc/init.cu);
+  which the CUDA init kernel re-implements independently (init_param_kernel in
+  paper_2504_09983_b200/csrc/glue.cu);
 * the workload recipes: model shapes of the paper's workloads (§5.1,
   lines 440-444: Llama-3 / Mixtral shaped layers, bf16) and the parameter table
   order (first-use order of the S_0 rewrite, §4.1).
