@@ -22,68 +22,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
-from oracle import sched as osd  # noqa: E402
 from oracle import sim  # noqa: E402
+from tests.sched_util import analytic_profile as profile  # noqa: E402
 from paper_2504_09983_b200 import dc  # noqa: E402
 
 GB = 10 ** 9
-
-
-def a256(b):
-    return (b + 255) // 256 * 256
-
-
-def profile(cfg, N, op_ms, checkpoint=True):
-    T, h, f = cfg.tokens, cfg.hidden, cfg.ffn
-    qd, kvd = cfg.q_dim, cfg.kv_dim
-    qkvd = qd + 2 * kvd
-    table = synth.param_table(cfg)
-    S = {p.id: -(-p.numel // (8 * N)) * 8 for p in table}
-    B = {p.id: N * S[p.id] * 2 for p in table}
-    E = sum(S.values())
-    layers = {}
-    for p in table:
-        layers.setdefault(p.layer, []).append(p.id)
-    grad_slot = max(sum(a256(B[i]) for i in ids) for ids in layers.values())
-    piece = {"attn_norm": T * h * 2 + T * 4, "qkv": T * qkvd * 2, "attn_mix": T * qd * 2, "o_proj": T * h * 2,
-             "mlp_norm": T * h * 2 + T * 4, "gate_up": T * 2 * f * 2, "act": T * f * 2, "down": T * h * 2}
-    layer_set = sum(a256(v) for v in piece.values())
-    ws = 2 * T * h * 2 + T * f * 2 + T * 2 * f * 2 + 2 * T * h * 2 + T * qkvd * 2 + (T // 16) * h * 4
-    static = E * 6 + 2 * grad_slot + ws + 2 * T * h * 2 + (layer_set - T * h * 2 if checkpoint else 0)
-    comp = synth.compute_ops(cfg, checkpoint=checkpoint)
-    s0 = osd.build_s0(comp)
-    live = osd.live_before_s0(s0, B)
-    act = 0
-    for o in s0:
-        o["p_mem"] = static + live[o["id"]] + act
-        o["transient"] = 0
-        nm = o["name"][3:] if o["name"].startswith("re_") else o["name"]
-        if o["kind"] == "rs":
-            o["dur_us"] = 1          # replaced below by the RS model
-        elif o["kind"] == "compute":
-            o["dur_us"] = max(1, int(round(op_ms.get(nm if o["phase"] == "fwd" else o["name"], 0.0) * 1000)))
-            if o["name"].startswith("re_"):
-                o["dur_us"] = max(1, int(round(op_ms.get(nm, 0.0) * 1000)))
-        else:
-            o["dur_us"] = 0
-        if o["kind"] == "compute":
-            if checkpoint:
-                if o["phase"] == "fwd" and o["name"] == "down":
-                    act += T * h * 2
-                elif o["phase"] == "bwd" and o["name"] == "attn_norm_bwd":
-                    act -= T * h * 2
-            elif o["phase"] == "fwd":
-                act += piece.get(o["name"], 0)
-            elif o["name"] == "attn_norm_bwd":
-                act -= layer_set
-    # optimizer-state fragments (layer, m | v): they define M_opt, which passes
-    # P and S add to P_mem (reading D14)
-    frags = []
-    for l, ids in sorted(layers.items()):
-        for _ in range(2):
-            frags.append(dict(id=len(frags), layer=l, bytes=4 * sum(S[i] for i in ids)))
-    return dict(ops=s0, params=[dict(id=i, bytes=b, layer=0) for i, b in sorted(B.items())], frags=frags,
-                tc=[]), E, B, layers
 
 
 def main():

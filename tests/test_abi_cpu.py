@@ -139,3 +139,26 @@ def test_plan_profile_errors():
     h = C.c_void_p()
     assert dc.lib.dc_plan(b'{"ops": [1.5]}', 10, None, C.byref(h)) == dc.DC_EPROFILE
     assert "profile" in dc.last_error()
+
+
+@pytest.mark.parametrize("name,L,N,ck,M_gb,passes", [
+    ("LLAMA3_8B", 32, 8, False, 155.7, "PS"),                 # configs[1] at N = 8
+    ("LLAMA3_70B", 80, 8, True, 130.0, "PS"),                 # configs[2]: tight M, layer recompute
+    ("MIXTRAL_8X7B", 32, 8, False, 155.7, "PS"),              # configs[3]: 31 tensors per layer
+    ("LLAMA3_70B", 16, 1, False, 165.6, "PSOH"),              # configs[4]: offload, host-resident states
+])
+def test_plan_parity_full_sizes(name, L, N, ck, M_gb, passes):
+    """dc_plan == the oracle scheduler, byte for byte, on S_0 profiles of the
+    BASELINE configurations at full size (up to 6017 ops), built without a GPU
+    (tests/sched_util.analytic_profile)."""
+    import dataclasses
+    cfg = dataclasses.replace(getattr(synth, name), layers=L, seq=2048, batch=1)
+    op_ms = {"qkv": 0.3, "o_proj": 0.2, "gate_up": 0.7, "down": 0.35, "attn_norm": 0.02, "mlp_norm": 0.02,
+             "act": 0.05, "attn_mix": 0.03}
+    prof, _, _, _ = su.analytic_profile(cfg, N, op_ms, checkpoint=ck)
+    prof["tc"] = [[0, 20], [1 << 34, 20 + int((1 << 34) / 630e3)]]
+    p = osd.PASSES_PS | (osd.PASS_OFFLOAD | osd.PASS_HOST_STATES if "O" in passes else 0)
+    o, c = _both(prof, int(M_gb * 1e9), 2 << 30, passes=p, strict=True)
+    assert isinstance(c, str) and o == c
+    plan = json.loads(c)
+    assert ("O" in passes) == bool(plan["offload"])
