@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--offload", action="store_true",
                     help="adaptive offload of optimizer states (Alg. 2, P:370-408) with host-resident fragments "
                          "(reading D28): BASELINE configs[4], e.g. --model llama3-70b --layers 16 --batch 1")
+    ap.add_argument("--offload-sync", action="store_true",
+                    help="the paper's comparison point for --offload (P:504-506): every optimizer-state fragment "
+                         "host-resident, reloaded synchronously before its layer's update")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--share-gpu", action="store_true",
                     help="test mode: every rank on cuda:0 (gloo host collectives, CUDA-IPC peer maps, fixed T_c); "
@@ -294,6 +297,8 @@ def model_config(args):
 
 def main():
     args = parse()
+    if args.offload_sync:
+        args.offload = True
     if args.impl == "reference":
         run_reference(args)
         return
@@ -390,9 +395,10 @@ def main():
     M = int(0.9 * (total - 7 * GiB))
     passes = dc.DC_PASS_SHARD | (dc.DC_PASS_PREFETCH if "P" in args.passes else 0) | \
         (dc.DC_PASS_UNSHARD if "S" in args.passes and args.passes != "S0" else 0) | \
-        (dc.DC_PASS_OFFLOAD | dc.DC_PASS_HOST_STATES if args.offload else 0)
+        (dc.DC_PASS_OFFLOAD | dc.DC_PASS_HOST_STATES if args.offload and not args.offload_sync else 0)
     t_plan = time.perf_counter()
-    sched = dc.plan(json.dumps(prof), M, passes=passes, strict=True)
+    # offload-all-sync: no memory plan for the states (none stays on the device)
+    sched = dc.plan(json.dumps(prof), (1 << 50) if args.offload_sync else M, passes=passes, strict=True)
     t_plan = time.perf_counter() - t_plan
     plan = json.loads(dc.schedule_json(sched))
     torch.cuda.synchronize()
@@ -404,12 +410,17 @@ def main():
         # extra ring slots (round-robin: a reload need not wait for the write-back
         # just issued) where the device has room beyond the plan, 6 GiB kept free
         fb = max(f["bytes"] for f in frags)
-        off_bytes = sum(frags[i]["bytes"] for i in plan["offload"])
+        if args.offload_sync:
+            dc.check(dc.lib.dc_model_set_option(st.model, b"offload_all_sync", 1))
+        off_bytes = sum(f["bytes"] for f in frags) if args.offload_sync else \
+            sum(frags[i]["bytes"] for i in plan["offload"])
         free_b = torch.cuda.mem_get_info(dev)[0]
         dev_states = 2 * st.layout.shard_elems * 4 - off_bytes
         extra = int(max(0, min(2, (free_b - 6 * GiB - dev_states - 4 * fb) // fb)))
         mf, vf, pool, hb = rt.bind_host_states(ranks, alloc_host=True, extra_slots=extra)[rank]
-        offload_info = {"pcie_peak_gbs": pcie_peaks(dev, torch),
+        offload_info = {"mode": "all fragments, synchronous reload (P:504 baseline)" if args.offload_sync else
+                        "adaptive (Alg. 2 + reload rule, host-resident fragments, D28)",
+                        "pcie_peak_gbs": pcie_peaks(dev, torch),
                         "offloaded_bytes": off_bytes, "fragments": len(plan["offload"]),
                         "fragment_bytes": max(f["bytes"] for f in frags), "pool_bytes": pool,
                         "device_state_bytes": 4 * (2 * st.layout.shard_elems - mf - vf),
@@ -569,7 +580,10 @@ def main():
     # allocator's peak is the device total; the plan's own bound beside it
     mem = {"device_peak_allocated": torch.cuda.max_memory_allocated(dev),
            "device_peak_reserved": torch.cuda.max_memory_reserved(dev),
-           "plan_peak": plan["peak_no_opt"] + plan.get("m_opt", 0), "M": M}
+           "plan_peak": plan["peak_no_opt"] + plan.get("m_opt", 0) -
+                         (offload_info["offloaded_bytes"] if offload_info else 0), "M": M}
+    if offload_info:   # the reload ring is a static allocation beside the plan's live bytes
+        mem["offload_pool"] = offload_info["pool_bytes"]
     exposed = {"ms": max(0.0, ms - busy_ms), "frac": max(0.0, ms - busy_ms) / ms,
                "note": "step time - compute-stream busy time of the last timed step (waits on gathers, "
                        "grad-slot / reduce-scatter flags and launch gaps); target < 10 % at N > 1"}

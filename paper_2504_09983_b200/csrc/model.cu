@@ -110,6 +110,10 @@ struct dc_model {
                                      // the power-capped N = 1 step (profiles/r01g/fuse_act_ab.md): off
   // host-resident optimizer states (reading D28): fragments written back after RS(layer)
   bool host_states = false;
+  // the paper's comparison point for adaptive offload: every
+  // optimizer-state fragment host-resident, reloaded synchronously right before
+  // its layer's update (the compute stream waits too), whatever the plan says
+  int offload_all_sync = 0;
   std::vector<std::vector<int>> wb_frags;   // per layer
   // write-backs (D2H) run on their own stream so they overlap the reloads
   // (H2D, copy stream): PCIe is full duplex.  wb_ev[f] = f's last write-back;
@@ -804,6 +808,9 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
     sched_op(sc, i, &kind, &id, &mem, &nm, &off, &bytes, &posts, &np, &waits, &nw);
     if (kind >= K_OFF) m->fused_active = m->side_active = false;
   }
+  if (m->offload_all_sync) {
+    m->fused_active = m->side_active = false;
+  }
   dc_status s = dc_step_begin(m->ctx, ++m->epoch, ucs);
   if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
   // streams must not run ahead of the previous step's tail on the compute stream
@@ -853,6 +860,18 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
         const S0& o = m->s0[id];
         cudaEventRecord(m->ev_pos[id], cs);
         cudaStreamWaitEvent(rss, m->ev_pos[id], 0);
+        if (m->host_states && m->offload_all_sync) {
+          // baseline: reload this layer's fragments now and block on them
+          cudaStreamWaitEvent(cps, m->ev_pos[id], 0);
+          for (int f : m->wb_frags[o.layer]) {
+            for (size_t g = 0; g < m->frag_slot.size(); ++g)
+              if (m->frag_slot[g] == m->frag_slot[f]) cudaStreamWaitEvent(cps, m->wb_ev[g], 0);
+            if ((s = dc_offload(m->ctx, f, DC_H2D_START, cps)) != DC_OK) break;
+            if ((s = dc_offload(m->ctx, f, DC_H2D_SYNC, rss)) != DC_OK) break;
+            if ((s = dc_offload(m->ctx, f, DC_H2D_SYNC, cs)) != DC_OK) break;
+          }
+          if (s != DC_OK) break;
+        }
         if (profile) cudaEventRecord(m->ev_t0[id], rss);
         if (m->fused_active)   // the weights were updated in their dW epilogues; the norm gains remain
           s = reduce_scatter_params(m->ctx, o.layer, step_t, o.micro, {m->pid(o.layer, P_G1), m->pid(o.layer, P_G2)},
@@ -954,6 +973,11 @@ extern "C" dc_status dc_model_set_option(dc_model* m, const char* key, int64_t v
     m->comm_sms = (int)value;
     return DC_OK;
   }
+  if (!strcmp(key, "offload_all_sync")) {
+    if (m->host_states) return mfail(m, DC_ESTATE, "offload_all_sync must be set before dc_model_bind_host_states");
+    m->offload_all_sync = value != 0;
+    return DC_OK;
+  }
   if (!strcmp(key, "fuse_act")) {
     if (value < 0 || value > 3) return mfail(m, DC_EINVAL, "fuse_act in [0, 3] (bit 0 forward, bit 1 backward)");
     m->fuse_act = (int)value;
@@ -1006,6 +1030,10 @@ static dc_status host_plan(dc_model* m, HostPlan* hp, int avail_slots = 0) {
       off[mem[0]] = 1;
     }
   }
+  if (m->offload_all_sync) {
+    if (nf == 0) return mfail(m, DC_EINVAL, "offload_all_sync: call dc_offload_fragments first");
+    std::fill(off.begin(), off.end(), (char)1);
+  }
   // whole (layer, state) fragments forming a prefix per state
   auto lay_lo = [&](int l) { return L.store_off[L.layer_first[l]]; };
   auto lay_n = [&](int l) {
@@ -1049,7 +1077,19 @@ static dc_status host_plan(dc_model* m, HostPlan* hp, int avail_slots = 0) {
       const int64_t* mem; const int* posts; const int* waits;
       int64_t ao, bytes;
       sched_op(sc, i, &kind, &id, &mem, &nm, &ao, &bytes, &posts, &np, &waits, &nw);
-      if (kind == K_RELOAD && off[mem[0]]) {
+      // offload_all_sync: a layer's fragments are reloaded at its RS op
+      std::vector<int> take;
+      if (kind == K_RELOAD && off[mem[0]] && !m->offload_all_sync) take.push_back((int)mem[0]);
+      if (kind == K_RS && m->offload_all_sync) {
+        const int layer = m->s0[id].layer;
+        for (int f = 0; f < nf; ++f) {
+          int fl, fs;
+          int64_t o, e;
+          ctx_frag(m->ctx, f, &fl, &fs, &o, &e);
+          if (fl == layer) take.push_back(f);
+        }
+      }
+      for (int f : take) {
         int sl = 0;
         if (n_fifo) {
           if (fifo.empty()) return mfail(m, DC_EOOM, "host states: pool slots exhausted");
@@ -1060,8 +1100,9 @@ static dc_status host_plan(dc_model* m, HostPlan* hp, int avail_slots = 0) {
           if (sl == (int)busy.size()) busy.push_back(0);
           busy[sl] = 1;
         }
-        hp->slot_of[mem[0]] = sl;
-      } else if (kind == K_RS) {
+        hp->slot_of[f] = sl;
+      }
+      if (kind == K_RS) {
         const int layer = m->s0[id].layer;
         for (int f = 0; f < nf; ++f) {
           int fl, fs;

@@ -157,3 +157,39 @@ def test_host_resident_states_bitexact_vs_resident(world, moe):
             m_off, v_off = rt.full_states(off[r])
             assert torch.equal(m_ref.view(torch.int32), m_off.view(torch.int32)), (t, r, "m")
             assert torch.equal(v_ref.view(torch.int32), v_off.view(torch.int32)), (t, r, "v")
+
+
+def test_offload_all_sync_baseline_bitexact():
+    """The paper's comparison point for adaptive offload (option
+    offload_all_sync): no optimizer state on the device, every fragment
+    reloaded synchronously before its layer's update and written back after;
+    bit-identical to the all-resident step."""
+    cfg = synth.small_llama(layers=3, seq=128)
+    table = synth.param_table(cfg)
+    n = sum(-(-p.numel // 8) * 8 for p in table)
+    runs = []
+    for sync in (False, True):
+        ranks = rt.create_ranks(table, 1, lr=LR, host_pinned_bytes=8 * n + 4096, defer_states=sync)
+        x, t = ost.rank_batch(cfg, 0)
+        rt.attach_model(ranks, cfg, {0: bf16_tensor(x)}, {0: bf16_tensor(t)})
+        st = ranks[0]
+        frags = rt.offload_fragments(st, rt.layer_state_bytes(table, 1))
+        prof = rt.profile_json(st, frags=frags)
+        rt.bind(ranks, {0: dc.plan(json.dumps(prof), 1 << 40, passes=dc.DC_PASS_SHARD)})
+        if sync:
+            dc.check(dc.lib.dc_model_set_option(st.model, b"offload_all_sync", 1))
+            mf, vf, pool, hb = rt.bind_host_states(ranks)[0]
+            assert mf == vf == st.layout.shard_elems and pool > 0 and hb == 8 * st.layout.shard_elems
+            assert dc.lib.dc_model_set_option(st.model, b"offload_all_sync", 0) == dc.DC_ESTATE
+        for s in (1, 2, 3):
+            rt.step(ranks, s)
+            torch.cuda.synchronize()
+            rt.poll(ranks)
+        runs.append(st)
+    a, b = runs
+    for k in ("master", "shard"):
+        dt = torch.int16 if k == "shard" else torch.int32
+        assert torch.equal(a.tensors[k].view(dt), b.tensors[k].view(dt)), k
+    m_b, v_b = rt.full_states(b)
+    assert torch.equal(a.tensors["m"].cpu().view(torch.int32), m_b.view(torch.int32))
+    assert torch.equal(a.tensors["v"].cpu().view(torch.int32), v_b.view(torch.int32))
