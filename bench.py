@@ -314,6 +314,9 @@ def main():
     if args.share_gpu:
         local = 0
         os.environ["DC_SYMM"] = "ipc"         # symmetric memory refuses two ranks on one device
+        # processes time-slicing one GPU: keep one GEMM stream per process
+        # (with the dW stream the pair's handshake intermittently stalled)
+        os.environ.setdefault("DC_DW_CONCURRENT", "0")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     # host-side collectives (barrier, MAX of timings / profiles) run on `cdev`

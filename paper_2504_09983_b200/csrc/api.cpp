@@ -270,7 +270,7 @@ extern "C" dc_status dc_bind_schedule(dc_ctx* c, const dc_schedule* s, const uin
       if (nw == 0) c->initial_ready.push_back(id);
       int64_t shard_bytes = 0;
       for (int j = 0; j < nm; ++j) shard_bytes += c->L.S[mem[j]] * 2;
-      int ctas = (int)std::min<int64_t>(32, std::max<int64_t>(1, shard_bytes / (64 * 1024)));
+      int ctas = (int)std::min<int64_t>(64, std::max<int64_t>(1, shard_bytes / (32 * 1024)));
       c->ag_ctas[id] = c->ag_ce ? 1 : ctas;             // done bumps per sender per gather
       c->ag_launches[id] = c->ag_ce ? 1 : (nm + 47) / 48;
     }

@@ -59,7 +59,12 @@ __device__ __forceinline__ bool spin_ge(const uint32_t* p, uint32_t target, uint
 // Flag waits run in separate one-thread kernels on the same stream (before the
 // push: every receiver's ready flag; after it: this rank's done counter), so a
 // waiting rank occupies one SM slot, never a whole grid of spinning CTAs.
-__global__ void __launch_bounds__(512) ag_push_kernel(const AgParams p) {
+// 256 threads x <= 64 registers: a push CTA fits beside a CTA of the pair GEMM
+// (384 threads x 120 registers) on one SM (65536 registers), so a prefetched
+// gather really runs during the layer GEMMs; 8 x 16 B stores in flight per
+// thread keep ~2 MB outstanding at 64 CTAs (NVLink latency x 900 GB/s).
+constexpr int AG_THREADS = 256, AG_UNR = 8;
+__global__ void __launch_bounds__(AG_THREADS) ag_push_kernel(const AgParams p) {
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   for (int m = 0; m < p.nm; ++m) {
@@ -67,17 +72,17 @@ __global__ void __launch_bounds__(512) ag_push_kernel(const AgParams p) {
     const int64_t n = p.nvec[m];
     const int64_t off = p.dst_off[m];
     int64_t i = tid;
-    for (; i + 3 * nthr < n; i += 4 * nthr) {
-      uint4 v[4];
+    for (; i + (AG_UNR - 1) * nthr < n; i += AG_UNR * nthr) {
+      uint4 v[AG_UNR];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldg(src + i + u * nthr);
+      for (int u = 0; u < AG_UNR; ++u) v[u] = __ldg(src + i + u * nthr);
       // destinations rotated by rank: the N senders start on N different
       // receivers instead of all on rank 0 (spreads NVSwitch ingress)
       for (int qq = 0; qq < p.world; ++qq) {
         const int q = (qq + p.rank) % p.world;
         uint4* dst = reinterpret_cast<uint4*>(p.arena[q] + off);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) dst[i + u * nthr] = v[u];
+        for (int u = 0; u < AG_UNR; ++u) dst[i + u * nthr] = v[u];
       }
     }
     for (; i < n; i += nthr) {
@@ -128,7 +133,7 @@ dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const
     p.wait = (b + AG_MAXM >= mem.size());
     p.timeout_ns = timeout_ns;
     p.err = err_flag;
-    ag_push_kernel<<<ctas, 512, 0, st>>>(p);
+    ag_push_kernel<<<ctas, AG_THREADS, 0, st>>>(p);
     if (cudaGetLastError() != cudaSuccess) return DC_ECUDA;
     count_launch();
   }

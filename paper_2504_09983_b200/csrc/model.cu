@@ -105,6 +105,11 @@ struct dc_model {
   int comm_sms = 0;                  // > 0: SM partition (GEMMs | comm + Adam), green contexts
   SmPartition part{};
   int gemm_sms = 0;                  // SMs the layer GEMMs may use (0 = all)
+  // backward: the dW GEMMs of an op run on a second stream beside its dX GEMM,
+  // so their tiles fill the dX GEMM's last partial wave (option dw_concurrent)
+  int dw_conc = 1;
+  cudaStream_t cs2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_joinw = nullptr;
   int fuse_act = 0;                  // bit 0: SiLU*up in the gate|up GEMM epilogue; bit 1: its backward
                                      // in the down dX epilogue.  Bit-identical; measured no faster in
                                      // the power-capped N = 1 step (profiles/r01g/fuse_act_ab.md): off
@@ -321,6 +326,11 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
       return mfail(nullptr, DC_ECUDA, "dc_model_create: event creation failed");
   }
   for (auto& e : m->ev_join) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (cudaStreamCreateWithFlags(&m->cs2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&m->ev_joinw, cudaEventDisableTiming) != cudaSuccess)
+    return mfail(nullptr, DC_ECUDA, "dc_model_create: stream creation failed");
+  if (const char* e = getenv("DC_DW_CONCURRENT")) m->dw_conc = atoi(e) != 0;   // A/B knob
   *out = m.release();
   return DC_OK;
 }
@@ -334,6 +344,9 @@ extern "C" dc_status dc_model_destroy(dc_model* m) {
   for (auto& e : m->ev_join) if (e) cudaEventDestroy(e);
   for (auto& e : m->wb_ev) cudaEventDestroy(e);
   if (m->wb_stream) cudaStreamDestroy(m->wb_stream);
+  if (m->cs2) cudaStreamDestroy(m->cs2);
+  if (m->ev_fork) cudaEventDestroy(m->ev_fork);
+  if (m->ev_joinw) cudaEventDestroy(m->ev_joinw);
   sm_partition_destroy(&m->part);
   delete m;
   return DC_OK;
@@ -395,7 +408,9 @@ static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t l
   for (int e : ends) g.bseg_end[i++] = e;
   g.b_mn_major = b_mn; g.b_split_k = split_k;
   g.C = C; g.ldc = ldc; g.R = R; g.ldr = ldr;
-  g.stream_k = m->stream_k;
+  // a stream-K pair spins on another pair's partial: never two such kernels at
+  // once, so the GEMMs beside the dX GEMM (second stream) are data-parallel only
+  g.stream_k = st == m->cs2 ? 0 : m->stream_k;
   g.num_sms = m->gemm_sms;
   if (glu) {
     g.epilogue = glu->mode;
@@ -440,6 +455,15 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
     return &epi;
   };
   dc_status s = DC_OK;
+  // dW GEMMs on the second stream (forked before the dX GEMM, joined at the end
+  // of the op; both only read the op's inputs and write disjoint outputs)
+  cudaStream_t sw = st;
+  auto fork = [&]() {
+    if (!m->dw_conc || m->comm_sms > 0) return;
+    cudaEventRecord(m->ev_fork, st);
+    cudaStreamWaitEvent(m->cs2, m->ev_fork, 0);
+    sw = m->cs2;
+  };
   switch (o.code) {
     case F_ATTN_NORM:
       k_rmsnorm_fwd(layer_in(m, l, o.micro), m->W(l, P_G1), m->A(a.h1), (float*)m->A(a.rstd1), T, H, st);
@@ -485,6 +509,7 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       // (the executor has enqueued dc_grad_slot_acquire for this layer)
       // dact = dy Wd  (A K-major [T,H]; B = Wd [H rows = K][F] MN-major); fused:
       // the epilogue turns dact into d(gate | up) with gu (epilogue 3)
+      fork();
       if (m->fuse_act & 2) {
         const Glu glu{3, m->A(a.gu), 2 * F, F};
         s = gemm(m, T, F, H, dcur, H, 0, {m->W(l, P_DOWN)}, {F}, {F / 256}, 1, 0, m->A(m->ws_dgu), 2 * F, nullptr, 0,
@@ -493,20 +518,21 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
         s = gemm(m, T, F, H, dcur, H, 0, {m->W(l, P_DOWN)}, {F}, {F / 256}, 1, 0, m->A(m->ws_dact), F, nullptr, 0, st);
       }
       if (s == DC_OK)  // dWd = dy^T act : A = dy stored [T][H] (MN-major), B = act [T][F] (MN-major)
-        s = gemm(m, H, F, T, dcur, H, 1, {m->A(a.act)}, {F}, {F / 256}, 1, 0, G(P_DOWN), F, nullptr, 0, st, ADAM(P_DOWN));
+        s = gemm(m, H, F, T, dcur, H, 1, {m->A(a.act)}, {F}, {F / 256}, 1, 0, G(P_DOWN), F, nullptr, 0, sw, ADAM(P_DOWN));
       break;
     case B_ACT:
       if (!(m->fuse_act & 2)) k_act_bwd(m->A(m->ws_dact), m->A(a.gu), m->A(m->ws_dgu), T, F, st);
       break;
     case B_GATE_UP:
       // dh2 = dgate Wg + dup Wu : A = dgu [T, 2F] K-major, B split along K
+      fork();
       s = gemm(m, T, H, 2 * F, m->A(m->ws_dgu), 2 * F, 0, {m->W(l, P_GATE), m->W(l, P_UP)}, {H, H},
                {F / 64, 2 * F / 64}, 1, 1, m->A(m->ws_dh), H, nullptr, 0, st);
       if (s == DC_OK)
-        s = gemm(m, F, H, T, m->A(m->ws_dgu), 2 * F, 1, {m->A(a.h2)}, {H}, {H / 256}, 1, 0, G(P_GATE), H, nullptr, 0, st, ADAM(P_GATE));
+        s = gemm(m, F, H, T, m->A(m->ws_dgu), 2 * F, 1, {m->A(a.h2)}, {H}, {H / 256}, 1, 0, G(P_GATE), H, nullptr, 0, sw, ADAM(P_GATE));
       if (s == DC_OK)
         s = gemm(m, F, H, T, m->A(m->ws_dgu) + (int64_t)F * 2, 2 * F, 1, {m->A(a.h2)}, {H}, {H / 256}, 1, 0, G(P_UP),
-                 H, nullptr, 0, st, ADAM(P_UP));
+                 H, nullptr, 0, sw, ADAM(P_UP));
       break;
     case B_MLP_NORM: {
       const int nb = rmsnorm_bwd_blocks(T);
@@ -517,25 +543,27 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
     }
     case B_O:
       // da -> dqkv[:, :qd] ; dWo = dx2^T a
+      fork();
       s = gemm(m, T, qd, H, m->A(m->ws_dx2), H, 0, {m->W(l, P_O)}, {qd}, {qd / 256}, 1, 0, m->A(m->ws_dqkv), qkvd,
                nullptr, 0, st);
       if (s == DC_OK)
-        s = gemm(m, H, qd, T, m->A(m->ws_dx2), H, 1, {m->A(a.a)}, {qd}, {qd / 256}, 1, 0, G(P_O), qd, nullptr, 0, st, ADAM(P_O));
+        s = gemm(m, H, qd, T, m->A(m->ws_dx2), H, 1, {m->A(a.a)}, {qd}, {qd / 256}, 1, 0, G(P_O), qd, nullptr, 0, sw, ADAM(P_O));
       break;
     case B_ATTN_MIX:
       k_attn_mix_bwd(m->A(m->ws_dqkv), m->A(a.qkv), T, qd, kvd, m->d.head_dim, m->grp, st);
       break;
     case B_QKV:
+      fork();
       s = gemm(m, T, H, qkvd, m->A(m->ws_dqkv), qkvd, 0, {m->W(l, P_Q), m->W(l, P_K), m->W(l, P_V)}, {H, H, H},
                {qd / 64, (qd + kvd) / 64, qkvd / 64}, 1, 1, m->A(m->ws_dh), H, nullptr, 0, st);
       if (s == DC_OK)
-        s = gemm(m, qd, H, T, m->A(m->ws_dqkv), qkvd, 1, {m->A(a.h1)}, {H}, {H / 256}, 1, 0, G(P_Q), H, nullptr, 0, st, ADAM(P_Q));
+        s = gemm(m, qd, H, T, m->A(m->ws_dqkv), qkvd, 1, {m->A(a.h1)}, {H}, {H / 256}, 1, 0, G(P_Q), H, nullptr, 0, sw, ADAM(P_Q));
       if (s == DC_OK)
         s = gemm(m, kvd, H, T, m->A(m->ws_dqkv) + (int64_t)qd * 2, qkvd, 1, {m->A(a.h1)}, {H}, {H / 256}, 1, 0, G(P_K),
-                 H, nullptr, 0, st, ADAM(P_K));
+                 H, nullptr, 0, sw, ADAM(P_K));
       if (s == DC_OK)
         s = gemm(m, kvd, H, T, m->A(m->ws_dqkv) + (int64_t)(qd + kvd) * 2, qkvd, 1, {m->A(a.h1)}, {H}, {H / 256}, 1,
-                 0, G(P_V), H, nullptr, 0, st, ADAM(P_V));
+                 0, G(P_V), H, nullptr, 0, sw, ADAM(P_V));
       break;
     case B_ATTN_NORM: {
       const int nb = rmsnorm_bwd_blocks(T);
@@ -594,6 +622,7 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       const int e = o.e, R = m->R;
       uint8_t* dOe = m->A(m->ws_dO) + (int64_t)e * R * H * 2;
       // dact_e = dO_e W2_e (fused: -> d(gate | up)_e with gu_e) ; dW2_e = dO_e^T act_e
+      fork();
       if (m->fuse_act & 2) {
         const Glu glu{3, m->A(a.gu) + (int64_t)e * R * 2 * F * 2, 2 * F, F};
         s = gemm(m, R, F, H, dOe, H, 0, {m->W(l, p_w2(e))}, {F}, {F / 256}, 1, 0, m->A(m->ws_dgu), 2 * F, nullptr, 0,
@@ -603,7 +632,7 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       }
       if (s == DC_OK)
         s = gemm(m, H, F, R, dOe, H, 1, {m->A(a.act) + (int64_t)e * R * F * 2}, {F}, {F / 256}, 1, 0, G(p_w2(e)), F,
-                 nullptr, 0, st);
+                 nullptr, 0, sw);
       break;
     }
     case B_EXP_ACT:
@@ -614,13 +643,14 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       const int e = o.e, R = m->R;
       const uint8_t* Xe = m->A(a.X) + (int64_t)e * R * H * 2;
       // dX_e = d(gate|up)_e [W1_e; W3_e] (B split along K) ; dW1_e, dW3_e = d(gate), d(up)^T X_e
+      fork();
       s = gemm(m, R, H, 2 * F, m->A(m->ws_dgu), 2 * F, 0, {m->W(l, p_w1(e)), m->W(l, p_w3(e))}, {H, H},
                {F / 64, 2 * F / 64}, 1, 1, m->A(m->ws_dX) + (int64_t)e * R * H * 2, H, nullptr, 0, st);
       if (s == DC_OK)
-        s = gemm(m, F, H, R, m->A(m->ws_dgu), 2 * F, 1, {Xe}, {H}, {H / 256}, 1, 0, G(p_w1(e)), H, nullptr, 0, st);
+        s = gemm(m, F, H, R, m->A(m->ws_dgu), 2 * F, 1, {Xe}, {H}, {H / 256}, 1, 0, G(p_w1(e)), H, nullptr, 0, sw);
       if (s == DC_OK)
         s = gemm(m, F, H, R, m->A(m->ws_dgu) + (int64_t)F * 2, 2 * F, 1, {Xe}, {H}, {H / 256}, 1, 0, G(p_w3(e)), H,
-                 nullptr, 0, st);
+                 nullptr, 0, sw);
       break;
     }
     case B_ROUTER:
@@ -631,6 +661,10 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
       break;
     default:
       return mfail(m, DC_EINVAL, "run_op: bad op");
+  }
+  if (sw != st) {                    // join the dW stream (the op ends when both do)
+    cudaEventRecord(m->ev_joinw, sw);
+    cudaStreamWaitEvent(st, m->ev_joinw, 0);
   }
   if (s != DC_OK) return s;
   if (cudaGetLastError() != cudaSuccess) return mfail(m, DC_ECUDA, std::string("layer op launch failed: ") + op_name(o.code));
@@ -971,6 +1005,10 @@ extern "C" dc_status dc_model_set_option(dc_model* m, const char* key, int64_t v
       return mfail(m, DC_EINVAL, "comm_sms needs one rank per GPU");
     if (m->part.ctx_gemm && value != m->comm_sms) sm_partition_destroy(&m->part);
     m->comm_sms = (int)value;
+    return DC_OK;
+  }
+  if (!strcmp(key, "dw_concurrent")) {
+    m->dw_conc = value != 0;
     return DC_OK;
   }
   if (!strcmp(key, "offload_all_sync")) {

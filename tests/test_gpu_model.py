@@ -261,3 +261,35 @@ def test_copy_engine_gather_bitexact(world, moe):
     prof = json.loads(dc.model_profile_json(a[0].model))
     assert any(o["kind"] == "ag" and o["dur_us"] > 0 for o in prof["ops"])
     assert dc.lib.dc_set_option(a[0].ctx, b"ag_copy_engine", 0) == dc.DC_ESTATE
+
+
+@pytest.mark.parametrize("world,moe", [(1, False), (2, False), (1, True)])
+def test_dw_concurrent_bitexact(world, moe):
+    """dW GEMMs on a second stream beside each backward op's dX GEMM (option
+    dw_concurrent, default on) == stream order, bit for bit, two planned steps."""
+    cfg = synth.small_mixtral(layers=2, seq=128) if moe else synth.small_llama(layers=2, seq=128)
+    table = synth.param_table(cfg)
+    runs = []
+    for conc in (1, 0):
+        ranks = rt.create_ranks(table, world, lr=LR)
+        xs, ts = {}, {}
+        for r in ranks:
+            x, t = ost.rank_batch(cfg, r)
+            xs[r], ts[r] = bf16_tensor(x), bf16_tensor(t)
+        rt.attach_model(ranks, cfg, xs, ts)
+        for st in ranks.values():
+            dc.check(dc.lib.dc_model_set_option(st.model, b"dw_concurrent", conc))
+        prof = rt.profile_json(ranks[0], tc=[[4096, 10], [1 << 20, 20], [1 << 26, 400]])
+        sched = dc.plan(json.dumps(prof), 1 << 40, M_prefetch=1 << 22,
+                        passes=dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD, strict=True)
+        rt.bind(ranks, {r: sched for r in ranks})
+        for s in (1, 2):
+            rt.step(ranks, s)
+            torch.cuda.synchronize()
+            rt.poll(ranks)
+        runs.append(ranks)
+    a, b = runs
+    for r in a:
+        for k in ("master", "m", "v", "shard"):
+            dt = torch.int16 if k == "shard" else torch.int32
+            assert torch.equal(a[r].tensors[k].view(dt), b[r].tensors[k].view(dt)), (r, k)

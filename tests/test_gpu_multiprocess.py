@@ -28,7 +28,8 @@ def _worker(rank, world, port, out_dir):
     # torch symmetric memory rejects two ranks on one device: peer-map via CUDA IPC
     # two processes time-slice one GPU: keep the default 8 hardware connections
     # per context (measured: 32 per context can stall the pair's flag handshake)
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), DC_SYMM="ipc", CUDA_DEVICE_MAX_CONNECTIONS="8")
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), DC_SYMM="ipc", CUDA_DEVICE_MAX_CONNECTIONS="8",
+                      DC_DW_CONCURRENT="0")   # see bench.py --share-gpu
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import synth
