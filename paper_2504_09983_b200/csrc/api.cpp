@@ -103,7 +103,7 @@ struct dc_ctx {
   int slot_use[2] = {0, 0};
   std::vector<int> layer_use;
   uint32_t rs_done_total = 0;
-  int rs_ctas = 0, rs_threads = 256;
+  int rs_ctas = 0, rs_threads = 256, rs_ctas_default = 296;
   // error word: host-mapped pinned (device writes on a flag-wait timeout)
   uint32_t* err_host = nullptr;
   uint32_t* err_dev = nullptr;
@@ -187,7 +187,14 @@ extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
   if (a->spin_limit) c->timeout_ns = (uint64_t)a->spin_limit * 1000ull * 1000ull;   // spin_limit in ms
   c->cur_off.assign(a->n_params, -1);
   c->layer_use.assign(c->L.n_layers, 0);
-  c->rs_ctas = 296;                     // rs_adam grid, two CTAs per SM (DC_RS_CTAS overrides)
+  // rs_adam grid.  N = 1: two 256-thread CTAs per SM — a local HBM-bound pass,
+  // fastest when it has the SMs to itself (profiles/r01g/rs_coresidency_ab.md).
+  // N > 1: one 128-thread CTA per SM (128 x 112 registers fits beside a pair-GEMM
+  // CTA), so the NVLink-bound reduce-scatter of layer l+1 runs during layer l's
+  // backward GEMMs instead of waiting for their SMs.  DC_RS_CTAS / DC_RS_THREADS override.
+  c->rs_ctas = a->world > 1 ? 148 : 296;
+  c->rs_threads = a->world > 1 ? 128 : 256;
+  c->rs_ctas_default = c->rs_ctas;
   if (const char* e = getenv("DC_RS_CTAS")) c->rs_ctas = std::max(1, atoi(e));
   if (const char* e = getenv("DC_RS_THREADS")) c->rs_threads = atoi(e) == 128 ? 128 : 256;
   DC_CUDA_TRY(cudaSetDevice(a->device), &c->err);
@@ -653,7 +660,7 @@ int64_t ctx_numel(const dc_ctx* c, int p) { return c->numel[p]; }
 int ctx_micro_steps(const dc_ctx* c) { return c->micro_steps; }
 uint32_t ctx_flags(const dc_ctx* c) { return c->flags; }
 void ctx_set_rs_ctas(dc_ctx* c, int ctas) {
-  c->rs_ctas = ctas > 0 ? ctas : 296;
+  c->rs_ctas = ctas > 0 ? ctas : c->rs_ctas_default;
   if (const char* e = getenv("DC_RS_CTAS")) c->rs_ctas = std::max(1, atoi(e));
 }
 }  // namespace dc
