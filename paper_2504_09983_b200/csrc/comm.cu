@@ -166,6 +166,9 @@ struct RsParams {
 #ifndef DC_RS_UNR
 #define DC_RS_UNR 2
 #endif
+#ifndef DC_RS_PREFETCH
+#define DC_RS_PREFETCH 0      // > 0: prefetch that many iterations ahead into L2 (A/B)
+#endif
 constexpr int RS_UNR = DC_RS_UNR;   // groups of 8 elements per thread per iteration (loads hoisted)
 
 // MODE (gradient accumulation; dc.h dc_reduce_scatter_step):
@@ -223,6 +226,17 @@ __global__ void __launch_bounds__(256) rs_adam_kernel(const RsParams p) {
       } else {
         constexpr bool ACC = MODE == RS_FINAL;
         for (int64_t i0 = tid; i0 < n8; i0 += nthr * RS_UNR) {
+#if DC_RS_PREFETCH
+          {   // pull the next iteration's state lines into L2 (more bytes in flight, no registers)
+            const int64_t j = i0 + (int64_t)DC_RS_PREFETCH * nthr * RS_UNR;
+            if (j < n8) {
+              asm volatile("prefetch.global.L2 [%0];" :: "l"(mst + 8 * j));
+              asm volatile("prefetch.global.L2 [%0];" :: "l"(mm + 8 * j));
+              asm volatile("prefetch.global.L2 [%0];" :: "l"(vv + 8 * j));
+              asm volatile("prefetch.global.L2 [%0];" :: "l"(p.slot[p.rank] + gbase + j * 16));
+            }
+          }
+#endif
           Group8<MAXQ> x[RS_UNR];
 #pragma unroll
           for (int u = 0; u < RS_UNR; ++u) {     // every load of RS_UNR groups before any math
