@@ -27,7 +27,6 @@ checked against torch.autograd in fp64 so a dropped term or sign fails).
 """
 import numpy as np
 
-from . import numerics as nx
 
 RMS_EPS = 1e-5
 

@@ -15,7 +15,6 @@ import json
 import os
 import threading
 
-import numpy as np
 import torch
 
 from . import dc

@@ -11,7 +11,7 @@ the order the fully-sharded rewrite gathers them in (§4.1).
 The compute-op graph (which op consumes which parameter) is also defined here:
 it is the workload's structure, not the method.
 """
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import List, Tuple
 
 from .gen import std_to_k, K_MLP

@@ -3,10 +3,8 @@ GPU path, with DC_DEBUG_POISON: once a fragment's D2H copy is synced the
 device slice is overwritten with NaNs, so a missing or misordered reload
 corrupts the Adam update.  The offloaded step must be bit-identical to the
 same step without offload."""
-import ctypes as C
 import json
 
-import numpy as np
 import pytest
 import torch
 
