@@ -511,15 +511,18 @@ def main():
     pk = peaks()
     achieved = gemm_fl / (gemm_us * 1e-6) / 1e12 if gemm_us else None
     ord_us = sum(o["dur_us"] for o in ordered["ops"] if o["kind"] == "compute" and gemm_flops(o["name"], cfg, T))
-    traffic = None
+    traffic, traffic_note = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            tj = json.load(f)
+        traffic = tj.get("dram_bytes_per_launch")
+        traffic_note = "%s; algorithmic %s B" % (tj.get("launch"), tj.get("algorithmic_bytes_per_launch"))
     except (OSError, ValueError):
         pass
     roofline = {"bound": "tensor", "kernel": "gemm_bf16_sm100 (tcgen05, all layer GEMMs)",
                 "achieved": achieved, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
                 "frac": achieved / pk["bf16_tflops_sustained"] if achieved else None, "traffic": traffic,
+                "traffic_note": traffic_note,
                 "peak_source": pk["source"] + ", sustained bf16 (kernel inside a long step)",
                 "flops_per_step": gemm_fl, "gemm_ms_per_step": gemm_us / 1e3,
                 "achieved_stream_ordered": gemm_fl / (ord_us * 1e-6) / 1e12 if ord_us else None,
