@@ -122,8 +122,37 @@ __global__ void __launch_bounds__(RN_T) rmsnorm_fwd_kernel(const bf16* __restric
   }
 }
 
+// Warp per row (default): no CTA-wide reduction, 8 rows per CTA in flight;
+// the row is re-read from L1/L2 for the scaling pass.
+__global__ void __launch_bounds__(256) rmsnorm_fwd_warp_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
+                                                              bf16* __restrict__ h, float* __restrict__ rstd, int T,
+                                                              int H) {
+  const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (row >= T) return;
+  const bf16* xr = x + (int64_t)row * H;
+  float ss = 0.0f;
+  for (int c = lane * 8; c < H; c += 256) {
+    float f[8];
+    load8(xr + c, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss = fmaf(f[i], f[i], ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float r = 1.0f / sqrtf(ss / (float)H + 1e-5f);
+  if (lane == 0) rstd[row] = r;
+  for (int c = lane * 8; c < H; c += 256) {
+    float f[8], gg[8];
+    load8(xr + c, f);
+    load8(g + c, gg);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = f[i] * r * gg[i];
+    store8(h + (int64_t)row * H + c, f);
+  }
+}
+
 void k_rmsnorm_fwd(const void* x, const void* g, void* h, float* rstd, int T, int H, cudaStream_t st) {
-  rmsnorm_fwd_kernel<<<T, RN_T, 0, st>>>((const bf16*)x, (const bf16*)g, (bf16*)h, rstd, H);
+  rmsnorm_fwd_warp_kernel<<<(T + 7) / 8, 256, 0, st>>>((const bf16*)x, (const bf16*)g, (bf16*)h, rstd, T, H);
   count_launch();
 }
 
@@ -288,16 +317,29 @@ void k_rmsnorm_bwd(const void* dh, const void* x, const void* g, const float* rs
   count_launch();
 }
 
-__global__ void colsum_kernel(const float* __restrict__ p, int nblk, int H, bf16* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= H) return;
+// out[c] = bf16(sum_b p[b][c]): a CTA owns 32 columns; warp w sums rows
+// w, w + 8, ... (coalesced 128 B per row), then the 8 partials are added in
+// warp order (fixed, deterministic)
+__global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ p, int nblk, int H,
+                                                     bf16* __restrict__ out) {
+  __shared__ float sh[8][33];
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+  const int c = blockIdx.x * 32 + lane;
   float s = 0.0f;
-  for (int b = 0; b < nblk; ++b) s += p[(int64_t)b * H + c];
-  out[c] = __float2bfloat16_rn(s);
+  if (c < H)
+    for (int b = w; b < nblk; b += 8) s += p[(int64_t)b * H + c];
+  sh[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < H) {
+    float t = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sh[k][lane];
+    out[c] = __float2bfloat16_rn(t);
+  }
 }
 
 void k_colsum_to_bf16(const float* partial, int nblk, int H, void* out, cudaStream_t st) {
-  colsum_kernel<<<(H + 255) / 256, 256, 0, st>>>(partial, nblk, H, (bf16*)out);
+  colsum_kernel<<<(H + 31) / 32, 256, 0, st>>>(partial, nblk, H, (bf16*)out);
   count_launch();
 }
 
@@ -469,6 +511,7 @@ cudaError_t preload_glue_kernels() {
                        (const void*)rmsnorm_bwd_kernel<1>, (const void*)rmsnorm_bwd_kernel<2>,
                        (const void*)rmsnorm_bwd_kernel<3>, (const void*)rmsnorm_bwd_kernel<4>, (const void*)colsum_kernel,
                        (const void*)rmsnorm_bwd_dot_kernel, (const void*)rmsnorm_bwd_dx_kernel,
+                       (const void*)rmsnorm_fwd_warp_kernel,
                        (const void*)attn_mix_fwd_kernel, (const void*)attn_mix_bwd_kernel,
                        (const void*)act_fwd_kernel, (const void*)act_bwd_kernel,
                        (const void*)loss_kernel, (const void*)loss_final_kernel};
