@@ -79,7 +79,7 @@ def a256(b):
     return (b + 255) // 256 * 256
 
 
-def analytic_profile(cfg, N, op_ms, checkpoint=True):
+def analytic_profile(cfg, N, op_ms, checkpoint=True, micro_steps=1):
     """S_0 profile of a synthetic layer stack at any size without a GPU: the
     executor's P_mem bookkeeping (model.cu compute_pmem: shard + master, two
     grad slots, workspace, inputs, saved activations of the layers between
@@ -102,19 +102,24 @@ def analytic_profile(cfg, N, op_ms, checkpoint=True):
              "mlp_norm": T * h * 2 + T * 4, "gate_up": T * 2 * f * 2, "act": T * f * 2, "down": T * h * 2}
     layer_set = sum(a256(v) for v in piece.values())
     ws = 2 * T * h * 2 + T * f * 2 + T * 2 * f * 2 + 2 * T * h * 2 + T * qkvd * 2 + (T // 16) * h * 4
-    static = E * 6 + 2 * grad_slot + ws + 2 * T * h * 2 + (layer_set - T * h * 2 if checkpoint else 0)
-    comp = synth.compute_ops(cfg, checkpoint=checkpoint)
+    static = E * 6 + 2 * grad_slot + ws + 2 * micro_steps * T * h * 2 + (layer_set - T * h * 2 if checkpoint else 0)
+    static += E * 4 if micro_steps > 1 else 0                      # fp32 grad accumulator
+    comp = synth.compute_ops(cfg, micro_steps=micro_steps, checkpoint=checkpoint)
     s0 = osd.build_s0(comp)
     live = osd.live_before_s0(s0, B)
     act = 0
+    held = {}
     for o in s0:
         o["p_mem"] = static + live[o["id"]] + act
         o["transient"] = 0
         nm = o["name"][3:] if o["name"].startswith("re_") else o["name"]
+        head, _, tail = nm.rpartition("_")
+        nm = head if tail.isdigit() else nm                    # exp_gu_3 -> exp_gu (per-expert ops)
+        oname = o["name"].rpartition("_")[0] if o["name"].rpartition("_")[2].isdigit() else o["name"]
         if o["kind"] == "rs":
             o["dur_us"] = 1          # replaced below by the RS model
         elif o["kind"] == "compute":
-            o["dur_us"] = max(1, int(round(op_ms.get(nm if o["phase"] == "fwd" else o["name"], 0.0) * 1000)))
+            o["dur_us"] = max(1, int(round(op_ms.get(nm if o["phase"] == "fwd" else oname, 0.0) * 1000)))
             if o["name"].startswith("re_"):
                 o["dur_us"] = max(1, int(round(op_ms.get(nm, 0.0) * 1000)))
         else:
@@ -126,9 +131,11 @@ def analytic_profile(cfg, N, op_ms, checkpoint=True):
                 elif o["phase"] == "bwd" and o["name"] == "attn_norm_bwd":
                     act -= T * h * 2
             elif o["phase"] == "fwd":
-                act += piece.get(o["name"], 0)
-            elif o["name"] == "attn_norm_bwd":
-                act -= layer_set
+                add = piece.get(o["name"], 0)
+                held[(o["micro"], o["layer"])] = held.get((o["micro"], o["layer"]), 0) + add
+                act += add
+            elif o["name"] == "attn_norm_bwd":          # the layer's saved activations are freed
+                act -= held.pop((o["micro"], o["layer"]), 0)
     # optimizer-state fragments (layer, m | v): they define M_opt, which passes
     # P and S add to P_mem (reading D14)
     frags = []
