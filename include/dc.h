@@ -118,7 +118,9 @@ typedef struct {
                                  /*   when micro_steps > 1, else may be NULL   */
 } dc_init_args;
 
-/* Validates, computes the layout, zeroes m/v and (with DC_INIT_WEIGHTS) fills
+/* Validates, computes the layout, zeroes m/v (not with DC_DEFER_STATES: then
+ * exp_avg / exp_avg_sq may be NULL until dc_model_bind_host_states, and a
+ * reduce-scatter before that is DC_ESTATE) and (with DC_INIT_WEIGHTS) fills
  * master = value(seed, param, idx) and shard = RNE_bf16(master) with the
  * counter-based generator on the device (synchronous). */
 dc_status dc_init(const dc_init_args* a, dc_ctx** out);
