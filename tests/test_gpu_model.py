@@ -50,7 +50,9 @@ def _loss(st):
 
 @pytest.mark.parametrize("world,passes,fused", [(1, dc.DC_PASS_SHARD, 0), (1, dc.DC_PASS_SHARD, 1),
                                                 (2, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH, 0),
-                                                (2, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD, 0)])
+                                                (2, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD, 0),
+                                                (4, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD, 0),
+                                                (8, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH, 0)])
 def test_step_matches_oracle(world, passes, fused):
     cfg = synth.small_llama(layers=2, seq=256)
     table, ranks = _setup(cfg, world, passes, fused=fused)

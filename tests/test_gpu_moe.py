@@ -61,7 +61,7 @@ def test_moe_s0_matches_workload_graph():
         assert n_ag == 2 * len(synth.param_table(cfg))        # one per param per phase (S_0)
 
 
-@pytest.mark.parametrize("world,passes", [(1, dc.DC_PASS_SHARD), (2, PS)])
+@pytest.mark.parametrize("world,passes", [(1, dc.DC_PASS_SHARD), (2, PS), (4, PS)])
 def test_moe_step_matches_oracle(world, passes):
     cfg = synth.small_mixtral(layers=2, seq=128)
     table, ranks, _ = _setup(cfg, world, passes)
