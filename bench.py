@@ -58,6 +58,9 @@ def parse():
                     help="the paper's comparison point for --offload (P:504-506): every optimizer-state fragment "
                          "host-resident, reloaded synchronously before its layer's update")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="N = 1 runs capture one planned step as a CUDA graph (dc_model_graph_capture) and replay "
+                         "it in the timed and e2e loops (dc_model_graph_launch); this flag keeps eager steps")
     ap.add_argument("--share-gpu", action="store_true",
                     help="test mode: every rank on cuda:0 (gloo host collectives, CUDA-IPC peer maps, fixed T_c); "
                          "exercises the N > 1 launch on a one-GPU box, numbers are not a bench value")
@@ -299,6 +302,7 @@ def main():
     args = parse()
     if args.offload_sync:
         args.offload = True
+    args.graph = args.gpus == 1 and not args.offload and not args.no_graph
     if args.impl == "reference":
         run_reference(args)
         return
@@ -340,6 +344,8 @@ def main():
         ranks = rt.create_ranks(table, world, local, virtual=False, group=group, rank=rank, lr=lr,
                                 micro_steps=n_micro, defer_states=args.offload)
     st = ranks[rank]
+    if args.graph:
+        dc.check(dc.lib.dc_set_option(st.ctx, b"graph_mode", 1), st.ctx)
     if os.environ.get("DC_AG_COPY_ENGINE") is not None:       # gathers on the copy engines (f-3)
         dc.check(dc.lib.dc_set_option(st.ctx, b"ag_copy_engine", int(os.environ["DC_AG_COPY_ENGINE"])), st.ctx)
     from oracle import numerics as nx          # bf16 rounding of the synthetic inputs only
@@ -438,8 +444,20 @@ def main():
     # ---- warm-up with the planned schedule
     for _ in range(max(3, args.warmup)):
         step_no += 1
-        rt.step(ranks, step_no)
+        rt.step(ranks, step_no, profile=2 if args.graph else 0)   # graph: per-op events of an eager step
     barrier()
+    if args.graph:
+        dc.check(dc.lib.dc_model_graph_capture(st.model, step_no + 1, *st.stream_handles()), st.ctx)
+        for _ in range(2):                                       # replay warm-up
+            step_no += 1
+            dc.check(dc.lib.dc_model_graph_launch(st.model, step_no, cs.cuda_stream), st.ctx)
+        barrier()
+
+    def one_step(profile=0):
+        if args.graph:
+            dc.check(dc.lib.dc_model_graph_launch(st.model, step_no, cs.cuda_stream), st.ctx)
+        else:
+            rt.step(ranks, step_no, profile=profile)
 
     # ---- timed region (device-timed on the compute stream, max over ranks)
     def timed(k, profile_last=True):
@@ -454,7 +472,7 @@ def main():
         launches = 0
         for i in range(k):
             step_no += 1
-            rt.step(ranks, step_no, profile=2 if (profile_last and i == k - 1) else 0)
+            one_step(profile=2 if (profile_last and i == k - 1) else 0)
             n = rt.C.c_int64()
             dc.check(dc.lib.dc_model_launch_count(st.model, rt.C.byref(n)))
             launches += n.value
@@ -553,7 +571,7 @@ def main():
             x_dev.view(-1).copy_(x_host, non_blocking=True)
             t_dev.view(-1).copy_(t_host, non_blocking=True)
         step_no += 1
-        rt.step(ranks, step_no)
+        one_step()
         with torch.cuda.stream(cs):
             loss_host.copy_(lp, non_blocking=True)
         cs.synchronize()
@@ -631,7 +649,7 @@ def main():
                                         (", layer activation checkpointing" if args.checkpoint else "")),
                            "model": "%s-shaped synthetic stack (random init)" % args.model,
                            "global_batch": world * args.batch * n_micro, "micro_steps": n_micro,
-                           "checkpoint": bool(args.checkpoint),
+                           "checkpoint": bool(args.checkpoint), "cuda_graph": bool(args.graph),
                            "seq_len": args.seq, "parallelism": "fsdp%d" % world, "passes": args.passes,
                            "mem_budget_M": M, "plan_ms": round(t_plan * 1e3, 2),
                            "unshard_params": len(plan["unshard"]), "offload": offload_info,

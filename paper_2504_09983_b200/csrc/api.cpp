@@ -57,7 +57,8 @@ static dc_status make_layout(int world, int n, const int64_t* numel, const int32
   L->f_gready = L->f_done + ops;
   L->f_gcons = L->f_gready + 2 * world;
   L->f_rsdone = L->f_gcons + 2 * world;
-  L->flag_words = L->f_rsdone + 1;
+  L->f_scal = L->f_rsdone + 1;
+  L->flag_words = L->f_scal + 2;
   return DC_OK;
 }
 
@@ -114,6 +115,10 @@ struct dc_ctx {
   std::vector<float*> lay_m, lay_v;     // per layer: m / v base for rs_adam (ring slot) or null
   cudaEvent_t gt_start = nullptr, gt_end = nullptr;   // one-shot gather timing (profiling)
   int ag_ce = 0;                        // 1: gathers as copy-engine peer copies (no SM time)
+  // graph mode (N = 1): every step restarts the grad-slot / rs counters and
+  // their flags from zero and reads its Adam scalars from device memory, so a
+  // captured step replays unchanged (dc_model_graph_capture)
+  bool graph_mode = false;
   std::string err;
 
   uint32_t* flag(int q, int64_t word) const { return reinterpret_cast<uint32_t*>(flag_peers[q]) + word; }
@@ -310,6 +315,13 @@ extern "C" dc_status dc_step_begin(dc_ctx* c, int32_t epoch, cudaStream_t st) {
   if ((uint32_t)epoch <= c->epoch) return fail(c, DC_EINVAL, "dc_step_begin: epochs must increase");
   c->epoch = (uint32_t)epoch;
   ++c->fepoch;
+  if (c->graph_mode) {     // N = 1: the previous step is complete (its streams joined this one)
+    c->slot_use[0] = c->slot_use[1] = 0;
+    std::fill(c->layer_use.begin(), c->layer_use.end(), 0);
+    c->rs_done_total = 0;
+    DC_CUDA_TRY(cudaMemsetAsync(c->myflag(c->L.f_gready), 0, (c->L.f_scal - c->L.f_gready) * 4, st), &c->err);
+    gemm_sk_reset(st);
+  }
   if (c->world == 1) return DC_OK;
   // ready flags for gathers without an in-step predecessor release (D26):
   // ready[g][me] in every rank's table
@@ -365,6 +377,11 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
 
 extern "C" dc_status dc_set_option(dc_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(c, DC_EINVAL, "dc_set_option: null argument");
+  if (!strcmp(key, "graph_mode")) {
+    if (value && c->world != 1) return fail(c, DC_EINVAL, "dc_set_option: graph_mode needs N == 1");
+    c->graph_mode = value != 0;
+    return DC_OK;
+  }
   if (!strcmp(key, "ag_copy_engine")) {
     if (c->sched) return fail(c, DC_ESTATE, "dc_set_option: ag_copy_engine must be set before dc_bind_schedule");
     c->ag_ce = value != 0;
@@ -511,7 +528,8 @@ dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, con
                           (uint32_t)u, peers_at(c, c->L.f_gcons + (int64_t)s * c->world + c->rank), (uint32_t)u,
                           c->myflag(c->L.f_rsdone), c->rs_done_total, c->master, mb, vb, c->shard, c->grad_acc,
                           mode, n, sc, cc,
-                          c->beta1, c->beta2, c->eps, ctas, c->rs_threads, c->timeout_ns, c->err_dev, st);
+                          c->beta1, c->beta2, c->eps, ctas, c->rs_threads, c->timeout_ns, c->err_dev, st,
+                          c->graph_mode ? reinterpret_cast<const float*>(c->myflag(c->L.f_scal)) : nullptr);
   if (r != DC_OK) return fail(c, r, "dc_reduce_scatter_step: launch failed");
   return DC_OK;
 }
@@ -614,6 +632,14 @@ extern "C" dc_status dc_offload(dc_ctx* c, int32_t fi, int32_t op, cudaStream_t 
 // internal accessors for model.cu
 namespace dc {
 int ctx_num_frags(const dc_ctx* c) { return (int)c->frags.size(); }
+bool ctx_graph_mode(const dc_ctx* c) { return c->graph_mode; }
+dc_status ctx_set_step_scalars(dc_ctx* c, int step_t, cudaStream_t st) {
+  // the same host arithmetic as reduce_scatter_params (reading D18)
+  const double bc1 = 1.0 - std::pow(c->beta1, step_t);
+  const double bc2 = 1.0 - std::pow(c->beta2, step_t);
+  k_set_scalars(reinterpret_cast<float*>(c->myflag(c->L.f_scal)), (float)(c->lr / bc1), (float)std::sqrt(bc2), st);
+  return cudaGetLastError() == cudaSuccess ? DC_OK : fail(c, DC_ECUDA, "set step scalars: launch failed");
+}
 void ctx_set_gather_timing(dc_ctx* c, cudaEvent_t start, cudaEvent_t end) { c->gt_start = start; c->gt_end = end; }
 void ctx_frag(const dc_ctx* c, int i, int* layer, int* state, int64_t* off, int64_t* elems) {
   const FragInfo& f = c->frags[i];

@@ -159,6 +159,7 @@ struct RsParams {
   float* master; float* m; float* v; bf16* shard;
   float* acc;                 // fp32 accumulated grad shard (gradient accumulation)
   float w1, w2, b2, neg_s, c, eps, invN;
+  const float* scal;          // graph mode: (s, c) of the step in device memory, else null
   uint64_t timeout_ns;
   uint32_t* err;
 };
@@ -180,7 +181,7 @@ template <int MAXQ, int MODE>
 __global__ void __launch_bounds__(256) rs_adam_kernel(const RsParams p) {
   {   // grad-ready of every rank was awaited by the preceding wait kernel
     const uint64_t pol = policy_evict_first();
-    const AdamScalars a{p.w1, p.w2, p.b2, p.neg_s, p.c, p.eps, p.invN};
+    const AdamScalars a{p.w1, p.w2, p.b2, p.scal ? -p.scal[0] : p.neg_s, p.scal ? p.scal[1] : p.c, p.eps, p.invN};
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     for (int mi = 0; mi < p.nm; ++mi) {
@@ -274,7 +275,7 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
                     uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master, float* m,
                     float* v, void* shard, float* acc, int mode, int micro_steps, float s, float c, double beta1,
                     double beta2, double eps, int ctas, int threads, uint64_t timeout_ns, uint32_t* err_flag,
-                    cudaStream_t st) {
+                    cudaStream_t st, const float* dev_scalars) {
   if (threads != 128 && threads != 256) return DC_EINVAL;
   if (mode < RS_UPDATE || mode > RS_FINAL || (mode != RS_UPDATE && !acc) || micro_steps < 1) return DC_EINVAL;
   if (mem.size() > (size_t)RS_MAXM) return DC_EINVAL;
@@ -300,6 +301,7 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
   p.b2 = (float)beta2;
   p.neg_s = -s;
   p.c = c;
+  p.scal = dev_scalars;
   p.eps = (float)eps;
   p.invN = (float)(1.0 / ((double)world * micro_steps));   // fp32(1/(N n)), one rounding
   p.timeout_ns = timeout_ns;
@@ -322,6 +324,15 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
   if (cudaGetLastError() != cudaSuccess) return DC_ECUDA;
   count_launch();
   return DC_OK;
+}
+
+__global__ void set_scalars_kernel(float* dst, float s, float c) {
+  dst[0] = s;
+  dst[1] = c;
+}
+void k_set_scalars(float* dst, float s, float c, cudaStream_t st) {
+  set_scalars_kernel<<<1, 1, 0, st>>>(dst, s, c);
+  count_launch();
 }
 
 // ------------------------------------------------------------------ flags
@@ -402,6 +413,7 @@ cudaError_t preload_comm_kernels() {
   pre(std::integral_constant<int, RS_FINAL>{});
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, post_flags_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, add_flags_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, set_scalars_kernel);
   return e;
 }
 }  // namespace dc

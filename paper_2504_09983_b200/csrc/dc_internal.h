@@ -32,6 +32,7 @@ struct Layout {
   int n_layers = 0;
   // flag table (uint32 words)
   int64_t f_ready = 0, f_done = 0, f_gready = 0, f_gcons = 0, f_rsdone = 0;
+  int64_t f_scal = 0;   // 2 words: this step's Adam scalars (s, c) as fp32 (graph mode)
 };
 
 struct dc_ctx_fwd;
@@ -103,6 +104,9 @@ uint64_t ctx_frag_host_end(const dc_ctx* c, int i);   // pinned host byte offset
 // every receiver is ready (after the ready-flag wait), `end` once every
 // sender's stores have landed here (after the done-counter wait)
 void ctx_set_gather_timing(dc_ctx* c, cudaEvent_t start, cudaEvent_t end);
+// graph mode (N = 1): per-step counter reset and the step's Adam scalars
+bool ctx_graph_mode(const dc_ctx* c);
+dc_status ctx_set_step_scalars(dc_ctx* c, int step_t, cudaStream_t st);
 // dc_reduce_scatter_step restricted to a subset of the layer's params
 dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, const std::vector<int>& params,
                                 cudaStream_t st);
@@ -157,7 +161,11 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
                     uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master,
                     float* m, float* v, void* shard, float* acc, int mode, int micro_steps, float s, float c,
                     double beta1, double beta2, double eps, int ctas, int threads, uint64_t timeout_ns,
-                    uint32_t* err_flag, cudaStream_t st);
+                    uint32_t* err_flag, cudaStream_t st, const float* dev_scalars = nullptr);
+// graph mode: write (s, c) of a step into the flag-table words the rs_adam
+// launches read, and reset a stream's stream-K flags / epochs
+void k_set_scalars(float* dst, float s, float c, cudaStream_t st);
+void gemm_sk_reset(cudaStream_t st);
 // reduce-scatter modes (gradient accumulation)
 enum { RS_UPDATE = 0, RS_FIRST = 1, RS_ADD = 2, RS_FINAL = 3 };
 dc_status k_ag_copy(const std::vector<AgMember>& mem, int world, const uint64_t* arena_peers,

@@ -829,10 +829,11 @@ static int num_sms_cached() {
 // stream-K workspace, one per stream (launches on one stream are ordered, so
 // they may share it; the epoch makes stale flags of earlier launches harmless)
 struct SkWorkspace { float* buf = nullptr; uint32_t* flags = nullptr; uint32_t epoch = 0; };
+static std::mutex g_sk_mu;
+static std::map<cudaStream_t, SkWorkspace> g_sk_ws;
 static SkWorkspace* sk_workspace(cudaStream_t st, int max_tiles, int bnt) {
-  static std::mutex mu;
-  static std::map<cudaStream_t, SkWorkspace> ws;
-  std::lock_guard<std::mutex> lock(mu);
+  std::lock_guard<std::mutex> lock(g_sk_mu);
+  auto& ws = g_sk_ws;
   auto it = ws.find(st);
   if (it != ws.end()) return &it->second;
   // capacity: 2 * 74 split tiles of 2 CTAs x 128 rows x 256 fp32 columns
@@ -843,6 +844,16 @@ static SkWorkspace* sk_workspace(cudaStream_t st, int max_tiles, int bnt) {
   if (cudaMalloc(&w.flags, tiles_cap * 2 * 4) != cudaSuccess) return nullptr;
   if (cudaMemsetAsync(w.flags, 0, tiles_cap * 2 * 4, st) != cudaSuccess) return nullptr;   // ordered before use
   return &(ws[st] = w);
+}
+
+// graph mode: a step starts from epoch 0 with cleared flags, so the epochs a
+// replayed graph baked in at capture never meet a previous replay's flags
+void gemm_sk_reset(cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g_sk_mu);
+  auto it = g_sk_ws.find(st);
+  if (it == g_sk_ws.end()) return;
+  cudaMemsetAsync(it->second.flags, 0, (2 * 74 + 2) * 2 * 4, st);
+  it->second.epoch = 0;
 }
 
 // 0: 256-wide 6 stages (default), 2: 256-wide 7 stages (DC_GEMM_STAGES=7)

@@ -108,6 +108,11 @@ struct dc_model {
   // backward: the dW GEMMs of an op run on a second stream beside its dX GEMM,
   // so their tiles fill the dX GEMM's last partial wave (option dw_concurrent)
   int dw_conc = 1;
+  // CUDA graph of one step (graph mode, N = 1): captured by
+  // dc_model_graph_capture, replayed by dc_model_graph_launch
+  bool capturing = false;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
   cudaStream_t cs2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_joinw = nullptr;
   int fuse_act = 0;                  // bit 0: SiLU*up in the gate|up GEMM epilogue; bit 1: its backward
@@ -344,6 +349,8 @@ extern "C" dc_status dc_model_destroy(dc_model* m) {
   for (auto& e : m->ev_join) if (e) cudaEventDestroy(e);
   for (auto& e : m->wb_ev) cudaEventDestroy(e);
   if (m->wb_stream) cudaStreamDestroy(m->wb_stream);
+  if (m->graph_exec) cudaGraphExecDestroy(m->graph_exec);
+  if (m->graph) cudaGraphDestroy(m->graph);
   if (m->cs2) cudaStreamDestroy(m->cs2);
   if (m->ev_fork) cudaEventDestroy(m->ev_fork);
   if (m->ev_joinw) cudaEventDestroy(m->ev_joinw);
@@ -799,6 +806,13 @@ extern "C" dc_status dc_model_profile_json(const dc_model* mc, char* buf, size_t
   return DC_OK;
 }
 
+// per-op timing event: inside a graph capture an external event-record node,
+// so every replay records it (the timed replays keep their per-op breakdown)
+static void prof_rec(dc_model* m, cudaEvent_t ev, cudaStream_t st) {
+  if (m->capturing) cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+  else cudaEventRecord(ev, st);
+}
+
 extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile, cudaStream_t ucs, cudaStream_t ags,
                                    cudaStream_t rss, cudaStream_t cps) {
   if (!m || !m->act) return mfail(m, DC_ESTATE, "dc_model_step: model not bound");
@@ -847,6 +861,10 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
   }
   dc_status s = dc_step_begin(m->ctx, ++m->epoch, ucs);
   if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
+  // graph mode: this step's Adam scalars go to device memory (a captured step
+  // leaves this to dc_model_graph_launch, which writes them before each replay)
+  if (ctx_graph_mode(m->ctx) && !m->capturing && (s = ctx_set_step_scalars(m->ctx, step_t, ucs)) != DC_OK)
+    return mfail(m, s, dc_last_error(m->ctx));
   // streams must not run ahead of the previous step's tail on the compute stream
   cudaEventRecord(m->ev_join[0], ucs);
   if (cs != ucs) cudaStreamWaitEvent(cs, m->ev_join[0], 0);
@@ -885,9 +903,9 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
           s = dc_grad_slot_acquire(m->ctx, o.layer, cs);
           if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
         }
-        if (profile) cudaEventRecord(m->ev_t0[id], cs);
+        if (profile) prof_rec(m, m->ev_t0[id], cs);
         s = run_op(m, o, cs);
-        if (profile) cudaEventRecord(m->ev_t1[id], cs);
+        if (profile) prof_rec(m, m->ev_t1[id], cs);
         break;
       }
       case K_RS: {
@@ -906,7 +924,7 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
           }
           if (s != DC_OK) break;
         }
-        if (profile) cudaEventRecord(m->ev_t0[id], rss);
+        if (profile) prof_rec(m, m->ev_t0[id], rss);
         if (m->fused_active)   // the weights were updated in their dW epilogues; the norm gains remain
           s = reduce_scatter_params(m->ctx, o.layer, step_t, o.micro, {m->pid(o.layer, P_G1), m->pid(o.layer, P_G2)},
                                     rss);
@@ -917,7 +935,7 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
           m->pending_mnk = 0;
         } else
           s = dc_reduce_scatter_step(m->ctx, o.layer, step_t, o.micro, rss);
-        if (profile) cudaEventRecord(m->ev_t1[id], rss);
+        if (profile) prof_rec(m, m->ev_t1[id], rss);
         if (s == DC_OK && m->host_states && !m->wb_frags[o.layer].empty()) {
           // reading D28: the updated host-resident fragments go straight back
           cudaEventRecord(m->ev_done[id], rss);
@@ -1220,6 +1238,52 @@ extern "C" dc_status dc_model_bind_host_states(dc_model* m, float* m_dev, float*
   s = ctx_bind_host_states(m->ctx, m_dev, hp.m_first, v_dev, hp.v_first, slot, host_pinned, host_bytes);
   if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
   m->host_states = need > 0;
+  return DC_OK;
+}
+
+// ------------------------------------------------------------------ CUDA graph of a step (N = 1)
+extern "C" dc_status dc_model_graph_capture(dc_model* m, int32_t step_t, cudaStream_t ucs, cudaStream_t ags,
+                                            cudaStream_t rss, cudaStream_t cps) {
+  if (!m || !m->act) return mfail(m, DC_ESTATE, "dc_model_graph_capture: model not bound");
+  if (!ctx_graph_mode(m->ctx)) return mfail(m, DC_ESTATE, "dc_model_graph_capture: set dc_set_option(graph_mode) first");
+  const dc_schedule* sc = ctx_sched(m->ctx);
+  if (!sc) return mfail(m, DC_ESTATE, "dc_model_graph_capture: no schedule bound");
+  for (int i = 0, n = sched_num_ops(sc); i < n; ++i) {
+    int kind, id, nm, np, nw;
+    const int64_t* mem; const int* posts; const int* waits;
+    int64_t off, bytes;
+    sched_op(sc, i, &kind, &id, &mem, &nm, &off, &bytes, &posts, &np, &waits, &nw);
+    if (kind >= K_OFF) return mfail(m, DC_EINVAL, "dc_model_graph_capture: offload schedules are not captured");
+  }
+  if (m->host_states || m->side_adam || m->fused_adam || m->comm_sms > 0)
+    return mfail(m, DC_EINVAL, "dc_model_graph_capture: host states / side / fused Adam / SM partition unsupported");
+  if (m->graph_exec) { cudaGraphExecDestroy(m->graph_exec); m->graph_exec = nullptr; }
+  if (m->graph) { cudaGraphDestroy(m->graph); m->graph = nullptr; }
+  if (cudaStreamBeginCapture(ucs, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return mfail(m, DC_ECUDA, "dc_model_graph_capture: begin capture failed");
+  m->capturing = true;
+  dc_status s = dc_model_step(m, step_t, 2, ucs, ags, rss, cps);   // with per-op event nodes
+  m->capturing = false;
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(ucs, &g);
+  if (s != DC_OK) { if (g) cudaGraphDestroy(g); return s; }
+  if (e != cudaSuccess || !g) return mfail(m, DC_ECUDA, std::string("dc_model_graph_capture: ") + cudaGetErrorString(e));
+  if (cudaGraphInstantiate(&m->graph_exec, g, 0) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return mfail(m, DC_ECUDA, "dc_model_graph_capture: instantiate failed");
+  }
+  m->graph = g;
+  return DC_OK;
+}
+
+extern "C" dc_status dc_model_graph_launch(dc_model* m, int32_t step_t, cudaStream_t ucs) {
+  if (!m || !m->graph_exec) return mfail(m, DC_ESTATE, "dc_model_graph_launch: no captured graph");
+  if (step_t < 1) return mfail(m, DC_EINVAL, "dc_model_graph_launch: step_t is 1-based");
+  dc_status s = dc_poll(m->ctx);
+  if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
+  if ((s = ctx_set_step_scalars(m->ctx, step_t, ucs)) != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
+  if (cudaGraphLaunch(m->graph_exec, ucs) != cudaSuccess) return mfail(m, DC_ECUDA, "dc_model_graph_launch: launch failed");
+  m->profile_pending = true;          // the replay re-recorded the per-op events
   return DC_OK;
 }
 

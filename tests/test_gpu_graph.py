@@ -1,0 +1,86 @@
+"""CUDA-graph capture of the scheduled step (SURVEY §8 f-4, N = 1): in graph
+mode every step restarts the grad-slot / reduce-scatter counters and flags and
+reads its Adam scalars from device memory, so one captured step replays for
+every later step.  Replays are bit-identical to eager steps."""
+import json
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import step as ost
+from tests.gpu_util import bf16_tensor
+
+pytestmark = pytest.mark.gpu
+
+dc = pytest.importorskip("paper_2504_09983_b200.dc")
+from paper_2504_09983_b200 import runtime as rt  # noqa: E402
+
+LR = 1e-3
+
+
+def _make(cfg, graph_mode, micro=1, ck=False):
+    table = synth.param_table(cfg)
+    ranks = rt.create_ranks(table, 1, lr=LR, micro_steps=micro)
+    st = ranks[0]
+    xs, ts = zip(*[ost.rank_batch(cfg, 0, mu) for mu in range(micro)])
+    x = bf16_tensor(np.concatenate(xs)).view(micro, cfg.tokens, cfg.hidden)
+    t = bf16_tensor(np.concatenate(ts)).view(micro, cfg.tokens, cfg.hidden)
+    rt.attach_model(ranks, cfg, {0: x}, {0: t}, checkpoint=ck)
+    if graph_mode:
+        dc.check(dc.lib.dc_set_option(st.ctx, b"graph_mode", 1), st.ctx)
+    prof = rt.profile_json(st)
+    sched = dc.plan(json.dumps(prof), 1 << 40, passes=dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD,
+                    strict=True)
+    rt.bind(ranks, {0: sched})
+    return ranks, st
+
+
+def _same(a, b):
+    for k in ("master", "m", "v", "shard"):
+        dt = torch.int16 if k == "shard" else torch.int32
+        assert torch.equal(a.tensors[k].view(dt), b.tensors[k].view(dt)), k
+    la = rt.view(rt.loss_ptr(a), 1, torch.float32).item()
+    lb = rt.view(rt.loss_ptr(b), 1, torch.float32).item()
+    assert la == lb
+
+
+@pytest.mark.parametrize("moe,micro,ck", [(False, 1, False), (True, 1, False), (False, 2, True)])
+def test_graph_replay_bitexact(moe, micro, ck):
+    """Llama, Mixtral, and gradient accumulation (2 micro-steps) with layer
+    recompute; replays also record the per-op timing events."""
+    cfg = synth.small_mixtral(layers=2, seq=128) if moe else synth.small_llama(layers=2, seq=256)
+    ref, rst = _make(cfg, False, micro, ck)
+    for t in (1, 2, 3, 4):
+        rt.step(ref, t)
+    torch.cuda.synchronize()
+    # eager steps in graph mode (counter / flag reset every step) == normal steps
+    eg, est = _make(cfg, True, micro, ck)
+    for t in (1, 2, 3, 4):
+        rt.step(eg, t)
+    torch.cuda.synchronize()
+    _same(rst, est)
+    # one eager step, capture (does not execute), then replays for steps 2..4
+    gr, gst = _make(cfg, True, micro, ck)
+    rt.step(gr, 1)
+    torch.cuda.synchronize()
+    cs = gst.stream_handles()
+    dc.check(dc.lib.dc_model_graph_capture(gst.model, 2, *cs), gst.ctx)
+    for t in (2, 3, 4):
+        dc.check(dc.lib.dc_model_graph_launch(gst.model, t, cs[0]), gst.ctx)
+    torch.cuda.synchronize()
+    rt.poll(gr)
+    _same(rst, gst)
+    prof = json.loads(dc.model_profile_json(gst.model))       # events of the last replay
+    assert all(o["dur_us"] > 0 for o in prof["ops"] if o["kind"] == "compute")
+
+
+def test_graph_mode_errors():
+    cfg = synth.small_llama(layers=1, seq=128)
+    ranks, st = _make(cfg, False)
+    cs = st.stream_handles()
+    assert dc.lib.dc_model_graph_capture(st.model, 1, *cs) == dc.DC_ESTATE     # graph_mode not set
+    assert dc.lib.dc_model_graph_launch(st.model, 1, cs[0]) == dc.DC_ESTATE    # nothing captured
+    two = rt.create_ranks(synth.param_table(cfg), 2)
+    assert dc.lib.dc_set_option(two[0].ctx, b"graph_mode", 1) == dc.DC_EINVAL  # N == 1 only
