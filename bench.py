@@ -507,7 +507,7 @@ def main():
     # compute-stream order: the GEMMs' own throughput without rs_adam holding
     # SMs (in the overlapped timed step a GEMM launched while rs_adam runs waits
     # for its CTAs, and that wait is inside the GEMM op's events)
-    ov = int(os.environ.get("DC_RS_OVERLAP", "1"))
+    ov = int(os.environ.get("DC_RS_OVERLAP", "1" if world > 1 else "0"))
     dc.check(dc.lib.dc_model_set_option(st.model, b"rs_overlap", 0))
     step_no += 1
     rt.step(ranks, step_no, profile=1)

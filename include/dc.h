@@ -334,7 +334,7 @@ dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t which, void
  * layer 0's update stays an rs_adam launch.  Same offload exclusion.
  * "stream_k" (default 1 unless N > 1 virtual ranks share the GPU): the layer
  * GEMMs split their last waves with stream-K (dc_gemm_args.stream_k).
- * "rs_overlap" (default 1): reduce-scatter + Adam on the rs stream beside the
+ * "rs_overlap" (default 1 at N > 1, 0 at N = 1): reduce-scatter + Adam on the rs stream beside the
  * backward GEMMs; 0 runs it in compute-stream order. */
 dc_status dc_model_set_option(dc_model* m, const char* key, int64_t value);
 /* Host-resident optimizer states (reading D28; §4.4 P:370-408 with

@@ -238,10 +238,13 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   // virtual ranks run their persistent GEMMs concurrently on one GPU: a
   // stream-K tail could then wait on a pair that cannot become resident
   m->stream_k = !((ctx_flags(ctx) & DC_VIRTUAL_RANKS) && ctx_world(ctx) > 1);
-  // RS + Adam beside the backward GEMMs.  At N = 1 it is a local HBM-bound
-  // pass that mostly trades SMs and clock with the power-capped GEMMs, but the
-  // overlap still measured 1-1.5 % faster than stream order (profiles/r01d)
-  m->rs_overlap = 1;
+  // RS + Adam beside the backward GEMMs at N > 1, where the reduce-scatter is
+  // NVLink-bound and must hide behind compute.  At N = 1 it is a local
+  // HBM-bound pass that only trades SMs and clock with the power-capped GEMMs:
+  // in compute-stream order the step is as fast (graph replay: 185.8-186.2 vs
+  // 185.5-186.5 ms, profiles/r01g/rs_order_ab.md) and no GEMM waits for SMs
+  // held by an rs_adam, so stream order is the N = 1 default
+  m->rs_overlap = ctx_world(ctx) > 1 ? 1 : 0;
   const Layout& L = ctx_layout(ctx);
   if (d->layers != L.n_layers) return mfail(nullptr, DC_EINVAL, "dc_model_create: layer count mismatch");
   if (d->n_heads % d->n_kv) return mfail(nullptr, DC_EINVAL, "dc_model_create: n_heads % n_kv != 0");

@@ -87,7 +87,7 @@ def _alloc_symmetric(nbytes, group, device):
 
 
 def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr=1e-3, beta1=0.9,
-                 beta2=0.999, eps=1e-8, seed=0, init=True, host_pinned_bytes=0, spin_ms=20000, extra_flags=0,
+                 beta2=0.999, eps=1e-8, seed=0, init=True, host_pinned_bytes=0, spin_ms=None, extra_flags=0,
                  micro_steps=1, defer_states=False):
     """Allocate and dc_init the ranks this process drives: all N virtual ranks,
     or this process's rank when `virtual` is False.  micro_steps > 1: gradient
@@ -95,6 +95,8 @@ def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr
     m / v are not allocated here; bind_host_states() sizes them from the plan
     (host-resident offload, reading D28)."""
     dev = torch.device("cuda", device)
+    if spin_ms is None:                      # device flag-wait bound (ms)
+        spin_ms = int(os.environ.get("DC_SPIN_MS", "20000"))
     numel, layer_of, init_k = table_arrays(table)
     mops = max_s0_ops(table, micro_steps)
     la = dc.LayoutArgs(world, len(table), dc.i64_array(numel), dc.i32_array(layer_of), mops)
