@@ -603,7 +603,9 @@ def main():
     # exposed communication (SURVEY §8 d): the compute stream's idle time in the
     # last timed step = step time - sum of compute-op events (each op's start
     # event is recorded after its waits on gathers / grad-slot flags)
-    busy_ms = sum(o["dur_us"] for o in last["ops"] if o["kind"] == "compute") / 1e3
+    rs_in_order = int(os.environ.get("DC_RS_OVERLAP", "1" if world > 1 else "0")) == 0
+    busy_ms = sum(o["dur_us"] for o in last["ops"]
+                  if o["kind"] == "compute" or (rs_in_order and o["kind"] == "rs")) / 1e3
     # peak memory (SURVEY §8 d): every device buffer of the run is a torch
     # allocation (states, grad slots, flags, arena, activations, pool), so the
     # allocator's peak is the device total; the plan's own bound beside it
@@ -615,7 +617,8 @@ def main():
         mem["offload_pool"] = offload_info["pool_bytes"]
     exposed = {"ms": max(0.0, ms - busy_ms), "frac": max(0.0, ms - busy_ms) / ms,
                "note": "step time - compute-stream busy time of the last timed step (waits on gathers, "
-                       "grad-slot / reduce-scatter flags and launch gaps); target < 10 % at N > 1"}
+                       "grad-slot / reduce-scatter flags and launch gaps; reduce-scatter ops count as busy when "
+                       "they run in compute-stream order); target < 10 % at N > 1"}
     coll = None
     if world > 1:
         # per issued gather of the last timed step: transfer time (every receiver
