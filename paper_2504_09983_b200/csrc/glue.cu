@@ -291,10 +291,97 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_dx_kernel(const bf16* __restr
   for (int i = 0; i < 8; ++i) dgp[(int64_t)blockIdx.x * H + c + i] = acc[i];
 }
 
+// Single pass, warp per row (default for H = 256 NCH <= 4096): the row's dh
+// and x stay in registers (bf16) between the dot and the dx pass, so each byte
+// is read once; dg partials accumulate per warp in shared memory (each lane
+// owns its columns: no atomics), then the 8 warps' rows are added in order.
+template <int NCH>
+__global__ void __launch_bounds__(256, 1) rmsnorm_bwd_row_kernel(const bf16* __restrict__ dh,
+                                                                const bf16* __restrict__ x,
+                                                                const bf16* __restrict__ g,
+                                                                const float* __restrict__ rstd,
+                                                                const bf16* __restrict__ dres, bf16* __restrict__ dx,
+                                                                float* __restrict__ dgp, int T, int H) {
+  extern __shared__ float wacc[];                      // [8 warps][H]
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float* acc = wacc + (int64_t)w * H;
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    float4* a4 = reinterpret_cast<float4*>(acc + lane * 8 + k * 256);
+    a4[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    a4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int r0 = blockIdx.x * RB_ROWS, r1 = min(T, r0 + RB_ROWS);
+  for (int row = r0 + w; row < r1; row += 8) {
+    const bf16* dhr = dh + (int64_t)row * H;
+    const bf16* xr = x + (int64_t)row * H;
+    const float rs = rstd[row];
+    float s = 0.0f;
+#pragma unroll 4
+    for (int k = 0; k < NCH; ++k) {        // pass 1: the row's dot (first read of dh, x)
+      float a[8], n[8], gg[8];
+      load8(dhr + lane * 8 + k * 256, a);
+      load8(xr + lane * 8 + k * 256, n);
+      load8(g + lane * 8 + k * 256, gg);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s = fmaf(a[i] * gg[i], n[i] * rs, s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float dm = s / (float)H;
+#pragma unroll 4
+    for (int k = 0; k < NCH; ++k) {        // pass 2: dx and dg (the row is re-read from L1 / L2)
+      const int c = lane * 8 + k * 256;
+      float a[8], n[8], gg[8], d[8];
+      load8(dhr + c, a);
+      load8(xr + c, n);
+      load8(g + c, gg);
+      if (dres) load8(dres + (int64_t)row * H + c, d);
+      float4* a4 = reinterpret_cast<float4*>(acc + c);     // 16-byte smem accesses: no bank conflicts
+      float4 q0 = a4[0], q1 = a4[1];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        n[i] = n[i] * rs;
+        d[i] = (dres ? d[i] : 0.0f) + rs * (a[i] * gg[i] - n[i] * dm);
+      }
+      q0.x += a[0] * n[0]; q0.y += a[1] * n[1]; q0.z += a[2] * n[2]; q0.w += a[3] * n[3];
+      q1.x += a[4] * n[4]; q1.y += a[5] * n[5]; q1.z += a[6] * n[6]; q1.w += a[7] * n[7];
+      a4[0] = q0;
+      a4[1] = q1;
+      store8(dx + (int64_t)row * H + c, d);
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < H; c += 256) {
+    float t = 0.0f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += wacc[q * H + c];
+    dgp[(int64_t)blockIdx.x * H + c] = t;
+  }
+}
+
 void k_rmsnorm_bwd(const void* dh, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
                    float* dg_partial, int T, int H, cudaStream_t st) {
-  static const bool one_pass = getenv("DC_RMSNORM_BWD_1PASS") && atoi(getenv("DC_RMSNORM_BWD_1PASS"));
-  if (!one_pass) {
+  static const int form = getenv("DC_RMSNORM_BWD") ? atoi(getenv("DC_RMSNORM_BWD")) : 0;   // A/B: 1 one-pass CTA, 2 two-pass
+  if (form == 0 && H % 256 == 0 && H <= 4096) {
+    const size_t smem = (size_t)8 * H * 4;
+#define DC_RR(NCH_)                                                                                \
+    rmsnorm_bwd_row_kernel<NCH_><<<rmsnorm_bwd_blocks(T), 256, smem, st>>>(                         \
+        (const bf16*)dh, (const bf16*)x, (const bf16*)g, rstd, (const bf16*)dres, (bf16*)dx, dg_partial, T, H)
+    switch (H / 256) {
+      case 1: DC_RR(1); break;
+      case 2: DC_RR(2); break;
+      case 4: DC_RR(4); break;
+      case 8: DC_RR(8); break;
+      case 16: DC_RR(16); break;
+      default: goto two_pass;
+    }
+#undef DC_RR
+    count_launch();
+    return;
+  }
+two_pass:
+  if (form != 1) {
     float* dot = dg_partial + (int64_t)rmsnorm_bwd_blocks(T) * H;    // T floats of scratch after the partials
     rmsnorm_bwd_dot_kernel<<<(T + RD_WARPS - 1) / RD_WARPS, RD_WARPS * 32, 0, st>>>(
         (const bf16*)dh, (const bf16*)x, (const bf16*)g, rstd, dot, T, H);
@@ -512,11 +599,22 @@ cudaError_t preload_glue_kernels() {
                        (const void*)rmsnorm_bwd_kernel<3>, (const void*)rmsnorm_bwd_kernel<4>, (const void*)colsum_kernel,
                        (const void*)rmsnorm_bwd_dot_kernel, (const void*)rmsnorm_bwd_dx_kernel,
                        (const void*)rmsnorm_fwd_warp_kernel,
+                       (const void*)rmsnorm_bwd_row_kernel<1>, (const void*)rmsnorm_bwd_row_kernel<2>,
+                       (const void*)rmsnorm_bwd_row_kernel<4>, (const void*)rmsnorm_bwd_row_kernel<8>,
+                       (const void*)rmsnorm_bwd_row_kernel<16>,
                        (const void*)attn_mix_fwd_kernel, (const void*)attn_mix_bwd_kernel,
                        (const void*)act_fwd_kernel, (const void*)act_bwd_kernel,
                        (const void*)loss_kernel, (const void*)loss_final_kernel};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  const void* rows[] = {(const void*)rmsnorm_bwd_row_kernel<1>, (const void*)rmsnorm_bwd_row_kernel<2>,
+                        (const void*)rmsnorm_bwd_row_kernel<4>, (const void*)rmsnorm_bwd_row_kernel<8>,
+                        (const void*)rmsnorm_bwd_row_kernel<16>};
+  const int nch[] = {1, 2, 4, 8, 16};
+  for (int i = 0; i < 5; ++i) {
+    cudaError_t e = cudaFuncSetAttribute(rows[i], cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * nch[i] * 256 * 4);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
