@@ -488,3 +488,70 @@ def test_exhaustive_tiny_regions_strict_safe():
         assert plan["peak_no_opt"] <= M                              # strict safety
         if not best_ok:
             assert all(slot[p] == first_use[p] for p in B)           # nothing safe to move
+
+
+def test_reload_host_states_brute_force():
+    """Reading D28 on random multi-layer profiles without gathers (so an op's
+    memory is its P_mem + transient): for every reload placed without the
+    synchronous fallback, (1) every backward op from the reload to its layer's
+    RS fits, counting the resident state and every placed reload live there
+    (a reload lives from its op to its RS), and (2) it is the earliest such
+    op: one backward op earlier (when allowed) breaks the bound."""
+    rng = random.Random(5)
+    checked = 0
+    for it in range(150):
+        L = rng.randint(2, 4)
+        comp = [("f%d" % l, "compute", "fwd", 0, l, []) for l in range(L)]
+        for l in reversed(range(L)):
+            comp += [("b%d_%d" % (l, j), "compute", "bwd", 0, l, []) for j in range(rng.randint(1, 3))]
+            comp.append(("rs%d" % l, "rs", "bwd", 0, l, []))
+        pm = {}
+        for i, c in enumerate(comp):
+            pm[i] = rng.randint(10, 60) if c[2] == "fwd" else rng.randint(5, 60)
+        frags = [dict(id=2 * l + s, layer=l, bytes=rng.randint(5, 20)) for l in range(L) for s in range(2)]
+        prof = make_profile(comp, {}, pm, frags=frags)
+        M_opt = sum(f["bytes"] for f in frags)
+        M = max(pm.values()) + rng.randint(0, M_opt)
+        try:
+            plan = osd.plan(prof, M, passes=PSO | osd.PASS_HOST_STATES)
+        except osd.Infeasible:
+            continue
+        off = plan["offload"]
+        if not off:
+            continue
+        fb = {f["id"]: f["bytes"] for f in frags}
+        fl = {f["id"]: f["layer"] for f in frags}
+        resident = M_opt - sum(fb[i] for i in off)
+        ops = plan["ops"]
+        # positions of compute-like ops in time order, and where each reload is issued
+        pos, reload_at, rs_at = [], {}, {}
+        pending = []
+        for o in ops:
+            if o["kind"] == "reload":
+                pending.append(o["members"][0])
+            elif o["kind"] in ("compute", "rs"):
+                k = len(pos)
+                pos.append(o["id"])
+                for f in pending:
+                    reload_at[f] = k
+                pending = []
+                if o["kind"] == "rs":
+                    rs_at[prof["ops"][o["id"]]["layer"]] = k
+        need = [prof["ops"][i]["p_mem"] + prof["ops"][i]["transient"] for i in pos]
+        first_bwd = next(k for k, i in enumerate(pos) if prof["ops"][i]["phase"] == "bwd")
+        fallback = {int(w.split("=")[1]) for w in plan["warnings"]}
+
+        order = list(reversed(off))                     # reloads placed in this order
+        for idx, f in enumerate(order):
+            if f in fallback:
+                continue
+            lo, hi = reload_at[f], rs_at[fl[f]]
+            placed = set(order[:idx])                   # reloads placed before f
+            live_before = lambda k: sum(fb[g] for g in placed if reload_at[g] <= k <= rs_at[fl[g]])
+            for k in range(lo, hi + 1):
+                assert need[k] + resident + live_before(k) + fb[f] <= M, (it, f, k)
+            prev = max([reload_at[g] for g in placed] + [first_bwd])
+            if lo - 1 >= prev:
+                assert any(need[k] + resident + live_before(k) + fb[f] > M for k in range(lo - 1, hi + 1)), (it, f)
+            checked += 1
+    assert checked > 100
