@@ -58,9 +58,11 @@ def parse():
                     help="the paper's comparison point for --offload (P:504-506): every optimizer-state fragment "
                          "host-resident, reloaded synchronously before its layer's update")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-graph", action="store_true",
-                    help="N = 1 runs capture one planned step as a CUDA graph (dc_model_graph_capture) and replay "
-                         "it in the timed and e2e loops (dc_model_graph_launch); this flag keeps eager steps")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="capture one planned step as a CUDA graph (dc_model_graph_capture) and replay it in the "
+                         "timed and e2e loops (dc_model_graph_launch); auto = at N = 1 (measured there), on = at "
+                         "any N (per-step device barrier + flag reset)")
+    ap.add_argument("--no-graph", action="store_true", help="same as --graph off")
     ap.add_argument("--share-gpu", action="store_true",
                     help="test mode: every rank on cuda:0 (gloo host collectives, CUDA-IPC peer maps, fixed T_c); "
                          "exercises the N > 1 launch on a one-GPU box, numbers are not a bench value")
@@ -302,7 +304,8 @@ def main():
     args = parse()
     if args.offload_sync:
         args.offload = True
-    args.graph = args.gpus == 1 and not args.offload and not args.no_graph
+    args.graph = not args.offload and not args.no_graph and args.graph != "off" and \
+        (args.graph == "on" or args.gpus == 1)
     if args.impl == "reference":
         run_reference(args)
         return

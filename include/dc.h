@@ -180,8 +180,8 @@ dc_status dc_step_begin(dc_ctx* ctx, int32_t epoch, cudaStream_t compute_stream)
  * ------------------------------------------------------------------------ */
 dc_status dc_gather(dc_ctx* ctx, int32_t gather_id, cudaStream_t ag_stream, cudaEvent_t done_evt);
 /* Unsharded tensor of param (row-major, numel elements; padding follows). */
-/* Context options.  "graph_mode" (N = 1 only, default 0): see
- * dc_model_graph_capture.  "ag_copy_engine" (default 0): 1 issues every gather's
+/* Context options.  "graph_mode" (default 0; before dc_bind_schedule, else
+ * DC_ESTATE): see dc_model_graph_capture.  "ag_copy_engine" (default 0): 1 issues every gather's
  * stores as cudaMemcpyAsync peer copies (copy engines; no SM time beside the
  * GEMMs) under the same ready / done flag protocol; bit-identical
  * gathered buffers.  Set before dc_bind_schedule (DC_ESTATE after). */
@@ -360,12 +360,15 @@ dc_status dc_model_host_states_query(dc_model* m, int64_t* m_first, int64_t* v_f
                                      uint64_t* host_bytes);
 dc_status dc_model_bind_host_states(dc_model* m, float* m_dev, float* v_dev, void* pool, uint64_t pool_bytes,
                                     void* host_pinned, uint64_t host_bytes);
-/* CUDA graph of the scheduled step (N = 1, context option
- * "graph_mode" set, no offload / host states / side or fused Adam / SM
- * partition).  In graph mode every step restarts the grad-slot and
- * reduce-scatter counters and their flags from zero (the previous step's
- * streams have joined) and rs_adam reads the step's Adam scalars from device
- * memory, so one captured step is valid for every later step.
+/* CUDA graph of the scheduled step (context option
+ * "graph_mode" set before dc_bind_schedule; no offload / host states / side or
+ * fused Adam / SM partition).  In graph mode every step restarts the whole
+ * flag protocol (gather ready / done, grad-slot and reduce-scatter counters,
+ * stream-K flags) from zero — at N > 1 between two rounds of a barrier on a
+ * device step counter (A: every rank finished the previous step; B: every
+ * rank cleared its table) — and rs_adam reads the step's Adam scalars from
+ * device memory, so one captured step is valid for every later step.  Each
+ * rank (process or virtual rank) captures and replays its own graph.
  * capture: records one dc_model_step on `compute` (the other streams fork from
  *   and join it) into a graph WITHOUT executing it; step_t only has to be >= 1.
  * launch: writes step_t's Adam scalars (same host arithmetic as the eager path)

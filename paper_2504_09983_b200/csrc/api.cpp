@@ -58,7 +58,9 @@ static dc_status make_layout(int world, int n, const int64_t* numel, const int32
   L->f_gcons = L->f_gready + 2 * world;
   L->f_rsdone = L->f_gcons + 2 * world;
   L->f_scal = L->f_rsdone + 1;
-  L->flag_words = L->f_scal + 2;
+  L->f_dep = L->f_scal + 2;
+  L->f_bar = L->f_dep + 1;
+  L->flag_words = L->f_bar + 2 * world;
   return DC_OK;
 }
 
@@ -315,12 +317,28 @@ extern "C" dc_status dc_step_begin(dc_ctx* c, int32_t epoch, cudaStream_t st) {
   if ((uint32_t)epoch <= c->epoch) return fail(c, DC_EINVAL, "dc_step_begin: epochs must increase");
   c->epoch = (uint32_t)epoch;
   ++c->fepoch;
-  if (c->graph_mode) {     // N = 1: the previous step is complete (its streams joined this one)
+  if (c->graph_mode) {
+    // every step restarts its flag protocol from zero, so one captured step is
+    // valid for all (the previous step's streams joined `st`).  N > 1: a
+    // two-round barrier on a device step counter brackets the reset — round A:
+    // every rank finished the previous step (no post of it still in flight);
+    // round B: every rank zeroed its table (no post of this step lands early)
+    uint32_t* dep = c->myflag(c->L.f_dep);
+    if (c->world > 1) {
+      k_inc_dev(dep, st);
+      k_post_dev(peers_at(c, c->L.f_bar + c->rank), dep, st);
+      k_wait_dev(c->myflag(c->L.f_bar), c->world, dep, c->timeout_ns, c->err_dev, st);
+    }
+    c->fepoch = 1;
     c->slot_use[0] = c->slot_use[1] = 0;
     std::fill(c->layer_use.begin(), c->layer_use.end(), 0);
     c->rs_done_total = 0;
-    DC_CUDA_TRY(cudaMemsetAsync(c->myflag(c->L.f_gready), 0, (c->L.f_scal - c->L.f_gready) * 4, st), &c->err);
+    DC_CUDA_TRY(cudaMemsetAsync(c->myflag(0), 0, c->L.f_scal * 4, st), &c->err);
     gemm_sk_reset(st);
+    if (c->world > 1) {
+      k_post_dev(peers_at(c, c->L.f_bar + c->world + c->rank), dep, st);
+      k_wait_dev(c->myflag(c->L.f_bar + c->world), c->world, dep, c->timeout_ns, c->err_dev, st);
+    }
   }
   if (c->world == 1) return DC_OK;
   // ready flags for gathers without an in-step predecessor release (D26):
@@ -368,7 +386,7 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
                     c->fepoch, peers_at(c, c->L.f_done + gid), c->myflag(c->L.f_done + gid), target, ctas,
                     c->timeout_ns, c->err_dev, st, c->gt_start);
     if (s != DC_OK) return fail(c, s, "dc_gather: launch failed");
-    if (c->gt_end) DC_CUDA_TRY(cudaEventRecord(c->gt_end, st), &c->err);
+    if (c->gt_end) record_event(c->gt_end, st);
   }
   c->gt_start = c->gt_end = nullptr;
   if (done_evt) DC_CUDA_TRY(cudaEventRecord(done_evt, st), &c->err);
@@ -378,7 +396,7 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
 extern "C" dc_status dc_set_option(dc_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(c, DC_EINVAL, "dc_set_option: null argument");
   if (!strcmp(key, "graph_mode")) {
-    if (value && c->world != 1) return fail(c, DC_EINVAL, "dc_set_option: graph_mode needs N == 1");
+    if (c->sched) return fail(c, DC_ESTATE, "dc_set_option: graph_mode must be set before dc_bind_schedule");
     c->graph_mode = value != 0;
     return DC_OK;
   }

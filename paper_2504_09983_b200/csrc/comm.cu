@@ -110,7 +110,7 @@ dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const
                     cudaEvent_t ev_after_ready) {
   wait_flags_kernel<<<1, 1, 0, st>>>(ready_local, world, epoch, timeout_ns, err_flag, 0x100u);
   count_launch();
-  if (ev_after_ready) cudaEventRecord(ev_after_ready, st);
+  if (ev_after_ready) record_event(ev_after_ready, st);
   // members beyond AG_MAXM go to extra launches
   for (size_t b = 0; b < mem.size(); b += AG_MAXM) {
     AgParams p{};
@@ -326,6 +326,7 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
   return DC_OK;
 }
 
+struct PeerFlagsArg { uint32_t* p[MAXW]; int n; };
 __global__ void set_scalars_kernel(float* dst, float s, float c) {
   dst[0] = s;
   dst[1] = c;
@@ -333,6 +334,41 @@ __global__ void set_scalars_kernel(float* dst, float s, float c) {
 void k_set_scalars(float* dst, float s, float c, cudaStream_t st) {
   set_scalars_kernel<<<1, 1, 0, st>>>(dst, s, c);
   count_launch();
+}
+
+__global__ void inc_dev_kernel(uint32_t* dep) { *dep += 1u; }
+__global__ void post_dev_kernel(const PeerFlagsArg d, const uint32_t* dep) {
+  const uint32_t v = *reinterpret_cast<const volatile uint32_t*>(dep);
+  __threadfence_system();
+  for (int i = 0; i < d.n; ++i) ptx::st_release_sys(d.p[i], v);
+}
+__global__ void wait_dev_kernel(const uint32_t* f, int n, const uint32_t* dep, uint64_t tmo, uint32_t* err) {
+  const uint32_t target = *reinterpret_cast<const volatile uint32_t*>(dep);
+  const uint64_t t0 = ptx::globaltimer();
+  for (int i = 0; i < n; ++i)
+    if (!spin_ge(f + i, target, t0, tmo, err, 0x500u | i)) return;
+}
+void k_inc_dev(uint32_t* dep, cudaStream_t st) {
+  inc_dev_kernel<<<1, 1, 0, st>>>(dep);
+  count_launch();
+}
+void k_post_dev(PeerFlags dst, const uint32_t* dep, cudaStream_t st) {
+  PeerFlagsArg a{};
+  a.n = dst.n;
+  for (int i = 0; i < dst.n; ++i) a.p[i] = dst.p[i];
+  post_dev_kernel<<<1, 1, 0, st>>>(a, dep);
+  count_launch();
+}
+void k_wait_dev(const uint32_t* flags, int n, const uint32_t* dep, uint64_t timeout_ns, uint32_t* err_flag,
+                cudaStream_t st) {
+  wait_dev_kernel<<<1, 1, 0, st>>>(flags, n, dep, timeout_ns, err_flag);
+  count_launch();
+}
+void record_event(cudaEvent_t ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+  else cudaEventRecord(ev, st);
 }
 
 // ------------------------------------------------------------------ flags
@@ -354,7 +390,7 @@ dc_status k_ag_copy(const std::vector<AgMember>& mem, int world, const uint64_t*
                     cudaEvent_t ev_after_ready) {
   wait_flags_kernel<<<1, 1, 0, st>>>(ready_local, world, epoch, timeout_ns, err_flag, 0x100u);
   count_launch();
-  if (ev_after_ready) cudaEventRecord(ev_after_ready, st);
+  if (ev_after_ready) record_event(ev_after_ready, st);
   for (const AgMember& a : mem)
     for (int q = 0; q < world; ++q)
       if (cudaMemcpyAsync(reinterpret_cast<uint8_t*>(arena_peers[q]) + a.dst_off_bytes, a.src, a.bytes,
@@ -414,6 +450,9 @@ cudaError_t preload_comm_kernels() {
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, post_flags_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, add_flags_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, set_scalars_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, inc_dev_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, post_dev_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, wait_dev_kernel);
   return e;
 }
 }  // namespace dc

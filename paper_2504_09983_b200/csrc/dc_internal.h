@@ -33,6 +33,8 @@ struct Layout {
   // flag table (uint32 words)
   int64_t f_ready = 0, f_done = 0, f_gready = 0, f_gcons = 0, f_rsdone = 0;
   int64_t f_scal = 0;   // 2 words: this step's Adam scalars (s, c) as fp32 (graph mode)
+  int64_t f_dep = 0;    // graph mode: device step counter (local, monotone)
+  int64_t f_bar = 0;    // graph mode: 2 x world barrier words (rounds A, B; one per source rank)
 };
 
 struct dc_ctx_fwd;
@@ -165,6 +167,14 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
 // graph mode: write (s, c) of a step into the flag-table words the rs_adam
 // launches read, and reset a stream's stream-K flags / epochs
 void k_set_scalars(float* dst, float s, float c, cudaStream_t st);
+// device-epoch barrier pieces (graph mode at N > 1): ++*dep; peers' word = *dep;
+// wait until every word of mine >= *dep
+void k_inc_dev(uint32_t* dep, cudaStream_t st);
+void k_post_dev(PeerFlags dst, const uint32_t* dep, cudaStream_t st);
+void k_wait_dev(const uint32_t* flags, int n, const uint32_t* dep, uint64_t timeout_ns, uint32_t* err_flag,
+                cudaStream_t st);
+// event record that survives CUDA-graph capture (an external record node)
+void record_event(cudaEvent_t ev, cudaStream_t st);
 void gemm_sk_reset(cudaStream_t st);
 // reduce-scatter modes (gradient accumulation)
 enum { RS_UPDATE = 0, RS_FIRST = 1, RS_ADD = 2, RS_FINAL = 3 };

@@ -1,7 +1,9 @@
-"""CUDA-graph capture of the scheduled step (SURVEY §8 f-4, N = 1): in graph
-mode every step restarts the grad-slot / reduce-scatter counters and flags and
-reads its Adam scalars from device memory, so one captured step replays for
-every later step.  Replays are bit-identical to eager steps."""
+"""CUDA-graph capture of the scheduled step: in graph mode
+every step restarts the flag protocol (gather ready / done, grad-slot and
+reduce-scatter counters) from zero — at N > 1 between two rounds of a barrier
+on a device step counter — and reads its Adam scalars from device memory, so
+one captured step replays for every later step.  Replays are bit-identical to
+eager steps (N = 1, and N = 2 / 4 virtual ranks replaying concurrently)."""
 import json
 
 import numpy as np
@@ -82,5 +84,49 @@ def test_graph_mode_errors():
     cs = st.stream_handles()
     assert dc.lib.dc_model_graph_capture(st.model, 1, *cs) == dc.DC_ESTATE     # graph_mode not set
     assert dc.lib.dc_model_graph_launch(st.model, 1, cs[0]) == dc.DC_ESTATE    # nothing captured
-    two = rt.create_ranks(synth.param_table(cfg), 2)
-    assert dc.lib.dc_set_option(two[0].ctx, b"graph_mode", 1) == dc.DC_EINVAL  # N == 1 only
+    assert dc.lib.dc_set_option(st.ctx, b"graph_mode", 1) == dc.DC_ESTATE      # after dc_bind_schedule
+
+
+def _make_n(cfg, world, graph_mode):
+    table = synth.param_table(cfg)
+    ranks = rt.create_ranks(table, world, lr=LR)
+    xs, ts = {}, {}
+    for r in ranks:
+        x, t = ost.rank_batch(cfg, r)
+        xs[r], ts[r] = bf16_tensor(x), bf16_tensor(t)
+    rt.attach_model(ranks, cfg, xs, ts)
+    if graph_mode:
+        for st in ranks.values():
+            dc.check(dc.lib.dc_set_option(st.ctx, b"graph_mode", 1), st.ctx)
+    prof = rt.profile_json(ranks[0], tc=[[4096, 10], [1 << 20, 20], [1 << 26, 400]])
+    sched = dc.plan(json.dumps(prof), 1 << 40, M_prefetch=1 << 22,
+                    passes=dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD, strict=True)
+    rt.bind(ranks, {r: sched for r in ranks})
+    return ranks
+
+
+@pytest.mark.parametrize("world,moe", [(2, False), (4, False), (2, True)])
+def test_graph_replay_virtual_ranks_bitexact(world, moe):
+    cfg = synth.small_mixtral(layers=2, seq=128) if moe else synth.small_llama(layers=2, seq=128)
+    ref = _make_n(cfg, world, False)
+    for t in (1, 2, 3, 4):
+        rt.step(ref, t)
+        torch.cuda.synchronize()
+    eg = _make_n(cfg, world, True)                 # eager steps with the per-step barrier + reset
+    for t in (1, 2, 3, 4):
+        rt.step(eg, t)
+        torch.cuda.synchronize()
+    rt.poll(eg)
+    gr = _make_n(cfg, world, True)
+    rt.step(gr, 1)
+    torch.cuda.synchronize()
+    rt.run_parallel(gr, lambda st: dc.check(dc.lib.dc_model_graph_capture(st.model, 2, *st.stream_handles()),
+                                            st.ctx))
+    for t in (2, 3, 4):
+        rt.run_parallel(gr, lambda st: dc.check(dc.lib.dc_model_graph_launch(st.model, t, st.stream_handles()[0]),
+                                                st.ctx))
+    torch.cuda.synchronize()
+    rt.poll(gr)
+    for r in ref:
+        _same(ref[r], eg[r])
+        _same(ref[r], gr[r])
