@@ -1260,6 +1260,10 @@ extern "C" dc_status dc_model_graph_capture(dc_model* m, int32_t step_t, cudaStr
   }
   if (m->host_states || m->side_adam || m->fused_adam || m->comm_sms > 0)
     return mfail(m, DC_EINVAL, "dc_model_graph_capture: host states / side / fused Adam / SM partition unsupported");
+  // at N = 1 no node may wait on another branch of the graph (branches can
+  // share a hardware queue): the reduce-scatter runs in compute-stream order
+  if (ctx_world(m->ctx) == 1 && m->rs_overlap)
+    return mfail(m, DC_EINVAL, "dc_model_graph_capture: set rs_overlap 0 at N = 1");
   if (m->graph_exec) { cudaGraphExecDestroy(m->graph_exec); m->graph_exec = nullptr; }
   if (m->graph) { cudaGraphDestroy(m->graph); m->graph = nullptr; }
   if (cudaStreamBeginCapture(ucs, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
