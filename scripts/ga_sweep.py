@@ -50,8 +50,8 @@ def main():
     N = 8
     bw = 0.7 * 900e3
     tc = [[0, 20], [1 << 34, 20 + int((1 << 34) / bw)]]
-    models = [("Mixtral-8x7B L = 32", synth.MIXTRAL_8X7B, 32, per_op_ms("profiles/r01g/bench_mixtral_L4.json", 4, 2)),
-              ("Llama-3-8B L = 32", synth.LLAMA3_8B, 32, per_op_ms("profiles/r01g/bench_llama8b_default.json", 32, 2))]
+    models = [("Mixtral-8x7B L = 32", synth.MIXTRAL_8X7B, 32, per_op_ms("profiles/r01g/lines_final/mix_b2.json", 4, 2)),
+              ("Llama-3-8B L = 32", synth.LLAMA3_8B, 32, per_op_ms("profiles/r01g/bench_default_final.json", 32, 2))]
     rows = []
     for label, base, L, op_ms in models:
         cfg = dataclasses.replace(base, layers=L, seq=2048, batch=1)

@@ -1,6 +1,7 @@
 """Per-op CUDA-event times of one profiled step (diagnostic): python
 scripts/op_times.py [model] [layers] [batch].  Prints the per-op-name sums and
-the first layer's forward sequence."""
+the first layer's forward sequence (DC_OPT_BWD=1: also the backward sequence
+of the last and the first layer; DC_OPT_PASSES: plan passes, default S_0)."""
 import dataclasses
 import json
 import os
@@ -27,7 +28,8 @@ for k, v in os.environ.items():
     if k.startswith("DCOPT_"):
         dc.check(dc.lib.dc_model_set_option(st.model, k[6:].lower().encode(), int(v)))
 prof = rt.profile_json(st)
-rt.bind(ranks, {0: dc.plan(json.dumps(prof), 1 << 50, passes=dc.DC_PASS_SHARD)})
+passes = int(os.environ.get("DC_OPT_PASSES", dc.DC_PASS_SHARD))
+rt.bind(ranks, {0: dc.plan(json.dumps(prof), 1 << 50, passes=passes)})
 for s in range(1, 4):
     rt.step(ranks, s)
 torch.cuda.synchronize()
@@ -44,3 +46,7 @@ for o in p["ops"]:
         agg[o["name"]] = agg.get(o["name"], 0) + o["dur_us"]
 print(json.dumps({k: v / 1e3 for k, v in sorted(agg.items(), key=lambda kv: -kv[1])[:25]}))
 print([(o["name"], o["dur_us"]) for o in p["ops"] if o["kind"] == "compute" and o["layer"] == 0 and o["phase"] == "fwd"])
+if os.environ.get("DC_OPT_BWD"):
+    for l in (L - 1, 0):
+        print("bwd layer", l, [(o["kind"], o["name"], o["dur_us"]) for o in p["ops"]
+                               if o["layer"] == l and o["phase"] == "bwd"])

@@ -6,7 +6,7 @@ an 8-rank 70B plan, so this runs dc_plan (the product planner, C ABI) on the
 executor's S_0 with an analytic P_mem that mirrors model.cu's bookkeeping, and
 times the schedules with the oracle's three-stream replay (oracle/sim.py,
 reading D23) from per-op durations measured on the B200 (70B layers at N = 1,
-profiles/r01g/bench_llama70b_L8.json) and an assumed T_c = 20 us + V / (0.7 x
+profiles/r01g/lines_final/llama70b_L8.json) and an assumed T_c = 20 us + V / (0.7 x
 900 GB/s).  Planning and memory numbers are exact; times are a model.
 
     python scripts/plan_sweep.py [--out profiles/r01g/plan_sweep_70b_n8.md]
@@ -36,7 +36,7 @@ def main():
     args = ap.parse_args()
     N = 8
     cfg = dataclasses.replace(synth.LLAMA3_70B, layers=args.layers, seq=2048, batch=1)
-    with open(os.path.join(ROOT, "profiles", "r01g", "bench_llama70b_L8.json")) as fh:
+    with open(os.path.join(ROOT, "profiles", "r01g", "lines_final", "llama70b_L8.json")) as fh:
         meas = json.load(fh)
     L_meas, b_meas = 8, 2
     # per layer, per op, at b = 1 (the measured run is 8 layers at b = 2)
@@ -82,7 +82,7 @@ def main():
              % (14 * E / GB, E / 1e9),
              "without m/v %.1f GB; serial compute %.0f ms per step (per-op durations measured on B200, 70B layers at"
              % (base_peak / GB, compute_ms),
-             "N = 1, profiles/r01g/bench_llama70b_L8.json, scaled to b = 1); T_c = 20 us + V / (0.7 x 900 GB/s)"
+             "N = 1, profiles/r01g/lines_final/llama70b_L8.json, scaled to b = 1); T_c = 20 us + V / (0.7 x 900 GB/s)"
              " (model, not measured: one GPU).", "",
              "| M (GB) | passes | step (ms, replay) | unsharded params | unsharded layers | gathers / step | peak incl. m,v / arena (GB) |",
              "|---|---|---|---|---|---|---|"]
