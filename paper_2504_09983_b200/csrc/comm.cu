@@ -165,23 +165,32 @@ struct RsParams {
 };
 
 #ifndef DC_RS_UNR
-#define DC_RS_UNR 2
+#define DC_RS_UNR 2           // N > 1: two groups' peer loads in flight per thread (NVLink latency)
 #endif
+#ifndef DC_RS_UNR_N1
+#define DC_RS_UNR_N1 1        // N = 1: one group (80 registers; 12-15 % faster in-step than two groups
+#endif                        // at 112 registers, profiles/r01g/rs_coresidency_ab.md)
 #ifndef DC_RS_PIPE
 #define DC_RS_PIPE 0          // > 0: software-pipelined groups per iteration (A/B)
 #endif
 #ifndef DC_RS_PREFETCH
 #define DC_RS_PREFETCH 0      // > 0: prefetch that many iterations ahead into L2 (A/B)
 #endif
-constexpr int RS_UNR = DC_RS_UNR;   // groups of 8 elements per thread per iteration (loads hoisted)
+// groups of 8 elements per thread per iteration (loads hoisted)
+template <int MAXQ>
+struct RsUnr { static constexpr int value = MAXQ == 1 ? DC_RS_UNR_N1 : DC_RS_UNR; };
 
 // MODE (gradient accumulation; dc.h dc_reduce_scatter_step):
 //   RS_UPDATE  g = sum * 1/N, Adam                      (n = 1)
 //   RS_FIRST   acc = sum                                (micro-step 0 of n > 1)
 //   RS_ADD     acc = acc + sum                          (micro-steps 1 .. n-2)
 //   RS_FINAL   g = (acc + sum) * 1/(N n), Adam          (micro-step n-1)
+#ifndef DC_RS_MINB
+#define DC_RS_MINB 1          // min resident CTAs per SM for the register budget (A/B)
+#endif
 template <int MAXQ, int MODE>
-__global__ void __launch_bounds__(256) rs_adam_kernel(const RsParams p) {
+__global__ void __launch_bounds__(256, DC_RS_MINB) rs_adam_kernel(const RsParams p) {
+  constexpr int RS_UNR = RsUnr<MAXQ>::value;
   {   // grad-ready of every rank was awaited by the preceding wait kernel
     const uint64_t pol = policy_evict_first();
     const AdamScalars a{p.w1, p.w2, p.b2, p.scal ? -p.scal[0] : p.neg_s, p.scal ? p.scal[1] : p.c, p.eps, p.invN};
