@@ -177,8 +177,11 @@ struct RsParams {
 #define DC_RS_PREFETCH 0      // > 0: prefetch that many iterations ahead into L2 (A/B)
 #endif
 // groups of 8 elements per thread per iteration (loads hoisted)
-template <int MAXQ>
-struct RsUnr { static constexpr int value = MAXQ == 1 ? DC_RS_UNR_N1 : DC_RS_UNR; };
+// (the accumulate-only modes keep two: few registers, few bytes per element)
+template <int MAXQ, int MODE>
+struct RsUnr {
+  static constexpr int value = (MAXQ == 1 && (MODE == RS_UPDATE || MODE == RS_FINAL)) ? DC_RS_UNR_N1 : DC_RS_UNR;
+};
 
 // MODE (gradient accumulation; dc.h dc_reduce_scatter_step):
 //   RS_UPDATE  g = sum * 1/N, Adam                      (n = 1)
@@ -190,7 +193,7 @@ struct RsUnr { static constexpr int value = MAXQ == 1 ? DC_RS_UNR_N1 : DC_RS_UNR
 #endif
 template <int MAXQ, int MODE>
 __global__ void __launch_bounds__(256, DC_RS_MINB) rs_adam_kernel(const RsParams p) {
-  constexpr int RS_UNR = RsUnr<MAXQ>::value;
+  constexpr int RS_UNR = RsUnr<MAXQ, MODE>::value;
   {   // grad-ready of every rank was awaited by the preceding wait kernel
     const uint64_t pol = policy_evict_first();
     const AdamScalars a{p.w1, p.w2, p.b2, p.scal ? -p.scal[0] : p.neg_s, p.scal ? p.scal[1] : p.c, p.eps, p.invN};
