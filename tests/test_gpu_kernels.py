@@ -262,10 +262,13 @@ def _bits_equal(got, ref, what):
 
 def _ragged_table():
     """Edge-case parameter sizes: smaller than one 16 B shard vector per rank
-    (1, 7), odd (13, 4099, 65537) and a 1 MiB tensor; two layers."""
+    (1, 7), odd (13, 4099, 65537) and a 1 MiB tensor; two layers.  Params 0
+    and 3 start at zero, so after step 1 their fp32 master IS the Adam update
+    (every bit visible: a 1-ulp error in sqrt(v)/c + eps or in the final
+    division, absorbed when added to a weight of ~0.02, fails here)."""
     sizes = [(0, 1), (0, 7), (0, 4099), (0, 1 << 19), (1, 13), (1, 65537), (1, 24)]
     k = float(synth.std_to_k(0.02))
-    return [synth.ParamSpec(id=i, layer=l, name="p%d" % i, shape=(n,), k=(0.0 if i == 0 else k), dtype="bf16")
+    return [synth.ParamSpec(id=i, layer=l, name="p%d" % i, shape=(n,), k=(0.0 if i in (0, 3) else k), dtype="bf16")
             for i, (l, n) in enumerate(sizes)]
 
 
@@ -330,6 +333,62 @@ def test_rs_adam_virtual_ranks(world, n, ragged):
                 for k, got, ref in (("master", ms, o_master), ("m", mm, o_m), ("v", vv, o_v)):
                     _bits_equal(got[off:off + sz], ref[r][i], (r, p.name, k, step))
                 assert np.array_equal(sh[off:off + sz], nx.bf16_bits(o_master[r][i]))
+
+
+@pytest.mark.parametrize("world,step", [(1, 7), (2, 1000)])
+def test_rs_adam_random_state(world, step):
+    """rs_adam on arbitrary optimizer states (random master / m / v, v >= 0
+    spanning 12 decades) at a later step t: every rounding of Adam's update —
+    the sqrt, both divisions, eps — hits general operands, not the
+    near-exact quotients of step 1 from a zero state (where sqrt(v)/c is
+    |g| almost exactly).  Bit-exact against the oracle."""
+    table = _ragged_table()
+    lr = 1e-3
+    ranks = rt.create_ranks(table, world, lr=lr)
+    S = [nx.shard_len(p.numel, world) for p in table]
+    rng = np.random.default_rng(11 + world)
+    states = {}
+    for r, st in ranks.items():
+        n = st.tensors["master"].numel()
+        ms = rng.normal(0.0, 0.02, n).astype(np.float32)
+        mm = rng.normal(0.0, 1e-3, n).astype(np.float32)
+        vv = (10.0 ** rng.uniform(-14, -2, n)).astype(np.float32)
+        for k, a in (("master", ms), ("m", mm), ("v", vv)):
+            st.tensors[k].copy_(torch.from_numpy(a))
+        states[r] = (ms, mm, vv)
+    grads = {q: _grads(world, table, S, q, step) for q in range(world)}
+
+    def work(st):
+        cs, rs = st.streams[0], st.streams[2]
+        for layer in (1, 0):
+            dc.check(dc.lib.dc_grad_slot_acquire(st.ctx, layer, cs.cuda_stream), st.ctx)
+            slot = C.c_void_p()
+            dc.check(dc.lib.dc_grad_slot(st.ctx, layer, C.byref(slot)), st.ctx)
+            with torch.cuda.stream(cs):
+                for i, p in enumerate(table):
+                    if p.layer == layer:
+                        v = rt.view(slot.value + rt.grad_offset(st, i), world * S[i], torch.bfloat16)
+                        v.copy_(bf16_tensor(grads[st.rank][i]))
+            dc.check(dc.lib.dc_grad_slot_publish(st.ctx, layer, cs.cuda_stream), st.ctx)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            rs.wait_event(ev)
+            dc.check(dc.lib.dc_reduce_scatter_step(st.ctx, layer, step, 0, rs.cuda_stream), st.ctx)
+        torch.cuda.synchronize()
+
+    rt.run_parallel(ranks, work)
+    rt.poll(ranks)
+    for r, st in ranks.items():
+        ms0, mm0, vv0 = states[r]
+        got = {k: st.tensors[k].cpu().numpy() for k in ("master", "m", "v")}
+        sh = st.tensors["shard"].view(torch.int16).cpu().numpy().view(np.uint16)
+        for i, p in enumerate(table):
+            off, sz = rt.shard_range(st, i)
+            sl = slice(off, off + sz)
+            ref = nx.rs_adam_shard([grads[q][i] for q in range(world)], ms0[sl], mm0[sl], vv0[sl], world, r, step, lr)
+            for k, refk in zip(("master", "m", "v"), ref[:3]):
+                _bits_equal(got[k][sl], refk, (r, p.name, k))
+            assert np.array_equal(sh[sl], nx.bf16_bits(ref[0])), (r, p.name)
 
 
 def test_rs_micro_out_of_range():
