@@ -568,16 +568,37 @@ def main():
                            "achieved_gbs": rs_bytes / (rs_us * 1e-6) / 1e9 if rs_us else None,
                            "peak_gbs": pk["hbm_gbs"], "bound": "hbm" if world == 1 else "nvlink+hbm"}}
 
-    # ---- end to end through the public API with HOST buffers
+    # ---- end to end through the public API with HOST buffers: every step's
+    # inputs cross PCIe from pinned memory inside the timed region, prefetched
+    # one step ahead on a copy stream into a device staging buffer (as a data
+    # loader would) and moved into the model's input buffers by a D2D copy at
+    # the step's start; the loss is read back to the host after every step
     loss_host = torch.empty(n_micro, dtype=torch.float32).pin_memory()
     lp = rt.view(rt.loss_ptr(st), n_micro, torch.float32, device=dev)
+    ps = torch.cuda.Stream(device=dev)
+    x_stage, t_stage = torch.empty_like(x_dev), torch.empty_like(t_dev)
+    ev_in, ev_used = torch.cuda.Event(), torch.cuda.Event()
+
+    def h2d_prefetch():
+        with torch.cuda.stream(ps):
+            x_stage.view(-1).copy_(x_host, non_blocking=True)
+            t_stage.view(-1).copy_(t_host, non_blocking=True)
+            ev_in.record(ps)
+
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(cs)
-    for _ in range(args.steps):
+    ps.wait_event(e0)
+    h2d_prefetch()
+    for k in range(args.steps):
         with torch.cuda.stream(cs):
-            x_dev.view(-1).copy_(x_host, non_blocking=True)
-            t_dev.view(-1).copy_(t_host, non_blocking=True)
+            cs.wait_event(ev_in)
+            x_dev.copy_(x_stage)
+            t_dev.copy_(t_stage)
+            ev_used.record(cs)
+        if k + 1 < args.steps:
+            ps.wait_event(ev_used)
+            h2d_prefetch()
         step_no += 1
         one_step()
         with torch.cuda.stream(cs):
