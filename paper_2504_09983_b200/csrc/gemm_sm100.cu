@@ -81,10 +81,10 @@ struct GemmParams {
   uint32_t sk_epoch;
 };
 // Tile order (tile index -> (m-tile, n-tile)): m fastest inside groups of
-// group_m m-tiles (group_m = m_tiles: m fastest over all of them).  Grouping
-// makes the CTA pairs resident at once cover a squarer block of tiles when
-// m_tiles >> n_tiles (the gate / up dW GEMMs: 56 x 16 tiles), so they share A
-// row blocks in L2 instead of streaming all of A once per wave (launch_gemm).
+// group_m m-tiles (group_m = m_tiles: m fastest over all of them).  When
+// m_tiles >> n_tiles (the gate / up dW GEMMs: 56 x 16 tiles) small groups make
+// the resident CTA pairs sweep every n-column of a few m-rows: B stays in L2
+// and A is streamed once, instead of all of A once per wave (launch_gemm).
 #ifndef DC_GEMM_GROUP_DEFAULT
 #define DC_GEMM_GROUP_DEFAULT 2
 #endif
