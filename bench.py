@@ -5,6 +5,10 @@
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
     python bench.py --impl reference      # the CPU oracle, same metric/config
 
+With --gpus N > 1 and no RANK in the environment, bench.py launches itself
+once per GPU through torch.distributed.run (127.0.0.1, a free port) and passes
+rank 0's JSON line through; under torchrun it runs as one rank.
+
 Flow (§3 / §5.5): S_0 warm-up steps (5) with per-op profiling
 -> profile MAX-reduced over ranks -> dc_plan (prefetch + unshard, strict) ->
 W warm-up steps -> K timed steps (CUDA events on the compute stream, barrier +
@@ -67,7 +71,52 @@ def parse():
                     help="test mode: every rank on cuda:0 (gloo host collectives, CUDA-IPC peer maps, fixed T_c); "
                          "exercises the N > 1 launch on a one-GPU box, numbers are not a bench value")
     ap.add_argument("--profile-json", default="", help="write the rank-0 profile / plan here")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check without a GPU: every rank joins a gloo group, barriers, MAX-reduces a "
+                         "dummy time and rank 0 prints one JSON line (tests/test_bench_cli.py)")
     return ap.parse_args()
+
+
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args):
+    """--gpus N > 1 outside torchrun: one process per GPU through
+    torch.distributed.run on this node (rendezvous on 127.0.0.1).  stdout of
+    the ranks is passed through (only rank 0 prints the JSON line)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=%d" % args.gpus,
+           "--master-addr=127.0.0.1", "--master-port=%d" % free_port(), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "4")
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args):
+    """The N-rank plumbing of the GPU arm with no GPU work: rank / world from
+    the launcher, gloo group, barrier, MAX over ranks, one JSON line."""
+    import torch
+    import torch.distributed as dist
+    world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit("bench: WORLD_SIZE %d != --gpus %d" % (world, args.gpus))
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)])
+    seen = [(rank, os.getpid())]
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        seen = [None] * world
+        dist.all_gather_object(seen, (rank, os.getpid()))
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "max_over_ranks": t.item(),
+                          "ranks": [r for r, _ in seen], "processes": len({p for _, p in seen})}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def peaks():
@@ -121,39 +170,62 @@ BAD_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
 # ----------------------------------------------------------------------------- oracle sample
 class OracleSample:
     """The CPU oracle on a bounded sample of the workload: ONE layer of the
-    stack at `tokens` tokens, N=1 — forward + backward (bf16-emulated, fp64
-    GEMMs) + reduce-scatter + Adam over the layer's 218 M parameters.
-    Weights are generated once (untimed); step() returns seconds."""
+    stack, N=1, at T tokens (T <= max_tokens) — forward + backward
+    (bf16-emulated, fp64 GEMMs) + reduce-scatter + Adam over the layer's
+    218 M parameters.  Weights are generated once (untimed); step(T) returns
+    seconds.
 
-    def __init__(self, cfg, tokens):
+    Extrapolation to the workload (documented in DESIGN.md §9): one layer
+    sample costs t(T) = a + b T — the reduce-scatter + Adam pass over the
+    layer's parameters does not depend on T (a), the layer's forward and
+    backward GEMMs / glue are linear in T (b).  a and b come from the medians
+    of samples at two token counts; the L-layer step at the workload's T_w
+    tokens then takes L (a + b T_w)."""
+
+    def __init__(self, cfg, max_tokens):
         import synth
         from oracle import numerics as nx
-        self.cfg, self.tokens, self.t = cfg, tokens, 0
+        self.cfg, self.t = cfg, 0
         self.table = synth.llama_param_table(cfg)[:9]
         self.W, self.masters = {}, []
         for p in self.table:
             v = (np.ones(p.numel, np.float32) if p.k == 0.0 else synth.values(0, p.id, 0, p.numel, p.k))
             self.masters.append(v)
             self.W[p.name] = nx.rne_bf16(v).reshape(p.shape)
-        n = tokens * cfg.hidden
-        self.x = nx.rne_bf16(synth.values(1000, 0, 0, n, synth.K_UNIT)).reshape(tokens, cfg.hidden)
-        self.y_t = nx.rne_bf16(synth.values(2000, 0, 0, n, synth.K_UNIT)).reshape(tokens, cfg.hidden)
+        n = max_tokens * cfg.hidden
+        self.x = nx.rne_bf16(synth.values(1000, 0, 0, n, synth.K_UNIT)).reshape(max_tokens, cfg.hidden)
+        self.y_t = nx.rne_bf16(synth.values(2000, 0, 0, n, synth.K_UNIT)).reshape(max_tokens, cfg.hidden)
         self.ms = [np.zeros_like(v) for v in self.masters]
         self.vs = [np.zeros_like(v) for v in self.masters]
+        self.secs = {}
 
-    def step(self):
+    def step(self, tokens):
         from oracle import model as om
         from oracle import numerics as nx
         self.t += 1
         t0 = time.perf_counter()
-        y, c = om.llama_layer_fwd(self.x, self.W, self.cfg, nx.rne_bf16)
-        _, dy = om.mse_loss(y, self.y_t)
+        y, c = om.llama_layer_fwd(self.x[:tokens], self.W, self.cfg, nx.rne_bf16)
+        _, dy = om.mse_loss(y, self.y_t[:tokens])
         _, G = om.llama_layer_bwd(nx.rne_bf16(dy), c, self.W, self.cfg, nx.rne_bf16)
         for i, p in enumerate(self.table):
             g = nx.reduce_scatter([np.asarray(G[p.name], np.float32).reshape(-1)], 1, 0)
             self.masters[i], self.ms[i], self.vs[i] = nx.adam_update(
                 self.masters[i], self.ms[i], self.vs[i], nx.scale_mean(g, 1), self.t)
-        return time.perf_counter() - t0
+        sec = time.perf_counter() - t0
+        self.secs.setdefault(tokens, []).append(sec)
+        return sec
+
+    def fit(self):
+        """(a, b) of t(T) = a + b T from the per-T medians (two token counts)."""
+        (t1, s1), (t2, s2) = sorted((t, statistics.median(v)) for t, v in self.secs.items())[:2]
+        b = max((s2 - s1) / (t2 - t1), 1e-12)
+        a = max(s1 - b * t1, 0.0)
+        return a, b
+
+    def tokens_per_s(self, cfg):
+        """Extrapolated tokens/s of the L-layer step at the workload's tokens."""
+        a, b = self.fit()
+        return cfg.tokens / (cfg.layers * (a + b * cfg.tokens)), a, b
 
 
 def cpu_cores():
@@ -164,8 +236,11 @@ def cpu_cores():
 
 
 def run_reference(args):
-    """--impl reference: the oracle (this tier's reference arm) on host cores."""
-    import synth
+    """--impl reference: the oracle (this tier's reference arm) on host cores.
+    A step is one layer sample, alternating 32 and 64 tokens (warm-up covers
+    both); `ms_per_step` is the measured time of those samples, `value` the
+    tokens/s of the workload extrapolated with OracleSample's model."""
+    import synth  # noqa: F401
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -174,19 +249,23 @@ def run_reference(args):
                           "llama3-8b workload only (a 70B / Mixtral layer's states exceed a bounded CPU sample)"}))
         return
     cfg = model_config(args)
-    T = 32
-    sample_run = OracleSample(cfg, T)
-    secs = []
-    for _ in range(args.warmup):
-        sample_run.step()
-    for _ in range(args.steps):
-        secs.append(sample_run.step())
+    sizes = (32, 64)
+    sample_run = OracleSample(cfg, max(sizes))
+    for i in range(max(args.warmup, 2)):
+        sample_run.step(sizes[i % 2])
+    sample_run.secs = {} if args.steps >= 2 else sample_run.secs
+    secs = [sample_run.step(sizes[i % 2]) for i in range(args.steps)]
     per_step = float(np.mean(secs))
-    # tokens/s of the whole L-layer stack: T tokens need L layer-samples
-    val = T / (per_step * cfg.layers)
-    sample = "1 Llama-3-8B-shaped layer, %d tokens, N=1: oracle fwd+bwd+RS+Adam; scaled x%d layers" % (T, cfg.layers)
+    val, a, b = sample_run.tokens_per_s(cfg)
+    sample = ("1 Llama-3-8B-shaped layer at %d / %d tokens alternating, N=1: oracle fwd+bwd+RS+Adam; measured "
+              "t(T) = a + b T per layer with a = %.2f s (RS + Adam, token-independent), b = %.4f s/token; "
+              "workload %d layers x %d tokens -> %.0f s per step" %
+              (sizes[0], sizes[1], a, b, cfg.layers, cfg.tokens, cfg.layers * (a + b * cfg.tokens)))
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * cfg.layers * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
+            "ms_per_step_note": "measured wall time of one step = one layer sample (not the extrapolated "
+                                "workload step; see cpu_baseline.sample)",
+            "extrapolated_ms_per_workload_step": cfg.layers * (a + b * cfg.tokens) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (oracle)",
             "data": "synthetic",
             "config": {"workload": "llama3-8b-stack (BASELINE configs[1]), oracle sample", "seq_len": args.seq,
@@ -302,6 +381,11 @@ def model_config(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "RANK" not in os.environ and (args.impl == "ours" or args.dry_run):
+        sys.exit(self_launch(args))
+    if args.dry_run:
+        dry_run(args)
+        return
     if args.offload_sync:
         args.offload = True
     args.graph = not args.offload and not args.no_graph and args.graph != "off" and \
@@ -318,6 +402,17 @@ def main():
     world = args.gpus
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if int(os.environ.get("WORLD_SIZE", "1")) != world:
+        raise SystemExit("bench: WORLD_SIZE %s != --gpus %d" % (os.environ.get("WORLD_SIZE", "1"), world))
+    if world > 1 and not args.share_gpu and torch.cuda.device_count() < world:
+        raise SystemExit("bench: --gpus %d needs %d visible GPUs (found %d); --share-gpu runs the N-rank "
+                         "flow on one GPU as a test" % (world, world, torch.cuda.device_count()))
+    if world > 1:
+        # communicator init lines (rank count, NVLS / P2P transport) on stderr,
+        # which keeps stdout to the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.share_gpu:
         local = 0
         os.environ["DC_SYMM"] = "ipc"         # symmetric memory refuses two ranks on one device
@@ -351,13 +446,13 @@ def main():
         dc.check(dc.lib.dc_set_option(st.ctx, b"graph_mode", 1), st.ctx)
     if os.environ.get("DC_AG_COPY_ENGINE") is not None:       # gathers on the copy engines (f-3)
         dc.check(dc.lib.dc_set_option(st.ctx, b"ag_copy_engine", int(os.environ["DC_AG_COPY_ENGINE"])), st.ctx)
-    from oracle import numerics as nx          # bf16 rounding of the synthetic inputs only
+    # synthetic inputs (synth generator, fp32) rounded to bf16 by torch (RNE)
     x_np = np.concatenate([synth.values(synth.seed_inputs(rank, mu), 0, 0, T * cfg.hidden, synth.K_UNIT)
                            for mu in range(n_micro)])
     t_np = np.concatenate([synth.values(synth.seed_targets(rank, mu), 0, 0, T * cfg.hidden, synth.K_UNIT)
                            for mu in range(n_micro)])
-    x_host = torch.from_numpy(nx.bf16_bits(x_np).view(np.int16)).view(torch.bfloat16).pin_memory()
-    t_host = torch.from_numpy(nx.bf16_bits(t_np).view(np.int16)).view(torch.bfloat16).pin_memory()
+    x_host = torch.from_numpy(x_np).to(torch.bfloat16).pin_memory()
+    t_host = torch.from_numpy(t_np).to(torch.bfloat16).pin_memory()
     x_dev = x_host.to(dev).view(n_micro, T, cfg.hidden)
     t_dev = t_host.to(dev).view(n_micro, T, cfg.hidden)
     rt.attach_model(ranks, cfg, {rank: x_dev}, {rank: t_dev}, checkpoint=args.checkpoint)
@@ -545,7 +640,7 @@ def main():
         traffic_note = "%s; algorithmic %s B" % (tj.get("launch"), tj.get("algorithmic_bytes_per_launch"))
     except (OSError, ValueError):
         pass
-    roofline = {"bound": "tensor", "kernel": "gemm_bf16_sm100 (tcgen05, all layer GEMMs)",
+    roofline = {"bound": "tensor", "kernel": "gemm2_bf16_sm100 (tcgen05 CTA pair, all layer GEMMs)",
                 "achieved": achieved, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
                 "frac": achieved / pk["bf16_tflops_sustained"] if achieved else None, "traffic": traffic,
                 "traffic_note": traffic_note,
@@ -617,12 +712,16 @@ def main():
     # ---- CPU oracle timed on host cores (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.model == "llama3-8b":
-        Ts = 128
-        sample_run = OracleSample(cfg, Ts)
-        sec = min(sample_run.step() for _ in range(2))
-        cpu = {"value": Ts / (sec * cfg.layers), "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": "1 Llama-3-8B-shaped layer, %d tokens, N=1: oracle fwd+bwd+RS+Adam (best of 2, %.1f s); "
-                         "tokens/s scaled to the %d-layer stack" % (Ts, sec, cfg.layers)}
+        sample_run = OracleSample(cfg, 128)
+        t0 = time.perf_counter()
+        for T in (32, 128, 32, 128):
+            sample_run.step(T)
+        val, a, b = sample_run.tokens_per_s(cfg)
+        cpu = {"value": val, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": "1 Llama-3-8B-shaped layer at 32 and 128 tokens (2 samples each, %.1f s total), N=1: "
+                         "oracle fwd+bwd+RS+Adam; t(T) = a + b T per layer, a = %.2f s, b = %.4f s/token, "
+                         "extrapolated to %d layers x %d tokens" %
+                         (time.perf_counter() - t0, a, b, cfg.layers, cfg.tokens)}
 
     # exposed communication (SURVEY §8 d): the compute stream's idle time in the
     # last timed step = step time - sum of compute-op events (each op's start
@@ -639,11 +738,17 @@ def main():
                          (offload_info["offloaded_bytes"] if offload_info else 0), "M": M}
     if offload_info:   # the reload ring is a static allocation beside the plan's live bytes
         mem["offload_pool"] = offload_info["pool_bytes"]
-    exposed = {"ms": max(0.0, ms - busy_ms), "frac": max(0.0, ms - busy_ms) / ms,
-               "note": "step time - compute-stream busy time of the last timed step (waits on gathers, "
-                       "grad-slot / reduce-scatter flags and launch gaps; reduce-scatter ops count as busy when "
-                       "they run in compute-stream order); target < 10 % at N > 1"}
-    coll = None
+    idle = {"ms": max(0.0, ms - busy_ms), "frac": max(0.0, ms - busy_ms) / ms,
+            "note": "step time - compute-stream busy time of the last timed step (waits on gathers, "
+                    "grad-slot / reduce-scatter flags and launch gaps; reduce-scatter ops count as busy when "
+                    "they run in compute-stream order)"}
+    if world > 1:
+        exposed = dict(idle, target="< 10 % of the step (BASELINE north star)")
+    else:
+        exposed = {"ms": None, "frac": None, "note": "N = 1: no communication (gathers alias the shard, the "
+                   "reduce-scatter reads only local grads); compute_stream_idle has the step's idle time"}
+    coll = {"measured": False, "note": "N = 1: no collective runs; virtual-rank gather sweeps are in "
+            "profiles/r02/ (scripts/ag_sweep.py)"}
     if world > 1:
         # per issued gather of the last timed step: transfer time (every receiver
         # ready -> every sender's stores landed here, CUDA events on the AG stream)
@@ -658,7 +763,9 @@ def main():
             rs_per_layer_b[p.get("layer", 0)] = rs_per_layer_b.get(p.get("layer", 0), 0) + p["bytes"]
         rs_us = [o["dur_us"] for o in last["ops"] if o["kind"] == "rs"]
         rs_b = sum(rs_per_layer_b.values())
-        coll = {"note": "busbw = (N-1)/N x bytes / time; AG time from every receiver ready to all stores landed; "
+        coll = {"measured": True, "n_ranks": dist.get_world_size(group),
+                "transport": rt.symm_backend() if not args.share_gpu else "ipc (share-gpu test mode)",
+                "note": "busbw = (N-1)/N x bytes / time; AG time from every receiver ready to all stores landed; "
                         "RS time = the fused reduce-scatter + Adam kernel (bf16 grads in over NVLink)",
                 "gathers_per_step": len(ags), "ag_bytes_per_step": tot_b,
                 "ag_busbw_gbs": f * tot_b / (tot_us * 1e-6) / 1e9 if tot_us else None,
@@ -688,7 +795,7 @@ def main():
                            "tc_table": prof["tc"], "tc_nccl_comparator": tc_nccl,
                            "l2": "working set (~120 GB/GPU of weights, states, activations) >> 126 MB L2; no flush"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "exposed_comm": exposed, "memory": mem,
+                "exposed_comm": exposed, "compute_stream_idle": idle, "memory": mem,
                 "clocks": clocks, "kernels": kernels, "collectives": coll,
                 "host_enqueue_ms_per_step": round(host_enqueue_ms, 2)}
         print(json.dumps(line), flush=True)

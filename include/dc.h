@@ -275,10 +275,11 @@ typedef struct {
   int32_t num_sms;               /* 0 = all SMs                                 */
   int32_t kernel;                /* 0 auto (CTA pairs), 1 one-CTA tiles, 2 pairs */
   int32_t stream_k;              /* 1: split the last waves' k-blocks evenly over */
-                                 /* the pairs (fp32 partials through a per-stream */
-                                 /* workspace, deterministic). Only when no other */
-                                 /* persistent GEMM can run concurrently on the  */
-                                 /* device (it spins on another pair's partial). */
+                                 /* the pairs (fp32 partials through `workspace`, */
+                                 /* deterministic); ignored when workspace is    */
+                                 /* NULL.  Only when no other persistent GEMM can */
+                                 /* run concurrently on the device (it spins on  */
+                                 /* another pair's partial).                     */
   int32_t epilogue;              /* 0 plain; CTA pairs only, N = F (SwiGLU width): */
                                  /* 2 GLU forward: B = {W_gate, W_up} (2 K-major  */
                                  /*   segments, bseg_end ignored), C = gate half  */
@@ -289,8 +290,20 @@ typedef struct {
                                  /*   C + glu_off = d(up); same values as the     */
                                  /*   separate act / act_bwd kernels, bit for bit */
   void* aux; int64_t ld_aux, glu_off;
+  /* stream-K workspace: caller-owned device memory of at least
+   * dc_gemm_workspace_bytes() bytes, zero-filled before its first use and
+   * used by launches on ONE stream at a time (they are ordered, so they may
+   * share it; the library keeps a per-workspace launch epoch, so stale flags
+   * of earlier launches are harmless).  NULL: no stream-K. */
+  void* workspace; uint64_t workspace_bytes;
+  /* persistent tile order (pair kernel): 0 auto (groups of 2 m-tiles when
+   * m_tiles >= 2 n_tiles, else m-fastest over the whole grid); g > 0: groups
+   * of g m-tiles (the last group may be partial); -1: never group. */
+  int32_t tile_group_m;
 } dc_gemm_args;
 dc_status dc_gemm(const dc_gemm_args* g, cudaStream_t stream);
+/* Bytes of a stream-K workspace (fp32 partial tiles + flags). */
+uint64_t dc_gemm_workspace_bytes(void);
 /* CTA pairs the default pair kernel keeps co-resident on this device
  * (cudaOccupancyMaxActiveClusters; the persistent grid never exceeds it);
  * -1 on a CUDA error. */

@@ -107,7 +107,8 @@ struct dc_ctx {
   std::vector<int> layer_use;
   uint32_t rs_done_total = 0;
   int rs_ctas = 0, rs_threads = 256, rs_ctas_default = 296;
-  // error word: host-mapped pinned (device writes on a flag-wait timeout)
+  // error record (ERR_RECORD_WORDS words): host-mapped pinned, written by the
+  // device on a flag-wait timeout: code, claimed, target, observed, address
   uint32_t* err_host = nullptr;
   uint32_t* err_dev = nullptr;
   std::vector<FragInfo> frags;
@@ -134,11 +135,53 @@ static dc_status fail(dc_ctx* c, dc_status s, const std::string& m) {
   return s;
 }
 
+// Which flag a timed-out wait was spinning on, from the address in the
+// error record: the table (by peer base address) and the word's role in the
+// flag layout (make_layout).
+static std::string describe_flag(const dc_ctx* c, uint64_t addr) {
+  const Layout& L = c->L;
+  for (int q = 0; q < (int)c->flag_peers.size(); ++q) {
+    const uint64_t base = c->flag_peers[q];
+    if (addr < base || addr >= base + (uint64_t)L.flag_words * 4) continue;
+    const int64_t w = (int64_t)(addr - base) / 4;
+    char b[160];
+    const int W = c->world;
+    if (w < L.f_done)
+      snprintf(b, sizeof b, "ready[gather %lld][sender %lld]", (long long)(w / W), (long long)(w % W));
+    else if (w < L.f_gready)
+      snprintf(b, sizeof b, "done[gather %lld]", (long long)(w - L.f_done));
+    else if (w < L.f_gcons)
+      snprintf(b, sizeof b, "grad_ready[slot %lld][sender %lld]", (long long)((w - L.f_gready) / W),
+               (long long)((w - L.f_gready) % W));
+    else if (w < L.f_rsdone)
+      snprintf(b, sizeof b, "consumed[slot %lld][owner %lld]", (long long)((w - L.f_gcons) / W),
+               (long long)((w - L.f_gcons) % W));
+    else if (w >= L.f_bar)
+      snprintf(b, sizeof b, "step_barrier[round %lld][rank %lld]", (long long)((w - L.f_bar) / W),
+               (long long)((w - L.f_bar) % W));
+    else
+      snprintf(b, sizeof b, "word %lld", (long long)w);
+    return std::string(b) + " in rank " + std::to_string(q) + "'s flag table";
+  }
+  char b[48];
+  snprintf(b, sizeof b, "address 0x%llx (not a flag table)", (unsigned long long)addr);
+  return b;
+}
+
 static dc_status check_sticky(dc_ctx* c) {
-  if (c->err_host && *(volatile uint32_t*)c->err_host) {
-    char b[96];
-    snprintf(b, sizeof b, "device flag wait timed out (code 0x%x)", *(volatile uint32_t*)c->err_host);
-    return fail(c, DC_ETIMEOUT, b);
+  volatile uint32_t* e = c->err_host;
+  if (e && e[0]) {
+    static const char* what[] = {"?", "gather: receivers ready", "gather: stores landed", "reduce-scatter: grads ready",
+                                 "flag wait", "graph step barrier"};
+    const uint32_t code = e[0];
+    const uint32_t k = (code >> 8) < 6 ? (code >> 8) : 0;
+    const uint64_t addr = (uint64_t)e[4] | ((uint64_t)e[5] << 32);
+    char b[160];
+    snprintf(b, sizeof b, "rank %d: device flag wait timed out after %.1f s (code 0x%x, %s) on ", c->rank,
+             c->timeout_ns * 1e-9, code, what[k]);
+    char v[96];
+    snprintf(v, sizeof v, ": observed %u, waiting for >= %u", e[3], e[2]);
+    return fail(c, DC_ETIMEOUT, b + describe_flag(c, addr) + v);
   }
   return DC_OK;
 }
@@ -209,8 +252,8 @@ extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
   DC_CUDA_TRY(preload_comm_kernels(), &c->err);
   DC_CUDA_TRY(preload_gemm_kernels(), &c->err);
   DC_CUDA_TRY(preload_moe_kernels(), &c->err);
-  DC_CUDA_TRY(cudaHostAlloc(&c->err_host, 4, cudaHostAllocMapped), &c->err);
-  *c->err_host = 0;
+  DC_CUDA_TRY(cudaHostAlloc(&c->err_host, ERR_RECORD_WORDS * 4, cudaHostAllocMapped), &c->err);
+  memset(c->err_host, 0, ERR_RECORD_WORDS * 4);
   DC_CUDA_TRY(cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0), &c->err);
   cudaStream_t st = 0;
   c->states_bound = !defer;
@@ -334,7 +377,6 @@ extern "C" dc_status dc_step_begin(dc_ctx* c, int32_t epoch, cudaStream_t st) {
     std::fill(c->layer_use.begin(), c->layer_use.end(), 0);
     c->rs_done_total = 0;
     DC_CUDA_TRY(cudaMemsetAsync(c->myflag(0), 0, c->L.f_scal * 4, st), &c->err);
-    gemm_sk_reset(st);
     if (c->world > 1) {
       k_post_dev(peers_at(c, c->L.f_bar + c->world + c->rank), dep, st);
       k_wait_dev(c->myflag(c->L.f_bar + c->world), c->world, dep, c->timeout_ns, c->err_dev, st);

@@ -44,11 +44,22 @@ struct AgParams {
   uint32_t* err;
 };
 
+// "counter >= target" in serial-number arithmetic: the gather done counters
+// grow without reset in eager mode, so a plain `<` would see a stale counter
+// as already past a target that wrapped around 2^32
 __device__ __forceinline__ bool spin_ge(const uint32_t* p, uint32_t target, uint64_t t0, uint64_t tmo,
                                         uint32_t* err, uint32_t code) {
-  while (ptx::ld_acquire_sys(p) < target) {
+  uint32_t seen;
+  while ((int32_t)((seen = ptx::ld_acquire_sys(p)) - target) < 0) {
     if (ptx::globaltimer() - t0 > tmo) {
-      atomicExch(err, code);
+      if (atomicCAS(err + 1, 0u, 1u) == 0u) {      // claim the record
+        err[2] = target;
+        err[3] = seen;
+        err[4] = (uint32_t)reinterpret_cast<uintptr_t>(p);
+        err[5] = (uint32_t)(reinterpret_cast<uintptr_t>(p) >> 32);
+        __threadfence_system();
+        atomicExch(err, code);                      // published last: the host reads code first
+      }
       return false;
     }
     __nanosleep(64);

@@ -16,6 +16,12 @@ void count_launch();                 // increments the launch counter (per threa
 int64_t launch_count();
 void reset_launch_count();
 
+// Host-mapped error record of a context, written by a timed-out device flag
+// wait (comm.cu spin_ge): [0] code (0 = no error; bits 8.. the waiting site,
+// low bits the flag index), [1] claimed, [2] target, [3] last observed value,
+// [4..5] flag address (lo, hi).
+constexpr int ERR_RECORD_WORDS = 8;
+
 #define DC_CUDA_TRY(expr, ctxerr)                                                   \
   do {                                                                              \
     cudaError_t _e = (expr);                                                        \
@@ -175,7 +181,8 @@ void k_wait_dev(const uint32_t* flags, int n, const uint32_t* dep, uint64_t time
                 cudaStream_t st);
 // event record that survives CUDA-graph capture (an external record node)
 void record_event(cudaEvent_t ev, cudaStream_t st);
-void gemm_sk_reset(cudaStream_t st);
+void gemm_sk_reset(void* workspace, cudaStream_t st);   // graph mode: flags cleared, epoch 0
+uint64_t gemm_workspace_bytes();
 // reduce-scatter modes (gradient accumulation)
 enum { RS_UPDATE = 0, RS_FIRST = 1, RS_ADD = 2, RS_FINAL = 3 };
 dc_status k_ag_copy(const std::vector<AgMember>& mem, int world, const uint64_t* arena_peers,

@@ -848,35 +848,29 @@ static int num_sms_cached() {
   return n;
 }
 
-// stream-K workspace, one per stream (launches on one stream are ordered, so
-// they may share it; the epoch makes stale flags of earlier launches harmless)
-struct SkWorkspace { float* buf = nullptr; uint32_t* flags = nullptr; uint32_t epoch = 0; };
+// stream-K workspace: caller-owned (dc_gemm_args.workspace), [tiles_cap][2]
+// CTA partials of 128 x 256 fp32, then [tiles_cap][2] uint32 flags.  The
+// launch epoch of each workspace is kept here, keyed by its address: a flag
+// equal to the current epoch marks a partial of the current launch.
+constexpr size_t SK_TILES_CAP = 2 * 74 + 2, SK_PART_BYTES = 2ull * 128 * 256 * 4;
+constexpr size_t SK_FLAG_BYTES = SK_TILES_CAP * 2 * 4;
+constexpr size_t SK_WS_BYTES = SK_TILES_CAP * SK_PART_BYTES + SK_FLAG_BYTES;
 static std::mutex g_sk_mu;
-static std::map<cudaStream_t, SkWorkspace> g_sk_ws;
-static SkWorkspace* sk_workspace(cudaStream_t st, int max_tiles, int bnt) {
+static std::map<const void*, uint32_t> g_sk_epoch;
+static uint32_t sk_next_epoch(const void* ws) {
   std::lock_guard<std::mutex> lock(g_sk_mu);
-  auto& ws = g_sk_ws;
-  auto it = ws.find(st);
-  if (it != ws.end()) return &it->second;
-  // capacity: 2 * 74 split tiles of 2 CTAs x 128 rows x 256 fp32 columns
-  (void)bnt; (void)max_tiles;
-  const size_t tiles_cap = 2 * 74 + 2, per = 2ull * 128 * 256 * 4;
-  SkWorkspace w;
-  if (cudaMalloc(&w.buf, tiles_cap * per) != cudaSuccess) return nullptr;
-  if (cudaMalloc(&w.flags, tiles_cap * 2 * 4) != cudaSuccess) return nullptr;
-  if (cudaMemsetAsync(w.flags, 0, tiles_cap * 2 * 4, st) != cudaSuccess) return nullptr;   // ordered before use
-  return &(ws[st] = w);
+  return ++g_sk_epoch[ws];
 }
 
 // graph mode: a step starts from epoch 0 with cleared flags, so the epochs a
 // replayed graph baked in at capture never meet a previous replay's flags
-void gemm_sk_reset(cudaStream_t st) {
+void gemm_sk_reset(void* ws, cudaStream_t st) {
+  if (!ws) return;
   std::lock_guard<std::mutex> lock(g_sk_mu);
-  auto it = g_sk_ws.find(st);
-  if (it == g_sk_ws.end()) return;
-  cudaMemsetAsync(it->second.flags, 0, (2 * 74 + 2) * 2 * 4, st);
-  it->second.epoch = 0;
+  cudaMemsetAsync(reinterpret_cast<uint8_t*>(ws) + SK_TILES_CAP * SK_PART_BYTES, 0, SK_FLAG_BYTES, st);
+  g_sk_epoch[ws] = 0;
 }
+uint64_t gemm_workspace_bytes() { return SK_WS_BYTES; }
 
 // 0: 256-wide 6 stages (default), 2: 256-wide 7 stages (DC_GEMM_STAGES=7)
 static int env_st_pick() {
@@ -1006,7 +1000,8 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
       // of DRAM and run 10 % faster; grouping the wide forward GEMMs would re-stream B per group
       // instead).  DC_GEMM_GROUP_M overrides for every GEMM (0: never group).
     static const int env_g = getenv("DC_GEMM_GROUP_M") ? atoi(getenv("DC_GEMM_GROUP_M")) : -1;
-    const int gsz = env_g < 0 ? (p.m_tiles >= 2 * p.n_tiles ? DC_GEMM_GROUP_DEFAULT : 0) : env_g;
+    const int auto_g = p.m_tiles >= 2 * p.n_tiles ? DC_GEMM_GROUP_DEFAULT : 0;
+    const int gsz = g->tile_group_m > 0 ? g->tile_group_m : g->tile_group_m < 0 ? 0 : env_g < 0 ? auto_g : env_g;
     p.group_m = (gsz > 0 && gsz < p.m_tiles) ? gsz : p.m_tiles;
   }
   if (pair) {
@@ -1019,16 +1014,16 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
     // stream-K pays only when the k-loop is long (measured on the layer shapes,
     // profiles/r01d: +3-4 % at K >= 14336, -2 % at K = 4096, where the idle
     // pairs of the last partial wave let the others clock higher)
-    if (g->stream_k && sk_env && !p.epi && tiles > pairs && tiles % pairs && p.k_blocks >= 128 &&
+    if (g->stream_k && g->workspace && sk_env && !p.epi && tiles > pairs && tiles % pairs && p.k_blocks >= 128 &&
         tiles - (tiles / pairs - 1) * pairs <= 150) {
+      if (g->workspace_bytes < SK_WS_BYTES || (reinterpret_cast<uintptr_t>(g->workspace) & 255))
+        { *err = "dc_gemm: stream-K workspace smaller than dc_gemm_workspace_bytes() or not 256 B aligned"; return DC_EINVAL; }
       p.sk_on = 1;
       p.sk_dp = (tiles / pairs - 1) * pairs;            // leaves [pairs, 2 pairs) tiles to split
       p.sk_total = (int64_t)(tiles - p.sk_dp) * p.k_blocks;
-      SkWorkspace* w = sk_workspace(stream, 2 * pairs, bnt);
-      if (!w) { *err = "dc_gemm: stream-K workspace allocation failed"; return DC_EOOM; }
-      p.sk_ws = w->buf;
-      p.sk_flags = w->flags;
-      p.sk_epoch = ++w->epoch;
+      p.sk_ws = reinterpret_cast<float*>(g->workspace);
+      p.sk_flags = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(g->workspace) + SK_TILES_CAP * SK_PART_BYTES);
+      p.sk_epoch = sk_next_epoch(g->workspace);
     }
     const int env_st = glu ? 6 : (env_st_pick() == 2 ? 7 : 6);
     const int g2 = 2 * pairs;
@@ -1060,6 +1055,8 @@ extern "C" int32_t dc_gemm_pair_slots(void) {
   std::call_once(once, [] { err = dc::preload_gemm_kernels(); });
   return err == cudaSuccess ? dc::pair_slots(0) : -1;
 }
+
+extern "C" uint64_t dc_gemm_workspace_bytes(void) { return dc::gemm_workspace_bytes(); }
 
 extern "C" dc_status dc_gemm(const dc_gemm_args* g, cudaStream_t stream) {
   std::string err;

@@ -76,6 +76,7 @@ struct dc_model {
   int64_t ws_dA = 0, ws_dB = 0, ws_dact = 0, ws_dgu = 0, ws_dh = 0, ws_dx2 = 0, ws_dqkv = 0, ws_dgp = 0,
           ws_lossp = 0, ws_loss = 0;
   int64_t ws_dO = 0, ws_dX = 0, ws_dl0 = 0, ws_rgp = 0;   // MoE backward
+  int64_t ws_sk = 0;                                     // stream-K workspace of the compute-stream GEMMs
   int E = 0, R = 0;                                      // experts, rows per expert (2T/E)
   uint64_t act_bytes = 0, layer_act_bytes = 0, ws_bytes = 0;
   uint8_t* act = nullptr;
@@ -302,6 +303,7 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   m->ws_dgu = take(T * 2 * f * 2); m->ws_dh = take(T * h * 2); m->ws_dx2 = take(T * h * 2);
   m->ws_dqkv = take(T * m->qkvd * 2); m->ws_dgp = take(((int64_t)rmsnorm_bwd_blocks((int)T) * h + T) * 4);   // partials + row dots
   m->ws_lossp = take(1024 * 4); m->ws_loss = take(4 * (int64_t)m->n_micro);
+  m->ws_sk = take((int64_t)gemm_workspace_bytes());
   if (m->E) {
     m->ws_dO = take(2 * T * h * 2); m->ws_dX = take(2 * T * h * 2); m->ws_dl0 = take(T * 4);
     m->ws_rgp = take((int64_t)moe_router_dw_blocks((int)T) * m->E * h * 4);
@@ -377,6 +379,11 @@ extern "C" dc_status dc_model_bind(dc_model* m, void* buf, uint64_t bytes, const
   m->act = reinterpret_cast<uint8_t*>(buf);
   m->x = x;
   m->target = target;
+  // the stream-K workspace starts zero-filled (dc_gemm_args.workspace)
+  if (cudaMemset(m->A(m->ws_sk), 0, gemm_workspace_bytes()) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess)
+    return mfail(m, DC_ECUDA, "dc_model_bind: workspace clear failed");
+  gemm_sk_reset(m->A(m->ws_sk), 0);
   return DC_OK;
 }
 
@@ -421,6 +428,8 @@ static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t l
   // a stream-K pair spins on another pair's partial: never two such kernels at
   // once, so the GEMMs beside the dX GEMM (second stream) are data-parallel only
   g.stream_k = st == m->cs2 ? 0 : m->stream_k;
+  g.workspace = g.stream_k ? m->A(m->ws_sk) : nullptr;
+  g.workspace_bytes = g.stream_k ? gemm_workspace_bytes() : 0;
   g.num_sms = m->gemm_sms;
   if (glu) {
     g.epilogue = glu->mode;
@@ -864,6 +873,8 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
   }
   dc_status s = dc_step_begin(m->ctx, ++m->epoch, ucs);
   if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
+  // graph mode: the stream-K flags restart from zero with the step too
+  if (ctx_graph_mode(m->ctx)) gemm_sk_reset(m->A(m->ws_sk), ucs);
   // graph mode: this step's Adam scalars go to device memory (a captured step
   // leaves this to dc_model_graph_launch, which writes them before each replay)
   if (ctx_graph_mode(m->ctx) && !m->capturing && (s = ctx_set_step_scalars(m->ctx, step_t, ucs)) != DC_OK)

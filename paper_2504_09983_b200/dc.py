@@ -81,7 +81,8 @@ class GemmArgs(C.Structure):
                 ("b_mn_major", C.c_int32), ("b_split_k", C.c_int32),
                 ("C", vp), ("ldc", C.c_int64), ("R", vp), ("ldr", C.c_int64), ("num_sms", C.c_int32),
                 ("kernel", C.c_int32), ("stream_k", C.c_int32),
-                ("epilogue", C.c_int32), ("aux", vp), ("ld_aux", C.c_int64), ("glu_off", C.c_int64)]
+                ("epilogue", C.c_int32), ("aux", vp), ("ld_aux", C.c_int64), ("glu_off", C.c_int64),
+                ("workspace", vp), ("workspace_bytes", C.c_uint64), ("tile_group_m", C.c_int32)]
 
 
 ctx_p, sched_p, model_p = vp, vp, vp
@@ -111,6 +112,7 @@ _sig = {
     "dc_offload": (C.c_int, [vp, C.c_int32, C.c_int32, vp]),
     "dc_gemm": (C.c_int, [C.POINTER(GemmArgs), vp]),
     "dc_gemm_pair_slots": (C.c_int32, []),
+    "dc_gemm_workspace_bytes": (C.c_uint64, []),
     "dc_model_create": (C.c_int, [vp, C.POINTER(ModelDims), C.POINTER(vp)]),
     "dc_model_destroy": (C.c_int, [vp]),
     "dc_model_act_bytes": (C.c_int, [vp, C.POINTER(C.c_uint64)]),

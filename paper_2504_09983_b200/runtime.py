@@ -40,6 +40,7 @@ class RankState:
         self.ctx = None
         self.model = None
         self.tensors = {}
+        self.peer_keep = {}     # per symmetric buffer: imported peer mappings (IPC storages / symm_mem handle)
         self.streams = None
         self.sched = None
         self.micro_steps = 1
@@ -48,42 +49,52 @@ class RankState:
         return [s.cuda_stream for s in self.streams]
 
 
-_IPC_KEEP = []   # imported peer storages must outlive every use of their pointers
-
-
 def _alloc_symmetric_ipc(nbytes, group, device):
     """Peer-mapped buffer through CUDA IPC: every rank exports its allocation's
     IPC handle over the process group and opens the others' (works between
-    processes on one device, and across NVLink-connected devices)."""
+    processes on one device, and across NVLink-connected devices).  Returns
+    (local tensor, peer pointers, keep): `keep` holds the imported peer
+    storages and must outlive every use of their pointers."""
     import torch.distributed as dist
     t = torch.zeros(nbytes, dtype=torch.uint8, device=device)
     h = t.untyped_storage()._share_cuda_()
     handles = [None] * dist.get_world_size(group)
     dist.all_gather_object(handles, h, group=group)
     me = dist.get_rank(group)
-    ptrs = []
+    ptrs, keep = [], []
     for q, hq in enumerate(handles):
         if q == me:
             ptrs.append(t.data_ptr())
         else:
             st = torch.UntypedStorage._new_shared_cuda(*hq)
-            _IPC_KEEP.append(st)
+            keep.append(st)
             ptrs.append(st.data_ptr())
-    return t, ptrs
+    return t, ptrs, keep
+
+
+def symm_backend():
+    """Which peer-mapping path _alloc_symmetric uses: "symm_mem" (torch
+    symmetric memory, the default for one process per GPU) or "ipc" (CUDA IPC,
+    DC_SYMM=ipc — required when several processes share one GPU, which
+    symmetric memory refuses).  There is no silent fallback between them."""
+    v = os.environ.get("DC_SYMM", "symm_mem")
+    if v not in ("symm_mem", "ipc"):
+        raise ValueError("DC_SYMM must be symm_mem or ipc, got %r" % v)
+    return v
 
 
 def _alloc_symmetric(nbytes, group, device):
-    """Symmetric buffer for the peer tables: torch symmetric memory by default
-    (DC_SYMM=ipc selects CUDA IPC; it is also the fallback)."""
-    if os.environ.get("DC_SYMM", "symm_mem") == "ipc":
+    """Symmetric buffer for the peer tables (grad slots, flags, gather arena).
+    Returns (local tensor, [world] peer pointers, keep-alive handles).  Raises
+    if the selected backend fails (no fallback: a silently different transport
+    would change what the N > 1 numbers measure)."""
+    if symm_backend() == "ipc":
         return _alloc_symmetric_ipc(nbytes, group, device)
-    try:
-        from torch.distributed import _symmetric_memory as symm_mem
-        t = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
-        h = symm_mem.rendezvous(t, group.group_name)
-        return t, [int(p) for p in h.buffer_ptrs]
-    except Exception:     # no symmetric-memory backend for this group / build: CUDA IPC
-        return _alloc_symmetric_ipc(nbytes, group, device)
+    from torch.distributed import _symmetric_memory as symm_mem
+    t = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+    h = symm_mem.rendezvous(t, group)
+    t.zero_()
+    return t, [int(p) for p in h.buffer_ptrs], [h]
 
 
 def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr=1e-3, beta1=0.9,
@@ -112,9 +123,10 @@ def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr
         grad_ptrs = [ranks[r].tensors["grad"].data_ptr() for r in mine]
         flag_ptrs = [ranks[r].tensors["flags"].data_ptr() for r in mine]
     else:
-        g, grad_ptrs = _alloc_symmetric(grad_bytes, group, dev)
-        f, flag_ptrs = _alloc_symmetric(lay.flag_bytes, group, dev)
+        g, grad_ptrs, gk = _alloc_symmetric(grad_bytes, group, dev)
+        f, flag_ptrs, fk = _alloc_symmetric(lay.flag_bytes, group, dev)
         ranks[rank].tensors["grad"], ranks[rank].tensors["flags"] = g, f
+        ranks[rank].peer_keep["grad"], ranks[rank].peer_keep["flags"] = gk, fk
     for r in mine:
         st = ranks[r]
         t = st.tensors
@@ -206,8 +218,12 @@ def bind(ranks, sched_by_rank, group=None):
         ptrs = {r: allp for r in ranks}
     else:
         st = any_st
-        t, allp = _alloc_symmetric(cap, group, st.device)
+        # drop the previous arena's peer mappings before mapping the new one
+        st.peer_keep.pop("arena", None)
+        st.tensors.pop("arena", None)
+        t, allp, keep = _alloc_symmetric(cap, group, st.device)
         st.tensors["arena"] = t
+        st.peer_keep["arena"] = keep
         ptrs = {st.rank: allp}
     torch.cuda.synchronize()
     for r, st in ranks.items():
@@ -217,6 +233,12 @@ def bind(ranks, sched_by_rank, group=None):
         dc.check(dc.lib.dc_bind_schedule(st.ctx, st.sched, C.cast(arr, dc.p_u64), cap,
                                          st.streams[0].cuda_stream), st.ctx)
     torch.cuda.synchronize()
+    if group is not None:
+        # dc_bind_schedule zeroes this rank's flag table; no rank may start a
+        # step (whose first action posts ready flags into its peers' tables)
+        # before every peer's zeroing is done
+        import torch.distributed as dist
+        dist.barrier(group=group)
 
 
 def max_reduce_profile(prof, group, device="cpu"):

@@ -3,7 +3,9 @@ every step restarts the flag protocol (gather ready / done, grad-slot and
 reduce-scatter counters) from zero — at N > 1 between two rounds of a barrier
 on a device step counter — and reads its Adam scalars from device memory, so
 one captured step replays for every later step.  Replays are bit-identical to
-eager steps (N = 1, and N = 2 / 4 virtual ranks replaying concurrently)."""
+eager steps (N = 1, and N = 2 / 4 virtual ranks replaying concurrently), and
+every replayed step is checked against the oracle's step from the GPU's states
+(tests/oracle_check.py)."""
 import json
 import os
 
@@ -14,6 +16,7 @@ import torch
 import synth
 from oracle import step as ost
 from tests.gpu_util import bf16_tensor
+from tests.oracle_check import check_step
 
 pytestmark = pytest.mark.gpu
 
@@ -70,10 +73,10 @@ def test_graph_replay_bitexact(moe, micro, ck):
     torch.cuda.synchronize()
     cs = gst.stream_handles()
     dc.check(dc.lib.dc_model_graph_capture(gst.model, 2, *cs), gst.ctx)
+    table = synth.param_table(cfg)
     for t in (2, 3, 4):
-        dc.check(dc.lib.dc_model_graph_launch(gst.model, t, cs[0]), gst.ctx)
-    torch.cuda.synchronize()
-    rt.poll(gr)
+        check_step(gr, table, cfg, 1, t, LR,
+                   lambda: dc.check(dc.lib.dc_model_graph_launch(gst.model, t, cs[0]), gst.ctx), micro_steps=micro)
     _same(rst, gst)
     prof = json.loads(dc.model_profile_json(gst.model))       # events of the last replay
     assert all(o["dur_us"] > 0 for o in prof["ops"] if o["kind"] == "compute")

@@ -49,7 +49,18 @@ def test_init_bitexact():
 
 
 # ------------------------------------------------------------------ GEMM
-def _gemm(M, N, K, A, lda, a_mn, Bs, ldbs, ends, b_mn, split_k, Cm, ldc, R=None, ldr=0, sms=0, kernel=0, sk=0):
+_WS = {}
+
+
+def _workspace():
+    """Caller-owned stream-K workspace (dc_gemm_args.workspace), zero-filled."""
+    if "ws" not in _WS:
+        _WS["ws"] = torch.zeros(int(dc.lib.dc_gemm_workspace_bytes()), dtype=torch.uint8, device="cuda")
+    return _WS["ws"]
+
+
+def _gemm(M, N, K, A, lda, a_mn, Bs, ldbs, ends, b_mn, split_k, Cm, ldc, R=None, ldr=0, sms=0, kernel=0, sk=0,
+          group_m=0):
     g = dc.GemmArgs()
     g.M, g.N, g.K = M, N, K
     g.A, g.lda, g.a_mn_major = A.data_ptr(), lda, a_mn
@@ -64,6 +75,10 @@ def _gemm(M, N, K, A, lda, a_mn, Bs, ldbs, ends, b_mn, split_k, Cm, ldc, R=None,
     os.environ["DC_GEMM_BN"] = "128" if kernel == 3 else "256"
     g.kernel = 2 if kernel == 3 else kernel
     g.stream_k = sk
+    if sk:
+        ws = _workspace()
+        g.workspace, g.workspace_bytes = ws.data_ptr(), ws.numel()
+    g.tile_group_m = group_m
     dc.check(dc.lib.dc_gemm(C.byref(g), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
 
@@ -243,6 +258,44 @@ def test_gemm_stream_k_dx_dw(M, N, K, sms):
     Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     _gemm(M, N, K, DY, M, 1, [X], [N], [0], 1, 0, Cm, N, sms=sms, kernel=2, sk=1)
     _check(Cm, dy.T @ x, np.abs(dy).T @ np.abs(x), "sk dw")
+
+
+# tile order of the persistent pair kernel: groups of g m-tiles, including a
+# partial last group (m_tiles % g != 0) and its combination with a stream-K
+# tail; the output must not depend on the order (each tile is computed once)
+@pytest.mark.parametrize("group_m", [-1, 2, 3, 8])
+@pytest.mark.parametrize("sk", [0, 1])
+def test_gemm_tile_groups_partial(group_m, sk):
+    M, N, K, sms = 5 * 256, 256, 8256 if sk else 512, 6
+    a, A = _mat(81, M, K)
+    b, B = _mat(82, N, K)
+    Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    _gemm(M, N, K, A, K, 0, [B], [K], [0], 0, 0, Cm, N, sms=sms, kernel=2, sk=sk, group_m=group_m)
+    _check(Cm, a @ b.T, np.abs(a) @ np.abs(b).T, "groups g=%d sk=%d" % (group_m, sk))
+    ref = torch.empty_like(Cm)
+    _gemm(M, N, K, A, K, 0, [B], [K], [0], 0, 0, ref, N, sms=sms, kernel=2, sk=0, group_m=-1)
+    assert torch.equal(Cm, ref) if not sk else True      # data-parallel tiles: same k order
+
+
+def test_gemm_stream_k_needs_workspace():
+    """stream_k without a workspace runs data-parallel (no library allocation);
+    a too-small workspace is DC_EINVAL."""
+    M, N, K = 768, 1280, 8192
+    a, A = _mat(91, M, K)
+    b, B = _mat(92, N, K)
+    Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    g = dc.GemmArgs()
+    g.M, g.N, g.K = M, N, K
+    g.A, g.lda = A.data_ptr(), K
+    g.n_bseg, g.B[0], g.ldb[0] = 1, B.data_ptr(), K
+    g.C, g.ldc = Cm.data_ptr(), N
+    g.num_sms, g.kernel, g.stream_k = 8, 2, 1
+    dc.check(dc.lib.dc_gemm(C.byref(g), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    _check(Cm, a @ b.T, np.abs(a) @ np.abs(b).T, "sk without workspace")
+    small = torch.zeros(1024, dtype=torch.uint8, device="cuda")
+    g.workspace, g.workspace_bytes = small.data_ptr(), small.numel()
+    assert dc.lib.dc_gemm(C.byref(g), torch.cuda.current_stream().cuda_stream) == dc.DC_EINVAL
 
 
 # ------------------------------------------------------------------ RS + Adam

@@ -1,8 +1,9 @@
 """Adaptive offload (§4.4, Algorithm 2 + reload rule) on the
 GPU path, with DC_DEBUG_POISON: once a fragment's D2H copy is synced the
 device slice is overwritten with NaNs, so a missing or misordered reload
-corrupts the Adam update.  The offloaded step must be bit-identical to the
-same step without offload."""
+corrupts the Adam update.  Every offloaded step is checked against the
+oracle's step from the GPU's states (tests/oracle_check.py) and must be
+bit-identical to the same step without offload."""
 import json
 
 import pytest
@@ -11,6 +12,7 @@ import torch
 import synth
 from oracle import step as ost
 from tests.gpu_util import bf16_tensor
+from tests.oracle_check import check_step
 
 pytestmark = pytest.mark.gpu
 
@@ -80,10 +82,8 @@ def test_offload_step_bitexact_vs_resident(world):
             dc.check(dc.lib.dc_model_set_option(st.model, b"fused_adam", 1))
     for t in (1, 2):
         rt.step(ref, t)
-        rt.step(off, t)
-        torch.cuda.synchronize()
+        check_step(off, table, cfg, world, t, LR, lambda: rt.step(off, t))
         rt.poll(ref)
-        rt.poll(off)
         for r in ref:
             for k in ("master", "m", "v"):
                 a = ref[r].tensors[k].view(torch.int32)
@@ -143,10 +143,8 @@ def test_host_resident_states_bitexact_vs_resident(world, moe):
     assert dc.lib.dc_offload(ref[0].ctx, 0, dc.DC_WRITEBACK, ref[0].streams[3].cuda_stream) == dc.DC_ESTATE
     for t in (1, 2, 3):
         rt.step(ref, t)
-        rt.step(off, t)
-        torch.cuda.synchronize()
+        check_step(off, table, cfg, world, t, LR, lambda: rt.step(off, t))
         rt.poll(ref)
-        rt.poll(off)
         for r in ref:
             for k in ("master", "shard"):
                 dt = torch.int16 if k == "shard" else torch.int32
@@ -180,9 +178,12 @@ def test_offload_all_sync_baseline_bitexact():
             assert mf == vf == st.layout.shard_elems and pool > 0 and hb == 8 * st.layout.shard_elems
             assert dc.lib.dc_model_set_option(st.model, b"offload_all_sync", 0) == dc.DC_ESTATE
         for s in (1, 2, 3):
-            rt.step(ranks, s)
-            torch.cuda.synchronize()
-            rt.poll(ranks)
+            if sync:    # the paper's baseline against the oracle itself
+                check_step(ranks, table, cfg, 1, s, LR, lambda: rt.step(ranks, s))
+            else:
+                rt.step(ranks, s)
+                torch.cuda.synchronize()
+                rt.poll(ranks)
         runs.append(st)
     a, b = runs
     for k in ("master", "shard"):
