@@ -107,6 +107,8 @@ struct dc_ctx {
   std::vector<int> layer_use;
   uint32_t rs_done_total = 0;
   int rs_ctas = 0, rs_threads = 256, rs_ctas_default = 296;
+  int rs_bulk = 0;                      // 1: bulk-copy pipelined rs_adam (UPDATE / FINAL), one CTA per SM
+  int num_sms = 148;
   // error record (ERR_RECORD_WORDS words): host-mapped pinned, written by the
   // device on a flag-wait timeout: code, claimed, target, observed, address
   uint32_t* err_host = nullptr;
@@ -248,6 +250,8 @@ extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
   if (const char* e = getenv("DC_RS_CTAS")) c->rs_ctas = std::max(1, atoi(e));
   if (const char* e = getenv("DC_RS_THREADS")) c->rs_threads = atoi(e) == 128 ? 128 : 256;
   DC_CUDA_TRY(cudaSetDevice(a->device), &c->err);
+  DC_CUDA_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, a->device), &c->err);
+  if (const char* e = getenv("DC_RS_BULK")) c->rs_bulk = atoi(e) != 0;
   DC_CUDA_TRY(preload_glue_kernels(), &c->err);
   DC_CUDA_TRY(preload_comm_kernels(), &c->err);
   DC_CUDA_TRY(preload_gemm_kernels(), &c->err);
@@ -442,6 +446,10 @@ extern "C" dc_status dc_set_option(dc_ctx* c, const char* key, int64_t value) {
     c->graph_mode = value != 0;
     return DC_OK;
   }
+  if (!strcmp(key, "rs_bulk")) {   // may change between steps (the launch reads it)
+    c->rs_bulk = value != 0;
+    return DC_OK;
+  }
   if (!strcmp(key, "ag_copy_engine")) {
     if (c->sched) return fail(c, DC_ESTATE, "dc_set_option: ag_copy_engine must be set before dc_bind_schedule");
     c->ag_ce = value != 0;
@@ -582,14 +590,20 @@ dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, con
   const double bc2 = 1.0 - std::pow(c->beta2, step_t);
   const float sc = (float)(c->lr / bc1);
   const float cc = (float)std::sqrt(bc2);
+  const bool bulk = c->rs_bulk && (mode == RS_UPDATE || mode == RS_FINAL);
   int ctas = (int)std::min<int64_t>(c->rs_ctas, std::max<int64_t>(1, elems / 8 / c->rs_threads));
+  if (bulk) {   // one CTA per SM (or per chunk, if fewer)
+    int64_t chunks = 0;
+    for (int i : params) chunks += (c->L.S[i] + RS_BULK_CHUNK - 1) / RS_BULK_CHUNK;
+    ctas = (int)std::min<int64_t>(c->num_sms, std::max<int64_t>(1, chunks));
+  }
   c->rs_done_total += (uint32_t)ctas;
   dc_status r = k_rs_adam(mem, c->world, c->rank, slots.data(), c->myflag(c->L.f_gready + (int64_t)s * c->world),
                           (uint32_t)u, peers_at(c, c->L.f_gcons + (int64_t)s * c->world + c->rank), (uint32_t)u,
                           c->myflag(c->L.f_rsdone), c->rs_done_total, c->master, mb, vb, c->shard, c->grad_acc,
                           mode, n, sc, cc,
                           c->beta1, c->beta2, c->eps, ctas, c->rs_threads, c->timeout_ns, c->err_dev, st,
-                          c->graph_mode ? reinterpret_cast<const float*>(c->myflag(c->L.f_scal)) : nullptr);
+                          c->graph_mode ? reinterpret_cast<const float*>(c->myflag(c->L.f_scal)) : nullptr, bulk);
   if (r != DC_OK) return fail(c, r, "dc_reduce_scatter_step: launch failed");
   return DC_OK;
 }

@@ -335,12 +335,165 @@ __global__ void __launch_bounds__(256, DC_RS_MINB) rs_adam_kernel(const RsParams
   }
 }
 
+// ------------------------------------------------------------------ rs_adam (bulk-copy pipeline)
+// The same arithmetic as rs_adam_kernel (UPDATE / FINAL modes), with the
+// memory side moved onto the copy engines of the SM: one producer thread
+// streams 2048-element chunks of every input (fp32 master / m / v [/ acc], the
+// bf16 grad slice of every rank) into a ring of shared-memory stages with
+// cp.async.bulk (completion on an mbarrier), 16 consumer warps apply the
+// update in place in shared memory (4 elements per thread: conflict-free
+// 16-byte accesses) and one consumer thread writes the stage back with bulk
+// stores.  The loads of the next stages stay in flight while the consumers do
+// the IEEE divisions / square roots, so the HBM stream does not stall on the
+// arithmetic (the register-bound LDG kernel keeps ~2 groups of 8 elements in
+// flight per thread and alternates between the two).
+constexpr int RSB_CH = RS_BULK_CHUNK;        // elements per chunk
+constexpr int RSB_CONSUMERS = 512;           // 16 warps, 4 elements each per chunk
+constexpr int RSB_THREADS = RSB_CONSUMERS + 32;
+template <int MAXQ, bool ACC>
+struct RsBulk {
+  static constexpr int STAGE = RSB_CH * (12 + 2 * MAXQ + 2 + (ACC ? 4 : 0));   // p m v, grads, shard, acc
+  static constexpr int ST = (200 * 1024 / STAGE) < 8 ? (200 * 1024 / STAGE) : 8;
+  static constexpr int SMEM = ST * STAGE + 2 * ST * 8 + 128;
+};
+
+__device__ __forceinline__ void bulk_g2s(void* s, const void* g, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               :: "r"(ptx::smem_u32(s)), "l"(g), "r"(bytes), "r"(ptx::smem_u32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* g, const void* s, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+               :: "l"(g), "r"(ptx::smem_u32(s)), "r"(bytes), "l"(pol) : "memory");
+}
+
+template <int MAXQ, int MODE>
+__global__ void __launch_bounds__(RSB_THREADS, 1) rs_adam_bulk_kernel(const RsParams p) {
+  constexpr bool ACC = MODE == RS_FINAL;
+  using B = RsBulk<MAXQ, ACC>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + B::ST * B::STAGE);
+  uint64_t* empty = full + B::ST;
+  // member chunk prefix (units = chunks of RSB_CH elements, member-major)
+  __shared__ int64_t cum[RS_MAXM + 1];
+  if (threadIdx.x == 0) {
+    cum[0] = 0;
+    for (int i = 0; i < p.nm; ++i) cum[i + 1] = cum[i] + (p.S[i] + RSB_CH - 1) / RSB_CH;
+    for (int s = 0; s < B::ST; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t units = cum[p.nm];
+  const uint64_t pol = policy_evict_first();
+  auto locate = [&](int64_t u, int& mi, int64_t& e0, int& n) {
+    mi = 0;
+    while (cum[mi + 1] <= u) ++mi;
+    e0 = (u - cum[mi]) * RSB_CH;
+    const int64_t rem = p.S[mi] - e0;
+    n = (int)(rem < RSB_CH ? rem : RSB_CH);
+  };
+  const int warp = threadIdx.x / 32;
+  if (warp == RSB_CONSUMERS / 32) {            // producer warp: one thread issues every load
+    if (threadIdx.x % 32 == 0) {
+      int k = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+        const int s = k % B::ST;
+        if (k >= B::ST) ptx::mbar_wait(&empty[s], ((k / B::ST) - 1) & 1);
+        int mi, n;
+        int64_t e0;
+        locate(u, mi, e0, n);
+        uint8_t* b = smem + (size_t)s * B::STAGE;
+        const int64_t so = p.store_off[mi] + e0;
+        const uint32_t f4 = (uint32_t)n * 4, h2 = (uint32_t)n * 2;
+        ptx::mbar_arrive_expect_tx(&full[s], 3 * f4 + p.world * h2 + (ACC ? f4 : 0));
+        bulk_g2s(b, p.master + so, f4, &full[s], pol);
+        bulk_g2s(b + RSB_CH * 4, p.m + so, f4, &full[s], pol);
+        bulk_g2s(b + RSB_CH * 8, p.v + so, f4, &full[s], pol);
+        const int64_t gb = p.goff[mi] + ((int64_t)p.rank * p.S[mi] + e0) * 2;
+        for (int q = 0; q < p.world; ++q) bulk_g2s(b + RSB_CH * (12 + 2 * q), p.slot[q] + gb, h2, &full[s], pol);
+        if constexpr (ACC) bulk_g2s(b + RSB_CH * (14 + 2 * MAXQ), p.acc + so, f4, &full[s], pol);
+      }
+    }
+  } else {                                     // consumers
+    const AdamScalars a{p.w1, p.w2, p.b2, p.scal ? -p.scal[0] : p.neg_s, p.scal ? p.scal[1] : p.c, p.eps, p.invN};
+    const int t = threadIdx.x;
+    int k = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+      const int s = k % B::ST;
+      int mi, n;
+      int64_t e0;
+      locate(u, mi, e0, n);
+      ptx::mbar_wait(&full[s], (k / B::ST) & 1);
+      uint8_t* b = smem + (size_t)s * B::STAGE;
+      if (4 * t < n) {
+        float4* P = reinterpret_cast<float4*>(b) + t;
+        float4* M = reinterpret_cast<float4*>(b + RSB_CH * 4) + t;
+        float4* V = reinterpret_cast<float4*>(b + RSB_CH * 8) + t;
+        float g[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {       // ascending rank from +0.0 (reading D19)
+          if (q < p.world) {
+            const uint2 raw = reinterpret_cast<const uint2*>(b + RSB_CH * (12 + 2 * q))[t];
+            const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+            const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+            g[0] = __fadd_rn(g[0], lo.x); g[1] = __fadd_rn(g[1], lo.y);
+            g[2] = __fadd_rn(g[2], hi.x); g[3] = __fadd_rn(g[3], hi.y);
+          }
+        }
+        if constexpr (ACC) {
+          const float4 A = reinterpret_cast<const float4*>(b + RSB_CH * (14 + 2 * MAXQ))[t];
+          g[0] = __fadd_rn(A.x, g[0]); g[1] = __fadd_rn(A.y, g[1]);
+          g[2] = __fadd_rn(A.z, g[2]); g[3] = __fadd_rn(A.w, g[3]);
+        }
+        float4 pp = *P, mm = *M, vv = *V;
+        adam_elem(g[0], pp.x, mm.x, vv.x, a);
+        adam_elem(g[1], pp.y, mm.y, vv.y, a);
+        adam_elem(g[2], pp.z, mm.z, vv.z, a);
+        adam_elem(g[3], pp.w, mm.w, vv.w, a);
+        *P = pp; *M = mm; *V = vv;
+        const __nv_bfloat162 s0 = __floats2bfloat162_rn(pp.x, pp.y), s1 = __floats2bfloat162_rn(pp.z, pp.w);
+        uint2 o;
+        o.x = *reinterpret_cast<const uint32_t*>(&s0);
+        o.y = *reinterpret_cast<const uint32_t*>(&s1);
+        reinterpret_cast<uint2*>(b + RSB_CH * (12 + 2 * MAXQ))[t] = o;
+      }
+      ptx::fence_proxy_async_smem();           // generic-proxy smem writes -> visible to the bulk stores
+      ptx::named_bar_sync(1, RSB_CONSUMERS);
+      if (t == 0) {
+        const int64_t so = p.store_off[mi] + e0;
+        const uint32_t f4 = (uint32_t)n * 4;
+        bulk_s2g(p.master + so, b, f4, pol);
+        bulk_s2g(p.m + so, b + RSB_CH * 4, f4, pol);
+        bulk_s2g(p.v + so, b + RSB_CH * 8, f4, pol);
+        bulk_s2g(p.shard + so, b + RSB_CH * (12 + 2 * MAXQ), (uint32_t)n * 2, pol);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        // every store group but the newest has finished reading its stage:
+        // hand the previous stage back to the producer
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (k >= 1) ptx::mbar_arrive(&empty[(k - 1) % B::ST]);
+      }
+    }
+    if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const uint32_t prev = atomicAdd(p.done_ctr, 1u);
+    if (prev + 1 == p.done_target) {            // last CTA: every slice pulled
+      __threadfence_system();
+      for (int q = 0; q < p.world; ++q) ptx::st_release_sys(p.consumed[q], p.consumed_value);
+    }
+  }
+}
+
 dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const uint64_t* slot_peers,
                     const uint32_t* ready_local, uint32_t ready_target, PeerFlags consumed_peers,
                     uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master, float* m,
                     float* v, void* shard, float* acc, int mode, int micro_steps, float s, float c, double beta1,
                     double beta2, double eps, int ctas, int threads, uint64_t timeout_ns, uint32_t* err_flag,
-                    cudaStream_t st, const float* dev_scalars) {
+                    cudaStream_t st, const float* dev_scalars, bool bulk) {
   if (threads != 128 && threads != 256) return DC_EINVAL;
   if (mode < RS_UPDATE || mode > RS_FINAL || (mode != RS_UPDATE && !acc) || micro_steps < 1) return DC_EINVAL;
   if (mem.size() > (size_t)RS_MAXM) return DC_EINVAL;
@@ -375,6 +528,14 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
   count_launch();
   auto launch = [&](auto mode_c) {
     constexpr int MODE = decltype(mode_c)::value;
+    if (bulk && (MODE == RS_UPDATE || MODE == RS_FINAL)) {   // bulk-copy pipeline, one CTA per SM
+      constexpr bool ACC = MODE == RS_FINAL;
+      if (world == 1) rs_adam_bulk_kernel<1, MODE><<<ctas, RSB_THREADS, RsBulk<1, ACC>::SMEM, st>>>(p);
+      else if (world == 2) rs_adam_bulk_kernel<2, MODE><<<ctas, RSB_THREADS, RsBulk<2, ACC>::SMEM, st>>>(p);
+      else if (world <= 4) rs_adam_bulk_kernel<4, MODE><<<ctas, RSB_THREADS, RsBulk<4, ACC>::SMEM, st>>>(p);
+      else rs_adam_bulk_kernel<MAXW, MODE><<<ctas, RSB_THREADS, RsBulk<MAXW, ACC>::SMEM, st>>>(p);
+      return;
+    }
     if (world == 1) rs_adam_kernel<1, MODE><<<ctas, threads, 0, st>>>(p);
     else if (world == 2) rs_adam_kernel<2, MODE><<<ctas, threads, 0, st>>>(p);
     else if (world <= 4) rs_adam_kernel<4, MODE><<<ctas, threads, 0, st>>>(p);
@@ -501,6 +662,18 @@ cudaError_t preload_comm_kernels() {
   cudaFuncAttributes a;
   cudaError_t e = cudaFuncGetAttributes(&a, ag_push_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, wait_flags_kernel);
+  auto pre_bulk = [&](auto mode_c) {
+    constexpr int MODE = decltype(mode_c)::value;
+    constexpr bool ACC = MODE == RS_FINAL;
+#define DC_RSB_ATTR(Q)                                                                              \
+    if (e == cudaSuccess)                                                                           \
+      e = cudaFuncSetAttribute(rs_adam_bulk_kernel<Q, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                               RsBulk<Q, ACC>::SMEM);
+    DC_RSB_ATTR(1) DC_RSB_ATTR(2) DC_RSB_ATTR(4) DC_RSB_ATTR(MAXW)
+#undef DC_RSB_ATTR
+  };
+  pre_bulk(std::integral_constant<int, RS_UPDATE>{});
+  pre_bulk(std::integral_constant<int, RS_FINAL>{});
   auto pre = [&](auto mode_c) {
     constexpr int MODE = decltype(mode_c)::value;
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, rs_adam_kernel<1, MODE>);

@@ -325,17 +325,25 @@ def _ragged_table():
             for i, (l, n) in enumerate(sizes)]
 
 
+RS_BULK = pytest.mark.parametrize("bulk", [0, 1], ids=["ldg", "bulk"])
+
+
+@RS_BULK
 @pytest.mark.parametrize("world,n,ragged", [(1, 1, False), (2, 1, False), (4, 1, False), (1, 2, False),
                                             (2, 3, False), (4, 2, False), (3, 1, True), (8, 2, True)])
-def test_rs_adam_virtual_ranks(world, n, ragged):
+def test_rs_adam_virtual_ranks(world, n, ragged, bulk):
     """rs_adam (n = 1) and its gradient-accumulation modes (n > 1: acc = rs,
     acc += rs, then Adam on (acc + rs) / (N n)) vs the oracle, bit-exact,
     two optimizer steps, the accumulator checked after every micro-step.
-    Ragged: tiny / odd tensors (mostly padding at N = 8) and N = 3 (1/N inexact)."""
+    Ragged: tiny / odd tensors (mostly padding at N = 8) and N = 3 (1/N inexact).
+    bulk: the bulk-copy pipelined kernel (update / final modes) — chunk tails
+    (S % 2048), members smaller than one chunk, more CTAs than chunks."""
     cfg = synth.small_llama(layers=2)
     table = _ragged_table() if ragged else synth.llama_param_table(cfg)
     lr = 1e-3
     ranks = rt.create_ranks(table, world, lr=lr, micro_steps=n)
+    for st in ranks.values():
+        dc.check(dc.lib.dc_set_option(st.ctx, b"rs_bulk", bulk), st.ctx)
     S = [nx.shard_len(p.numel, world) for p in table]
     full = ost.init_full_params(table)
     o_master = [[nx.shard_of(full[i], world, r) for i in range(len(table))] for r in range(world)]
@@ -388,8 +396,9 @@ def test_rs_adam_virtual_ranks(world, n, ragged):
                 assert np.array_equal(sh[off:off + sz], nx.bf16_bits(o_master[r][i]))
 
 
+@RS_BULK
 @pytest.mark.parametrize("world,step", [(1, 7), (2, 1000)])
-def test_rs_adam_random_state(world, step):
+def test_rs_adam_random_state(world, step, bulk):
     """rs_adam on arbitrary optimizer states (random master / m / v, v >= 0
     spanning 12 decades) at a later step t: every rounding of Adam's update —
     the sqrt, both divisions, eps — hits general operands, not the
@@ -398,6 +407,8 @@ def test_rs_adam_random_state(world, step):
     table = _ragged_table()
     lr = 1e-3
     ranks = rt.create_ranks(table, world, lr=lr)
+    for st in ranks.values():
+        dc.check(dc.lib.dc_set_option(st.ctx, b"rs_bulk", bulk), st.ctx)
     S = [nx.shard_len(p.numel, world) for p in table]
     rng = np.random.default_rng(11 + world)
     states = {}

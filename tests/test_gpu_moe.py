@@ -72,8 +72,11 @@ def test_moe_step_matches_oracle(world, passes):
 
 
 def test_moe_layer_outputs_gates_and_routing():
-    """Per layer: the gates (fp32), the expert-major token gather X (exact: a
-    permutation of h2) and the layer output y against the oracle's layer."""
+    """Per layer, given the layer's own input on the GPU (the bf16 x for layer 0,
+    the GPU's layer-0 output for layer 1): the gates (fp32), the expert-major
+    token gather X (exact: a permutation of h2) and the layer output y against
+    the oracle's layer on that input.  (Whole-stack chains against the oracle's
+    own activations: test_moe_step_matches_oracle.)"""
     cfg = synth.small_mixtral(layers=2, seq=128)
     table, ranks, _ = _setup(cfg, 1, dc.DC_PASS_SHARD)
     st = ranks[0]
@@ -106,7 +109,7 @@ def test_moe_layer_outputs_gates_and_routing():
             assert np.array_equal(X[e], h2[om.expert_tokens(T, E, e)])
         y = act(l, 7, T * H, torch.bfloat16).reshape(T, H)
         assert_bf16_close(y, y_ref, "moe layer %d output" % l, rows=T)
-        h = y_ref
+        h = y
 
 
 @pytest.mark.parametrize("world,passes", [(1, dc.DC_PASS_SHARD), (2, PS)])
