@@ -251,6 +251,9 @@ extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
   if (const char* e = getenv("DC_RS_THREADS")) c->rs_threads = atoi(e) == 128 ? 128 : 256;
   DC_CUDA_TRY(cudaSetDevice(a->device), &c->err);
   DC_CUDA_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, a->device), &c->err);
+  // bulk-copy rs_adam at N = 1: 5.75 vs 4.9 TB/s in-step (profiles/r02/rs_bulk/);
+  // at N > 1 the LDG kernel's small CTAs co-reside with the backward GEMMs it overlaps
+  c->rs_bulk = a->world == 1;
   if (const char* e = getenv("DC_RS_BULK")) c->rs_bulk = atoi(e) != 0;
   DC_CUDA_TRY(preload_glue_kernels(), &c->err);
   DC_CUDA_TRY(preload_comm_kernels(), &c->err);
@@ -592,10 +595,10 @@ dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, con
   const float cc = (float)std::sqrt(bc2);
   const bool bulk = c->rs_bulk && (mode == RS_UPDATE || mode == RS_FINAL);
   int ctas = (int)std::min<int64_t>(c->rs_ctas, std::max<int64_t>(1, elems / 8 / c->rs_threads));
-  if (bulk) {   // one CTA per SM (or per chunk, if fewer)
+  if (bulk) {   // a fixed number of CTAs per SM (or one per chunk, if fewer)
     int64_t chunks = 0;
     for (int i : params) chunks += (c->L.S[i] + RS_BULK_CHUNK - 1) / RS_BULK_CHUNK;
-    ctas = (int)std::min<int64_t>(c->num_sms, std::max<int64_t>(1, chunks));
+    ctas = (int)std::min<int64_t>((int64_t)c->num_sms * rs_bulk_ctas_per_sm(), std::max<int64_t>(1, chunks));
   }
   c->rs_done_total += (uint32_t)ctas;
   dc_status r = k_rs_adam(mem, c->world, c->rank, slots.data(), c->myflag(c->L.f_gready + (int64_t)s * c->world),

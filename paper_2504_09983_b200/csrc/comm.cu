@@ -350,10 +350,18 @@ __global__ void __launch_bounds__(256, DC_RS_MINB) rs_adam_kernel(const RsParams
 constexpr int RSB_CH = RS_BULK_CHUNK;        // elements per chunk
 constexpr int RSB_CONSUMERS = 512;           // 16 warps, 4 elements each per chunk
 constexpr int RSB_THREADS = RSB_CONSUMERS + 32;
+#ifndef DC_RSB_CTAS_PER_SM
+#define DC_RSB_CTAS_PER_SM 2    // two independent pipelines per SM: one CTA's arithmetic overlaps the other's barrier / store turn
+#endif
+constexpr int RSB_CTAS_PER_SM = DC_RSB_CTAS_PER_SM;
+int rs_bulk_ctas_per_sm() { return RSB_CTAS_PER_SM; }
+
 template <int MAXQ, bool ACC>
 struct RsBulk {
   static constexpr int STAGE = RSB_CH * (12 + 2 * MAXQ + 2 + (ACC ? 4 : 0));   // p m v, grads, shard, acc
-  static constexpr int ST = (200 * 1024 / STAGE) < 8 ? (200 * 1024 / STAGE) : 8;
+  static constexpr int BUDGET = (220 * 1024) / RSB_CTAS_PER_SM;
+  static constexpr int ST0 = BUDGET / STAGE < 8 ? BUDGET / STAGE : 8;
+  static constexpr int ST = ST0 < 2 ? 2 : ST0;
   static constexpr int SMEM = ST * STAGE + 2 * ST * 8 + 128;
 };
 
@@ -367,7 +375,7 @@ __device__ __forceinline__ void bulk_s2g(void* g, const void* s, uint32_t bytes,
 }
 
 template <int MAXQ, int MODE>
-__global__ void __launch_bounds__(RSB_THREADS, 1) rs_adam_bulk_kernel(const RsParams p) {
+__global__ void __launch_bounds__(RSB_THREADS, RSB_CTAS_PER_SM) rs_adam_bulk_kernel(const RsParams p) {
   constexpr bool ACC = MODE == RS_FINAL;
   using B = RsBulk<MAXQ, ACC>;
   extern __shared__ __align__(128) uint8_t smem[];

@@ -171,6 +171,7 @@ dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const
                     double beta1, double beta2, double eps, int ctas, int threads, uint64_t timeout_ns,
                     uint32_t* err_flag, cudaStream_t st, const float* dev_scalars = nullptr, bool bulk = false);
 constexpr int RS_BULK_CHUNK = 2048;   // elements per chunk of the bulk-copy rs_adam (comm.cu RSB_CH)
+int rs_bulk_ctas_per_sm();             // its resident CTAs per SM (grid = SMs x this)
 // graph mode: write (s, c) of a step into the flag-table words the rs_adam
 // launches read, and reset a stream's stream-K flags / epochs
 void k_set_scalars(float* dst, float s, float c, cudaStream_t st);
