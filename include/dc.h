@@ -179,13 +179,22 @@ dc_status dc_step_begin(dc_ctx* ctx, int32_t epoch, cudaStream_t compute_stream)
  * done_evt (may be NULL) is recorded on ag_stream after the kernel.
  * ------------------------------------------------------------------------ */
 dc_status dc_gather(dc_ctx* ctx, int32_t gather_id, cudaStream_t ag_stream, cudaEvent_t done_evt);
-/* Unsharded tensor of param (row-major, numel elements; padding follows). */
 /* Context options.  "graph_mode" (default 0; before dc_bind_schedule, else
  * DC_ESTATE): see dc_model_graph_capture.  "ag_copy_engine" (default 0): 1 issues every gather's
  * stores as cudaMemcpyAsync peer copies (copy engines; no SM time beside the
  * GEMMs) under the same ready / done flag protocol; bit-identical
- * gathered buffers.  Set before dc_bind_schedule (DC_ESTATE after). */
+ * gathered buffers.  Set before dc_bind_schedule (DC_ESTATE after).
+ * "rs_bulk" (default 1 at N = 1, 0 at N > 1; any time): the reduce-scatter +
+ * Adam of dc_reduce_scatter_step (update / final micro-step) runs as the
+ * bulk-copy pipelined kernel (two CTAs of 544 threads and ~110 KB of shared
+ * memory per SM) instead of the register-streaming one; bit-identical.
+ * "ag_skip_waits" (profiling only, default 0): dc_gather launches the push
+ * without its ready / done flag waits (for ncu, which serialises kernels);
+ * the gathered buffer is then NOT guaranteed complete. */
 dc_status dc_set_option(dc_ctx* ctx, const char* key, int64_t value);
+/* Unsharded tensor of param (row-major, numel elements; padding follows):
+ * valid between its gather's completion and its release.  At N = 1 the
+ * shard itself.  DC_ESTATE if the param is not gathered. */
 dc_status dc_tensor_ptr(const dc_ctx* ctx, int32_t param, void** full_ptr);
 /* Release op `release_id` (schedule op id): posts the ready flags listed in
  * its posts_ready_for to every peer, on compute_stream.  */

@@ -120,6 +120,7 @@ struct dc_ctx {
   std::vector<float*> lay_m, lay_v;     // per layer: m / v base for rs_adam (ring slot) or null
   cudaEvent_t gt_start = nullptr, gt_end = nullptr;   // one-shot gather timing (profiling)
   int ag_ce = 0;                        // 1: gathers as copy-engine peer copies (no SM time)
+  int ag_skip_waits = 0;                // profiling only: push without the ready / done flag waits
   // graph mode (N = 1): every step restarts the grad-slot / rs counters and
   // their flags from zero and reads its Adam scalars from device memory, so a
   // captured step replays unchanged (dc_model_graph_capture)
@@ -433,7 +434,7 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
                     st, c->gt_start)
         : k_ag_push(am, c->world, c->rank, c->arena_peers.data(), c->myflag(c->L.f_ready + (int64_t)gid * c->world),
                     c->fepoch, peers_at(c, c->L.f_done + gid), c->myflag(c->L.f_done + gid), target, ctas,
-                    c->timeout_ns, c->err_dev, st, c->gt_start);
+                    c->timeout_ns, c->err_dev, st, c->gt_start, c->ag_skip_waits != 0);
     if (s != DC_OK) return fail(c, s, "dc_gather: launch failed");
     if (c->gt_end) record_event(c->gt_end, st);
   }
@@ -447,6 +448,14 @@ extern "C" dc_status dc_set_option(dc_ctx* c, const char* key, int64_t value) {
   if (!strcmp(key, "graph_mode")) {
     if (c->sched) return fail(c, DC_ESTATE, "dc_set_option: graph_mode must be set before dc_bind_schedule");
     c->graph_mode = value != 0;
+    return DC_OK;
+  }
+  if (!strcmp(key, "ag_skip_waits")) {
+    // profiling only (ncu serialises kernels, so a flag wait on another rank's
+    // kernel would never return): the push runs without its ready / done
+    // waits — the caller guarantees the receivers' buffers are free and reads
+    // nothing it gathered this way
+    c->ag_skip_waits = value != 0;
     return DC_OK;
   }
   if (!strcmp(key, "rs_bulk")) {   // may change between steps (the launch reads it)

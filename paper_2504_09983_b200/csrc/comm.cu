@@ -118,9 +118,11 @@ __global__ void wait_flags_kernel(const uint32_t* f, int n, uint32_t target, uin
 dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const uint64_t* arena_peers,
                     const uint32_t* ready_local, uint32_t epoch, PeerFlags done_peers, const uint32_t* done_local,
                     uint32_t done_target, int ctas, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st,
-                    cudaEvent_t ev_after_ready) {
-  wait_flags_kernel<<<1, 1, 0, st>>>(ready_local, world, epoch, timeout_ns, err_flag, 0x100u);
-  count_launch();
+                    cudaEvent_t ev_after_ready, bool skip_waits) {
+  if (!skip_waits) {
+    wait_flags_kernel<<<1, 1, 0, st>>>(ready_local, world, epoch, timeout_ns, err_flag, 0x100u);
+    count_launch();
+  }
   if (ev_after_ready) record_event(ev_after_ready, st);
   // members beyond AG_MAXM go to extra launches
   for (size_t b = 0; b < mem.size(); b += AG_MAXM) {
@@ -148,8 +150,10 @@ dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const
     if (cudaGetLastError() != cudaSuccess) return DC_ECUDA;
     count_launch();
   }
-  wait_flags_kernel<<<1, 1, 0, st>>>(done_local, 1, done_target, timeout_ns, err_flag, 0x200u);
-  count_launch();
+  if (!skip_waits) {
+    wait_flags_kernel<<<1, 1, 0, st>>>(done_local, 1, done_target, timeout_ns, err_flag, 0x200u);
+    count_launch();
+  }
   return cudaGetLastError() == cudaSuccess ? DC_OK : DC_ECUDA;
 }
 

@@ -62,6 +62,21 @@ def main():
         # per rank (virtual ranks share the GPU: at N > 1 the device total is N x this)
         return {"ms_median": t, "tb_s_per_rank": elems * (26 + 2 * world) / (t * 1e-3) / 1e12}
 
+    if os.environ.get("RS_SERIAL"):
+        # for ncu (kernels serialised): every rank publishes before any rank's
+        # reduce-scatter waits, all from this thread
+        bulk = int(os.environ.get("DC_RS_BULK", "0"))
+        for t in (1, 2):
+            for st in ranks.values():
+                dc.check(dc.lib.dc_set_option(st.ctx, b"rs_bulk", bulk), st.ctx)
+                dc.check(dc.lib.dc_grad_slot_acquire(st.ctx, 0, st.streams[0].cuda_stream), st.ctx)
+                dc.check(dc.lib.dc_grad_slot_publish(st.ctx, 0, st.streams[0].cuda_stream), st.ctx)
+            torch.cuda.synchronize()
+            for st in ranks.values():
+                dc.check(dc.lib.dc_reduce_scatter_step(st.ctx, 0, t, 0, st.streams[0].cuda_stream), st.ctx)
+            torch.cuda.synchronize()
+        rt.poll(ranks)
+        return
     for _ in range(2):
         out["ldg"] = run(0)
         out["bulk"] = run(1)
