@@ -179,6 +179,11 @@ dc_status dc_step_begin(dc_ctx* ctx, int32_t epoch, cudaStream_t compute_stream)
  * done_evt (may be NULL) is recorded on ag_stream after the kernel.
  * ------------------------------------------------------------------------ */
 dc_status dc_gather(dc_ctx* ctx, int32_t gather_id, cudaStream_t ag_stream, cudaEvent_t done_evt);
+/* Profiling: the NEXT dc_gather (N > 1) records after_ready on ag_stream once
+ * every receiver's ready flag was seen and after_done once every sender's
+ * stores landed here (either may be NULL) — the transfer time T_c of P:305
+ * without the wait for the receivers.  One-shot. */
+dc_status dc_gather_timing(dc_ctx* ctx, cudaEvent_t after_ready, cudaEvent_t after_done);
 /* Context options.  "graph_mode" (default 0; before dc_bind_schedule, else
  * DC_ESTATE): see dc_model_graph_capture.  "ag_copy_engine" (default 0): 1 issues every gather's
  * stores as cudaMemcpyAsync peer copies (copy engines; no SM time beside the

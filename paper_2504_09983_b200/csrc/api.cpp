@@ -121,6 +121,9 @@ struct dc_ctx {
   cudaEvent_t gt_start = nullptr, gt_end = nullptr;   // one-shot gather timing (profiling)
   int ag_ce = 0;                        // 1: gathers as copy-engine peer copies (no SM time)
   int ag_skip_waits = 0;                // profiling only: push without the ready / done flag waits
+  // push CTAs per gather: 64 x 256 threads x 8 x 16 B keeps ~2 MB of stores in
+  // flight (NVLink latency x 900 GB/s) and fits beside a GEMM CTA per SM
+  int ag_max_ctas = 64;
   // graph mode (N = 1): every step restarts the grad-slot / rs counters and
   // their flags from zero and reads its Adam scalars from device memory, so a
   // captured step replays unchanged (dc_model_graph_capture)
@@ -256,6 +259,7 @@ extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
   // at N > 1 the LDG kernel's small CTAs co-reside with the backward GEMMs it overlaps
   c->rs_bulk = a->world == 1;
   if (const char* e = getenv("DC_RS_BULK")) c->rs_bulk = atoi(e) != 0;
+  if (const char* e = getenv("DC_AG_MAX_CTAS")) c->ag_max_ctas = std::max(1, std::min(1024, atoi(e)));
   DC_CUDA_TRY(preload_glue_kernels(), &c->err);
   DC_CUDA_TRY(preload_comm_kernels(), &c->err);
   DC_CUDA_TRY(preload_gemm_kernels(), &c->err);
@@ -335,7 +339,7 @@ extern "C" dc_status dc_bind_schedule(dc_ctx* c, const dc_schedule* s, const uin
       if (nw == 0) c->initial_ready.push_back(id);
       int64_t shard_bytes = 0;
       for (int j = 0; j < nm; ++j) shard_bytes += c->L.S[mem[j]] * 2;
-      int ctas = (int)std::min<int64_t>(64, std::max<int64_t>(1, shard_bytes / (32 * 1024)));
+      int ctas = (int)std::min<int64_t>(c->ag_max_ctas, std::max<int64_t>(1, shard_bytes / (32 * 1024)));
       c->ag_ctas[id] = c->ag_ce ? 1 : ctas;             // done bumps per sender per gather
       c->ag_launches[id] = c->ag_ce ? 1 : (nm + 47) / 48;
     }
@@ -440,6 +444,13 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
   }
   c->gt_start = c->gt_end = nullptr;
   if (done_evt) DC_CUDA_TRY(cudaEventRecord(done_evt, st), &c->err);
+  return DC_OK;
+}
+
+extern "C" dc_status dc_gather_timing(dc_ctx* c, cudaEvent_t after_ready, cudaEvent_t after_done) {
+  if (!c) return fail(c, DC_EINVAL, "dc_gather_timing: null ctx");
+  c->gt_start = after_ready;
+  c->gt_end = after_done;
   return DC_OK;
 }
 

@@ -101,6 +101,7 @@ _sig = {
     "dc_schedule_free": (None, [vp]),
     "dc_bind_schedule": (C.c_int, [vp, vp, p_u64, C.c_uint64, vp]),
     "dc_step_begin": (C.c_int, [vp, C.c_int32, vp]),
+    "dc_gather_timing": (C.c_int, [vp, vp, vp]),
     "dc_gather": (C.c_int, [vp, C.c_int32, vp, vp]),
     "dc_tensor_ptr": (C.c_int, [vp, C.c_int32, C.POINTER(vp)]),
     "dc_release": (C.c_int, [vp, C.c_int32, vp]),

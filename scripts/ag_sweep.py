@@ -7,9 +7,11 @@ with one parameter of each size (one layer each), an S_0 profile of gather /
 consume / release per parameter, dc_plan (passes: shard), dc_bind_schedule,
 then per step dc_step_begin + dc_gather / dc_release on every rank.
 
-Each gather is timed on every rank's AG stream with CUDA events around
-dc_gather (ready wait -> stores -> done wait), max over ranks; median over
-steps.  On one GPU all N ranks' stores land in the same HBM, so the figure of
+Each gather is timed on every rank's AG stream with the events of
+dc_gather_timing: from "every receiver ready" to "every sender's stores landed
+here" (the transfer time T_c the planner uses; the wait for the
+receivers, which on one GPU is dominated by the Python threads' enqueue skew,
+is excluded), max over ranks; median over steps.  On one GPU all N ranks' stores land in the same HBM, so the figure of
 merit is the device's HBM traffic: every rank reads its shard once and writes
 it into N arenas -> V (reads) + N V (writes) bytes per gather, against the
 measured copy peak (MEASURED_PEAKS.json hbm_gbs, read + write).  The
@@ -75,6 +77,10 @@ def sweep(world, sizes, steps, copy_engine, hbm_peak):
     times = {o["id"]: [] for o in ag}
     evs = {r: {o["id"]: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for o in ag}
            for r in ranks}
+    for per in evs.values():             # torch creates the CUDA event at its first record
+        for e0, e1 in per.values():
+            e0.record()
+            e1.record()
 
     def one_step(st, t):
         cs, ags = st.streams[0], st.streams[1]
@@ -84,9 +90,8 @@ def sweep(world, sizes, steps, copy_engine, hbm_peak):
             ev = torch.cuda.Event()
             ev.record(cs)
             ags.wait_event(ev)
-            e0.record(ags)
+            dc.check(dc.lib.dc_gather_timing(st.ctx, C.c_void_p(e0.cuda_event), C.c_void_p(e1.cuda_event)), st.ctx)
             dc.check(dc.lib.dc_gather(st.ctx, o["id"], ags.cuda_stream, None), st.ctx)
-            e1.record(ags)
             cs.wait_event(e1)
             dc.check(dc.lib.dc_release(st.ctx, rel[o["members"][0]], cs.cuda_stream), st.ctx)
         torch.cuda.synchronize()
