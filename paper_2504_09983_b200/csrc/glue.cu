@@ -407,6 +407,156 @@ two_pass:
   count_launch();
 }
 
+// One pass (default): a CTA of up to 512 threads owns the whole width (each
+// thread 8 x CH columns) and a contiguous range of rows, processed in groups
+// of RBF rows.  Per group every input byte is read once: dh and x (prefetched
+// one group ahead, so their loads are in flight during the previous group's
+// reduction), the group's RBF row dots are reduced together (one CTA barrier
+// per group instead of per row), then dx = dres + rstd (dh g - n dot / H) is
+// written and the thread's dg columns accumulate (rows in order).  The last
+// CTA to finish (counter) adds the per-CTA dg partials in CTA order and
+// writes bf16 dg, so no separate column-sum launch.  Deterministic.
+constexpr int RBF = 4;
+template <int CH>
+__global__ void __launch_bounds__(512, 1) rmsnorm_bwd_fused_kernel(
+    const bf16* __restrict__ dh, const bf16* __restrict__ x, const bf16* __restrict__ g,
+    const float* __restrict__ rstd, const bf16* __restrict__ dres, bf16* __restrict__ dx, float* __restrict__ part,
+    uint32_t* __restrict__ counter, bf16* __restrict__ dg, int T, int H, int rows_per_cta) {
+  __shared__ float red[2][RBF][16];
+  __shared__ int last;
+  const int nt = blockDim.x, nw = nt / 32, w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float gg[CH][8], acc[CH][8];
+  bool ok[CH];
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    const int c = (threadIdx.x + j * nt) * 8;
+    ok[j] = c < H;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { gg[j][i] = 0.0f; acc[j][i] = 0.0f; }
+    if (ok[j]) load8(g + c, gg[j]);
+  }
+  const int r0 = blockIdx.x * rows_per_cta, r1 = min(T, r0 + rows_per_cta);
+  uint4 A[RBF][CH], X[RBF][CH];
+  auto fetch = [&](int rb) {
+#pragma unroll
+    for (int r = 0; r < RBF; ++r)
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int c = (threadIdx.x + j * nt) * 8;
+        if (rb + r < r1 && ok[j]) {
+          A[r][j] = *reinterpret_cast<const uint4*>(dh + (int64_t)(rb + r) * H + c);
+          X[r][j] = *reinterpret_cast<const uint4*>(x + (int64_t)(rb + r) * H + c);
+        }
+      }
+  };
+  if (r0 < r1) fetch(r0);
+  int buf = 0;
+  for (int rb = r0; rb < r1; rb += RBF, buf ^= 1) {
+    float a[RBF][CH][8], n[RBF][CH][8], rs[RBF], sdot[RBF];
+#pragma unroll
+    for (int r = 0; r < RBF; ++r) {
+      rs[r] = rb + r < r1 ? rstd[rb + r] : 0.0f;
+      sdot[r] = 0.0f;
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const bf162* ha = reinterpret_cast<const bf162*>(&A[r][j]);
+        const bf162* hx = reinterpret_cast<const bf162*>(&X[r][j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 fa = __bfloat1622float2(ha[i]), fx = __bfloat1622float2(hx[i]);
+          a[r][j][2 * i] = fa.x; a[r][j][2 * i + 1] = fa.y;
+          n[r][j][2 * i] = fx.x * rs[r]; n[r][j][2 * i + 1] = fx.y * rs[r];
+        }
+        if (!(rb + r < r1 && ok[j]))
+#pragma unroll
+          for (int i = 0; i < 8; ++i) { a[r][j][i] = 0.0f; n[r][j][i] = 0.0f; }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sdot[r] = fmaf(a[r][j][i] * gg[j][i], n[r][j][i], sdot[r]);
+      }
+    }
+    if (rb + RBF < r1) fetch(rb + RBF);      // next group's loads in flight across the reduction
+#pragma unroll
+    for (int r = 0; r < RBF; ++r) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sdot[r] += __shfl_xor_sync(0xffffffffu, sdot[r], o);
+      if (lane == 0) red[buf][r][w] = sdot[r];
+    }
+    __syncthreads();                          // (double-buffered `red`: one barrier per group)
+#pragma unroll
+    for (int r = 0; r < RBF; ++r) {
+      float t = 0.0f;
+      for (int q = 0; q < nw; ++q) t += red[buf][r][q];   // warp order: fixed
+      sdot[r] = t / (float)H;
+    }
+#pragma unroll
+    for (int r = 0; r < RBF; ++r) {
+      if (rb + r >= r1) continue;
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        if (!ok[j]) continue;
+        const int c = (threadIdx.x + j * nt) * 8;
+        float d[8];
+        if (dres) load8(dres + (int64_t)(rb + r) * H + c, d);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          acc[j][i] += a[r][j][i] * n[r][j][i];
+          d[i] = (dres ? d[i] : 0.0f) + rs[r] * (a[r][j][i] * gg[j][i] - n[r][j][i] * sdot[r]);
+        }
+        store8(dx + (int64_t)(rb + r) * H + c, d);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    const int c = (threadIdx.x + j * nt) * 8;
+    if (ok[j]) {
+      float4* p4 = reinterpret_cast<float4*>(part + (int64_t)blockIdx.x * H + c);
+      p4[0] = make_float4(acc[j][0], acc[j][1], acc[j][2], acc[j][3]);
+      p4[1] = make_float4(acc[j][4], acc[j][5], acc[j][6], acc[j][7]);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int c = threadIdx.x; c < H; c += nt) {       // CTA order: deterministic
+    float t = 0.0f;
+    for (int b = 0; b < (int)gridDim.x; ++b) t += __ldcg(part + (int64_t)b * H + c);
+    dg[c] = __float2bfloat16_rn(t);
+  }
+  if (threadIdx.x == 0) *counter = 0u;               // ready for the next launch
+}
+
+int rmsnorm_bwd_fused_grid(int T) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = 148;
+  }
+  const int g = (T + RBF - 1) / RBF;
+  return g < sms ? g : sms;
+}
+
+dc_status k_rmsnorm_bwd_dg(const void* dh, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
+                           void* dg, float* part, uint32_t* counter, int T, int H, cudaStream_t st) {
+  if (H % 8 || H > 8192) return DC_EINVAL;
+  const int grid = rmsnorm_bwd_fused_grid(T);
+  const int rows = (T + grid - 1) / grid;
+  int nt = H / 8 < 512 ? H / 8 : 512;
+  nt = (nt + 31) / 32 * 32;
+  if (H <= 8 * nt)
+    rmsnorm_bwd_fused_kernel<1><<<grid, nt, 0, st>>>((const bf16*)dh, (const bf16*)x, (const bf16*)g, rstd,
+                                                     (const bf16*)dres, (bf16*)dx, part, counter, (bf16*)dg, T, H, rows);
+  else
+    rmsnorm_bwd_fused_kernel<2><<<grid, nt, 0, st>>>((const bf16*)dh, (const bf16*)x, (const bf16*)g, rstd,
+                                                     (const bf16*)dres, (bf16*)dx, part, counter, (bf16*)dg, T, H, rows);
+  count_launch();
+  return cudaGetLastError() == cudaSuccess ? DC_OK : DC_ECUDA;
+}
+
 // out[c] = bf16(sum_b p[b][c]): a CTA owns 32 columns; warp w sums rows
 // w, w + 8, ... (coalesced 128 B per row), then the 8 partials are added in
 // warp order (fixed, deterministic)
@@ -602,6 +752,7 @@ cudaError_t preload_glue_kernels() {
                        (const void*)rmsnorm_bwd_kernel<3>, (const void*)rmsnorm_bwd_kernel<4>, (const void*)colsum_kernel,
                        (const void*)rmsnorm_bwd_dot_kernel, (const void*)rmsnorm_bwd_dx_kernel,
                        (const void*)rmsnorm_fwd_warp_kernel,
+                       (const void*)rmsnorm_bwd_fused_kernel<1>, (const void*)rmsnorm_bwd_fused_kernel<2>,
                        (const void*)rmsnorm_bwd_row_kernel<1>, (const void*)rmsnorm_bwd_row_kernel<2>,
                        (const void*)rmsnorm_bwd_row_kernel<4>, (const void*)rmsnorm_bwd_row_kernel<8>,
                        (const void*)rmsnorm_bwd_row_kernel<16>,

@@ -77,6 +77,8 @@ struct dc_model {
           ws_lossp = 0, ws_loss = 0;
   int64_t ws_dO = 0, ws_dX = 0, ws_dl0 = 0, ws_rgp = 0;   // MoE backward
   int64_t ws_sk = 0;                                     // stream-K workspace of the compute-stream GEMMs
+  int64_t ws_rnp = 0, ws_rnc = 0;                        // fused RMSNorm backward: dg partials, counter
+  int rn_two_pass = 0;                                   // A/B: the two-pass RMSNorm backward + colsum
   int E = 0, R = 0;                                      // experts, rows per expert (2T/E)
   uint64_t act_bytes = 0, layer_act_bytes = 0, ws_bytes = 0;
   uint8_t* act = nullptr;
@@ -304,6 +306,8 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   m->ws_dqkv = take(T * m->qkvd * 2); m->ws_dgp = take(((int64_t)rmsnorm_bwd_blocks((int)T) * h + T) * 4);   // partials + row dots
   m->ws_lossp = take(1024 * 4); m->ws_loss = take(4 * (int64_t)m->n_micro);
   m->ws_sk = take((int64_t)gemm_workspace_bytes());
+  m->ws_rnp = take((int64_t)rmsnorm_bwd_fused_grid((int)T) * h * 4);
+  m->ws_rnc = take(256);
   if (m->E) {
     m->ws_dO = take(2 * T * h * 2); m->ws_dX = take(2 * T * h * 2); m->ws_dl0 = take(T * 4);
     m->ws_rgp = take((int64_t)moe_router_dw_blocks((int)T) * m->E * h * 4);
@@ -341,6 +345,7 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
       cudaEventCreateWithFlags(&m->ev_joinw, cudaEventDisableTiming) != cudaSuccess)
     return mfail(nullptr, DC_ECUDA, "dc_model_create: stream creation failed");
   if (const char* e = getenv("DC_DW_CONCURRENT")) m->dw_conc = atoi(e) != 0;   // A/B knob
+  if (const char* e = getenv("DC_RMSNORM_TWO_PASS")) m->rn_two_pass = atoi(e) != 0;   // A/B knob
   *out = m.release();
   return DC_OK;
 }
@@ -379,8 +384,9 @@ extern "C" dc_status dc_model_bind(dc_model* m, void* buf, uint64_t bytes, const
   m->act = reinterpret_cast<uint8_t*>(buf);
   m->x = x;
   m->target = target;
-  // the stream-K workspace starts zero-filled (dc_gemm_args.workspace)
+  // the stream-K workspace and the RMSNorm-backward counter start zero-filled
   if (cudaMemset(m->A(m->ws_sk), 0, gemm_workspace_bytes()) != cudaSuccess ||
+      cudaMemset(m->A(m->ws_rnc), 0, 256) != cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess)
     return mfail(m, DC_ECUDA, "dc_model_bind: workspace clear failed");
   gemm_sk_reset(m->A(m->ws_sk), 0);
@@ -441,6 +447,18 @@ static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t l
   dc_status s = launch_gemm(&g, st, &err, adam, side);
   if (s != DC_OK) return mfail(m, s, err);
   return DC_OK;
+}
+
+// RMSNorm backward: dx = dres + rstd (dh g - n mean(dh g n)), dg = sum_rows dh n
+static dc_status rmsnorm_bwd(dc_model* m, const void* dh, const void* x, const void* g, const float* rstd,
+                             const void* dres, void* dx, void* dg, cudaStream_t st) {
+  const int T = m->d.tokens, H = m->d.hidden;
+  if (m->rn_two_pass) {
+    k_rmsnorm_bwd(dh, x, g, rstd, dres, dx, (float*)m->A(m->ws_dgp), T, H, st);
+    k_colsum_to_bf16((float*)m->A(m->ws_dgp), rmsnorm_bwd_blocks(T), H, dg, st);
+    return DC_OK;
+  }
+  return k_rmsnorm_bwd_dg(dh, x, g, rstd, dres, dx, dg, (float*)m->A(m->ws_rnp), (uint32_t*)m->A(m->ws_rnc), T, H, st);
 }
 
 // micro-batch mu of the bound [n][T][H] inputs
@@ -553,13 +571,10 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
         s = gemm(m, F, H, T, m->A(m->ws_dgu) + (int64_t)F * 2, 2 * F, 1, {m->A(a.h2)}, {H}, {H / 256}, 1, 0, G(P_UP),
                  H, nullptr, 0, sw, ADAM(P_UP));
       break;
-    case B_MLP_NORM: {
-      const int nb = rmsnorm_bwd_blocks(T);
-      k_rmsnorm_bwd(m->A(m->ws_dh), m->A(a.x2), m->W(l, P_G2), (float*)m->A(a.rstd2), dcur, m->A(m->ws_dx2),
-                    (float*)m->A(m->ws_dgp), T, H, st);
-      k_colsum_to_bf16((float*)m->A(m->ws_dgp), nb, H, G(P_G2), st);
+    case B_MLP_NORM:
+      s = rmsnorm_bwd(m, m->A(m->ws_dh), m->A(a.x2), m->W(l, P_G2), (float*)m->A(a.rstd2), dcur, m->A(m->ws_dx2),
+                      G(P_G2), st);
       break;
-    }
     case B_O:
       // da -> dqkv[:, :qd] ; dWo = dx2^T a
       fork();
@@ -585,10 +600,9 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
                  0, G(P_V), H, nullptr, 0, sw, ADAM(P_V));
       break;
     case B_ATTN_NORM: {
-      const int nb = rmsnorm_bwd_blocks(T);
-      k_rmsnorm_bwd(m->A(m->ws_dh), layer_in(m, l, o.micro), m->W(l, P_G1), (float*)m->A(a.rstd1), m->A(m->ws_dx2), dnext,
-                    (float*)m->A(m->ws_dgp), T, H, st);
-      k_colsum_to_bf16((float*)m->A(m->ws_dgp), nb, H, G(P_G1), st);
+      s = rmsnorm_bwd(m, m->A(m->ws_dh), layer_in(m, l, o.micro), m->W(l, P_G1), (float*)m->A(a.rstd1),
+                      m->A(m->ws_dx2), dnext, G(P_G1), st);
+      if (s != DC_OK) return mfail(m, s, "rmsnorm backward launch failed");
       if ((s = dc_grad_slot_publish(m->ctx, l, st)) != DC_OK) return s;
       if (m->pending_layer >= 0) {     // the hosted RS + Adam is complete (stream order)
         if (m->pending_assigned != m->pending.g1) return mfail(m, DC_ESTATE, "side job not fully assigned");
