@@ -185,12 +185,6 @@ struct RsParams {
 #ifndef DC_RS_UNR_N1
 #define DC_RS_UNR_N1 1        // N = 1: one group (80 registers; 12-15 % faster in-step than two groups
 #endif                        // at 112 registers, profiles/r01g/rs_coresidency_ab.md)
-#ifndef DC_RS_PIPE
-#define DC_RS_PIPE 0          // > 0: software-pipelined groups per iteration (A/B)
-#endif
-#ifndef DC_RS_PREFETCH
-#define DC_RS_PREFETCH 0      // > 0: prefetch that many iterations ahead into L2 (A/B)
-#endif
 // groups of 8 elements per thread per iteration (loads hoisted)
 // (the accumulate-only modes keep two: few registers, few bytes per element)
 template <int MAXQ, int MODE>
@@ -256,56 +250,7 @@ __global__ void __launch_bounds__(256, DC_RS_MINB) rs_adam_kernel(const RsParams
         }
       } else {
         constexpr bool ACC = MODE == RS_FINAL;
-#if DC_RS_PIPE
-        // software pipeline (A/B): the next PIPE groups' loads are issued
-        // before this iteration's arithmetic, two register sets in turn
-        constexpr int U = DC_RS_PIPE;
-        Group8<MAXQ> xa[U], xb[U];
-        auto load_set = [&](Group8<MAXQ>(&x)[U], int64_t i0) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int64_t i = i0 + u * nthr;
-            if (i < n8) {
-              const uint8_t* gp[MAXQ];
-#pragma unroll
-              for (int q = 0; q < MAXQ; ++q) gp[q] = q < p.world ? p.slot[q] + gbase + i * 16 : nullptr;
-              load_group8<MAXQ, ACC>(x[u], gp, p.world, mst + 8 * i, mm + 8 * i, vv + 8 * i, pol, acc + 8 * i);
-            }
-          }
-        };
-        auto finish_set = [&](const Group8<MAXQ>(&x)[U], int64_t i0) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int64_t i = i0 + u * nthr;
-            if (i < n8)
-              finish_group8<MAXQ, ACC>(x[u], p.world, mst + 8 * i, mm + 8 * i, vv + 8 * i, sh + 8 * i, a, pol);
-          }
-        };
-        const int64_t stride = nthr * U;
-        int64_t i0 = tid;
-        if (i0 < n8) load_set(xa, i0);
-        while (i0 < n8) {
-          if (i0 + stride < n8) load_set(xb, i0 + stride);
-          finish_set(xa, i0);
-          i0 += stride;
-          if (i0 >= n8) break;
-          if (i0 + stride < n8) load_set(xa, i0 + stride);
-          finish_set(xb, i0);
-          i0 += stride;
-        }
-#else
         for (int64_t i0 = tid; i0 < n8; i0 += nthr * RS_UNR) {
-#if DC_RS_PREFETCH
-          {   // pull the next iteration's state lines into L2 (more bytes in flight, no registers)
-            const int64_t j = i0 + (int64_t)DC_RS_PREFETCH * nthr * RS_UNR;
-            if (j < n8) {
-              asm volatile("prefetch.global.L2 [%0];" :: "l"(mst + 8 * j));
-              asm volatile("prefetch.global.L2 [%0];" :: "l"(mm + 8 * j));
-              asm volatile("prefetch.global.L2 [%0];" :: "l"(vv + 8 * j));
-              asm volatile("prefetch.global.L2 [%0];" :: "l"(p.slot[p.rank] + gbase + j * 16));
-            }
-          }
-#endif
           Group8<MAXQ> x[RS_UNR];
 #pragma unroll
           for (int u = 0; u < RS_UNR; ++u) {     // every load of RS_UNR groups before any math
@@ -324,7 +269,6 @@ __global__ void __launch_bounds__(256, DC_RS_MINB) rs_adam_kernel(const RsParams
               finish_group8<MAXQ, ACC>(x[u], p.world, mst + 8 * i, mm + 8 * i, vv + 8 * i, sh + 8 * i, a, pol);
           }
         }
-#endif
       }
     }
   }

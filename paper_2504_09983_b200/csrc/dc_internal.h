@@ -128,12 +128,6 @@ void k_rmsnorm_fwd(const void* x, const void* g, void* h, float* rstd, int T, in
 void k_rmsnorm_bwd(const void* dh, const void* x, const void* g, const float* rstd, const void* dres,
                    void* dx, float* dg_partial, int T, int H, cudaStream_t st);
 int rmsnorm_bwd_blocks(int T);
-// one-pass RMSNorm backward with the dg column sum folded in (last CTA):
-// part = rmsnorm_bwd_fused_grid(T) x H fp32, counter = one uint32, zero before
-// the first launch (each launch leaves it zero)
-int rmsnorm_bwd_fused_grid(int T);
-dc_status k_rmsnorm_bwd_dg(const void* dh, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
-                           void* dg, float* part, uint32_t* counter, int T, int H, cudaStream_t st);
 void k_colsum_to_bf16(const float* partial, int nblk, int H, void* out, cudaStream_t st);
 void k_attn_mix_fwd(const void* qkv, void* a, int T, int qd, int kvd, int hd, int grp, cudaStream_t st);
 void k_attn_mix_bwd(void* dqkv, const void* qkv, int T, int qd, int kvd, int hd, int grp, cudaStream_t st);

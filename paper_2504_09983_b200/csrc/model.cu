@@ -77,8 +77,6 @@ struct dc_model {
           ws_lossp = 0, ws_loss = 0;
   int64_t ws_dO = 0, ws_dX = 0, ws_dl0 = 0, ws_rgp = 0;   // MoE backward
   int64_t ws_sk = 0;                                     // stream-K workspace of the compute-stream GEMMs
-  int64_t ws_rnp = 0, ws_rnc = 0;                        // fused RMSNorm backward: dg partials, counter
-  int rn_two_pass = 0;                                   // A/B: the two-pass RMSNorm backward + colsum
   int E = 0, R = 0;                                      // experts, rows per expert (2T/E)
   uint64_t act_bytes = 0, layer_act_bytes = 0, ws_bytes = 0;
   uint8_t* act = nullptr;
@@ -306,8 +304,6 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   m->ws_dqkv = take(T * m->qkvd * 2); m->ws_dgp = take(((int64_t)rmsnorm_bwd_blocks((int)T) * h + T) * 4);   // partials + row dots
   m->ws_lossp = take(1024 * 4); m->ws_loss = take(4 * (int64_t)m->n_micro);
   m->ws_sk = take((int64_t)gemm_workspace_bytes());
-  m->ws_rnp = take((int64_t)rmsnorm_bwd_fused_grid((int)T) * h * 4);
-  m->ws_rnc = take(256);
   if (m->E) {
     m->ws_dO = take(2 * T * h * 2); m->ws_dX = take(2 * T * h * 2); m->ws_dl0 = take(T * 4);
     m->ws_rgp = take((int64_t)moe_router_dw_blocks((int)T) * m->E * h * 4);
@@ -345,7 +341,6 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
       cudaEventCreateWithFlags(&m->ev_joinw, cudaEventDisableTiming) != cudaSuccess)
     return mfail(nullptr, DC_ECUDA, "dc_model_create: stream creation failed");
   if (const char* e = getenv("DC_DW_CONCURRENT")) m->dw_conc = atoi(e) != 0;   // A/B knob
-  if (const char* e = getenv("DC_RMSNORM_TWO_PASS")) m->rn_two_pass = atoi(e) != 0;   // A/B knob
   *out = m.release();
   return DC_OK;
 }
@@ -384,9 +379,8 @@ extern "C" dc_status dc_model_bind(dc_model* m, void* buf, uint64_t bytes, const
   m->act = reinterpret_cast<uint8_t*>(buf);
   m->x = x;
   m->target = target;
-  // the stream-K workspace and the RMSNorm-backward counter start zero-filled
+  // the stream-K workspace starts zero-filled (dc_gemm_args.workspace)
   if (cudaMemset(m->A(m->ws_sk), 0, gemm_workspace_bytes()) != cudaSuccess ||
-      cudaMemset(m->A(m->ws_rnc), 0, 256) != cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess)
     return mfail(m, DC_ECUDA, "dc_model_bind: workspace clear failed");
   gemm_sk_reset(m->A(m->ws_sk), 0);
@@ -450,15 +444,14 @@ static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t l
 }
 
 // RMSNorm backward: dx = dres + rstd (dh g - n mean(dh g n)), dg = sum_rows dh n
+// (two passes + the dg column sum; a one-pass form with the column sum in the
+// last CTA measured 1.9x slower in the step, r02: 4.0 vs 2.1 ms per step)
 static dc_status rmsnorm_bwd(dc_model* m, const void* dh, const void* x, const void* g, const float* rstd,
                              const void* dres, void* dx, void* dg, cudaStream_t st) {
   const int T = m->d.tokens, H = m->d.hidden;
-  if (m->rn_two_pass) {
-    k_rmsnorm_bwd(dh, x, g, rstd, dres, dx, (float*)m->A(m->ws_dgp), T, H, st);
-    k_colsum_to_bf16((float*)m->A(m->ws_dgp), rmsnorm_bwd_blocks(T), H, dg, st);
-    return DC_OK;
-  }
-  return k_rmsnorm_bwd_dg(dh, x, g, rstd, dres, dx, dg, (float*)m->A(m->ws_rnp), (uint32_t*)m->A(m->ws_rnc), T, H, st);
+  k_rmsnorm_bwd(dh, x, g, rstd, dres, dx, (float*)m->A(m->ws_dgp), T, H, st);
+  k_colsum_to_bf16((float*)m->A(m->ws_dgp), rmsnorm_bwd_blocks(T), H, dg, st);
+  return DC_OK;
 }
 
 // micro-batch mu of the bound [n][T][H] inputs
