@@ -772,7 +772,9 @@ def main():
                 "ag_busbw_gbs_ge_64MiB": (f * sum(b for b, _ in big) / (sum(us for _, us in big) * 1e-6) / 1e9
                                           if big else None),
                 "rs_busbw_gbs": f * rs_b / (sum(rs_us) * 1e-6) / 1e9 if rs_us and sum(rs_us) else None,
-                "nvlink_peak_gbs": 900}
+                "nvlink_peak_gbs": 900,
+                "nvls": st.nvls or {"requested": 0, "note": "DC_NVLS=1|2|3 selects the multimem gather / "
+                                    "ld_reduce reduce-scatter where the fabric gives multicast addresses"}}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

@@ -195,8 +195,26 @@ dc_status dc_gather_timing(dc_ctx* ctx, cudaEvent_t after_ready, cudaEvent_t aft
  * memory per SM) instead of the register-streaming one; bit-identical.
  * "ag_skip_waits" (profiling only, default 0): dc_gather launches the push
  * without its ready / done flag waits (for ncu, which serialises kernels);
- * the gathered buffer is then NOT guaranteed complete. */
+ * the gathered buffer is then NOT guaranteed complete.
+ * "nvls" (default 0, any time; SURVEY §8 f-3, P:438 collectives): bit 0 —
+ * gathers store each shard vector ONCE with multimem.st to the arena's
+ * multicast address (the NVSwitch replicates it into every rank's arena;
+ * bit-identical buffers, same ready / done protocol, done bumped on every rank
+ * by one multimem.red); bit 1 — the reduce-scatter reads slice r of every
+ * rank's grads with one multimem.ld_reduce (fp32 accumulation in the switch,
+ * bf16 result; NOT bit-exact with the ascending-rank fp32 sum) before 1/N and
+ * Adam.  Each bit takes effect only while dc_bind_multicast holds the
+ * corresponding multicast address; otherwise the unicast kernels run. */
 dc_status dc_set_option(dc_ctx* ctx, const char* key, int64_t value);
+/* Multicast (NVLS) addresses of this rank's symmetric buffers, as mapped by
+ * the caller (torch symmetric memory's multicast_ptr): the gather arena bound
+ * by the last dc_bind_schedule, the grad slots and the flag table of dc_init
+ * (byte addresses of their first byte, 16 B aligned; 0 = not available).
+ * dc_bind_schedule forgets arena_mc (a new arena), so call this after every
+ * bind.  DC_ESTATE before the first dc_bind_schedule; DC_EINVAL for non-zero
+ * addresses with N = 1 or virtual ranks, or arena / grad addresses without
+ * the flag table's. */
+dc_status dc_bind_multicast(dc_ctx* ctx, uint64_t arena_mc, uint64_t grad_mc, uint64_t flags_mc);
 /* Unsharded tensor of param (row-major, numel elements; padding follows):
  * valid between its gather's completion and its release.  At N = 1 the
  * shard itself.  DC_ESTATE if the param is not gathered. */

@@ -17,7 +17,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "--expt-relaxed-constexpr"]
 FLAGS += os.environ.get("DC_NVCC_EXTRA", "").split()        # A/B experiments only (e.g. -DDC_RS_UNR=4)
 
-SOURCES = ["api.cpp", "planner.cpp", "gemm_sm100.cu", "glue.cu", "comm.cu", "model.cu", "moe.cu", "sm_partition.cpp"]
+SOURCES = ["api.cpp", "planner.cpp", "gemm_sm100.cu", "glue.cu", "comm.cu", "nvls.cu", "model.cu", "moe.cu", "sm_partition.cpp"]
 
 
 def _newer(src, dst, deps=()):

@@ -121,6 +121,11 @@ struct dc_ctx {
   cudaEvent_t gt_start = nullptr, gt_end = nullptr;   // one-shot gather timing (profiling)
   int ag_ce = 0;                        // 1: gathers as copy-engine peer copies (no SM time)
   int ag_skip_waits = 0;                // profiling only: push without the ready / done flag waits
+  // NVLS: multicast addresses of the arena / grad slots / flag
+  // table (dc_bind_multicast; 0 = none) and option "nvls" (bit 0 gathers,
+  // bit 1 reduce-scatter)
+  uint64_t arena_mc = 0, grad_mc = 0, flags_mc = 0;
+  int nvls = 0;
   // push CTAs per gather: 64 x 256 threads x 8 x 16 B keeps ~2 MB of stores in
   // flight (NVLink latency x 900 GB/s) and fits beside a GEMM CTA per SM
   int ag_max_ctas = 64;
@@ -262,6 +267,7 @@ extern "C" dc_status dc_init(const dc_init_args* a, dc_ctx** out) {
   if (const char* e = getenv("DC_AG_MAX_CTAS")) c->ag_max_ctas = std::max(1, std::min(1024, atoi(e)));
   DC_CUDA_TRY(preload_glue_kernels(), &c->err);
   DC_CUDA_TRY(preload_comm_kernels(), &c->err);
+  DC_CUDA_TRY(preload_nvls_kernels(), &c->err);
   DC_CUDA_TRY(preload_gemm_kernels(), &c->err);
   DC_CUDA_TRY(preload_moe_kernels(), &c->err);
   DC_CUDA_TRY(cudaHostAlloc(&c->err_host, ERR_RECORD_WORDS * 4, cudaHostAllocMapped), &c->err);
@@ -348,6 +354,7 @@ extern "C" dc_status dc_bind_schedule(dc_ctx* c, const dc_schedule* s, const uin
   c->arena_peers.assign(arena_peer_ptrs ? arena_peer_ptrs : nullptr, arena_peer_ptrs ? arena_peer_ptrs + c->world : nullptr);
   if (c->world > 1 && (int)c->arena_peers.size() != c->world) return fail(c, DC_EINVAL, "dc_bind_schedule: arena peers");
   c->arena_bytes = arena_bytes;
+  c->arena_mc = 0;                      // a new arena: its multicast mapping is bound again
   c->epoch = 0;
   c->fepoch = 0;
   c->slot_use[0] = c->slot_use[1] = 0;
@@ -432,7 +439,12 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
     }
     const int ctas = c->ag_ctas[gid];
     const uint32_t target = c->fepoch * (uint32_t)(c->world * ctas * c->ag_launches[gid]);
-    dc_status s = c->ag_ce
+    dc_status s = ((c->nvls & 1) && c->arena_mc && !c->ag_ce)
+        ? k_ag_multimem(am, reinterpret_cast<uint8_t*>(c->arena_mc),
+                        reinterpret_cast<uint32_t*>(c->flags_mc) + c->L.f_done + gid, ctas,
+                        c->myflag(c->L.f_ready + (int64_t)gid * c->world), c->world, c->fepoch,
+                        c->myflag(c->L.f_done + gid), target, c->timeout_ns, c->err_dev, st, c->gt_start)
+        : c->ag_ce
         ? k_ag_copy(am, c->world, c->arena_peers.data(), c->myflag(c->L.f_ready + (int64_t)gid * c->world), c->fepoch,
                     peers_at(c, c->L.f_done + gid), c->myflag(c->L.f_done + gid), target, c->timeout_ns, c->err_dev,
                     st, c->gt_start)
@@ -473,12 +485,31 @@ extern "C" dc_status dc_set_option(dc_ctx* c, const char* key, int64_t value) {
     c->rs_bulk = value != 0;
     return DC_OK;
   }
+  if (!strcmp(key, "nvls")) {   // bit 0: multimem gathers, bit 1: multimem.ld_reduce reduce-scatter
+    if (value < 0 || value > 3) return fail(c, DC_EINVAL, "dc_set_option: nvls in [0, 3]");
+    c->nvls = (int)value;
+    return DC_OK;
+  }
   if (!strcmp(key, "ag_copy_engine")) {
     if (c->sched) return fail(c, DC_ESTATE, "dc_set_option: ag_copy_engine must be set before dc_bind_schedule");
     c->ag_ce = value != 0;
     return DC_OK;
   }
   return fail(c, DC_EINVAL, std::string("dc_set_option: unknown key ") + key);
+}
+
+extern "C" dc_status dc_bind_multicast(dc_ctx* c, uint64_t arena_mc, uint64_t grad_mc, uint64_t flags_mc) {
+  if (!c) return fail(c, DC_EINVAL, "dc_bind_multicast: null ctx");
+  if (!c->sched) return fail(c, DC_ESTATE, "dc_bind_multicast: bind a schedule (and its arena) first");
+  if ((arena_mc || grad_mc || flags_mc) && (c->world < 2 || (c->flags & DC_VIRTUAL_RANKS)))
+    return fail(c, DC_EINVAL, "dc_bind_multicast: multicast needs N > 1 ranks on N GPUs (not virtual ranks)");
+  if ((arena_mc || grad_mc) && !flags_mc)
+    return fail(c, DC_EINVAL, "dc_bind_multicast: the flag table's multicast address is required");
+  if ((arena_mc | grad_mc | flags_mc) & 15) return fail(c, DC_EINVAL, "dc_bind_multicast: addresses must be 16 B aligned");
+  c->arena_mc = arena_mc;
+  c->grad_mc = grad_mc;
+  c->flags_mc = flags_mc;
+  return DC_OK;
 }
 
 extern "C" dc_status dc_tensor_ptr(const dc_ctx* c, int32_t p, void** ptr) {
@@ -621,6 +652,16 @@ dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, con
     ctas = (int)std::min<int64_t>((int64_t)c->num_sms * rs_bulk_ctas_per_sm(), std::max<int64_t>(1, chunks));
   }
   c->rs_done_total += (uint32_t)ctas;
+  if ((c->nvls & 2) && c->grad_mc) {      // f-3: the switch sums the slices (not bit-exact, opt-in)
+    dc_status r = k_rs_adam_nvls(mem, c->world, c->rank,
+                                 reinterpret_cast<const uint8_t*>(c->grad_mc) + (int64_t)s * c->L.grad_slot_bytes,
+                                 c->myflag(c->L.f_gready + (int64_t)s * c->world), (uint32_t)u,
+                                 peers_at(c, c->L.f_gcons + (int64_t)s * c->world + c->rank), (uint32_t)u,
+                                 c->myflag(c->L.f_rsdone), c->rs_done_total, c->master, mb, vb, c->shard, c->grad_acc,
+                                 mode, n, sc, cc, c->beta1, c->beta2, c->eps, ctas, c->timeout_ns, c->err_dev, st,
+                                 c->graph_mode ? reinterpret_cast<const float*>(c->myflag(c->L.f_scal)) : nullptr);
+    return r == DC_OK ? DC_OK : fail(c, r, "dc_reduce_scatter_step: NVLS launch failed");
+  }
   dc_status r = k_rs_adam(mem, c->world, c->rank, slots.data(), c->myflag(c->L.f_gready + (int64_t)s * c->world),
                           (uint32_t)u, peers_at(c, c->L.f_gcons + (int64_t)s * c->world + c->rank), (uint32_t)u,
                           c->myflag(c->L.f_rsdone), c->rs_done_total, c->master, mb, vb, c->shard, c->grad_acc,

@@ -193,6 +193,19 @@ dc_status k_ag_copy(const std::vector<AgMember>& mem, int world, const uint64_t*
                     uint32_t done_target, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st,
                     cudaEvent_t ev_after_ready);
 void k_post_flags(PeerFlags dst, uint32_t value, cudaStream_t st);
+// nvls.cu: multicast all-gather (one multimem.st per 16 B,
+// the switch replicates) and multimem.ld_reduce reduce-scatter + Adam
+dc_status k_ag_multimem(const std::vector<AgMember>& mem, uint8_t* arena_mc, uint32_t* done_mc, int ctas,
+                        const uint32_t* ready_local, int world, uint32_t epoch, const uint32_t* done_local,
+                        uint32_t done_target, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st,
+                        cudaEvent_t ev_after_ready);
+dc_status k_rs_adam_nvls(const std::vector<RsMember>& mem, int world, int rank, const uint8_t* slot_mc,
+                         const uint32_t* ready_local, uint32_t ready_target, PeerFlags consumed_peers,
+                         uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master, float* m,
+                         float* v, void* shard, float* acc, int mode, int micro_steps, float s, float c, double beta1,
+                         double beta2, double eps, int ctas, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st,
+                         const float* dev_scalars);
+cudaError_t preload_nvls_kernels();
 void k_wait_flags(const uint32_t* flags, int n, uint32_t target, uint64_t timeout_ns,
                   uint32_t* err_flag, cudaStream_t st);
 

@@ -41,6 +41,7 @@ class RankState:
         self.model = None
         self.tensors = {}
         self.peer_keep = {}     # per symmetric buffer: imported peer mappings (IPC storages / symm_mem handle)
+        self.nvls = None        # what bind_multicast selected (N > 1, DC_NVLS)
         self.streams = None
         self.sched = None
         self.micro_steps = 1
@@ -95,6 +96,33 @@ def _alloc_symmetric(nbytes, group, device):
     h = symm_mem.rendezvous(t, group)
     t.zero_()
     return t, [int(p) for p in h.buffer_ptrs], [h]
+
+
+def multicast_ptr(keep):
+    """Multicast (NVLS) address of a symmetric buffer allocated through torch
+    symmetric memory (0 when the driver / fabric gives none: one-GPU boxes,
+    the CUDA-IPC backend, virtual ranks)."""
+    for h in keep or ():
+        mc = getattr(h, "multicast_ptr", 0)
+        if mc:
+            return int(mc)
+    return 0
+
+
+def bind_multicast(st, bits):
+    """hand this rank's multicast addresses of the arena, grad
+    slots and flag table to the library and select the NVLS kernels (option
+    "nvls", bit 0 gathers, bit 1 reduce-scatter).  Returns what was bound;
+    the library keeps the unicast kernels for any address that is 0."""
+    mc = {k: multicast_ptr(st.peer_keep.get(k)) for k in ("arena", "grad", "flags")}
+    if not mc["flags"]:
+        mc = {k: 0 for k in mc}
+    dc.check(dc.lib.dc_bind_multicast(st.ctx, mc["arena"] if bits & 1 else 0, mc["grad"] if bits & 2 else 0,
+                                      mc["flags"]), st.ctx)
+    dc.check(dc.lib.dc_set_option(st.ctx, b"nvls", bits), st.ctx)
+    st.nvls = {"requested": bits, "ag_multimem": bool(bits & 1 and mc["arena"]),
+               "rs_ld_reduce": bool(bits & 2 and mc["grad"])}
+    return st.nvls
 
 
 def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr=1e-3, beta1=0.9,
@@ -233,6 +261,9 @@ def bind(ranks, sched_by_rank, group=None):
         dc.check(dc.lib.dc_bind_schedule(st.ctx, st.sched, C.cast(arr, dc.p_u64), cap,
                                          st.streams[0].cuda_stream), st.ctx)
     torch.cuda.synchronize()
+    nvls = int(os.environ.get("DC_NVLS", "0"))
+    if group is not None and nvls:
+        bind_multicast(any_st, nvls)
     if group is not None:
         # dc_bind_schedule zeroes this rank's flag table; no rank may start a
         # step (whose first action posts ready flags into its peers' tables)
