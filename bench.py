@@ -71,6 +71,10 @@ def parse():
                     help="test mode: every rank on cuda:0 (gloo host collectives, CUDA-IPC peer maps, fixed T_c); "
                          "exercises the N > 1 launch on a one-GPU box, numbers are not a bench value")
     ap.add_argument("--profile-json", default="", help="write the rank-0 profile / plan here")
+    ap.add_argument("--tc-table", default="",
+                    help="plan with this T_c(V) table instead of the measured / zero one (what-if, SURVEY §8 a-3): "
+                         "a JSON file [[bytes, us], ...], or SWEEP.json:N:mode to take the median times of "
+                         "scripts/ag_sweep.py's run at N virtual ranks (mode sm | ce)")
     ap.add_argument("--dry-run", action="store_true",
                     help="launcher check without a GPU: every rank joins a gloo group, barriers, MAX-reduces a "
                          "dummy time and rank 0 prints one JSON line (tests/test_bench_cli.py)")
@@ -370,6 +374,24 @@ def measure_tc(group, world, dev, torch, dist):
     return pts
 
 
+def load_tc_table(spec):
+    """--tc-table: [[bytes, us], ...] (integer us, strictly increasing bytes,
+    made non-decreasing in time) from a file or from an ag_sweep.json run."""
+    path, _, sel = spec.partition(":")
+    with open(path) as f:
+        d = json.load(f)
+    if sel:
+        n, _, mode = sel.partition(":")
+        run = [r for r in d["runs"] if r["world"] == int(n) and r["mode"] == (mode or "sm")][0]
+        pts = [[int(r["bytes"]), max(1, int(round(r["us"])))] for r in run["rows"]]
+    else:
+        pts = [[int(b), int(u)] for b, u in d]
+    pts.sort()
+    for i in range(1, len(pts)):
+        pts[i][1] = max(pts[i][1], pts[i - 1][1])
+    return pts
+
+
 def model_config(args):
     import dataclasses
 
@@ -446,6 +468,8 @@ def main():
         dc.check(dc.lib.dc_set_option(st.ctx, b"graph_mode", 1), st.ctx)
     if os.environ.get("DC_AG_COPY_ENGINE") is not None:       # gathers on the copy engines (f-3)
         dc.check(dc.lib.dc_set_option(st.ctx, b"ag_copy_engine", int(os.environ["DC_AG_COPY_ENGINE"])), st.ctx)
+    if os.environ.get("DC_FUSED_AG") is not None:             # fused all-gather -> GEMM (f-4)
+        dc.check(dc.lib.dc_set_option(st.ctx, b"fused_ag", int(os.environ["DC_FUSED_AG"])), st.ctx)
     # synthetic inputs (synth generator, fp32) rounded to bf16 by torch (RNE)
     x_np = np.concatenate([synth.values(synth.seed_inputs(rank, mu), 0, 0, T * cfg.hidden, synth.K_UNIT)
                            for mu in range(n_micro)])
@@ -495,6 +519,10 @@ def main():
         tc = [[0, 0], [1 << 40, 0]]
     if world > 1 and len(tc) < 2:
         tc = [[0, tc[0][1]], tc[0]]
+    tc_source = ("our gathers in the profiled S_0 step" if world > 1 and tc is not tc_nccl else
+                 "NCCL all-gather comparator" if world > 1 else "none (N = 1: gathers alias the shard)")
+    if args.tc_table:
+        tc, tc_source = load_tc_table(args.tc_table), "what-if: " + args.tc_table
     prof = rt.profile_json(st, tc=tc, frags=frags)
     if world > 1:   # element-wise MAX over ranks (reading D12)
         prof = rt.max_reduce_profile(prof, group, device=cdev)
@@ -738,6 +766,13 @@ def main():
                          (offload_info["offloaded_bytes"] if offload_info else 0), "M": M}
     if offload_info:   # the reload ring is a static allocation beside the plan's live bytes
         mem["offload_pool"] = offload_info["pool_bytes"]
+    mem["note"] = ("P_mem (a-3) is the executor's exact bookkeeping of its static allocations: bf16 shard + fp32 "
+                   "master, grad slots, workspace, inputs, the saved activations live at each op and the gathered "
+                   "buffers live under the schedule (m / v excluded, reading D14, added back as M_opt). " +
+                   ("At N = 1 a gather aliases the shard, so the plan counts the gathered weights the device never "
+                    "allocates (up to the bf16 weight bytes above the allocator's peak)." if world == 1 else
+                    "At N > 1 the arena is one allocation of the plan's capacity, so the allocator's peak is the "
+                    "plan's static part + arena capacity + every layer's activation buffer."))
     idle = {"ms": max(0.0, ms - busy_ms), "frac": max(0.0, ms - busy_ms) / ms,
             "note": "step time - compute-stream busy time of the last timed step (waits on gathers, "
                     "grad-slot / reduce-scatter flags and launch gaps; reduce-scatter ops count as busy when "
@@ -794,7 +829,9 @@ def main():
                            "seq_len": args.seq, "parallelism": "fsdp%d" % world, "passes": args.passes,
                            "mem_budget_M": M, "plan_ms": round(t_plan * 1e3, 2),
                            "unshard_params": len(plan["unshard"]), "offload": offload_info,
-                           "tc_table": prof["tc"], "tc_nccl_comparator": tc_nccl,
+                           "tc_table": prof["tc"], "tc_source": tc_source, "tc_nccl_comparator": tc_nccl,
+                           "fused_groups": sum(1 for o in plan["ops"] if o["kind"] == "ag" and
+                                               len(o.get("members", [])) > 1),
                            "l2": "working set (~120 GB/GPU of weights, states, activations) >> 126 MB L2; no flush"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "exposed_comm": exposed, "compute_stream_idle": idle, "memory": mem,

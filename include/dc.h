@@ -204,7 +204,18 @@ dc_status dc_gather_timing(dc_ctx* ctx, cudaEvent_t after_ready, cudaEvent_t aft
  * rank's grads with one multimem.ld_reduce (fp32 accumulation in the switch,
  * bf16 result; NOT bit-exact with the ascending-rank fp32 sum) before 1/N and
  * Adam.  Each bit takes effect only while dc_bind_multicast holds the
- * corresponding multicast address; otherwise the unicast kernels run. */
+ * corresponding multicast address; otherwise the unicast kernels run.
+ * "fused_ag" (default 0; before dc_bind_schedule, else DC_ESTATE; SURVEY §8
+ * f-4): N > 1 gathers by the SM push are stored chunk by chunk (<= 64
+ * chunks of >= 4096 elements per shard) and, once a chunk's stores landed on
+ * every receiver, the sender writes the gather's value into that chunk's word
+ * of every receiver's flag table; dc_model_step's GEMMs that read a gathered
+ * weight as their B operand then wait per tile for just the chunks they load
+ * (dc_gemm_args.chunk_*) instead of the compute stream waiting for the whole
+ * gather.  Bit-identical results.  With virtual ranks every rank's GEMMs get
+ * 1/N of the SMs (co-residency on one GPU).
+ * "ag_delay_us" (testing, default 0): every push starts this long after its
+ * ready wait (consumers then run ahead of the data). */
 dc_status dc_set_option(dc_ctx* ctx, const char* key, int64_t value);
 /* Multicast (NVLS) addresses of this rank's symmetric buffers, as mapped by
  * the caller (torch symmetric memory's multicast_ptr): the gather arena bound
@@ -332,6 +343,18 @@ typedef struct {
    * m_tiles >= 2 n_tiles, else m-fastest over the whole grid); g > 0: groups
    * of g m-tiles (the last group may be partial); -1: never group. */
   int32_t tile_group_m;
+  /* fused all-gather -> GEMM (CTA-pair kernel only): for a B
+   * segment s with chunk_flags[s] != NULL the producer, before loading B
+   * elements of that segment (flat row-major index into the segment's tensor
+   * of chunk_numel[s] elements), waits until every chunk overlapping them
+   * holds a value >= chunk_value[s] (serial-number compare): chunk (q, j) is
+   * the flat range [q S + j E, min(q S + (j + 1) E, (q + 1) S)), its word
+   * chunk_flags[s][q * 64 + j], S = chunk_S[s] (shard elements), E =
+   * chunk_E[s].  Acquire loads, then fence.proxy.async before the TMA loads.
+   * A wait longer than chunk_timeout_ns writes the device error record at
+   * chunk_err (the ctx's, reported by dc_poll as DC_ETIMEOUT) and proceeds. */
+  const uint32_t* chunk_flags[4]; int64_t chunk_S[4], chunk_E[4], chunk_numel[4]; uint32_t chunk_value[4];
+  uint32_t* chunk_err; uint64_t chunk_timeout_ns;
 } dc_gemm_args;
 dc_status dc_gemm(const dc_gemm_args* g, cudaStream_t stream);
 /* Bytes of a stream-K workspace (fp32 partial tiles + flags). */

@@ -54,7 +54,8 @@ static dc_status make_layout(int world, int n, const int64_t* numel, const int32
   const int64_t ops = std::max(max_ops, 1);
   L->f_ready = 0;
   L->f_done = L->f_ready + ops * world;
-  L->f_gready = L->f_done + ops;
+  L->f_chunk = L->f_done + ops;
+  L->f_gready = L->f_chunk + (int64_t)n * world * AG_CHUNKS;
   L->f_gcons = L->f_gready + 2 * world;
   L->f_rsdone = L->f_gcons + 2 * world;
   L->f_scal = L->f_rsdone + 1;
@@ -126,6 +127,15 @@ struct dc_ctx {
   // bit 1 reduce-scatter)
   uint64_t arena_mc = 0, grad_mc = 0, flags_mc = 0;
   int nvls = 0;
+  // fused all-gather -> GEMM (option "fused_ag"): gathers push
+  // in chunks and post per-chunk values; the executor's GEMMs wait per tile.
+  // ag_inst[gid][j] = 1-based instance of member j's gather among that param's
+  // gathers in the schedule; the value posted at flag epoch e is
+  // (e - 1) * ag_ninst + instance (monotone over steps and within a step)
+  int fused_ag = 0;
+  std::map<int, std::vector<uint32_t>> ag_inst;
+  uint32_t ag_ninst = 1;
+  uint32_t ag_delay_us = 0;             // testing: each push starts this long after its ready wait
   // push CTAs per gather: 64 x 256 threads x 8 x 16 B keeps ~2 MB of stores in
   // flight (NVLink latency x 900 GB/s) and fits beside a GEMM CTA per SM
   int ag_max_ctas = 64;
@@ -159,8 +169,11 @@ static std::string describe_flag(const dc_ctx* c, uint64_t addr) {
     const int W = c->world;
     if (w < L.f_done)
       snprintf(b, sizeof b, "ready[gather %lld][sender %lld]", (long long)(w / W), (long long)(w % W));
-    else if (w < L.f_gready)
+    else if (w < L.f_chunk)
       snprintf(b, sizeof b, "done[gather %lld]", (long long)(w - L.f_done));
+    else if (w < L.f_gready)
+      snprintf(b, sizeof b, "chunk[param %lld][sender %lld][%lld]", (long long)((w - L.f_chunk) / (W * AG_CHUNKS)),
+               (long long)((w - L.f_chunk) / AG_CHUNKS % W), (long long)((w - L.f_chunk) % AG_CHUNKS));
     else if (w < L.f_gcons)
       snprintf(b, sizeof b, "grad_ready[slot %lld][sender %lld]", (long long)((w - L.f_gready) / W),
                (long long)((w - L.f_gready) % W));
@@ -183,9 +196,9 @@ static dc_status check_sticky(dc_ctx* c) {
   volatile uint32_t* e = c->err_host;
   if (e && e[0]) {
     static const char* what[] = {"?", "gather: receivers ready", "gather: stores landed", "reduce-scatter: grads ready",
-                                 "flag wait", "graph step barrier"};
+                                 "flag wait", "graph step barrier", "GEMM: gathered chunk landed"};
     const uint32_t code = e[0];
-    const uint32_t k = (code >> 8) < 6 ? (code >> 8) : 0;
+    const uint32_t k = (code >> 8) < 7 ? (code >> 8) : 0;
     const uint64_t addr = (uint64_t)e[4] | ((uint64_t)e[5] << 32);
     char b[160];
     snprintf(b, sizeof b, "rank %d: device flag wait timed out after %.1f s (code 0x%x, %s) on ", c->rank,
@@ -329,11 +342,20 @@ extern "C" dc_status dc_bind_schedule(dc_ctx* c, const dc_schedule* s, const uin
   c->initial_ready.clear();
   c->ag_ctas.clear();
   c->ag_launches.clear();
+  c->ag_inst.clear();
+  c->ag_ninst = 1;
+  std::vector<uint32_t> inst_cnt(c->n_params, 0);
   for (int i = 0; i < n; ++i) {
     int kind, id, nm, np, nw;
     const int64_t* mem; const int* posts; const int* waits;
     int64_t off, bytes;
     sched_op(s, i, &kind, &id, &mem, &nm, &off, &bytes, &posts, &np, &waits, &nw);
+    if (kind == K_AG)
+      for (int j = 0; j < nm; ++j)
+        if (mem[j] >= 0 && mem[j] < c->n_params) {
+          c->ag_inst[id].push_back(++inst_cnt[mem[j]]);
+          c->ag_ninst = std::max(c->ag_ninst, inst_cnt[mem[j]]);
+        }
     if (kind == K_AG || kind == K_REL) {
       if (id < 0 || id >= c->max_ops) return fail(c, DC_EINVAL, "dc_bind_schedule: op id exceeds max_s0_ops");
       c->op_index[id] = i;
@@ -433,6 +455,10 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
       a.src = reinterpret_cast<const uint16_t*>(c->shard) + c->L.store_off[p];
       a.dst_off_bytes = cur + (int64_t)c->rank * c->L.S[p] * 2;
       a.bytes = c->L.S[p] * 2;
+      if (c->fused_ag) {
+        a.chunk_word = c->L.f_chunk + ((int64_t)p * c->world + c->rank) * AG_CHUNKS;
+        a.chunk_value = (c->fepoch - 1) * c->ag_ninst + c->ag_inst[gid][j];
+      }
       am.push_back(a);
       c->cur_off[p] = cur;
       cur += align256(c->numel[p] > 0 ? c->L.S[p] * c->world * 2 : 0);
@@ -450,7 +476,8 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
                     st, c->gt_start)
         : k_ag_push(am, c->world, c->rank, c->arena_peers.data(), c->myflag(c->L.f_ready + (int64_t)gid * c->world),
                     c->fepoch, peers_at(c, c->L.f_done + gid), c->myflag(c->L.f_done + gid), target, ctas,
-                    c->timeout_ns, c->err_dev, st, c->gt_start, c->ag_skip_waits != 0);
+                    c->timeout_ns, c->err_dev, st, c->gt_start, c->ag_skip_waits != 0, c->ag_delay_us,
+                    c->flag_peers.data());
     if (s != DC_OK) return fail(c, s, "dc_gather: launch failed");
     if (c->gt_end) record_event(c->gt_end, st);
   }
@@ -483,6 +510,16 @@ extern "C" dc_status dc_set_option(dc_ctx* c, const char* key, int64_t value) {
   }
   if (!strcmp(key, "rs_bulk")) {   // may change between steps (the launch reads it)
     c->rs_bulk = value != 0;
+    return DC_OK;
+  }
+  if (!strcmp(key, "fused_ag")) {   // chunked pushes + per-tile GEMM waits (dc_model_step), SURVEY §8 f-4
+    if (c->sched) return fail(c, DC_ESTATE, "dc_set_option: fused_ag must be set before dc_bind_schedule");
+    c->fused_ag = value != 0;
+    return DC_OK;
+  }
+  if (!strcmp(key, "ag_delay_us")) {   // testing: start every push this long after its ready wait
+    if (value < 0 || value > 1000000) return fail(c, DC_EINVAL, "dc_set_option: ag_delay_us in [0, 1e6]");
+    c->ag_delay_us = (uint32_t)value;
     return DC_OK;
   }
   if (!strcmp(key, "nvls")) {   // bit 0: multimem gathers, bit 1: multimem.ld_reduce reduce-scatter
@@ -532,6 +569,9 @@ extern "C" dc_status dc_release(dc_ctx* c, int32_t rid, cudaStream_t st) {
   int64_t off, bytes;
   sched_op(c->sched, it->second, &kind, &id, &mem, &nm, &off, &bytes, &posts, &np, &waits, &nw);
   if (kind != K_REL) return fail(c, DC_EINVAL, "dc_release: op is not a release");
+  if (c->world > 1 && (c->flags & DC_DEBUG_POISON) && c->cur_off[mem[0]] >= 0)   // stale reads become NaN
+    DC_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<uint8_t*>(c->arena_peers[c->rank]) + c->cur_off[mem[0]], 0xFF,
+                                c->L.S[mem[0]] * c->world * 2, st), &c->err);
   if (c->world > 1) c->cur_off[mem[0]] = -1;
   if (c->world == 1) return DC_OK;
   for (int j = 0; j < np; ++j)
@@ -576,6 +616,31 @@ void ctx_adam_scalars(const dc_ctx* c, int step_t, EpiAdam* o) {
   o->neg_s = -(float)(c->lr / bc1);
   o->c = (float)std::sqrt(bc2);
   o->eps = (float)c->eps;
+}
+
+bool ctx_fused_ag(const dc_ctx* c) { return c->fused_ag && c->world > 1 && !c->ag_ce && !(c->nvls & 1); }
+bool ctx_virtual(const dc_ctx* c) { return (c->flags & DC_VIRTUAL_RANKS) != 0; }
+void ctx_wait_err(dc_ctx* c, uint32_t** err, uint64_t* timeout_ns) {
+  *err = c->err_dev;
+  *timeout_ns = c->timeout_ns;
+}
+bool ctx_chunk_wait(const dc_ctx* c, int gid, int param, ChunkWait* out) {
+  auto it = c->op_index.find(gid);
+  auto in = c->ag_inst.find(gid);
+  if (it == c->op_index.end() || in == c->ag_inst.end()) return false;
+  int kind, id, nm, np, nw;
+  const int64_t* mem; const int* posts; const int* waits;
+  int64_t off, bytes;
+  sched_op(c->sched, it->second, &kind, &id, &mem, &nm, &off, &bytes, &posts, &np, &waits, &nw);
+  for (int j = 0; j < nm; ++j)
+    if (mem[j] == param) {
+      out->flags = c->myflag(c->L.f_chunk + (int64_t)param * c->world * AG_CHUNKS);
+      out->S = c->L.S[param];
+      out->E = ag_chunk_elems(out->S);
+      out->value = (c->fepoch - 1) * c->ag_ninst + in->second[j];
+      return true;
+    }
+  return false;
 }
 
 void ctx_param_state(const dc_ctx* c, int p, float** master, float** m, float** v, void** shard) {

@@ -108,6 +108,66 @@ __global__ void __launch_bounds__(AG_THREADS) ag_push_kernel(const AgParams p) {
   }
 }
 
+// Chunked push (fused all-gather -> GEMM): the same stores as
+// ag_push, but chunk by chunk (chunk j of member m = elements
+// [j E, min((j+1) E, S)) of this rank's shard; CTA b takes chunks b, b + grid,
+// ... of the members' chunk list in order, so the first chunks land first),
+// and after each chunk's stores have landed on every receiver the CTA writes
+// the gather's value into chunk[param][rank][j] of every receiver's flag
+// table: a GEMM there may start on the rows that already arrived.
+struct AgChunkParams {
+  int nm, world, rank;
+  const uint4* src[AG_MAXM];
+  int64_t dst_off[AG_MAXM];
+  int64_t nvec[AG_MAXM];
+  int64_t evec[AG_MAXM];      // 16-byte vectors per chunk
+  int cum[AG_MAXM + 1];       // chunk list prefix: member m owns chunks [cum[m], cum[m + 1])
+  int64_t word[AG_MAXM];      // chunk[param][rank][0] word in every table
+  uint32_t value[AG_MAXM];
+  uint8_t* arena[MAXW];
+  uint32_t* flags[MAXW];      // every rank's flag table
+  uint32_t* done_peer[MAXW];
+};
+
+__global__ void __launch_bounds__(AG_THREADS) ag_push_chunked_kernel(const AgChunkParams p) {
+  int m = 0;
+  for (int c = blockIdx.x; c < p.cum[p.nm]; c += gridDim.x) {
+    while (c >= p.cum[m + 1]) ++m;
+    const int j = c - p.cum[m];
+    const int64_t v0 = (int64_t)j * p.evec[m];
+    const int64_t v1 = min(v0 + p.evec[m], p.nvec[m]);
+    const uint4* src = p.src[m];
+    for (int64_t i = v0 + threadIdx.x; i < v1; i += AG_UNR * AG_THREADS) {
+      uint4 v[AG_UNR];
+#pragma unroll
+      for (int u = 0; u < AG_UNR; ++u)
+        if (i + u * AG_THREADS < v1) v[u] = __ldg(src + i + u * AG_THREADS);
+      for (int qq = 0; qq < p.world; ++qq) {
+        uint4* dst = reinterpret_cast<uint4*>(p.arena[(qq + p.rank) % p.world] + p.dst_off[m]);
+#pragma unroll
+        for (int u = 0; u < AG_UNR; ++u)
+          if (i + u * AG_THREADS < v1) dst[i + u * AG_THREADS] = v[u];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int q = 0; q < p.world; ++q) ptx::st_release_sys(p.flags[q] + p.word[m] + j, p.value[m]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < p.world; ++q) ptx::red_add_release_sys(p.done_peer[q], 1u);
+  }
+}
+
+// testing (option ag_delay_us): hold the AG stream so the consumers start first
+__global__ void delay_kernel(uint32_t us) {
+  const uint64_t t0 = ptx::globaltimer();
+  while (ptx::globaltimer() - t0 < (uint64_t)us * 1000u) __nanosleep(1000);
+}
+
 __global__ void wait_flags_kernel(const uint32_t* f, int n, uint32_t target, uint64_t tmo, uint32_t* err,
                                   uint32_t code) {
   const uint64_t t0 = ptx::globaltimer();
@@ -118,12 +178,48 @@ __global__ void wait_flags_kernel(const uint32_t* f, int n, uint32_t target, uin
 dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const uint64_t* arena_peers,
                     const uint32_t* ready_local, uint32_t epoch, PeerFlags done_peers, const uint32_t* done_local,
                     uint32_t done_target, int ctas, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st,
-                    cudaEvent_t ev_after_ready, bool skip_waits) {
+                    cudaEvent_t ev_after_ready, bool skip_waits, uint32_t delay_us, const uint64_t* flag_peers) {
   if (!skip_waits) {
     wait_flags_kernel<<<1, 1, 0, st>>>(ready_local, world, epoch, timeout_ns, err_flag, 0x100u);
     count_launch();
   }
   if (ev_after_ready) record_event(ev_after_ready, st);
+  if (delay_us) {
+    delay_kernel<<<1, 1, 0, st>>>(delay_us);
+    count_launch();
+  }
+  if (!mem.empty() && mem[0].chunk_word >= 0) {   // chunked pushes (fused all-gather -> GEMM)
+    if (!flag_peers) return DC_EINVAL;
+    for (size_t b = 0; b < mem.size(); b += AG_MAXM) {
+      AgChunkParams p{};
+      p.nm = (int)std::min<size_t>(AG_MAXM, mem.size() - b);
+      p.world = world; p.rank = rank;
+      p.cum[0] = 0;
+      for (int i = 0; i < p.nm; ++i) {
+        const AgMember& a = mem[b + i];
+        p.src[i] = reinterpret_cast<const uint4*>(a.src);
+        p.dst_off[i] = a.dst_off_bytes;
+        p.nvec[i] = a.bytes / 16;
+        p.evec[i] = ag_chunk_elems(a.bytes / 2) / 8;
+        p.cum[i + 1] = p.cum[i] + (int)((p.nvec[i] + p.evec[i] - 1) / p.evec[i]);
+        p.word[i] = a.chunk_word;
+        p.value[i] = a.chunk_value;
+      }
+      for (int q = 0; q < world; ++q) {
+        p.arena[q] = reinterpret_cast<uint8_t*>(arena_peers[q]);
+        p.flags[q] = reinterpret_cast<uint32_t*>(flag_peers[q]);
+        p.done_peer[q] = done_peers.p[q];
+      }
+      ag_push_chunked_kernel<<<ctas, AG_THREADS, 0, st>>>(p);
+      if (cudaGetLastError() != cudaSuccess) return DC_ECUDA;
+      count_launch();
+    }
+    if (!skip_waits) {
+      wait_flags_kernel<<<1, 1, 0, st>>>(done_local, 1, done_target, timeout_ns, err_flag, 0x200u);
+      count_launch();
+    }
+    return cudaGetLastError() == cudaSuccess ? DC_OK : DC_ECUDA;
+  }
   // members beyond AG_MAXM go to extra launches
   for (size_t b = 0; b < mem.size(); b += AG_MAXM) {
     AgParams p{};
@@ -617,6 +713,8 @@ namespace dc {
 cudaError_t preload_comm_kernels() {
   cudaFuncAttributes a;
   cudaError_t e = cudaFuncGetAttributes(&a, ag_push_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, ag_push_chunked_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, delay_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, wait_flags_kernel);
   auto pre_bulk = [&](auto mode_c) {
     constexpr int MODE = decltype(mode_c)::value;

@@ -38,6 +38,7 @@ struct Layout {
   int n_layers = 0;
   // flag table (uint32 words)
   int64_t f_ready = 0, f_done = 0, f_gready = 0, f_gcons = 0, f_rsdone = 0;
+  int64_t f_chunk = 0;  // fused AG -> GEMM: [param][sender][AG_CHUNKS] chunk-landed values
   int64_t f_scal = 0;   // 2 words: this step's Adam scalars (s, c) as fp32 (graph mode)
   int64_t f_dep = 0;    // graph mode: device step counter (local, monotone)
   int64_t f_bar = 0;    // graph mode: 2 x world barrier words (rounds A, B; one per source rank)
@@ -153,8 +154,35 @@ cudaError_t preload_gemm_kernels();
 
 // comm.cu
 constexpr int MAXW = 8;                       // max ranks on one NVSwitch box
+// fused all-gather -> GEMM: a sender's shard of a param is
+// pushed in at most AG_CHUNKS chunks of >= AG_CHUNK_MIN elements (multiples of
+// 8); after a chunk's stores land on every receiver the sender writes the
+// gather's value into chunk[param][sender][j] of every receiver's flag table.
+constexpr int AG_CHUNKS = 64;
+constexpr int64_t AG_CHUNK_MIN = 4096;
+inline int64_t ag_chunk_elems(int64_t S) {
+  int64_t e = (S + AG_CHUNKS - 1) / AG_CHUNKS;
+  e = (e + 7) / 8 * 8;
+  return e < AG_CHUNK_MIN ? AG_CHUNK_MIN : e;
+}
+// the consumer side: wait until every chunk overlapping flat elements
+// [e0, e1) of a gathered tensor carries `value` (GemmParams / dc_gemm_args)
+struct ChunkWait {
+  const uint32_t* flags = nullptr;   // &chunk[param][0][0] in this rank's table
+  int64_t S = 0, E = 0;              // shard elements, chunk elements
+  uint32_t value = 0;
+};
+bool ctx_fused_ag(const dc_ctx* c);      // option fused_ag at N > 1 (SM push gathers)
+bool ctx_virtual(const dc_ctx* c);
+void ctx_wait_err(dc_ctx* c, uint32_t** err, uint64_t* timeout_ns);
+// the chunk wait of member `param` of gather `gid` issued in the current step
+bool ctx_chunk_wait(const dc_ctx* c, int gid, int param, ChunkWait* out);
 struct PeerFlags { uint32_t* p[MAXW]; int n; };
-struct AgMember { const void* src; int64_t dst_off_bytes; int64_t bytes; };
+struct AgMember {
+  const void* src; int64_t dst_off_bytes; int64_t bytes;
+  int64_t chunk_word = -1;   // fused AG -> GEMM: word of chunk[param][rank][0] in every table (-1: off)
+  uint32_t chunk_value = 0;
+};
 struct RsMember {
   int64_t goff_bytes;      // member's padded full tensor inside the grad slot
   int64_t S;               // shard elements
@@ -164,7 +192,7 @@ dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const
                     const uint32_t* ready_local, uint32_t epoch, PeerFlags done_peers,
                     const uint32_t* done_local, uint32_t done_target, int ctas, uint64_t timeout_ns,
                     uint32_t* err_flag, cudaStream_t st, cudaEvent_t ev_after_ready = nullptr,
-                    bool skip_waits = false);
+                    bool skip_waits = false, uint32_t delay_us = 0, const uint64_t* flag_peers = nullptr);
 dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const uint64_t* slot_peers,
                     const uint32_t* ready_local, uint32_t ready_target, PeerFlags consumed_peers,
                     uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master,

@@ -79,7 +79,44 @@ struct GemmParams {
   float* sk_ws;
   uint32_t* sk_flags;
   uint32_t sk_epoch;
+  // fused all-gather -> GEMM (dc_gemm_args.chunk_*): per B segment
+  const uint32_t* cf[4];
+  int64_t cS[4], cE[4], cn[4], cld[4];
+  uint32_t cval[4];
+  uint32_t* cerr;
+  uint64_t ctmo;
 };
+
+// Wait until every gather chunk overlapping flat elements [e0, e1) of B
+// segment s has landed (fused all-gather -> GEMM).  One thread (the producer).
+__device__ __noinline__ void chunk_wait(const GemmParams& p, int s, int64_t e0, int64_t e1) {
+  e1 = e1 < p.cn[s] ? e1 : p.cn[s];
+  const int64_t S = p.cS[s], E = p.cE[s];
+  uint64_t t0 = 0;
+  for (int64_t e = e0; e < e1;) {
+    const int64_t q = e / S, j = (e - q * S) / E;
+    const uint32_t* f = p.cf[s] + q * AG_CHUNKS + j;
+    uint32_t seen;
+    while ((int32_t)((seen = ptx::ld_acquire_sys(f)) - p.cval[s]) < 0) {
+      if (!t0) t0 = ptx::globaltimer();
+      if (ptx::globaltimer() - t0 > p.ctmo) {
+        if (p.cerr && atomicCAS(p.cerr + 1, 0u, 1u) == 0u) {   // error record (comm.cu spin_ge layout)
+          p.cerr[2] = p.cval[s];
+          p.cerr[3] = seen;
+          p.cerr[4] = (uint32_t)reinterpret_cast<uintptr_t>(f);
+          p.cerr[5] = (uint32_t)(reinterpret_cast<uintptr_t>(f) >> 32);
+          __threadfence_system();
+          atomicExch(p.cerr, 0x600u);
+        }
+        return;
+      }
+      __nanosleep(128);
+    }
+    const int64_t end = j * E + E < S ? j * E + E : S;
+    e = q * S + end;
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");   // generic-proxy (peer) stores -> TMA reads
+}
 // Tile order (tile index -> (m-tile, n-tile)): m fastest inside groups of
 // group_m m-tiles (group_m = m_tiles: m fastest over all of them).  When
 // m_tiles >> n_tiles (the gate / up dW GEMMs: 56 x 16 tiles) small groups make
@@ -598,6 +635,8 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     if (lane == 0) {
       // ----------------------------------------------------------- producer (both CTAs)
       int stage = 0; uint32_t phase = 0;
+      int v_seg = -1;                                 // chunk waits: verified flat range of one segment
+      int64_t v_lo = 0, v_hi = 0;
       for (int ui = 0; ui < nunits; ++ui) {
         const Unit un = unit_at(p, wl, pair, npairs, ui);
         const int tile = un.tile;
@@ -634,6 +673,16 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             kk0 = (kb - (s ? p.seg_end[s - 1] : 0)) * BK;
           }
           const CUtensorMap* mb = s == 0 ? &mapB0 : s == 1 ? &mapB1 : s == 2 ? &mapB2 : &mapB3;
+          if (p.cf[s]) {     // fused all-gather: the rows this load reads must have landed
+            const int64_t e0 = p.b_mn ? (int64_t)kk0 * p.cld[s] + n0 : (int64_t)n0 * p.cld[s];
+            const int64_t e1 = p.b_mn ? (int64_t)(kk0 + BK - 1) * p.cld[s] + n0 + BNT / 2
+                                      : (int64_t)(n0 + BNT / 2) * p.cld[s];
+            if (s != v_seg || e0 < v_lo || e1 > v_hi) {
+              chunk_wait(p, s, e0, e1);
+              if (s == v_seg && e0 >= v_lo && e0 <= v_hi) v_hi = e1 > v_hi ? e1 : v_hi;
+              else { v_seg = s; v_lo = e0; v_hi = e1; }
+            }
+          }
           if (!p.b_mn) {
             ptx::tma_load_2d_2sm(b, mb, lbar, kk0, n0);
           } else {
@@ -944,6 +993,18 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
     if (!pair) { *err = "dc_gemm: a side job needs the CTA-pair kernel"; return DC_EINVAL; }
     p.side = *side;
   }
+  for (int s = 0; s < g->n_bseg; ++s) {
+    if (!g->chunk_flags[s]) continue;
+    if (!pair || g->chunk_S[s] < 8 || g->chunk_E[s] < 8 || g->chunk_numel[s] < 1 ||
+        (g->chunk_S[s] + g->chunk_E[s] - 1) / g->chunk_E[s] > AG_CHUNKS)
+      { *err = "dc_gemm: chunk waits need the CTA-pair kernel, S, E >= 8 and at most 64 chunks per shard"; return DC_EINVAL; }
+    p.cf[s] = g->chunk_flags[s];
+    p.cS[s] = g->chunk_S[s]; p.cE[s] = g->chunk_E[s]; p.cn[s] = g->chunk_numel[s];
+    p.cld[s] = g->ldb[s];
+    p.cval[s] = g->chunk_value[s];
+  }
+  p.cerr = g->chunk_err;
+  p.ctmo = g->chunk_timeout_ns ? g->chunk_timeout_ns : 20ull * 1000 * 1000 * 1000;
   const int glu = g->epilogue;
   if (glu) {
     if (glu != 2 && glu != 3) { *err = "dc_gemm: epilogue is 0, 2 or 3"; return DC_EINVAL; }

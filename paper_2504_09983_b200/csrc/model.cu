@@ -56,6 +56,19 @@ struct S0 {
   int e = -1;       // expert of a per-expert MoE op
 };
 
+// ops whose every param is read only as a GEMM B operand (their gathers may be
+// consumed chunk by chunk: fused all-gather -> GEMM); norm gains and the router
+// are read by other kernels and always wait for the whole gather
+static bool gemm_b_op(int code) {
+  switch (code) {
+    case F_QKV: case B_QKV: case F_O: case B_O: case F_GATE_UP: case B_GATE_UP: case F_DOWN: case B_DOWN:
+    case F_EXP_GU: case B_EXP_GU: case F_EXP_DOWN: case B_EXP_DOWN:
+      return true;
+    default:
+      return false;
+  }
+}
+
 std::string op_label(const S0& o) {
   std::string s = (o.re ? "re_" : "") + std::string(op_name(o.code));
   if (o.e >= 0) s += "_" + std::to_string(o.e);
@@ -106,6 +119,11 @@ struct dc_model {
   int comm_sms = 0;                  // > 0: SM partition (GEMMs | comm + Adam), green contexts
   SmPartition part{};
   int gemm_sms = 0;                  // SMs the layer GEMMs may use (0 = all)
+  // fused all-gather -> GEMM (ctx option fused_ag): the current
+  // op's B operands whose gathers the GEMM waits for per chunk (instead of the
+  // compute stream waiting for the whole gather)
+  std::vector<std::pair<const void*, ChunkWait>> cw;
+  bool fused_ag = false;
   // backward: the dW GEMMs of an op run on a second stream beside its dX GEMM,
   // so their tiles fill the dX GEMM's last partial wave (option dw_concurrent)
   int dw_conc = 1;
@@ -424,10 +442,20 @@ static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t l
   i = 0;
   for (int e : ends) g.bseg_end[i++] = e;
   g.b_mn_major = b_mn; g.b_split_k = split_k;
+  for (int s = 0; s < g.n_bseg; ++s)
+    for (const auto& w : m->cw)
+      if (w.first == g.B[s]) {
+        g.chunk_flags[s] = w.second.flags;
+        g.chunk_S[s] = w.second.S;
+        g.chunk_E[s] = w.second.E;
+        g.chunk_numel[s] = w.second.S * ctx_world(m->ctx);
+        g.chunk_value[s] = w.second.value;
+      }
+  if (!m->cw.empty()) ctx_wait_err(m->ctx, &g.chunk_err, &g.chunk_timeout_ns);
   g.C = C; g.ldc = ldc; g.R = R; g.ldr = ldr;
   // a stream-K pair spins on another pair's partial: never two such kernels at
   // once, so the GEMMs beside the dX GEMM (second stream) are data-parallel only
-  g.stream_k = st == m->cs2 ? 0 : m->stream_k;
+  g.stream_k = (st == m->cs2 || (m->fused_ag && ctx_virtual(m->ctx))) ? 0 : m->stream_k;
   g.workspace = g.stream_k ? m->A(m->ws_sk) : nullptr;
   g.workspace_bytes = g.stream_k ? gemm_workspace_bytes() : 0;
   g.num_sms = m->gemm_sms;
@@ -489,7 +517,7 @@ static dc_status run_op(dc_model* m, const S0& o, cudaStream_t st) {
   // of the op; both only read the op's inputs and write disjoint outputs)
   cudaStream_t sw = st;
   auto fork = [&]() {
-    if (!m->dw_conc || m->comm_sms > 0) return;
+    if (!m->dw_conc || m->comm_sms > 0 || (m->fused_ag && ctx_virtual(m->ctx))) return;
     cudaEventRecord(m->ev_fork, st);
     cudaStreamWaitEvent(m->cs2, m->ev_fork, 0);
     sw = m->cs2;
@@ -861,6 +889,17 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
     m->gemm_sms = 0;
     ctx_set_rs_ctas(m->ctx, 0);
   }
+  m->fused_ag = N > 1 && ctx_fused_ag(m->ctx);
+  if (m->fused_ag && ctx_virtual(m->ctx)) {
+    // virtual ranks share one GPU: a GEMM waiting for another rank's chunks
+    // must not keep that rank's GEMMs off the SMs, so every rank's persistent
+    // GEMM gets 1/N of the SMs (all N resident at once) and no second GEMM
+    // stream; one process per GPU needs none of this
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    m->gemm_sms = std::max(2, sms / N / 2 * 2);
+  }
   if (!m->rs_overlap) rss = cs;
   // an offloaded fragment is reloaded before its layer's RS op (reading D17),
   // i.e. after the dW GEMMs: the fused update needs every state resident
@@ -894,6 +933,7 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
   cudaStreamWaitEvent(cps, m->ev_join[0], 0);
   if (m->host_states) cudaStreamWaitEvent(m->wb_stream, m->ev_join[0], 0);
   std::vector<cudaEvent_t> gather_ev(ctx_layout(m->ctx).S.size(), nullptr);
+  std::vector<int> gather_id(ctx_layout(m->ctx).S.size(), -1);
   const int nops = sched_num_ops(sc);
   for (int i = 0; i < nops; ++i) {
     int kind, id, nm, np, nw;
@@ -907,7 +947,10 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
           cudaStreamWaitEvent(ags, m->ev_pos[id], 0);
           if (profile) ctx_set_gather_timing(m->ctx, m->ev_t0[id], m->ev_t1[id]);   // transfer time
           s = dc_gather(m->ctx, id, ags, m->ev_done[id]);
-          for (int j = 0; j < nm; ++j) gather_ev[mem[j]] = m->ev_done[id];
+          for (int j = 0; j < nm; ++j) {
+            gather_ev[mem[j]] = m->ev_done[id];
+            gather_id[mem[j]] = id;
+          }
         } else {
           s = dc_gather(m->ctx, id, ags, nullptr);
         }
@@ -917,15 +960,26 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
         break;
       case K_COMPUTE: {
         const S0& o = m->s0[id];
+        m->cw.clear();
         if (N > 1)
-          for (int p : o.params)
-            if (gather_ev[p]) cudaStreamWaitEvent(cs, gather_ev[p], 0);
+          for (int p : o.params) {
+            if (!gather_ev[p]) continue;
+            ChunkWait w;
+            if (m->fused_ag && gemm_b_op(o.code) && ctx_chunk_wait(m->ctx, gather_id[p], p, &w)) {
+              void* full = nullptr;           // the op's GEMMs wait per chunk of this B operand
+              dc_tensor_ptr(m->ctx, p, &full);
+              m->cw.push_back({full, w});
+            } else {
+              cudaStreamWaitEvent(cs, gather_ev[p], 0);
+            }
+          }
         if (o.code == B_DOWN || o.code == B_MOE_COMBINE) {   // first non-recompute backward op of the layer
           s = dc_grad_slot_acquire(m->ctx, o.layer, cs);
           if (s != DC_OK) return mfail(m, s, dc_last_error(m->ctx));
         }
         if (profile) prof_rec(m, m->ev_t0[id], cs);
         s = run_op(m, o, cs);
+        m->cw.clear();
         if (profile) prof_rec(m, m->ev_t1[id], cs);
         break;
       }

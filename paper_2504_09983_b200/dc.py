@@ -82,7 +82,10 @@ class GemmArgs(C.Structure):
                 ("C", vp), ("ldc", C.c_int64), ("R", vp), ("ldr", C.c_int64), ("num_sms", C.c_int32),
                 ("kernel", C.c_int32), ("stream_k", C.c_int32),
                 ("epilogue", C.c_int32), ("aux", vp), ("ld_aux", C.c_int64), ("glu_off", C.c_int64),
-                ("workspace", vp), ("workspace_bytes", C.c_uint64), ("tile_group_m", C.c_int32)]
+                ("workspace", vp), ("workspace_bytes", C.c_uint64), ("tile_group_m", C.c_int32),
+                ("chunk_flags", vp * 4), ("chunk_S", C.c_int64 * 4), ("chunk_E", C.c_int64 * 4),
+                ("chunk_numel", C.c_int64 * 4), ("chunk_value", C.c_uint32 * 4),
+                ("chunk_err", vp), ("chunk_timeout_ns", C.c_uint64)]
 
 
 ctx_p, sched_p, model_p = vp, vp, vp
