@@ -215,7 +215,11 @@ dc_status dc_gather_timing(dc_ctx* ctx, cudaEvent_t after_ready, cudaEvent_t aft
  * gather.  Bit-identical results.  With virtual ranks every rank's GEMMs get
  * 1/N of the SMs (co-residency on one GPU).
  * "ag_delay_us" (testing, default 0): every push starts this long after its
- * ready wait (consumers then run ahead of the data). */
+ * ready wait (consumers then run ahead of the data).
+ * "jitter_us" / "jitter_seed" (testing, default 0): random delays in
+ * [0, jitter_us) before every push, every release's ready posts and every
+ * reduce-scatter (a counter-based hash of seed, rank, op and step), so ranks
+ * interleave differently at every op (race detection). */
 dc_status dc_set_option(dc_ctx* ctx, const char* key, int64_t value);
 /* Multicast (NVLS) addresses of this rank's symmetric buffers, as mapped by
  * the caller (torch symmetric memory's multicast_ptr): the gather arena bound

@@ -136,6 +136,18 @@ struct dc_ctx {
   std::map<int, std::vector<uint32_t>> ag_inst;
   uint32_t ag_ninst = 1;
   uint32_t ag_delay_us = 0;             // testing: each push starts this long after its ready wait
+  // testing (SURVEY §5 race detection): random delays in [0, jitter_us) before
+  // every push, every release's ready posts and every reduce-scatter, from a
+  // counter-based hash of (seed, rank, op, epoch) — reorders the ranks
+  uint32_t jitter_us = 0, jitter_seed = 0;
+  uint32_t jitter(int op) const {
+    if (!jitter_us) return 0;
+    uint64_t z = ((uint64_t)jitter_seed << 40) ^ ((uint64_t)rank << 32) ^ ((uint64_t)(uint32_t)op << 12) ^ fepoch;
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return (uint32_t)((z ^ (z >> 31)) % jitter_us);
+  }
   // push CTAs per gather: 64 x 256 threads x 8 x 16 B keeps ~2 MB of stores in
   // flight (NVLink latency x 900 GB/s) and fits beside a GEMM CTA per SM
   int ag_max_ctas = 64;
@@ -476,8 +488,8 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
                     st, c->gt_start)
         : k_ag_push(am, c->world, c->rank, c->arena_peers.data(), c->myflag(c->L.f_ready + (int64_t)gid * c->world),
                     c->fepoch, peers_at(c, c->L.f_done + gid), c->myflag(c->L.f_done + gid), target, ctas,
-                    c->timeout_ns, c->err_dev, st, c->gt_start, c->ag_skip_waits != 0, c->ag_delay_us,
-                    c->flag_peers.data());
+                    c->timeout_ns, c->err_dev, st, c->gt_start, c->ag_skip_waits != 0,
+                    c->ag_delay_us + c->jitter(gid), c->flag_peers.data());
     if (s != DC_OK) return fail(c, s, "dc_gather: launch failed");
     if (c->gt_end) record_event(c->gt_end, st);
   }
@@ -520,6 +532,15 @@ extern "C" dc_status dc_set_option(dc_ctx* c, const char* key, int64_t value) {
   if (!strcmp(key, "ag_delay_us")) {   // testing: start every push this long after its ready wait
     if (value < 0 || value > 1000000) return fail(c, DC_EINVAL, "dc_set_option: ag_delay_us in [0, 1e6]");
     c->ag_delay_us = (uint32_t)value;
+    return DC_OK;
+  }
+  if (!strcmp(key, "jitter_us")) {   // testing: random delays (value = max us; the seed is set by "jitter_seed")
+    if (value < 0 || value > 1000000) return fail(c, DC_EINVAL, "dc_set_option: jitter_us in [0, 1e6]");
+    c->jitter_us = (uint32_t)value;
+    return DC_OK;
+  }
+  if (!strcmp(key, "jitter_seed")) {
+    c->jitter_seed = (uint32_t)value;
     return DC_OK;
   }
   if (!strcmp(key, "nvls")) {   // bit 0: multimem gathers, bit 1: multimem.ld_reduce reduce-scatter
@@ -574,6 +595,7 @@ extern "C" dc_status dc_release(dc_ctx* c, int32_t rid, cudaStream_t st) {
                                 c->L.S[mem[0]] * c->world * 2, st), &c->err);
   if (c->world > 1) c->cur_off[mem[0]] = -1;
   if (c->world == 1) return DC_OK;
+  k_delay(c->jitter(rid + 0x40000), st);
   for (int j = 0; j < np; ++j)
     k_post_flags(peers_at(c, c->L.f_ready + (int64_t)posts[j] * c->world + c->rank), c->fepoch, st);
   if (cudaGetLastError() != cudaSuccess) return fail(c, DC_ECUDA, "dc_release: launch failed");
@@ -717,6 +739,7 @@ dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, con
     ctas = (int)std::min<int64_t>((int64_t)c->num_sms * rs_bulk_ctas_per_sm(), std::max<int64_t>(1, chunks));
   }
   c->rs_done_total += (uint32_t)ctas;
+  k_delay(c->jitter(layer + 0x80000), st);
   if ((c->nvls & 2) && c->grad_mc) {      // f-3: the switch sums the slices (not bit-exact, opt-in)
     dc_status r = k_rs_adam_nvls(mem, c->world, c->rank,
                                  reinterpret_cast<const uint8_t*>(c->grad_mc) + (int64_t)s * c->L.grad_slot_bytes,

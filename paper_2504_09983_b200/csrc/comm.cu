@@ -689,6 +689,12 @@ __global__ void post_flags_kernel(const PostParams p) {
   __threadfence_system();
   for (int i = 0; i < p.n; ++i) ptx::st_release_sys(p.p[i], p.value);
 }
+void k_delay(uint32_t us, cudaStream_t st) {
+  if (!us) return;
+  delay_kernel<<<1, 1, 0, st>>>(us);
+  count_launch();
+}
+
 void k_post_flags(PeerFlags dst, uint32_t value, cudaStream_t st) {
   PostParams p{};
   p.n = dst.n;

@@ -221,6 +221,7 @@ dc_status k_ag_copy(const std::vector<AgMember>& mem, int world, const uint64_t*
                     uint32_t done_target, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st,
                     cudaEvent_t ev_after_ready);
 void k_post_flags(PeerFlags dst, uint32_t value, cudaStream_t st);
+void k_delay(uint32_t us, cudaStream_t st);   // one-thread spin on globaltimer (testing)
 // nvls.cu: multicast all-gather (one multimem.st per 16 B,
 // the switch replicates) and multimem.ld_reduce reduce-scatter + Adam
 dc_status k_ag_multimem(const std::vector<AgMember>& mem, uint8_t* arena_mc, uint32_t* done_mc, int ctas,

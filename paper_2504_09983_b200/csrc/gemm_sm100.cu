@@ -89,24 +89,26 @@ struct GemmParams {
 
 // Wait until every gather chunk overlapping flat elements [e0, e1) of B
 // segment s has landed (fused all-gather -> GEMM).  One thread (the producer).
-__device__ __noinline__ void chunk_wait(const GemmParams& p, int s, int64_t e0, int64_t e1) {
-  e1 = e1 < p.cn[s] ? e1 : p.cn[s];
-  const int64_t S = p.cS[s], E = p.cE[s];
+// (scalars by value: a reference to the kernel's GemmParams would make the
+// compiler copy the whole parameter block to local memory for every thread)
+__device__ __noinline__ void chunk_wait(const uint32_t* flags, int64_t S, int64_t E, int64_t numel, uint32_t value,
+                                        uint32_t* err, uint64_t tmo, int64_t e0, int64_t e1) {
+  e1 = e1 < numel ? e1 : numel;
   uint64_t t0 = 0;
   for (int64_t e = e0; e < e1;) {
     const int64_t q = e / S, j = (e - q * S) / E;
-    const uint32_t* f = p.cf[s] + q * AG_CHUNKS + j;
+    const uint32_t* f = flags + q * AG_CHUNKS + j;
     uint32_t seen;
-    while ((int32_t)((seen = ptx::ld_acquire_sys(f)) - p.cval[s]) < 0) {
+    while ((int32_t)((seen = ptx::ld_acquire_sys(f)) - value) < 0) {
       if (!t0) t0 = ptx::globaltimer();
-      if (ptx::globaltimer() - t0 > p.ctmo) {
-        if (p.cerr && atomicCAS(p.cerr + 1, 0u, 1u) == 0u) {   // error record (comm.cu spin_ge layout)
-          p.cerr[2] = p.cval[s];
-          p.cerr[3] = seen;
-          p.cerr[4] = (uint32_t)reinterpret_cast<uintptr_t>(f);
-          p.cerr[5] = (uint32_t)(reinterpret_cast<uintptr_t>(f) >> 32);
+      if (ptx::globaltimer() - t0 > tmo) {
+        if (err && atomicCAS(err + 1, 0u, 1u) == 0u) {   // error record (comm.cu spin_ge layout)
+          err[2] = value;
+          err[3] = seen;
+          err[4] = (uint32_t)reinterpret_cast<uintptr_t>(f);
+          err[5] = (uint32_t)(reinterpret_cast<uintptr_t>(f) >> 32);
           __threadfence_system();
-          atomicExch(p.cerr, 0x600u);
+          atomicExch(err, 0x600u);
         }
         return;
       }
@@ -678,7 +680,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             const int64_t e1 = p.b_mn ? (int64_t)(kk0 + BK - 1) * p.cld[s] + n0 + BNT / 2
                                       : (int64_t)(n0 + BNT / 2) * p.cld[s];
             if (s != v_seg || e0 < v_lo || e1 > v_hi) {
-              chunk_wait(p, s, e0, e1);
+              chunk_wait(p.cf[s], p.cS[s], p.cE[s], p.cn[s], p.cval[s], p.cerr, p.ctmo, e0, e1);
               if (s == v_seg && e0 >= v_lo && e0 <= v_hi) v_hi = e1 > v_hi ? e1 : v_hi;
               else { v_seg = s; v_lo = e0; v_hi = e1; }
             }

@@ -162,3 +162,25 @@ def test_plan_parity_full_sizes(name, L, N, ck, M_gb, passes):
     assert isinstance(c, str) and o == c
     plan = json.loads(c)
     assert ("O" in passes) == bool(plan["offload"])
+
+
+def test_hot_kernels_have_no_local_memory():
+    """The hot kernels keep their parameter block in constant memory and their
+    state in registers: no stack frame / local memory (cuobjdump -res-usage of
+    the built library).  Guards against, e.g., passing the GEMM's kernel
+    parameters by reference to a non-inlined helper, which copies the whole
+    block to local memory for every thread (measured 12 % slower step, r02).
+    The fused-Adam GEMM epilogue (EPI = 1, opt-in) keeps a 16-byte frame."""
+    import shutil
+    import subprocess
+    from paper_2504_09983_b200 import build as b
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "-res-usage", b.LIB], capture_output=True, text=True, timeout=300).stdout
+    funcs = re.findall(r"Function (\S+):\s*\n\s*REG:(\d+) STACK:(\d+) SHARED:\d+ LOCAL:(\d+)", out)
+    assert funcs
+    hot = [f for f in funcs if re.search(r"gemm2_bf16_sm100ILi\d+ELi\d+ELi[023]E|rs_adam|ag_push|ag_multimem", f[0])]
+    assert len(hot) >= 8, [f[0] for f in hot]
+    bad = [(f[0], f[2], f[3]) for f in hot if int(f[2]) or int(f[3])]
+    assert not bad, bad

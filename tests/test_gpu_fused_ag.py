@@ -97,3 +97,22 @@ def test_fused_ag_option_rules():
     sched = dc.plan(json.dumps(rt.profile_json(st, tc=TC)), 1 << 40, passes=dc.DC_PASS_SHARD)
     rt.bind(ranks, {r: sched for r in ranks})
     assert dc.lib.dc_set_option(st.ctx, b"fused_ag", 1) == dc.DC_ESTATE      # after the bind
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_random_delay_injection_matches_oracle(fused):
+    """SURVEY §5 race detection: every push, every release's ready posts and
+    every reduce-scatter start after a random delay (option jitter_us, a
+    counter-based hash of (seed, rank, op, step)), so the 4 virtual ranks
+    interleave differently at every op; released arena intervals are poisoned.
+    Two planned steps still match the oracle exactly."""
+    cfg = synth.small_llama(layers=2, seq=128)
+    table, ranks = _ranks(cfg, 4, fused, 0)
+    for r, st in ranks.items():
+        dc.check(dc.lib.dc_set_option(st.ctx, b"jitter_us", 3000), st.ctx)
+        dc.check(dc.lib.dc_set_option(st.ctx, b"jitter_seed", 17 + r), st.ctx)
+    prof = rt.profile_json(ranks[0], tc=TC)
+    sched = dc.plan(json.dumps(prof), 1 << 40, M_prefetch=1 << 22, passes=PS, strict=True)
+    rt.bind(ranks, {r: sched for r in ranks})
+    for s in (1, 2):
+        check_step(ranks, table, cfg, 4, s, LR, lambda: rt.step(ranks, s))

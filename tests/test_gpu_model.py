@@ -11,6 +11,7 @@ oracle's grads).
 """
 import ctypes as C
 import json
+import os
 
 import numpy as np
 import pytest
@@ -217,7 +218,11 @@ def test_fused_act_epilogues_bitexact(moe, checkpoint):
 # (N = 2 only: with more virtual ranks on one GPU their copies share copy-engine
 # queues, and a copy gated on a cross-rank flag wait can head-of-line block
 # another rank's copies — one stall in ~15 runs at N = 4)
-@pytest.mark.parametrize("world,moe", [(2, False), (2, True)])
+@pytest.mark.parametrize("world,moe", [(2, False), (2, True),
+                                       pytest.param(4, False, marks=pytest.mark.skipif(
+                                           not os.environ.get("DC_TEST_CE4"),
+                                           reason="4 virtual ranks' copy-engine gathers share copy-engine queues "
+                                                  "on one GPU (head-of-line stall risk); DC_TEST_CE4=1 opts in"))])
 def test_copy_engine_gather_bitexact(world, moe):
     """ag_copy_engine: every gather as cudaMemcpyAsync peer
     copies under the same ready / done flag protocol.  Two planned steps
