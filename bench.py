@@ -779,6 +779,9 @@ def main():
                     "they run in compute-stream order)"}
     if world > 1:
         exposed = dict(idle, target="< 10 % of the step (BASELINE north star)")
+        if os.environ.get("DC_FUSED_AG", "0") not in ("", "0"):
+            exposed["note"] += ("; fused_ag: a GEMM's waits for gather chunks fall inside its op events, so this "
+                                "is a lower bound")
     else:
         exposed = {"ms": None, "frac": None, "note": "N = 1: no communication (gathers alias the shard, the "
                    "reduce-scatter reads only local grads); compute_stream_idle has the step's idle time"}
