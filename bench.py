@@ -607,6 +607,8 @@ def main():
             n = rt.C.c_int64()
             dc.check(dc.lib.dc_model_launch_count(st.model, rt.C.byref(n)))
             launches += n.value
+        # host-resident states: the last step's state write-backs are inside the timed region
+        dc.check(dc.lib.dc_model_join_states(st.model, cs.cuda_stream))
         e1.record(cs)
         barrier()
         clocks = clk.stop()
@@ -728,6 +730,7 @@ def main():
             loss_host.copy_(lp, non_blocking=True)
         cs.synchronize()
         _ = loss_host.tolist()
+    dc.check(dc.lib.dc_model_join_states(st.model, cs.cuda_stream))
     e1.record(cs)
     barrier()
     ems = torch.tensor([e0.elapsed_time(e1) / args.steps], device=cdev)

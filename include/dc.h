@@ -214,6 +214,11 @@ dc_status dc_gather_timing(dc_ctx* ctx, cudaEvent_t after_ready, cudaEvent_t aft
  * (dc_gemm_args.chunk_*) instead of the compute stream waiting for the whole
  * gather.  Bit-identical results.  With virtual ranks every rank's GEMMs get
  * 1/N of the SMs (co-residency on one GPU).
+ * "ag_bulk" (default 0, any time): the SM push moves its data with the bulk-
+ * copy (TMA) engine — one thread per CTA streams 8 KB pieces of the shard into
+ * a 4-stage shared-memory ring (cp.async.bulk + mbarrier) and issues one bulk
+ * store per receiver; same done protocol, bit-identical buffers (ignored for
+ * fused_ag's chunked pushes).
  * "ag_delay_us" (testing, default 0): every push starts this long after its
  * ready wait (consumers then run ahead of the data).
  * "jitter_us" / "jitter_seed" (testing, default 0): random delays in
@@ -449,6 +454,13 @@ dc_status dc_model_bind_host_states(dc_model* m, float* m_dev, float* v_dev, voi
 dc_status dc_model_graph_capture(dc_model* m, int32_t step_t, cudaStream_t compute, cudaStream_t ag,
                                  cudaStream_t rs, cudaStream_t copy);
 dc_status dc_model_graph_launch(dc_model* m, int32_t step_t, cudaStream_t compute);
+/* Host-resident states (reading D28): dc_model_step does not join the
+ * write-back stream into the compute stream — the write-backs of the step's
+ * last updated fragments overlap the next step's forward, whose reloads wait
+ * for them.  This enqueues on `stream` a wait for every write-back issued so
+ * far (call before reading the host copies from the stream, or before the
+ * end event of a timed region); DC_OK and nothing enqueued otherwise. */
+dc_status dc_model_join_states(dc_model* m, cudaStream_t stream);
 /* Number of kernels the last dc_model_step launched. */
 dc_status dc_model_launch_count(const dc_model* m, int64_t* n);
 

@@ -121,6 +121,7 @@ struct dc_ctx {
   std::vector<float*> lay_m, lay_v;     // per layer: m / v base for rs_adam (ring slot) or null
   cudaEvent_t gt_start = nullptr, gt_end = nullptr;   // one-shot gather timing (profiling)
   int ag_ce = 0;                        // 1: gathers as copy-engine peer copies (no SM time)
+  int ag_bulk = 0;                      // 1: the push's data path on the bulk-copy (TMA) engine
   int ag_skip_waits = 0;                // profiling only: push without the ready / done flag waits
   // NVLS: multicast addresses of the arena / grad slots / flag
   // table (dc_bind_multicast; 0 = none) and option "nvls" (bit 0 gathers,
@@ -489,7 +490,7 @@ extern "C" dc_status dc_gather(dc_ctx* c, int32_t gid, cudaStream_t st, cudaEven
         : k_ag_push(am, c->world, c->rank, c->arena_peers.data(), c->myflag(c->L.f_ready + (int64_t)gid * c->world),
                     c->fepoch, peers_at(c, c->L.f_done + gid), c->myflag(c->L.f_done + gid), target, ctas,
                     c->timeout_ns, c->err_dev, st, c->gt_start, c->ag_skip_waits != 0,
-                    c->ag_delay_us + c->jitter(gid), c->flag_peers.data());
+                    c->ag_delay_us + c->jitter(gid), c->flag_peers.data(), c->ag_bulk != 0);
     if (s != DC_OK) return fail(c, s, "dc_gather: launch failed");
     if (c->gt_end) record_event(c->gt_end, st);
   }
@@ -522,6 +523,10 @@ extern "C" dc_status dc_set_option(dc_ctx* c, const char* key, int64_t value) {
   }
   if (!strcmp(key, "rs_bulk")) {   // may change between steps (the launch reads it)
     c->rs_bulk = value != 0;
+    return DC_OK;
+  }
+  if (!strcmp(key, "ag_bulk")) {   // any time (read at each dc_gather)
+    c->ag_bulk = value != 0;
     return DC_OK;
   }
   if (!strcmp(key, "fused_ag")) {   // chunked pushes + per-tile GEMM waits (dc_model_step), SURVEY §8 f-4

@@ -175,10 +175,14 @@ __global__ void wait_flags_kernel(const uint32_t* f, int n, uint32_t target, uin
     if (!spin_ge(f + i, target, t0, tmo, err, code | i)) return;
 }
 
+dc_status launch_ag_bulk(const std::vector<AgMember>& mem, int world, int rank, const uint64_t* arena_peers,
+                         PeerFlags done_peers, int ctas, cudaStream_t st);
+
 dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const uint64_t* arena_peers,
                     const uint32_t* ready_local, uint32_t epoch, PeerFlags done_peers, const uint32_t* done_local,
                     uint32_t done_target, int ctas, uint64_t timeout_ns, uint32_t* err_flag, cudaStream_t st,
-                    cudaEvent_t ev_after_ready, bool skip_waits, uint32_t delay_us, const uint64_t* flag_peers) {
+                    cudaEvent_t ev_after_ready, bool skip_waits, uint32_t delay_us, const uint64_t* flag_peers,
+                    bool bulk) {
   if (!skip_waits) {
     wait_flags_kernel<<<1, 1, 0, st>>>(ready_local, world, epoch, timeout_ns, err_flag, 0x100u);
     count_launch();
@@ -187,6 +191,15 @@ dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const
   if (delay_us) {
     delay_kernel<<<1, 1, 0, st>>>(delay_us);
     count_launch();
+  }
+  if (bulk && (mem.empty() || mem[0].chunk_word < 0)) {   // bulk-copy pipeline (option ag_bulk)
+    dc_status r = launch_ag_bulk(mem, world, rank, arena_peers, done_peers, ctas, st);
+    if (r != DC_OK) return r;
+    if (!skip_waits) {
+      wait_flags_kernel<<<1, 1, 0, st>>>(done_local, 1, done_target, timeout_ns, err_flag, 0x200u);
+      count_launch();
+    }
+    return cudaGetLastError() == cudaSuccess ? DC_OK : DC_ECUDA;
   }
   if (!mem.empty() && mem[0].chunk_word >= 0) {   // chunked pushes (fused all-gather -> GEMM)
     if (!flag_peers) return DC_EINVAL;
@@ -416,6 +429,109 @@ __device__ __forceinline__ void bulk_g2s(void* s, const void* g, uint32_t bytes,
 __device__ __forceinline__ void bulk_s2g(void* g, const void* s, uint32_t bytes, uint64_t pol) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
                :: "l"(g), "r"(ptx::smem_u32(s)), "r"(bytes), "l"(pol) : "memory");
+}
+
+// ------------------------------------------------------------------ ag_push (bulk-copy pipeline)
+// The push with its data path on the SM's bulk-copy (TMA) engine instead of
+// per-thread 16-byte loads / stores: one thread streams PIECE-byte pieces of
+// the members' shards into a ring of AGB_ST shared-memory stages
+// (cp.async.bulk global -> shared, mbarrier completion) and, for each landed
+// piece, issues one bulk store per receiver (cp.async.bulk shared -> global,
+// bulk groups; ranks rotated as in ag_push).  A stage is refilled once its
+// stores have READ it (wait_group.read), so the next pieces' loads stay in
+// flight behind the stores.  32 KB of shared memory and one warp per CTA: it
+// fits beside a pair-GEMM CTA (193 KB, 384 threads).  Completion: wait_group 0
+// (stores performed), proxy fence, system fence, red.release.sys of every
+// receiver's done counter — the same done protocol as ag_push.
+constexpr int AGB_PIECE = 8192, AGB_ST = 4, AGB_SMEM = AGB_PIECE * AGB_ST + 128;
+struct AgBulkParams {
+  int nm, world, rank;
+  const uint8_t* src[AG_MAXM];
+  int64_t dst_off[AG_MAXM];
+  int64_t bytes[AG_MAXM];
+  int cum[AG_MAXM + 1];       // piece list prefix: member m owns pieces [cum[m], cum[m + 1])
+  uint8_t* arena[MAXW];
+  uint32_t* done_peer[MAXW];
+};
+
+__global__ void __launch_bounds__(32) ag_push_bulk_kernel(const AgBulkParams p) {
+  extern __shared__ __align__(128) uint8_t agb_smem[];
+  uint8_t* buf = agb_smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(agb_smem + AGB_PIECE * AGB_ST);
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < AGB_ST; ++s) ptx::mbar_init(&full[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const uint64_t pol = policy_evict_first();
+  const int total = p.cum[p.nm];
+  // piece k of this CTA = global piece blockIdx.x + k * gridDim.x
+  auto locate = [&](int c, int& m, int64_t& off, uint32_t& n) {
+    m = 0;
+    while (c >= p.cum[m + 1]) ++m;
+    off = (int64_t)(c - p.cum[m]) * AGB_PIECE;
+    const int64_t rem = p.bytes[m] - off;
+    n = (uint32_t)(rem < AGB_PIECE ? rem : AGB_PIECE);
+  };
+  auto load = [&](int k) {
+    const int c = blockIdx.x + k * gridDim.x;
+    if (c >= total) return;
+    int m; int64_t off; uint32_t n;
+    locate(c, m, off, n);
+    uint64_t* bar = &full[k % AGB_ST];
+    ptx::mbar_arrive_expect_tx(bar, n);
+    bulk_g2s(buf + (k % AGB_ST) * AGB_PIECE, p.src[m] + off, n, bar, pol);
+  };
+  // loads run AGB_AHEAD pieces ahead; the stores of up to AGB_ST - AGB_AHEAD
+  // pieces stay in flight (a stage is refilled once the stores of the piece
+  // that used it AGB_ST pieces earlier have read it)
+  constexpr int AGB_AHEAD = 2;
+  for (int k = 0; k < AGB_AHEAD; ++k) load(k);
+  for (int k = 0;; ++k) {
+    const int c = blockIdx.x + k * gridDim.x;
+    if (c >= total) break;
+    int m; int64_t off; uint32_t n;
+    locate(c, m, off, n);
+    ptx::mbar_wait(&full[k % AGB_ST], (k / AGB_ST) & 1);
+    const uint8_t* st = buf + (k % AGB_ST) * AGB_PIECE;
+    for (int qq = 0; qq < p.world; ++qq) {
+      uint8_t* dst = p.arena[(qq + p.rank) % p.world] + p.dst_off[m] + off;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   :: "l"(dst), "r"(ptx::smem_u32(st)), "r"(n) : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    // piece k + AHEAD goes to the stage of piece k + AHEAD - ST: its stores
+    // (committed ST - AHEAD groups ago) must have read it
+    asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(AGB_ST - AGB_AHEAD) : "memory");
+    load(k + AGB_AHEAD);
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");      // every store performed
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __threadfence_system();
+  for (int q = 0; q < p.world; ++q) ptx::red_add_release_sys(p.done_peer[q], 1u);
+}
+
+dc_status launch_ag_bulk(const std::vector<AgMember>& mem, int world, int rank, const uint64_t* arena_peers,
+                         PeerFlags done_peers, int ctas, cudaStream_t st) {
+  for (size_t b = 0; b < mem.size(); b += AG_MAXM) {
+    AgBulkParams p{};
+    p.nm = (int)std::min<size_t>(AG_MAXM, mem.size() - b);
+    p.world = world; p.rank = rank;
+    p.cum[0] = 0;
+    for (int i = 0; i < p.nm; ++i) {
+      const AgMember& a = mem[b + i];
+      p.src[i] = reinterpret_cast<const uint8_t*>(a.src);
+      p.dst_off[i] = a.dst_off_bytes;
+      p.bytes[i] = a.bytes;
+      p.cum[i + 1] = p.cum[i] + (int)((a.bytes + AGB_PIECE - 1) / AGB_PIECE);
+    }
+    for (int q = 0; q < world; ++q) {
+      p.arena[q] = reinterpret_cast<uint8_t*>(arena_peers[q]);
+      p.done_peer[q] = done_peers.p[q];
+    }
+    ag_push_bulk_kernel<<<ctas, 32, AGB_SMEM, st>>>(p);
+    if (cudaGetLastError() != cudaSuccess) return DC_ECUDA;
+    count_launch();
+  }
+  return DC_OK;
 }
 
 template <int MAXQ, int MODE>
@@ -720,6 +836,7 @@ cudaError_t preload_comm_kernels() {
   cudaFuncAttributes a;
   cudaError_t e = cudaFuncGetAttributes(&a, ag_push_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, ag_push_chunked_kernel);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(ag_push_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AGB_SMEM);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, delay_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, wait_flags_kernel);
   auto pre_bulk = [&](auto mode_c) {

@@ -192,7 +192,8 @@ dc_status k_ag_push(const std::vector<AgMember>& mem, int world, int rank, const
                     const uint32_t* ready_local, uint32_t epoch, PeerFlags done_peers,
                     const uint32_t* done_local, uint32_t done_target, int ctas, uint64_t timeout_ns,
                     uint32_t* err_flag, cudaStream_t st, cudaEvent_t ev_after_ready = nullptr,
-                    bool skip_waits = false, uint32_t delay_us = 0, const uint64_t* flag_peers = nullptr);
+                    bool skip_waits = false, uint32_t delay_us = 0, const uint64_t* flag_peers = nullptr,
+                    bool bulk = false);
 dc_status k_rs_adam(const std::vector<RsMember>& mem, int world, int rank, const uint64_t* slot_peers,
                     const uint32_t* ready_local, uint32_t ready_target, PeerFlags consumed_peers,
                     uint32_t consumed_value, uint32_t* done_ctr, uint32_t done_target, float* master,

@@ -87,20 +87,34 @@ struct GemmParams {
   uint64_t ctmo;
 };
 
+__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(ptx::smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" :: "r"(ptx::smem_u32(p)), "r"(v) : "memory");
+}
+
 // Wait until every gather chunk overlapping flat elements [e0, e1) of B
 // segment s has landed (fused all-gather -> GEMM).  One thread (the producer).
 // (scalars by value: a reference to the kernel's GemmParams would make the
 // compiler copy the whole parameter block to local memory for every thread)
-__device__ __noinline__ void chunk_wait(const uint32_t* flags, int64_t S, int64_t E, int64_t numel, uint32_t value,
-                                        uint32_t* err, uint64_t tmo, int64_t e0, int64_t e1) {
+// Returns the flat end of the last chunk verified (>= e1): the caller's cache.
+__device__ __noinline__ int64_t chunk_wait(const uint32_t* flags, int64_t S, int64_t E, int64_t numel, uint32_t value,
+                                           uint32_t* err, uint64_t tmo, int64_t e0, int64_t e1) {
   e1 = e1 < numel ? e1 : numel;
   uint64_t t0 = 0;
-  for (int64_t e = e0; e < e1;) {
+  int64_t e = e0;
+  while (e < e1) {
     const int64_t q = e / S, j = (e - q * S) / E;
     const uint32_t* f = flags + q * AG_CHUNKS + j;
     uint32_t seen;
     while ((int32_t)((seen = ptx::ld_acquire_sys(f)) - value) < 0) {
       if (!t0) t0 = ptx::globaltimer();
+      // after any recorded timeout (this or another wait) fail fast: the
+      // sticky error is reported by the next host call on the ctx
+      if (err && *reinterpret_cast<volatile uint32_t*>(err)) return e1;
       if (ptx::globaltimer() - t0 > tmo) {
         if (err && atomicCAS(err + 1, 0u, 1u) == 0u) {   // error record (comm.cu spin_ge layout)
           err[2] = value;
@@ -110,14 +124,14 @@ __device__ __noinline__ void chunk_wait(const uint32_t* flags, int64_t S, int64_
           __threadfence_system();
           atomicExch(err, 0x600u);
         }
-        return;
+        return e1;
       }
-      __nanosleep(128);
+      __nanosleep(64);
     }
     const int64_t end = j * E + E < S ? j * E + E : S;
     e = q * S + end;
   }
-  asm volatile("fence.proxy.async.global;" ::: "memory");   // generic-proxy (peer) stores -> TMA reads
+  return e;
 }
 // Tile order (tile index -> (m-tile, n-tile)): m fastest inside groups of
 // group_m m-tiles (group_m = m_tiles: m fastest over all of them).  When
@@ -595,7 +609,10 @@ template <int BNT, int ST> struct Pair {
 
 constexpr int GEMM2_THREADS = 384;          // + side-job warps 8..11
 
-template <int BNT, int ST, int EPI>
+// CW: per-tile chunk waits of a fused all-gather (dc_gemm_args.chunk_*); a
+// separate instantiation, so the default kernels carry none of that code
+// (r02: even the untaken branch and its call made the step ~6 % slower)
+template <int BNT, int ST, int EPI, bool CW = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
 gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
                  const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
@@ -611,6 +628,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
+  [[maybe_unused]] uint32_t* cw_progress = tmem_slot + 1;   // CW: B loads the watcher has cleared
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_ctarank();
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
@@ -625,6 +643,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     if (p.nseg > 3) ptx::tma_prefetch(&mapB3);
     for (int s = 0; s < Pair<BNT, ST>::STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { ptx::mbar_init(&tfull[b], 1); ptx::mbar_init(&tempty[b], 8); }
+    if constexpr (CW) *cw_progress = 0u;
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, Pair<BNT, ST>::TMEM);
@@ -637,8 +656,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     if (lane == 0) {
       // ----------------------------------------------------------- producer (both CTAs)
       int stage = 0; uint32_t phase = 0;
-      int v_seg = -1;                                 // chunk waits: verified flat range of one segment
-      int64_t v_lo = 0, v_hi = 0;
+      [[maybe_unused]] int cw_step = 0;               // chunk waits: this load's index in the watcher's walk
       for (int ui = 0; ui < nunits; ++ui) {
         const Unit un = unit_at(p, wl, pair, npairs, ui);
         const int tile = un.tile;
@@ -675,15 +693,10 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             kk0 = (kb - (s ? p.seg_end[s - 1] : 0)) * BK;
           }
           const CUtensorMap* mb = s == 0 ? &mapB0 : s == 1 ? &mapB1 : s == 2 ? &mapB2 : &mapB3;
-          if (p.cf[s]) {     // fused all-gather: the rows this load reads must have landed
-            const int64_t e0 = p.b_mn ? (int64_t)kk0 * p.cld[s] + n0 : (int64_t)n0 * p.cld[s];
-            const int64_t e1 = p.b_mn ? (int64_t)(kk0 + BK - 1) * p.cld[s] + n0 + BNT / 2
-                                      : (int64_t)(n0 + BNT / 2) * p.cld[s];
-            if (s != v_seg || e0 < v_lo || e1 > v_hi) {
-              chunk_wait(p.cf[s], p.cS[s], p.cE[s], p.cn[s], p.cval[s], p.cerr, p.ctmo, e0, e1);
-              if (s == v_seg && e0 >= v_lo && e0 <= v_hi) v_hi = e1 > v_hi ? e1 : v_hi;
-              else { v_seg = s; v_lo = e0; v_hi = e1; }
-            }
+          if constexpr (CW) {  // fused all-gather: the watcher (warp 3) has seen this load's chunks land
+            while (ld_acquire_cta(cw_progress) <= (uint32_t)cw_step) {}
+            asm volatile("fence.proxy.async.global;" ::: "memory");   // peer (generic) stores -> TMA reads
+            ++cw_step;
           }
           if (!p.b_mn) {
             ptx::tma_load_2d_2sm(b, mb, lbar, kk0, n0);
@@ -729,6 +742,58 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         if (ptx::elect_one()) ptx::umma_commit_2sm_mc(&tfull[acc], 0x3);
         __syncwarp();
         if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+  } else if (CW && warp == 3) {   // (warp 3 is a side-job warp otherwise)
+    if constexpr (CW) {
+      if (lane == 0) {
+        // ------------------------------------------------------- chunk watcher (fused all-gather)
+        // Walks the producer's sequence of B loads ahead of it; for each one
+        // waits (acquire, system scope) until the gather chunks it reads have
+        // landed and then publishes the count of cleared loads in shared
+        // memory, so the system-scope flag latency stays off the producer's
+        // critical path.  A verified chunk range is cached (end of the last
+        // chunk seen), so consecutive k-blocks / tiles rarely touch a flag.
+        int v_seg = -1;
+        int64_t v_lo = 0, v_hi = 0;
+        uint32_t n = 0;
+        for (int ui = 0; ui < nunits; ++ui) {
+          const Unit un = unit_at(p, wl, pair, npairs, ui);
+          int mt, nt;
+          tile_mn(p, un.tile, mt, nt);
+          int bseg = 0, n0 = nt * BNT;
+          if constexpr (EPI == 2) {
+            bseg = (int)rank;
+            n0 = nt * (BNT / 2);
+          } else {
+            if (!p.split_k) {
+              bseg = seg_of(p, nt);
+              n0 = (nt - (bseg ? p.seg_end[bseg - 1] : 0)) * BNT;
+            }
+            n0 += (int)rank * (BNT / 2);
+          }
+          for (int kb = un.kb0; kb < un.kb1; ++kb) {
+            int sg = bseg, kk0 = kb * BK;
+            if (p.split_k) {
+              sg = seg_of(p, kb);
+              kk0 = (kb - (sg ? p.seg_end[sg - 1] : 0)) * BK;
+            }
+            if (p.cf[sg]) {
+              const int64_t e0 = p.b_mn ? (int64_t)kk0 * p.cld[sg] + n0 : (int64_t)n0 * p.cld[sg];
+              const int64_t e1 = p.b_mn ? (int64_t)(kk0 + BK - 1) * p.cld[sg] + n0 + BNT / 2
+                                        : (int64_t)(n0 + BNT / 2) * p.cld[sg];
+              if (sg != v_seg || e0 < v_lo || e1 > v_hi) {
+                const bool extend = sg == v_seg && e0 >= v_lo && e0 <= v_hi;
+                const int64_t from = extend ? v_hi : e0;
+                const int64_t end = chunk_wait(p.cf[sg], p.cS[sg], p.cE[sg], p.cn[sg], p.cval[sg], p.cerr, p.ctmo,
+                                               from, e1);
+                if (extend) v_hi = end;
+                else { v_seg = sg; v_lo = e0; v_hi = end; }
+              }
+            }
+            st_release_cta(cw_progress, ++n);
+          }
+        }
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -1093,7 +1158,13 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
 #define DC_PAIR_LAUNCH(BN_, ST_)                                                                   \
     (p.epi ? gemm2_bf16_sm100<BN_, ST_, 1><<<g2, GEMM2_THREADS, Pair<BN_, ST_>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p) \
            : gemm2_bf16_sm100<BN_, ST_, 0><<<g2, GEMM2_THREADS, Pair<BN_, ST_>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p))
-    if (glu == 2) gemm2_bf16_sm100<256, 6, 2><<<g2, GEMM2_THREADS, Pair<256, 6>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+    bool cw = false;
+    for (int s = 0; s < 4; ++s) cw = cw || p.cf[s];
+    if (cw && (bnt != 256 || (p.epi != 0 && p.epi != 2)))
+      { *err = "dc_gemm: chunk waits need the 256-wide pair kernel with epilogue 0 or 2"; return DC_EINVAL; }
+    if (cw && glu == 2) gemm2_bf16_sm100<256, 6, 2, true><<<g2, GEMM2_THREADS, Pair<256, 6>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+    else if (cw) gemm2_bf16_sm100<256, 6, 0, true><<<g2, GEMM2_THREADS, Pair<256, 6>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+    else if (glu == 2) gemm2_bf16_sm100<256, 6, 2><<<g2, GEMM2_THREADS, Pair<256, 6>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
     else if (glu == 3) gemm2_bf16_sm100<256, 6, 3><<<g2, GEMM2_THREADS, Pair<256, 6>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
     else if (bnt == 128) DC_PAIR_LAUNCH(128, 9);
     else if (env_st == 6) DC_PAIR_LAUNCH(256, 6);
@@ -1153,6 +1224,12 @@ cudaError_t preload_gemm_kernels() {
   DC_PAIR_ATTR(128, 9, 0)
   DC_PAIR_ATTR(128, 9, 1)
 #undef DC_PAIR_ATTR
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm2_bf16_sm100<256, 6, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Pair<256, 6>::SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm2_bf16_sm100<256, 6, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Pair<256, 6>::SMEM);
   if (e == cudaSuccess) e = query_pair_slots<256, 6>(&g_pair_slots[0]);
   if (e == cudaSuccess) e = query_pair_slots<128, 9>(&g_pair_slots[1]);
   if (e == cudaSuccess) e = query_pair_slots<256, 7>(&g_pair_slots[2]);

@@ -1051,10 +1051,10 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
   cudaStreamWaitEvent(ucs, m->ev_join[1], 0);
   cudaStreamWaitEvent(ucs, m->ev_join[2], 0);
   cudaStreamWaitEvent(ucs, m->ev_join[3], 0);
-  if (m->host_states) {
-    cudaEventRecord(m->ev_join[3], m->wb_stream);
-    cudaStreamWaitEvent(ucs, m->ev_join[3], 0);
-  }
+  // host-resident states (D28): the write-backs of the last updated fragments
+  // are NOT joined here — they overlap the next step's forward (the next
+  // reload of a fragment, and of its ring slot, waits for them: wb_ev);
+  // dc_model_join_states orders a stream after them
   if (cs != ucs) {
     cudaEventRecord(m->ev_join[4], cs);
     cudaStreamWaitEvent(ucs, m->ev_join[4], 0);
@@ -1065,6 +1065,15 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
     m->profile_pending = true;
     if (profile == 1) return collect_profile(m);   // 2: events only, read later
   }
+  return DC_OK;
+}
+
+extern "C" dc_status dc_model_join_states(dc_model* m, cudaStream_t stream) {
+  if (!m) return mfail(nullptr, DC_EINVAL, "dc_model_join_states: null model");
+  if (!m->host_states || !m->wb_stream) return DC_OK;
+  if (cudaEventRecord(m->ev_join[3], m->wb_stream) != cudaSuccess ||
+      cudaStreamWaitEvent(stream, m->ev_join[3], 0) != cudaSuccess)
+    return mfail(m, DC_ECUDA, "dc_model_join_states: event failed");
   return DC_OK;
 }
 

@@ -129,6 +129,7 @@ _sig = {
     "dc_model_set_option": (C.c_int, [vp, C.c_char_p, C.c_int64]),
     "dc_set_option": (C.c_int, [vp, C.c_char_p, C.c_int64]),
     "dc_bind_multicast": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_uint64]),
+    "dc_model_join_states": (C.c_int, [vp, vp]),
     "dc_model_graph_capture": (C.c_int, [vp, C.c_int32, vp, vp, vp, vp]),
     "dc_model_graph_launch": (C.c_int, [vp, C.c_int32, vp]),
     "dc_model_host_states_query": (C.c_int, [vp, p_i64, p_i64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),

@@ -62,12 +62,14 @@ def s0_profile(n, world, sizes):
     return {"ops": ops, "params": params, "frags": [], "tc": [[0, 0], [1 << 40, 0]]}
 
 
-def sweep(world, sizes, steps, copy_engine, hbm_peak):
+def sweep(world, sizes, steps, mode, hbm_peak):
+    """mode: sm (16-byte stores), ce (copy engines), bulk (bulk-copy / TMA pipeline)."""
     table = table_of(sizes)
     ranks = rt.create_ranks(table, world, init=False)
     for st in ranks.values():
         st.tensors["shard"].view(torch.int16).random_(-30000, 30000)
-        dc.check(dc.lib.dc_set_option(st.ctx, b"ag_copy_engine", int(copy_engine)), st.ctx)
+        dc.check(dc.lib.dc_set_option(st.ctx, b"ag_copy_engine", int(mode == "ce")), st.ctx)
+        dc.check(dc.lib.dc_set_option(st.ctx, b"ag_bulk", int(mode == "bulk")), st.ctx)
     prof = s0_profile(len(sizes), world, sizes)
     sched = dc.plan(json.dumps(prof), 1 << 50, passes=dc.DC_PASS_SHARD)
     plan = json.loads(dc.schedule_json(sched))
@@ -115,7 +117,7 @@ def sweep(world, sizes, steps, copy_engine, hbm_peak):
     return rows
 
 
-def push_only(world, sizes, reps=2):
+def push_only(world, sizes, reps=2, mode="sm"):
     """For ncu (kernels serialised: a flag wait on another rank's kernel would
     never return): rank 0 alone pushes each size with ag_skip_waits, so every
     ag_push launch runs by itself; nothing gathered this way is read."""
@@ -123,6 +125,7 @@ def push_only(world, sizes, reps=2):
     ranks = rt.create_ranks(table, world, init=False)
     st = ranks[0]
     dc.check(dc.lib.dc_set_option(st.ctx, b"ag_skip_waits", 1), st.ctx)
+    dc.check(dc.lib.dc_set_option(st.ctx, b"ag_bulk", int(mode == "bulk")), st.ctx)
     sched = dc.plan(json.dumps(s0_profile(len(sizes), world, sizes)), 1 << 50, passes=dc.DC_PASS_SHARD)
     plan = json.loads(dc.schedule_json(sched))
     rt.bind(ranks, {r: sched for r in ranks})
@@ -145,7 +148,7 @@ def main():
     args = ap.parse_args()
     if args.ncu_push:
         torch.cuda.set_device(0)
-        push_only(args.ncu_push, [1 << k for k in range(24, args.max_log2 + 1, 2)])
+        push_only(args.ncu_push, [1 << k for k in range(24, args.max_log2 + 1, 2)], mode=args.modes.split(",")[0])
         return
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -157,7 +160,7 @@ def main():
     out = {"hbm_peak_gbs": hbm_peak, "note": __doc__.split("\n\n")[1], "runs": []}
     for world in [int(w) for w in args.worlds.split(",")]:
         for mode in args.modes.split(","):
-            rows = sweep(world, sizes, args.steps, mode == "ce", hbm_peak)
+            rows = sweep(world, sizes, args.steps, mode, hbm_peak)
             out["runs"].append({"world": world, "mode": mode, "rows": rows,
                                 "tc_table": [[r["bytes"], max(1, int(round(r["us"])))] for r in rows]})
             big = [r for r in rows if r["bytes"] >= (64 << 20)]

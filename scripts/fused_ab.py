@@ -61,7 +61,8 @@ def main():
     for _ in range(3):
         step += 1
         rt.step(ranks, step)
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        rt.poll(ranks)
     cs = ranks[0].streams[0]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ms = []

@@ -7,6 +7,12 @@
 mkdir -p gpurun_out/r02run4
 R=gpurun_out/r02run4/summary.txt
 : > $R
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/r02run4/bench.json 2> gpurun_out/r02run4/bench.err
+timeout 900 python -m pytest tests/test_gpu_fused_ag.py -q -p no:cacheprovider > gpurun_out/r02run4/fused_ag.log 2>&1
+echo "fused_ag + jitter tests rc=$? $(tail -1 gpurun_out/r02run4/fused_ag.log)" >> $R
+timeout 1800 compute-sanitizer --tool racecheck python -c "import __graft_entry__ as g; g.smoke()" \
+    > gpurun_out/r02run4/racecheck_smoke.txt 2>&1
+echo "racecheck rc=$? $(tail -2 gpurun_out/r02run4/racecheck_smoke.txt | tr '\n' ' ')" >> $R
 for c in 1 32; do
   for i in 1 2 3; do
     CUDA_DEVICE_MAX_CONNECTIONS=$c DC_SPIN_MS=5000 DC_TEST_GRAPH_N=1 timeout 600 python -m pytest tests/test_gpu_graph.py \

@@ -470,15 +470,18 @@ def _ops(sched):
     return json.loads(dc.schedule_json(sched))["ops"]
 
 
-@pytest.mark.parametrize("world,ce", [(3, 0), (8, 0), (8, 1)])
-def test_ag_ragged_virtual_ranks(world, ce):
+@pytest.mark.parametrize("world,mode", [(3, "sm"), (8, "sm"), (8, "ce"), (3, "bulk"), (8, "bulk"), (8, "chunked")])
+def test_ag_ragged_virtual_ranks(world, mode):
     """Gathers of ragged tensors (1 .. 2^19 elements, padded shards) through a
     planned schedule without a model: every gathered buffer == the padded
-    concatenation of the shards, bit for bit; SM push and copy-engine modes."""
+    concatenation of the shards, bit for bit; SM push (16-byte stores), copy
+    engines, bulk-copy pipeline (option ag_bulk) and chunked pushes (fused_ag)."""
     table = _ragged_table()
     ranks = rt.create_ranks(table, world)
     for st in ranks.values():
-        dc.check(dc.lib.dc_set_option(st.ctx, b"ag_copy_engine", ce), st.ctx)
+        dc.check(dc.lib.dc_set_option(st.ctx, b"ag_copy_engine", int(mode == "ce")), st.ctx)
+        dc.check(dc.lib.dc_set_option(st.ctx, b"ag_bulk", int(mode == "bulk")), st.ctx)
+        dc.check(dc.lib.dc_set_option(st.ctx, b"fused_ag", int(mode == "chunked")), st.ctx)
     B = {p.id: nx.shard_len(p.numel, world) * world * 2 for p in table}
     comp = [("f%d" % p.id, "compute", "fwd", 0, p.layer, [p.id]) for p in table]
     comp += [("b%d" % p.id, "compute", "bwd", 0, p.layer, [p.id]) for p in reversed(table)]
