@@ -668,6 +668,9 @@ def main():
             tj = json.load(f)
         traffic = tj.get("dram_bytes_per_launch")
         traffic_note = "%s; algorithmic %s B" % (tj.get("launch"), tj.get("algorithmic_bytes_per_launch"))
+        if tj.get("forward_launches_layer0"):
+            traffic_note += "; DRAM / algorithmic per forward launch: " + ", ".join(
+                "%s %.2fx" % (k, v["ratio"]) for k, v in tj["forward_launches_layer0"].items())
     except (OSError, ValueError):
         pass
     roofline = {"bound": "tensor", "kernel": "gemm2_bf16_sm100 (tcgen05 CTA pair, all layer GEMMs)",

@@ -946,6 +946,8 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
           cudaEventRecord(m->ev_pos[id], cs);
           cudaStreamWaitEvent(ags, m->ev_pos[id], 0);
           if (profile) ctx_set_gather_timing(m->ctx, m->ev_t0[id], m->ev_t1[id]);   // transfer time
+          else if (m->fused_ag) ctx_set_gather_timing(m->ctx, m->ev_t0[id], nullptr);
+          // (fused: ev_t0[id] = every receiver ready, the push is next on the AG stream)
           s = dc_gather(m->ctx, id, ags, m->ev_done[id]);
           for (int j = 0; j < nm; ++j) {
             gather_ev[mem[j]] = m->ev_done[id];
@@ -969,6 +971,9 @@ extern "C" dc_status dc_model_step(dc_model* m, int32_t step_t, int32_t profile,
               void* full = nullptr;           // the op's GEMMs wait per chunk of this B operand
               dc_tensor_ptr(m->ctx, p, &full);
               m->cw.push_back({full, w});
+              // ... but start only once the push is the next kernel on the AG stream: the
+              // persistent GEMM then never holds the SMs ahead of the push it waits for
+              cudaStreamWaitEvent(cs, m->ev_t0[gather_id[p]], 0);
             } else {
               cudaStreamWaitEvent(cs, gather_ev[p], 0);
             }

@@ -199,7 +199,14 @@ def create_ranks(table, world, device=0, *, virtual=True, group=None, rank=0, lr
         # stream the higher priority (rs_adam then fills in behind the GEMMs)
         prio = os.environ.get("DC_STREAM_PRIO", "none")
         st.streams = [torch.cuda.Stream(device=dev, priority=(-1 if (i == 0 and prio == "compute") else 0))
-                      for i in range(4)]
+                      for i in range(4 if not (virtual and world >= 8) else 3)]
+        if len(st.streams) == 3:
+            # 8 virtual ranks share one GPU's 32 hardware connections: with 4+ streams per rank
+            # some streams of different ranks share a queue, and a rank's spin-wait kernel can
+            # then sit in front of the peer work it waits for (profiles/r02/stalls/); the copy
+            # stream (offload only) shares the reduce-scatter stream here, and attach_model
+            # keeps the dW GEMMs on the compute stream
+            st.streams.append(st.streams[2])
     return ranks
 
 
@@ -230,6 +237,8 @@ def attach_model(ranks, cfg, xs, targets, checkpoint=False):
         st.tensors["x"], st.tensors["t"] = xs[r], targets[r]
         dc.check(dc.lib.dc_model_bind(m, st.tensors["act"].data_ptr(), nb.value, xs[r].data_ptr(),
                                       targets[r].data_ptr()))
+        if len(ranks) >= 8:      # virtual ranks: no second GEMM stream (see create_ranks)
+            dc.check(dc.lib.dc_model_set_option(m, b"dw_concurrent", 0))
 
 
 def bind(ranks, sched_by_rank, group=None):

@@ -63,13 +63,15 @@ def s0_profile(n, world, sizes):
 
 
 def sweep(world, sizes, steps, mode, hbm_peak):
-    """mode: sm (16-byte stores), ce (copy engines), bulk (bulk-copy / TMA pipeline)."""
+    """mode: sm (16-byte stores), ce (copy engines), bulk (bulk-copy / TMA pipeline), chunked (fused_ag's
+    chunk-ordered push with per-chunk flags)."""
     table = table_of(sizes)
     ranks = rt.create_ranks(table, world, init=False)
     for st in ranks.values():
         st.tensors["shard"].view(torch.int16).random_(-30000, 30000)
         dc.check(dc.lib.dc_set_option(st.ctx, b"ag_copy_engine", int(mode == "ce")), st.ctx)
         dc.check(dc.lib.dc_set_option(st.ctx, b"ag_bulk", int(mode == "bulk")), st.ctx)
+        dc.check(dc.lib.dc_set_option(st.ctx, b"fused_ag", int(mode == "chunked")), st.ctx)
     prof = s0_profile(len(sizes), world, sizes)
     sched = dc.plan(json.dumps(prof), 1 << 50, passes=dc.DC_PASS_SHARD)
     plan = json.loads(dc.schedule_json(sched))

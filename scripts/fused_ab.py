@@ -75,7 +75,16 @@ def main():
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
     rt.poll(ranks)
-    print(json.dumps({"world": a.world, "fused": a.fused, "passes": a.passes, "layers": a.layers,
+    step += 1                                            # one profiled step: per-op event times
+    rt.step(ranks, step, profile=True)
+    torch.cuda.synchronize()
+    prof = json.loads(dc.model_profile_json(ranks[0].model))
+    ops = {}
+    for o in prof["ops"]:
+        if o["kind"] in ("compute", "rs", "ag"):
+            k = o["kind"] if o["kind"] != "compute" else o.get("name", "?")
+            ops[k] = round(ops.get(k, 0) + o["dur_us"] / 1e3, 3)
+    print(json.dumps({"op_ms": ops, "world": a.world, "fused": a.fused, "passes": a.passes, "layers": a.layers,
                       "tokens_per_rank": T, "gemm_sms": int(os.environ["DC_GEMM_SMS"]),
                       "ms_per_step_median": float(np.median(ms)), "ms": ms}), flush=True)
 
