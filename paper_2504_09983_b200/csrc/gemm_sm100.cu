@@ -97,41 +97,64 @@ __device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
 }
 
 // Wait until every gather chunk overlapping flat elements [e0, e1) of B
-// segment s has landed (fused all-gather -> GEMM).  One thread (the producer).
-// (scalars by value: a reference to the kernel's GemmParams would make the
-// compiler copy the whole parameter block to local memory for every thread)
-// Returns the flat end of the last chunk verified (>= e1): the caller's cache.
+// segment s has landed (fused all-gather -> GEMM), called by a whole warp (the
+// watcher; warp-uniform arguments).  Chunks in linear order L = q nj + j
+// (sender q, j-th of nj = ceil(S / E) chunks; word flags[q * 64 + j]): the 32
+// lanes test chunks L .. L + 31 with one acquire load each, so a run of chunks
+// that already landed costs one round trip, not one per chunk; the first chunk
+// not landed yet is then awaited.  Keeps going past e1 over chunks that
+// already landed (up to 32 at a time) and returns the flat end of the last
+// verified chunk — the caller's cache.  Scalars by value: a reference to the
+// kernel's GemmParams would put the whole parameter block in local memory.
 __device__ __noinline__ int64_t chunk_wait(const uint32_t* flags, int64_t S, int64_t E, int64_t numel, uint32_t value,
                                            uint32_t* err, uint64_t tmo, int64_t e0, int64_t e1) {
+  const int lane = threadIdx.x % 32;
   e1 = e1 < numel ? e1 : numel;
+  if (e0 >= e1) return e1;
+  const int64_t nj = (S + E - 1) / E;
+  const int64_t nL = ((numel + S - 1) / S) * nj;     // chunks that exist
+  auto chunk_end = [&](int64_t L) {                  // flat end of linear chunk L
+    const int64_t q = L / nj, j = L - q * nj;
+    return q * S + ((j + 1) * E < S ? (j + 1) * E : S);
+  };
+  int64_t L = (e0 / S) * nj + (e0 - (e0 / S) * S) / E;
   uint64_t t0 = 0;
-  int64_t e = e0;
-  while (e < e1) {
-    const int64_t q = e / S, j = (e - q * S) / E;
-    const uint32_t* f = flags + q * AG_CHUNKS + j;
-    uint32_t seen;
-    while ((int32_t)((seen = ptx::ld_acquire_sys(f)) - value) < 0) {
-      if (!t0) t0 = ptx::globaltimer();
-      // after any recorded timeout (this or another wait) fail fast: the
-      // sticky error is reported by the next host call on the ctx
-      if (err && *reinterpret_cast<volatile uint32_t*>(err)) return e1;
-      if (ptx::globaltimer() - t0 > tmo) {
-        if (err && atomicCAS(err + 1, 0u, 1u) == 0u) {   // error record (comm.cu spin_ge layout)
-          err[2] = value;
-          err[3] = seen;
-          err[4] = (uint32_t)reinterpret_cast<uintptr_t>(f);
-          err[5] = (uint32_t)(reinterpret_cast<uintptr_t>(f) >> 32);
-          __threadfence_system();
-          atomicExch(err, 0x600u);
-        }
-        return e1;
-      }
-      __nanosleep(64);
+  while (true) {
+    const int64_t Ll = L + lane;
+    bool ok = true;
+    uint32_t seen = value;
+    if (Ll < nL) {
+      seen = ptx::ld_acquire_sys(flags + (Ll / nj) * AG_CHUNKS + (Ll % nj));
+      ok = (int32_t)(seen - value) >= 0;
     }
-    const int64_t end = j * E + E < S ? j * E + E : S;
-    e = q * S + end;
+    const uint32_t bad = __ballot_sync(0xffffffffu, !ok);
+    const int f = bad ? __ffs(bad) - 1 : 32;          // chunks L .. L + f - 1 landed
+    if (f > 0) {
+      L += f;
+      t0 = 0;
+      if (L >= nL || chunk_end(L - 1) >= e1) {         // the range is covered
+        if (bad || L >= nL) return chunk_end(L - 1);
+        continue;                                      // all 32 landed: look further ahead
+      }
+      continue;
+    }
+    // chunk L itself has not landed: wait (bounded), fail fast after any timeout
+    if (!t0) t0 = ptx::globaltimer();
+    if ((err && *reinterpret_cast<volatile uint32_t*>(err)) || ptx::globaltimer() - t0 > tmo) {
+      if (lane == 0 && err && !*reinterpret_cast<volatile uint32_t*>(err) && atomicCAS(err + 1, 0u, 1u) == 0u) {
+        const uint32_t* fp = flags + (L / nj) * AG_CHUNKS + (L % nj);
+        err[2] = value;
+        err[3] = __shfl_sync(0x1u, seen, 0);
+        err[4] = (uint32_t)reinterpret_cast<uintptr_t>(fp);
+        err[5] = (uint32_t)(reinterpret_cast<uintptr_t>(fp) >> 32);
+        __threadfence_system();
+        atomicExch(err, 0x600u);
+      }
+      __syncwarp();
+      return e1;
+    }
+    __nanosleep(128);
   }
-  return e;
 }
 // Tile order (tile index -> (m-tile, n-tile)): m fastest inside groups of
 // group_m m-tiles (group_m = m_tiles: m fastest over all of them).  When
@@ -694,7 +717,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           }
           const CUtensorMap* mb = s == 0 ? &mapB0 : s == 1 ? &mapB1 : s == 2 ? &mapB2 : &mapB3;
           if constexpr (CW) {  // fused all-gather: the watcher (warp 3) has seen this load's chunks land
-            while (ld_acquire_cta(cw_progress) <= (uint32_t)cw_step) {}
+            while (ld_acquire_cta(cw_progress) <= (uint32_t)cw_step) __nanosleep(32);
             asm volatile("fence.proxy.async.global;" ::: "memory");   // peer (generic) stores -> TMA reads
             ++cw_step;
           }
@@ -746,7 +769,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     }
   } else if (CW && warp == 3) {   // (warp 3 is a side-job warp otherwise)
     if constexpr (CW) {
-      if (lane == 0) {
+      {
         // ------------------------------------------------------- chunk watcher (fused all-gather)
         // Walks the producer's sequence of B loads ahead of it; for each one
         // waits (acquire, system scope) until the gather chunks it reads have
@@ -791,7 +814,9 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                 else { v_seg = sg; v_lo = e0; v_hi = end; }
               }
             }
-            st_release_cta(cw_progress, ++n);
+            ++n;
+            __syncwarp();
+            if (lane == 0) st_release_cta(cw_progress, n);
           }
         }
       }
