@@ -37,3 +37,20 @@ def test_gemm_flops_llama_and_moe():
     R = 2 * moe.tokens // moe.n_experts
     assert bench.gemm_flops("exp_gu_5", moe, moe.tokens) == 2 * R * moe.hidden * 2 * moe.ffn
     assert bench.gemm_flops("exp_down_bwd_0", moe, moe.tokens) == 4 * R * moe.ffn * moe.hidden
+
+
+def test_load_tc_table_from_sweep_and_list(tmp_path):
+    """--tc-table: an ag_sweep.py run (median us per size) or a plain [[bytes, us]] list ->
+    integer, size-sorted, non-decreasing T_c table (the form dc_plan takes)."""
+    import json
+
+    import bench
+    sweep = {"runs": [{"world": 8, "mode": "sm", "rows": [{"bytes": 4096, "us": 30.4}, {"bytes": 1024, "us": 41.2},
+                                                         {"bytes": 1 << 20, "us": 55.6}]},
+                      {"world": 2, "mode": "sm", "rows": [{"bytes": 1024, "us": 1.0}]}]}
+    p = tmp_path / "sweep.json"
+    p.write_text(json.dumps(sweep))
+    assert bench.load_tc_table(str(p) + ":8:sm") == [[1024, 41], [4096, 41], [1 << 20, 56]]
+    q = tmp_path / "list.json"
+    q.write_text(json.dumps([[2048, 9], [1024, 5]]))
+    assert bench.load_tc_table(str(q)) == [[1024, 5], [2048, 9]]
