@@ -9,7 +9,7 @@ release after: no prefetch, no unshard) is the ZeRO-3-like baseline of the
 same executor; P+S is DeepCompile's schedule.  Plans and memory are exact;
 times are a model.
 
-    python scripts/ga_sweep.py [--out profiles/r01g/ga_sweep_n8.md]
+    python tests/tools/ga_sweep.py [--out profiles/r01g/ga_sweep_n8.md]
 """
 import argparse
 import dataclasses
@@ -18,7 +18,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
@@ -79,7 +79,7 @@ def main():
             print(label, n, {k: round(v[0], 1) for k, v in res.items()}, flush=True)
     lines = ["# Gradient accumulation at N = 8: S_0 (ZeRO-3-like) vs prefetch vs prefetch + selective unshard",
              "",
-             "`python scripts/ga_sweep.py` (host-only; dc_plan on full-size S_0 profiles with n micro-steps; oracle",
+             "`python tests/tools/ga_sweep.py` (host-only; dc_plan on full-size S_0 profiles with n micro-steps; oracle",
              "three-stream replay, D23; per-op durations measured on B200 at N = 1 (profiles/r01g), b = 1, seq 2048;",
              "T_c = 20 us + V / (0.7 x 900 GB/s), RS(l) = (N-1)/N of the layer's bytes at the same rate; M = 155.7 GB).",
              "Times are a model; the plans (gathers, unsharded parameters) are the planner's exact output.", "",

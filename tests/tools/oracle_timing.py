@@ -10,7 +10,7 @@
 Each timed with BLAS threads = 1 and with all cores (the thread count is set
 per child process, before numpy loads).  Prints one JSON object.
 
-    python scripts/oracle_timing.py [--out profiles/r01g/oracle_timing.json]
+    python tests/tools/oracle_timing.py [--out profiles/r01g/oracle_timing.json]
 """
 import argparse
 import json
@@ -20,7 +20,7 @@ import subprocess
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
 def child(item):

@@ -9,7 +9,7 @@ reading D23) from per-op durations measured on the B200 (70B layers at N = 1,
 profiles/r01g/lines_final/llama70b_L8.json) and an assumed T_c = 20 us + V / (0.7 x
 900 GB/s).  Planning and memory numbers are exact; times are a model.
 
-    python scripts/plan_sweep.py [--out profiles/r01g/plan_sweep_70b_n8.md]
+    python tests/tools/plan_sweep.py [--out profiles/r01g/plan_sweep_70b_n8.md]
 """
 import argparse
 import dataclasses
@@ -18,7 +18,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
@@ -77,7 +77,7 @@ def main():
     compute_ms = sum(o["dur_us"] for o in prof["ops"] if o["kind"] == "compute") / 1e3
     lines = ["# Config 3 plan study: Llama-3-70B-shaped, L = %d, N = 8, b = 1, seq 2048, layer checkpointing" % cfg.layers,
              "",
-             "`python scripts/plan_sweep.py` (host-only; dc_plan = the product planner; times from the oracle's",
+             "`python tests/tools/plan_sweep.py` (host-only; dc_plan = the product planner; times from the oracle's",
              "three-stream replay, reading D23).  Per-rank state %.1f GB (14 B x %.1f G shard elements), S_0 peak"
              % (14 * E / GB, E / 1e9),
              "without m/v %.1f GB; serial compute %.0f ms per step (per-op durations measured on B200, 70B layers at"
