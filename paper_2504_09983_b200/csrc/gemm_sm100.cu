@@ -1164,10 +1164,11 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
     const int slots = pair_slots(bnt == 128 ? 1 : env_st_pick());
     const int pairs = std::min(tiles, std::min(sms / 2, slots > 0 ? slots : sms / 2));
     static const bool sk_env = !(getenv("DC_GEMM_SK") && atoi(getenv("DC_GEMM_SK")) == 0);
+    static const int sk_min_kb = getenv("DC_GEMM_SK_MINKB") ? atoi(getenv("DC_GEMM_SK_MINKB")) : 128;   // A/B knob
     // stream-K pays only when the k-loop is long (measured on the layer shapes,
     // profiles/r01d: +3-4 % at K >= 14336, -2 % at K = 4096, where the idle
     // pairs of the last partial wave let the others clock higher)
-    if (g->stream_k && g->workspace && sk_env && !p.epi && tiles > pairs && tiles % pairs && p.k_blocks >= 128 &&
+    if (g->stream_k && g->workspace && sk_env && !p.epi && tiles > pairs && tiles % pairs && p.k_blocks >= sk_min_kb &&
         tiles - (tiles / pairs - 1) * pairs <= 150) {
       if (g->workspace_bytes < SK_WS_BYTES || (reinterpret_cast<uintptr_t>(g->workspace) & 255))
         { *err = "dc_gemm: stream-K workspace smaller than dc_gemm_workspace_bytes() or not 256 B aligned"; return DC_EINVAL; }
