@@ -74,6 +74,12 @@ struct GemmParams {
   // npairs contiguous ranges.  A tile cut by a range boundary is computed in two
   // parts: the head's fp32 partial goes through sk_ws (flag sk_flags = sk_epoch),
   // the pair holding the tail adds it in its epilogue, which it runs last.
+  // half-width tail (pair kernel, plain epilogue, no stream-K): tiles [0, ht_dp)
+  // run whole; each remaining tile of the partial last wave runs as two
+  // 256 x 128 halves (UMMA N = 128, instruction descriptor idesc_half), so that
+  // wave has twice as many, half-length units for the idle pairs
+  int ht_on, ht_dp;
+  uint32_t idesc_half;
   int sk_on, sk_dp;
   int64_t sk_total;
   float* sk_ws;
@@ -176,20 +182,28 @@ __device__ __forceinline__ void tile_mn(const GemmParams& p, int tile, int& mt, 
 
 // One unit of a pair's work list: k-blocks [kb0, kb1) of `tile`;
 // mode 0 full tile, 1 head of a split tile (write fp32 partial), 2 tail (add it)
-struct Unit { int tile, kb0, kb1, mode; };
+struct Unit { int tile, kb0, kb1, mode, half; };   // half: -1 whole tile, 0 / 1 the 128-column halves
 
 struct WorkList {
-  int n_dp, n_rest, finish;     // DP tiles, SK units without a wait, trailing tail unit
+  int n_dp, n_rest, finish;     // DP tiles, SK units (or half-tail units) without a wait, trailing tail unit
   int ta, ka, tb;               // first SK tile / its start k-block, first non-tail SK tile
   int64_t s1;                   // end of this pair's SK range (k-block index)
   __device__ __forceinline__ int count() const { return n_dp + n_rest + finish; }
 };
 
+template <bool HT = false>
 __device__ __forceinline__ WorkList work_list(const GemmParams& p, int pair, int npairs) {
   WorkList w{};
   const int tiles = p.m_tiles * p.n_tiles;
-  const int dp = p.sk_on ? p.sk_dp : tiles;
+  const int dp = p.sk_on ? p.sk_dp : (HT && p.ht_on) ? p.ht_dp : tiles;
   w.n_dp = pair < dp ? (dp - 1 - pair) / npairs + 1 : 0;
+  if constexpr (HT) {
+    if (p.ht_on) {                               // half units h = pair, pair + npairs, ... < 2 (tiles - dp)
+      const int nh = 2 * (tiles - dp);
+      w.n_rest = pair < nh ? (nh - 1 - pair) / npairs + 1 : 0;
+      return w;
+    }
+  }
   if (!p.sk_on) return w;
   const int KB = p.k_blocks;
   const int64_t s0 = (int64_t)pair * p.sk_total / npairs;
@@ -203,10 +217,19 @@ __device__ __forceinline__ WorkList work_list(const GemmParams& p, int pair, int
   return w;
 }
 
+template <bool HT = false>
 __device__ __forceinline__ Unit unit_at(const GemmParams& p, const WorkList& w, int pair, int npairs, int i) {
   Unit u;
+  u.half = -1;
   if (i < w.n_dp) { u.tile = pair + i * npairs; u.kb0 = 0; u.kb1 = p.k_blocks; u.mode = 0; return u; }
   i -= w.n_dp;
+  if constexpr (HT) {
+    if (p.ht_on) {
+      const int h = pair + i * npairs;
+      u.tile = p.ht_dp + h / 2; u.half = h % 2; u.kb0 = 0; u.kb1 = p.k_blocks; u.mode = 0;
+      return u;
+    }
+  }
   const int KB = p.k_blocks;
   if (i < w.n_rest) {
     u.tile = w.tb + i;
@@ -635,7 +658,8 @@ constexpr int GEMM2_THREADS = 384;          // + side-job warps 8..11
 // CW: per-tile chunk waits of a fused all-gather (dc_gemm_args.chunk_*); a
 // separate instantiation, so the default kernels carry none of that code
 // (r02: even the untaken branch and its call made the step ~6 % slower)
-template <int BNT, int ST, int EPI, bool CW = false>
+// HT: half-width tail units (p.ht_on), also a separate instantiation
+template <int BNT, int ST, int EPI, bool CW = false, bool HT = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
 gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
                  const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
@@ -655,7 +679,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_ctarank();
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
-  const WorkList wl = work_list(p, pair, npairs);
+  const WorkList wl = work_list<HT>(p, pair, npairs);
   const int nunits = wl.count();
 
   if (warp == 0 && lane == 0) {
@@ -681,7 +705,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       int stage = 0; uint32_t phase = 0;
       [[maybe_unused]] int cw_step = 0;               // chunk waits: this load's index in the watcher's walk
       for (int ui = 0; ui < nunits; ++ui) {
-        const Unit un = unit_at(p, wl, pair, npairs, ui);
+        const Unit un = unit_at<HT>(p, wl, pair, npairs, ui);
         const int tile = un.tile;
         int mt, nt;
         tile_mn(p, tile, mt, nt);
@@ -695,11 +719,17 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             bseg = seg_of(p, nt);
             n0 = (nt - (bseg ? p.seg_end[bseg - 1] : 0)) * BNT;
           }
-          n0 += (int)rank * (BNT / 2);
+          if constexpr (HT)    // half tile: columns [half 128, half 128 + 128) of the tile, 64 per CTA
+            n0 += un.half < 0 ? (int)rank * (BNT / 2) : un.half * (BNT / 2) + (int)rank * (BNT / 4);
+          else
+            n0 += (int)rank * (BNT / 2);
         }
+        // an MN-major half tile loads one 64-column box per CTA instead of two
+        uint32_t b_bytes = Pair<BNT, ST>::B_STAGE;
+        if constexpr (HT) b_bytes = (un.half >= 0 && p.b_mn) ? Pair<BNT, ST>::B_STAGE / 2 : Pair<BNT, ST>::B_STAGE;
         for (int kb = un.kb0; kb < un.kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (A2_STAGE + Pair<BNT, ST>::B_STAGE));
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (A2_STAGE + b_bytes));
           const uint32_t lbar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
           uint8_t* a = smA + stage * A2_STAGE;
           uint8_t* b = smB + stage * Pair<BNT, ST>::B_STAGE;
@@ -723,6 +753,9 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           }
           if (!p.b_mn) {
             ptx::tma_load_2d_2sm(b, mb, lbar, kk0, n0);
+          } else if constexpr (HT) {
+            const int nbox = un.half < 0 ? BNT / 128 : BNT / 256;
+            for (int j = 0; j < nbox; ++j) ptx::tma_load_2d_2sm(b + j * 8192, mb, lbar, n0 + 64 * j, kk0);
           } else {
 #pragma unroll
             for (int j = 0; j < BNT / 128; ++j) ptx::tma_load_2d_2sm(b + j * 8192, mb, lbar, n0 + 64 * j, kk0);
@@ -744,7 +777,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t aphase = 0;
       for (int ui = 0; ui < nunits; ++ui) {
-        const Unit un = unit_at(p, wl, pair, npairs, ui);
+        const Unit un = unit_at<HT>(p, wl, pair, npairs, ui);
         ptx::mbar_wait(&tempty[acc], aphase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + acc * BNT;
@@ -756,7 +789,8 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           if (ptx::elect_one()) {
 #pragma unroll
             for (int k = 0; k < BK / UMMA_K; ++k)
-              ptx::umma_f16_2sm(d, ad + k * a_ks, bd + k * b_ks, p.idesc, (kb != un.kb0) | (k != 0));
+              ptx::umma_f16_2sm(d, ad + k * a_ks, bd + k * b_ks, (HT && un.half >= 0) ? p.idesc_half : p.idesc,
+                                (kb != un.kb0) | (k != 0));
             ptx::umma_commit_2sm_mc(&empty[stage], 0x3);
           }
           __syncwarp();
@@ -781,7 +815,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         int64_t v_lo = 0, v_hi = 0;
         uint32_t n = 0;
         for (int ui = 0; ui < nunits; ++ui) {
-          const Unit un = unit_at(p, wl, pair, npairs, ui);
+          const Unit un = unit_at<HT>(p, wl, pair, npairs, ui);
           int mt, nt;
           tile_mn(p, un.tile, mt, nt);
           int bseg = 0, n0 = nt * BNT;
@@ -827,7 +861,7 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     const int rl = q * 32 + lane;                 // this thread's row inside the CTA's 128
     int acc = 0; uint32_t aphase = 0;
     for (int ui = 0; ui < nunits; ++ui) {
-      const Unit un = unit_at(p, wl, pair, npairs, ui);
+      const Unit un = unit_at<HT>(p, wl, pair, npairs, ui);
       const int tile = un.tile;
       int mt, nt;
         tile_mn(p, tile, mt, nt);
@@ -857,12 +891,16 @@ gemm2_bf16_sm100(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           if (row_ok && col0 < p.N) glu_fwd_chunk(p, row, col0, vg, vu);
         }
       }
+      int nchunk = EPI == 2 ? 0 : BNT / 32, colh = 0;
+      if constexpr (HT) {
+        if (un.half >= 0) { nchunk = BNT / 64; colh = un.half * (BNT / 2); }
+      }
 #pragma unroll 1
-      for (int c = 0; c < (EPI == 2 ? 0 : BNT / 32); ++c) {
+      for (int c = 0; c < nchunk; ++c) {
         uint32_t v[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BNT + c * 32, v);
         ptx::tmem_ld_wait();
-        const int col0 = nt * BNT + c * 32;
+        const int col0 = nt * BNT + colh + c * 32;
         if (un.mode == 1) {                        // head: store the raw fp32 partial
           float4* w4 = reinterpret_cast<float4*>(ws) + (int64_t)c * 8 * 128 + rl;
 #pragma unroll
@@ -1179,19 +1217,37 @@ dc_status launch_gemm(const dc_gemm_args* g, cudaStream_t stream, std::string* e
       p.sk_flags = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(g->workspace) + SK_TILES_CAP * SK_PART_BYTES);
       p.sk_epoch = sk_next_epoch(g->workspace);
     }
+    bool cw = false;
+    for (int s = 0; s < 4; ++s) cw = cw || p.cf[s];
+    {   // half-width tail units when the partial last wave fits in one wave of halves; forward-form
+        // GEMMs only (A and B K-major): measured in-step, the dX / dW GEMMs of the backward (which
+        // share the device with each other, dw_concurrent) got 7-25 % slower with them, the
+        // forward ones 1-7 % faster (profiles/r02/half_tail/)
+      static const int ht_env = getenv("DC_GEMM_HALF_TAIL") ? atoi(getenv("DC_GEMM_HALF_TAIL")) : 1;
+      const int dp = tiles / pairs * pairs;
+      if (ht_env && bnt == 256 && !p.sk_on && !p.epi && !cw && !(side && side->nm > 0) && tiles > pairs &&
+          !p.a_mn && !p.b_mn &&
+          tiles > dp && 2 * (tiles - dp) <= pairs) {
+        p.ht_on = 1;
+        p.ht_dp = dp;
+        p.idesc_half = (p.idesc & ~(0x3Fu << 17)) | ((uint32_t)(128 >> 3) << 17);
+      }
+    }
     const int env_st = glu ? 6 : (env_st_pick() == 2 ? 7 : 6);
     const int g2 = 2 * pairs;
 #define DC_PAIR_LAUNCH(BN_, ST_)                                                                   \
     (p.epi ? gemm2_bf16_sm100<BN_, ST_, 1><<<g2, GEMM2_THREADS, Pair<BN_, ST_>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p) \
            : gemm2_bf16_sm100<BN_, ST_, 0><<<g2, GEMM2_THREADS, Pair<BN_, ST_>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p))
-    bool cw = false;
-    for (int s = 0; s < 4; ++s) cw = cw || p.cf[s];
     if (cw && (bnt != 256 || (p.epi != 0 && p.epi != 2)))
       { *err = "dc_gemm: chunk waits need the 256-wide pair kernel with epilogue 0 or 2"; return DC_EINVAL; }
     if (cw && glu == 2) gemm2_bf16_sm100<256, 6, 2, true><<<g2, GEMM2_THREADS, Pair<256, 6>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
     else if (cw) gemm2_bf16_sm100<256, 6, 0, true><<<g2, GEMM2_THREADS, Pair<256, 6>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
     else if (glu == 2) gemm2_bf16_sm100<256, 6, 2><<<g2, GEMM2_THREADS, Pair<256, 6>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
     else if (glu == 3) gemm2_bf16_sm100<256, 6, 3><<<g2, GEMM2_THREADS, Pair<256, 6>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+    else if (p.ht_on && env_st == 6)
+      gemm2_bf16_sm100<256, 6, 0, false, true><<<g2, GEMM2_THREADS, Pair<256, 6>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
+    else if (p.ht_on)
+      gemm2_bf16_sm100<256, 7, 0, false, true><<<g2, GEMM2_THREADS, Pair<256, 7>::SMEM, stream>>>(mA, mB[0], mB[1], mB[2], mB[3], p);
     else if (bnt == 128) DC_PAIR_LAUNCH(128, 9);
     else if (env_st == 6) DC_PAIR_LAUNCH(256, 6);
     else DC_PAIR_LAUNCH(256, 7);
@@ -1253,6 +1309,12 @@ cudaError_t preload_gemm_kernels() {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(gemm2_bf16_sm100<256, 6, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Pair<256, 6>::SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm2_bf16_sm100<256, 6, 0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Pair<256, 6>::SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm2_bf16_sm100<256, 7, 0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Pair<256, 7>::SMEM);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(gemm2_bf16_sm100<256, 6, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Pair<256, 6>::SMEM);

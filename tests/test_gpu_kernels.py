@@ -558,3 +558,35 @@ def test_ag_push_virtual_ranks(world, passes):
     assert checked == set(range(len(table)))
     for st in ranks.values():
         assert dc.lib.dc_step_begin(st.ctx, 2, st.streams[0].cuda_stream) == dc.DC_OK   # no sticky timeout
+
+
+# half-width tail units (pair kernel, forward-form GEMMs): when the tiles of the
+# partial last wave fit twice over in one wave, each runs as two 256 x 128
+# halves (UMMA N = 128).  sms = 8 -> 4 pairs; (M, N) = (512, 1280) -> 10 tiles =
+# 2 waves of 4 + 2 tail tiles -> 4 half units.  Forward (K-major B, 2
+# N-segments, residual, ragged N) against fp64; the dX / dW forms of the same
+# shape (no half tails: MN-major operands) beside it.
+@pytest.mark.parametrize("M,N,K", [(512, 1280, 512), (512, 1192, 320)])
+def test_gemm_half_tail_units(M, N, K):
+    sms = 8
+    a, A = _mat(91, M, K)
+    n1 = 512
+    b1, B1 = _mat(92, n1, K)
+    b2, B2 = _mat(93, N - n1, K)
+    r, R = _mat(94, M, N)
+    Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    _gemm(M, N, K, A, K, 0, [B1, B2], [K, K], [n1 // 256, -(-N // 256)], 0, 0, Cm, N, R=R, ldr=N, sms=sms, kernel=2)
+    bcat = np.concatenate([b1, b2])
+    _check(Cm, a @ bcat.T + r, np.abs(a) @ np.abs(bcat).T + np.abs(r), "half-tail fwd")
+    k1 = (K // 2) // 64 * 64
+    w1, W1 = _mat(95, k1, N)
+    w2, W2 = _mat(96, K - k1, N)
+    Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    _gemm(M, N, K, A, K, 0, [W1, W2], [N, N], [k1 // 64, -(-K // 64)], 1, 1, Cm, N, sms=sms, kernel=2)
+    wcat = np.concatenate([w1, w2])
+    _check(Cm, a @ wcat, np.abs(a) @ np.abs(wcat), "half-tail dx")
+    dy, DY = _mat(97, K, M)
+    x, X = _mat(98, K, N)
+    Cm = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    _gemm(M, N, K, DY, M, 1, [X], [N], [0], 1, 0, Cm, N, sms=sms, kernel=2)
+    _check(Cm, dy.T @ x, np.abs(dy).T @ np.abs(x), "half-tail dw")
