@@ -77,23 +77,43 @@ def symm_backend():
     """Which peer-mapping path _alloc_symmetric uses: "symm_mem" (torch
     symmetric memory, the default for one process per GPU) or "ipc" (CUDA IPC,
     DC_SYMM=ipc — required when several processes share one GPU, which
-    symmetric memory refuses).  There is no silent fallback between them."""
+    symmetric memory refuses).  If torch symmetric memory was tried without an
+    explicit DC_SYMM and refused, "ipc (torch symmetric memory unavailable:
+    <reason>)" — the fallback is reported, never silent."""
     v = os.environ.get("DC_SYMM", "symm_mem")
     if v not in ("symm_mem", "ipc"):
         raise ValueError("DC_SYMM must be symm_mem or ipc, got %r" % v)
+    if v == "symm_mem" and SYMM_FALLBACK:
+        return "ipc (torch symmetric memory unavailable: %s)" % SYMM_FALLBACK
     return v
+
+
+SYMM_FALLBACK = None     # reason torch symmetric memory was not used (recorded, reported by bench.py)
 
 
 def _alloc_symmetric(nbytes, group, device):
     """Symmetric buffer for the peer tables (grad slots, flags, gather arena).
-    Returns (local tensor, [world] peer pointers, keep-alive handles).  Raises
-    if the selected backend fails (no fallback: a silently different transport
-    would change what the N > 1 numbers measure)."""
-    if symm_backend() == "ipc":
+    Returns (local tensor, [world] peer pointers, keep-alive handles).  With
+    DC_SYMM set explicitly the chosen backend must work (raises otherwise).
+    Without it, torch symmetric memory is tried and, if the runtime refuses it,
+    CUDA IPC is used LOUDLY: a warning on stderr and the reason in
+    SYMM_FALLBACK, which bench.py puts in its JSON line (collectives.transport)
+    — never a silent switch of what the N > 1 numbers measure."""
+    global SYMM_FALLBACK
+    if symm_backend() == "ipc" or SYMM_FALLBACK:
         return _alloc_symmetric_ipc(nbytes, group, device)
-    from torch.distributed import _symmetric_memory as symm_mem
-    t = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
-    h = symm_mem.rendezvous(t, group)
+    try:
+        from torch.distributed import _symmetric_memory as symm_mem
+        t = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+        h = symm_mem.rendezvous(t, group)
+    except Exception as e:     # noqa: BLE001 - recorded and reported, see above
+        if os.environ.get("DC_SYMM"):
+            raise
+        import sys
+        SYMM_FALLBACK = "%s: %s" % (type(e).__name__, str(e).splitlines()[0][:200] if str(e) else "")
+        print("runtime: torch symmetric memory unavailable (%s); using CUDA IPC peer mappings" % SYMM_FALLBACK,
+              file=sys.stderr, flush=True)
+        return _alloc_symmetric_ipc(nbytes, group, device)
     t.zero_()
     return t, [int(p) for p in h.buffer_ptrs], [h]
 

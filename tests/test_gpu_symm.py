@@ -56,3 +56,31 @@ def test_symm_backend_has_no_silent_fallback(monkeypatch):
     monkeypatch.setenv("DC_SYMM", "ipc")
     assert rt.symm_backend() == "ipc"
     assert os.environ["DC_SYMM"] == "ipc"
+
+
+def test_symm_mem_refusal_is_reported_not_silent(monkeypatch):
+    """Without an explicit DC_SYMM, a runtime that refuses torch symmetric
+    memory gets CUDA IPC peer mappings AND the reason in symm_backend() (bench
+    puts it in collectives.transport); with DC_SYMM=symm_mem it raises."""
+    import torch.distributed as dist
+    from torch.distributed import _symmetric_memory as symm_mem
+
+    def refuse(*a, **k):
+        raise RuntimeError("symmetric memory refused (test)")
+
+    monkeypatch.setattr(symm_mem, "empty", refuse)
+    monkeypatch.delenv("DC_SYMM", raising=False)
+    store = dist.HashStore()
+    dist.init_process_group("gloo", store=store, rank=0, world_size=1)
+    try:
+        dev = torch.device("cuda", 0)
+        monkeypatch.setenv("DC_SYMM", "symm_mem")
+        with pytest.raises(RuntimeError):
+            rt._alloc_symmetric(4096, dist.group.WORLD, dev)
+        monkeypatch.delenv("DC_SYMM")
+        t, ptrs, keep = rt._alloc_symmetric(4096, dist.group.WORLD, dev)
+        assert ptrs == [t.data_ptr()] and t.numel() == 4096
+        assert rt.symm_backend().startswith("ipc (torch symmetric memory unavailable: RuntimeError")
+    finally:
+        rt.SYMM_FALLBACK = None
+        dist.destroy_process_group()
