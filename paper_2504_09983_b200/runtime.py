@@ -58,6 +58,8 @@ def _alloc_symmetric_ipc(nbytes, group, device):
     storages and must outlive every use of their pointers."""
     import torch.distributed as dist
     t = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+    if dist.get_world_size(group) == 1:          # nothing to export
+        return t, [t.data_ptr()], []
     h = t.untyped_storage()._share_cuda_()
     handles = [None] * dist.get_world_size(group)
     dist.all_gather_object(handles, h, group=group)
