@@ -265,13 +265,24 @@ void k_colsum_to_bf16(const float* partial, int nblk, int H, void* out, cudaStre
 
 // ------------------------------------------------------------------ attention surrogate
 // a = bf16(q + rep(k) * rep(v)); qkv row = [q (qd) | k (kvd) | v (kvd)].
+// (row, column) of flat element e of a [rows][n] tensor with 32-bit unsigned
+// arithmetic (every glue tensor has < 2^32 elements; a 64-bit division is a
+// ~70-instruction software routine in the elementwise loops' index math)
+__device__ __forceinline__ void rc32(int64_t e, int n, int& r, int& c) {
+  const uint32_t e32 = (uint32_t)e, n32 = (uint32_t)n;
+  const uint32_t q = e32 / n32;
+  r = (int)q;
+  c = (int)(e32 - q * n32);
+}
+
 __global__ void attn_mix_fwd_kernel(const bf16* __restrict__ qkv, bf16* __restrict__ a, int T, int qd, int kvd,
                                     int hd, int grp) {
   const int ld = qd + 2 * kvd;
   const int64_t n8 = (int64_t)T * qd / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i * 8;
-    const int t = (int)(e / qd), c = (int)(e % qd);
+    int t, c;
+    rc32(e, qd, t, c);
     const int head = c / hd, d = c % hd;
     const int kc = (head / grp) * hd + d;
     const bf16* row = qkv + (int64_t)t * ld;
@@ -305,7 +316,8 @@ __global__ void attn_mix_bwd_kernel(bf16* __restrict__ dqkv, const bf16* __restr
   const int64_t n8 = (int64_t)T * kvd / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i * 8;
-    const int t = (int)(e / kvd), kc = (int)(e % kvd);
+    int t, kc;
+    rc32(e, kvd, t, kc);
     const int j = kc / hd, d = kc % hd;
     const bf16* row = qkv + (int64_t)t * ld;
     bf16* drow = dqkv + (int64_t)t * ld;
@@ -339,7 +351,8 @@ __global__ void act_fwd_kernel(const bf16* __restrict__ gu, bf16* __restrict__ a
   const int64_t n8 = (int64_t)T * F / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i * 8;
-    const int t = (int)(e / F), c = (int)(e % F);
+    int t, c;
+    rc32(e, F, t, c);
     const bf16* row = gu + (int64_t)t * 2 * F;
     float g[8], u[8], o[8];
     load8(row + c, g);
@@ -361,7 +374,8 @@ __global__ void act_bwd_kernel(const bf16* __restrict__ dact, const bf16* __rest
   const int64_t n8 = (int64_t)T * F / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i * 8;
-    const int t = (int)(e / F), c = (int)(e % F);
+    int t, c;
+    rc32(e, F, t, c);
     const bf16* row = gu + (int64_t)t * 2 * F;
     float g[8], u[8], da[8], dg[8], du[8];
     load8(row + c, g);

@@ -274,6 +274,9 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   if (d->hidden % 256 || d->ffn % 256 || m->qd % 256 || m->kvd % 256 || d->hidden > 8192 || d->tokens % 8)
     return mfail(nullptr, DC_EINVAL, "dc_model_create: hidden/ffn/q/kv dims must be multiples of 256, hidden <= 8192");
   const int64_t h = d->hidden, f = d->ffn;
+  // the elementwise glue kernels index [tokens][width] activations with 32-bit math
+  if ((int64_t)d->tokens * std::max<int64_t>({2 * f, (int64_t)m->qkvd, h}) >= (1LL << 32))
+    return mfail(nullptr, DC_EINVAL, "dc_model_create: tokens x widest activation must stay below 2^32 elements");
   m->E = d->n_experts;
   if (m->E != 0 && (m->E < 2 || m->E > 8 || d->tokens % (4 * m->E)))
     return mfail(nullptr, DC_EINVAL, "dc_model_create: n_experts is 0 or 2..8, tokens % (4 n_experts) == 0");

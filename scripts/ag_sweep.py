@@ -62,6 +62,9 @@ def s0_profile(n, world, sizes):
     return {"ops": ops, "params": params, "frags": [], "tc": [[0, 0], [1 << 40, 0]]}
 
 
+GATE = True
+
+
 def sweep(world, sizes, steps, mode, hbm_peak):
     """mode: sm (16-byte stores), ce (copy engines), bulk (bulk-copy / TMA pipeline), chunked (fused_ag's
     chunk-ordered push with per-chunk flags)."""
@@ -86,8 +89,13 @@ def sweep(world, sizes, steps, mode, hbm_peak):
             e0.record()
             e1.record()
 
+    gate_stream = torch.cuda.Stream()
+    gate = {}
+
     def one_step(st, t):
         cs, ags = st.streams[0], st.streams[1]
+        if GATE:
+            cs.wait_event(gate["ev"])    # the device starts this step only after every rank enqueued it
         dc.check(dc.lib.dc_step_begin(st.ctx, t, cs.cuda_stream), st.ctx)
         for o in ag:
             e0, e1 = evs[st.rank][o["id"]]
@@ -101,6 +109,11 @@ def sweep(world, sizes, steps, mode, hbm_peak):
         torch.cuda.synchronize()
 
     for t in range(1, steps + 3):
+        if GATE:      # a ~50 ms spin on a side stream holds every rank's step until all are enqueued, so
+            with torch.cuda.stream(gate_stream):     # small gathers are not timed against host enqueue skew
+                torch.cuda._sleep(int(50e-3 * 2e9))
+                gate["ev"] = torch.cuda.Event()
+                gate["ev"].record(gate_stream)
         rt.run_parallel(ranks, lambda st: one_step(st, t))
         rt.poll(ranks)
         if t > 2:                                   # two warm-up steps
@@ -147,7 +160,11 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "ag_sweep.json"))
     ap.add_argument("--modes", default="sm,ce")
     ap.add_argument("--ncu-push", type=int, default=0, help="push-only run for ncu at this N (sizes >= 2^24)")
+    ap.add_argument("--no-gate", action="store_true",
+                    help="let each rank's step start as its host thread enqueues it (the r02 sweeps before the gate)")
     args = ap.parse_args()
+    global GATE
+    GATE = not args.no_gate
     if args.ncu_push:
         torch.cuda.set_device(0)
         push_only(args.ncu_push, [1 << k for k in range(24, args.max_log2 + 1, 2)], mode=args.modes.split(",")[0])
