@@ -125,10 +125,12 @@ dc_status reduce_scatter_params(dc_ctx* c, int layer, int step_t, int micro, con
 void k_init_param(uint64_t seed, int32_t tensor_id, int64_t numel, int32_t world, int32_t rank,
                   int64_t S, float k, float* master, void* shard, cudaStream_t st);
 void k_rmsnorm_fwd(const void* x, const void* g, void* h, float* rstd, int T, int H, cudaStream_t st);
-// dg_partial: rmsnorm_bwd_blocks(T) x H fp32 partials, followed by T floats of scratch
-void k_rmsnorm_bwd(const void* dh, const void* x, const void* g, const float* rstd, const void* dres,
-                   void* dx, float* dg_partial, int T, int H, cudaStream_t st);
+// dg_partial: rmsnorm_bwd_ws_floats(T, H) floats of scratch; returns the number of
+// H-float partial rows written at its start (input of k_colsum_to_bf16)
+int k_rmsnorm_bwd(const void* dh, const void* x, const void* g, const float* rstd, const void* dres,
+                  void* dx, float* dg_partial, int T, int H, cudaStream_t st);
 int rmsnorm_bwd_blocks(int T);
+int64_t rmsnorm_bwd_ws_floats(int T, int H);
 void k_colsum_to_bf16(const float* partial, int nblk, int H, void* out, cudaStream_t st);
 void k_attn_mix_fwd(const void* qkv, void* a, int T, int qd, int kvd, int hd, int grp, cudaStream_t st);
 void k_attn_mix_bwd(void* dqkv, const void* qkv, int T, int qd, int kvd, int hd, int grp, cudaStream_t st);

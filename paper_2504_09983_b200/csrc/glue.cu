@@ -225,8 +225,160 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_dx_kernel(const bf16* __restr
   for (int i = 0; i < 8; ++i) dgp[(int64_t)blockIdx.x * H + c + i] = acc[i];
 }
 
-void k_rmsnorm_bwd(const void* dh, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
-                   float* dg_partial, int T, int H, cudaStream_t st) {
+// One-pass form (default when H = 256 V G, V in {1, 2, 4}, G in {1, 2, 4, 8}):
+// a row group of G warps owns one row at a time, lane l of warp w of the group
+// owns the V chunks of 8 columns c = ((k G + w) 32 + l) 8, k < V.  The row's dh
+// and x stay in registers between the two halves of the row: (1) dot partials
+// and the dg column partials (dh n, n = x rstd: needs no dot) in registers,
+// the dot summed over the group (shuffle tree, then the G warp sums in warp
+// order through shared memory, one named barrier per row, slot double
+// buffered); (2) dx = dres + rstd (dh g - n dot / H) from the same registers.
+// So dh, x and dres are read once and dx written once (4 T H 2 B, the
+// algorithmic bytes); each CTA of R = 8 / G row groups strides over rows and
+// adds its groups' dg partials in group order into one partial row.
+constexpr int RF_WARPS = 8, RF_CTAS = 296;   // 2 CTAs per SM on 148 SMs
+template <int V>
+__global__ void __launch_bounds__(RF_WARPS * 32, 2) rmsnorm_bwd_fused_kernel(
+    const bf16* __restrict__ dh, const bf16* __restrict__ x, const bf16* __restrict__ g,
+    const float* __restrict__ rstd, const bf16* __restrict__ dres, bf16* __restrict__ dx, float* __restrict__ dgp,
+    int T, int H, int G) {
+  __shared__ float red[2][RF_WARPS];
+  extern __shared__ float4 dgs4[];                       // R x H fp32: each group's dg partial (own columns)
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int grp = warp / G, wig = warp % G, R = RF_WARPS / G;
+  const int col0 = (wig * 32 + lane) * 8, cstep = G * 256;   // lane's chunk k: col0 + k cstep
+  float* dgs = reinterpret_cast<float*>(dgs4);
+  float* acc = dgs + (int64_t)grp * H;                   // lane-private columns: no conflicts, no barrier
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    reinterpret_cast<float4*>(acc + (col0 + k * cstep))[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    reinterpret_cast<float4*>(acc + (col0 + k * cstep))[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  int par = 0;
+  const int stride = gridDim.x * R;
+  // every group runs the same number of iterations (named barriers need all G warps)
+  for (int row = blockIdx.x * R + grp; row - grp < T; row += stride, par ^= 1) {
+    const bool live = row < T;
+    const float rs = live ? rstd[row] : 0.0f;
+    // dh, x and dres of the row issued together: one memory round trip per row
+    const int64_t off = (int64_t)row * H + col0;
+    uint4 a[V], n[V], r[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      a[k] = n[k] = r[k] = make_uint4(0, 0, 0, 0);
+      if (live) {
+        a[k] = *reinterpret_cast<const uint4*>(dh + off + k * cstep);
+        n[k] = *reinterpret_cast<const uint4*>(x + off + k * cstep);
+        if (dres) r[k] = *reinterpret_cast<const uint4*>(dres + off + k * cstep);
+      }
+    }
+    float s = 0.0f;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const uint4 gq = __ldg(reinterpret_cast<const uint4*>(g + (col0 + k * cstep)));   // gamma: L1-resident
+      const bf162* ah = reinterpret_cast<const bf162*>(&a[k]);
+      const bf162* nh = reinterpret_cast<const bf162*>(&n[k]);
+      const bf162* gh = reinterpret_cast<const bf162*>(&gq);
+      float4* ap = reinterpret_cast<float4*>(acc + (col0 + k * cstep));
+      float4 c0 = ap[0], c1 = ap[1];
+      float* c = reinterpret_cast<float*>(&c0);
+      float* cc = reinterpret_cast<float*>(&c1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 af = __bfloat1622float2(ah[i]), nf = __bfloat1622float2(nh[i]), gf = __bfloat1622float2(gh[i]);
+        const float n0 = nf.x * rs, n1 = nf.y * rs;
+        float* t = i < 2 ? c : cc;
+        t[(2 * i) % 4] = fmaf(af.x, n0, t[(2 * i) % 4]);
+        t[(2 * i + 1) % 4] = fmaf(af.y, n1, t[(2 * i + 1) % 4]);
+        s = fmaf(af.x * gf.x, n0, s);
+        s = fmaf(af.y * gf.y, n1, s);
+      }
+      ap[0] = c0;
+      ap[1] = c1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (G > 1) {
+      if (lane == 0) red[par][warp] = s;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(G * 32) : "memory");
+      s = 0.0f;
+      for (int w = 0; w < G; ++w) s += red[par][grp * G + w];
+    }
+    if (!live) continue;
+    const float dm = s / (float)H;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const uint4 gq = __ldg(reinterpret_cast<const uint4*>(g + (col0 + k * cstep)));
+      const bf162* ah = reinterpret_cast<const bf162*>(&a[k]);
+      const bf162* nh = reinterpret_cast<const bf162*>(&n[k]);
+      const bf162* gh = reinterpret_cast<const bf162*>(&gq);
+      const bf162* rh = reinterpret_cast<const bf162*>(&r[k]);
+      float d[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 af = __bfloat1622float2(ah[i]), nf = __bfloat1622float2(nh[i]), gf = __bfloat1622float2(gh[i]);
+        const float2 rf = __bfloat1622float2(rh[i]);   // zero when dres is null
+        d[2 * i] = rf.x + rs * (af.x * gf.x - nf.x * rs * dm);
+        d[2 * i + 1] = rf.y + rs * (af.y * gf.y - nf.y * rs * dm);
+      }
+      store8(dx + off + k * cstep, d);
+    }
+  }
+  // dg partial row of this CTA: group 0 + group 1 + ... in group order, per column
+  __syncthreads();
+  for (int c = threadIdx.x * 4; c < H; c += RF_WARPS * 32 * 4) {
+    float4 t = *reinterpret_cast<const float4*>(dgs + c);
+    for (int q = 1; q < R; ++q) {
+      const float4 u = *reinterpret_cast<const float4*>(dgs + (int64_t)q * H + c);
+      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+    }
+    *reinterpret_cast<float4*>(dgp + (int64_t)blockIdx.x * H + c) = t;
+  }
+}
+
+// (V, G) of the one-pass form for H, or V = 0 (two-pass form)
+static void rmsnorm_fused_shape(int H, int& V, int& G) {
+  V = 0;
+  G = 0;
+  if (H <= 0 || H % 256 != 0 || std::getenv("DC_RMSNORM_TWO_PASS")) return;
+  const int c = H / 256;
+  const int v = c >= 4 ? 4 : c;
+  if (c % v != 0) return;
+  const int g = c / v;
+  if (g != 1 && g != 2 && g != 4 && g != 8) return;
+  V = v;
+  G = g;
+}
+
+static int rmsnorm_fused_ctas(int T, int H, int G) {
+  const int R = RF_WARPS / G;
+  const int need = (T + R - 1) / R;
+  return need < RF_CTAS ? (need > 0 ? need : 1) : RF_CTAS;
+}
+
+int64_t rmsnorm_bwd_ws_floats(int T, int H) {
+  const int64_t two = (int64_t)rmsnorm_bwd_blocks(T) * H + T;
+  const int64_t one = (int64_t)RF_CTAS * H;
+  return two > one ? two : one;
+}
+
+int k_rmsnorm_bwd(const void* dh, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
+                  float* dg_partial, int T, int H, cudaStream_t st) {
+  int V, G;
+  rmsnorm_fused_shape(H, V, G);
+  if (V > 0) {
+    const int ctas = rmsnorm_fused_ctas(T, H, G);
+    const size_t smem = (size_t)(RF_WARPS / G) * H * sizeof(float);
+    auto launch = [&](auto kern) {   // smem = R H 4 B <= 32 KiB (H = 256 V G, R = 8 / G)
+      kern<<<ctas, RF_WARPS * 32, smem, st>>>((const bf16*)dh, (const bf16*)x, (const bf16*)g, rstd,
+                                                (const bf16*)dres, (bf16*)dx, dg_partial, T, H, G);
+    };
+    if (V == 4) launch(rmsnorm_bwd_fused_kernel<4>);
+    else if (V == 2) launch(rmsnorm_bwd_fused_kernel<2>);
+    else launch(rmsnorm_bwd_fused_kernel<1>);
+    count_launch();
+    return ctas;
+  }
   float* dot = dg_partial + (int64_t)rmsnorm_bwd_blocks(T) * H;    // T floats of scratch after the partials
   rmsnorm_bwd_dot_kernel<<<(T + RD_WARPS - 1) / RD_WARPS, RD_WARPS * 32, 0, st>>>(
       (const bf16*)dh, (const bf16*)x, (const bf16*)g, rstd, dot, T, H);
@@ -235,6 +387,7 @@ void k_rmsnorm_bwd(const void* dh, const void* x, const void* g, const float* rs
                                                (const bf16*)dres, (bf16*)dx, dg_partial, T, H);
   count_launch();
   count_launch();
+  return rmsnorm_bwd_blocks(T);
 }
 
 // out[c] = bf16(sum_b p[b][c]): a CTA owns 32 columns; warp w sums rows
@@ -247,6 +400,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ p
   const int c = blockIdx.x * 32 + lane;
   float s = 0.0f;
   if (c < H)
+#pragma unroll 8
     for (int b = w; b < nblk; b += 8) s += p[(int64_t)b * H + c];
   sh[w][lane] = s;
   __syncthreads();

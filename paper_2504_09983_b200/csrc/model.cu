@@ -322,7 +322,7 @@ extern "C" dc_status dc_model_create(dc_ctx* ctx, const dc_model_dims* d, dc_mod
   const uint64_t ws0 = off;
   m->ws_dA = take(T * h * 2); m->ws_dB = take(T * h * 2); m->ws_dact = take(T * f * 2);
   m->ws_dgu = take(T * 2 * f * 2); m->ws_dh = take(T * h * 2); m->ws_dx2 = take(T * h * 2);
-  m->ws_dqkv = take(T * m->qkvd * 2); m->ws_dgp = take(((int64_t)rmsnorm_bwd_blocks((int)T) * h + T) * 4);   // partials + row dots
+  m->ws_dqkv = take(T * m->qkvd * 2); m->ws_dgp = take(rmsnorm_bwd_ws_floats((int)T, (int)h) * 4);   // dg partials (+ row dots)
   m->ws_lossp = take(1024 * 4); m->ws_loss = take(4 * (int64_t)m->n_micro);
   m->ws_sk = take((int64_t)gemm_workspace_bytes());
   if (m->E) {
@@ -475,13 +475,13 @@ static dc_status gemm(dc_model* m, int M, int N, int K, const void* A, int64_t l
 }
 
 // RMSNorm backward: dx = dres + rstd (dh g - n mean(dh g n)), dg = sum_rows dh n
-// (two passes + the dg column sum; a one-pass form with the column sum in the
-// last CTA measured 1.9x slower in the step, r02: 4.0 vs 2.1 ms per step)
+// (one pass with register-resident rows, or two passes for other H; then the
+// dg column sum of the partial rows)
 static dc_status rmsnorm_bwd(dc_model* m, const void* dh, const void* x, const void* g, const float* rstd,
                              const void* dres, void* dx, void* dg, cudaStream_t st) {
   const int T = m->d.tokens, H = m->d.hidden;
-  k_rmsnorm_bwd(dh, x, g, rstd, dres, dx, (float*)m->A(m->ws_dgp), T, H, st);
-  k_colsum_to_bf16((float*)m->A(m->ws_dgp), rmsnorm_bwd_blocks(T), H, dg, st);
+  const int nblk = k_rmsnorm_bwd(dh, x, g, rstd, dres, dx, (float*)m->A(m->ws_dgp), T, H, st);
+  k_colsum_to_bf16((float*)m->A(m->ws_dgp), nblk, H, dg, st);
   return DC_OK;
 }
 
