@@ -436,12 +436,18 @@ def run_parallel(ranks, fn):
 
 def step(ranks, t, profile=False):
     """One dc_model_step per rank (profile: False/0, True/1 = record+read,
-    2 = record only)."""
+    2 = record only).  Several virtual ranks in this process: returns once
+    their step has finished on the device, so the spin-waits of one set of
+    virtual ranks never share hardware queues with another set's work that
+    a later call enqueues (a wait at a queue's head blocks everything behind
+    it: profiles/r02/stalls/).  One rank per process: asynchronous."""
     mode = int(profile) if not isinstance(profile, bool) else (1 if profile else 0)
 
     def one(st):
         dc.check(dc.lib.dc_model_step(st.model, t, mode, *st.stream_handles()), st.ctx)
     run_parallel(ranks, one)
+    if len(ranks) > 1:
+        torch.cuda.synchronize()
 
 
 def poll(ranks):
