@@ -345,12 +345,15 @@ static void rmsnorm_fused_shape(int H, int& V, int& G) {
   G = 0;
   if (H <= 0 || H % 256 != 0 || std::getenv("DC_RMSNORM_TWO_PASS")) return;   // A/B: previous kernels
   const int c = H / 256;
-  const int v = c >= 4 ? 4 : c;
-  if (c % v != 0) return;
-  const int g = c / v;
-  if (g != 1 && g != 2 && g != 4 && g != 8) return;
-  V = v;
-  G = g;
+  for (int v = 4; v >= 1; v /= 2) {            // largest V in {4, 2, 1} with G = c / V in {1, 2, 4, 8}
+    if (c % v) continue;
+    const int g = c / v;
+    if (g == 1 || g == 2 || g == 4 || g == 8) {
+      V = v;
+      G = g;
+    }
+    return;                                      // (H = 768: c = 3 -> two-pass form)
+  }
 }
 
 static int rmsnorm_fused_ctas(int T, int H, int G) {

@@ -70,6 +70,19 @@ def test_step_matches_oracle(world, passes, fused):
         check_step(ranks, table, cfg, world, t, LR, lambda: rt.step(ranks, t), skip_grads=skip)
 
 
+@pytest.mark.parametrize("hidden,heads,kv", [(256, 2, 2), (768, 6, 2), (1024, 8, 2), (2048, 16, 4), (8192, 64, 8)])
+def test_hidden_sizes_match_oracle(hidden, heads, kv):
+    """Every row split of the one-pass RMSNorm backward (H = 256 V G: V = 1,
+    G = 1; V = 4 with G = 1 / 2 / 8) and the two-pass fallback (H = 768), each
+    through a whole step checked against the oracle (gamma gradients
+    element-wise, update exact); T = 40 tokens (not a multiple of the
+    kernel's rows per CTA x grid)."""
+    import dataclasses
+    cfg = dataclasses.replace(synth.small_llama(layers=1, seq=40), hidden=hidden, ffn=256, n_heads=heads, n_kv=kv)
+    table, ranks = _setup(cfg, 1, dc.DC_PASS_SHARD)
+    check_step(ranks, table, cfg, 1, 1, LR, lambda: rt.step(ranks, 1))
+
+
 def test_layer_outputs_and_two_steps():
     cfg = synth.small_llama(layers=2, seq=256)
     table, ranks = _setup(cfg, 1, dc.DC_PASS_SHARD)
