@@ -371,6 +371,8 @@ def measure_tc(group, world, dev, torch, dist):
         pts.append([full, max(1, int(round(us.item())))])
     for i in range(1, len(pts)):
         pts[i][1] = max(pts[i][1], pts[i - 1][1])
+    del x, out
+    torch.cuda.empty_cache()          # the sweep's buffers (up to 1 GiB) leave the allocator's cache
     return pts
 
 
