@@ -396,30 +396,31 @@ int k_rmsnorm_bwd(const void* dh, const void* x, const void* g, const float* rst
   return rmsnorm_bwd_blocks(T);
 }
 
-// out[c] = bf16(sum_b p[b][c]): a CTA owns 32 columns; warp w sums rows
-// w, w + 8, ... (coalesced 128 B per row), then the 8 partials are added in
-// warp order (fixed, deterministic)
+// out[c] = bf16(sum_b p[b][c]): a CTA owns 8 columns (one 32-byte sector per
+// row); thread t sums rows t / 8, t / 8 + 32, ... of column t % 8, then the 32
+// row-lane partials of a column are added in order (fixed, deterministic).
+// 8 columns per CTA spreads the few-hundred-row sums over H / 8 CTAs.
 __global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ p, int nblk, int H,
                                                      bf16* __restrict__ out) {
-  __shared__ float sh[8][33];
-  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
-  const int c = blockIdx.x * 32 + lane;
+  __shared__ float sh[32][9];
+  const int cl = threadIdx.x % 8, rl = threadIdx.x / 8;
+  const int c = blockIdx.x * 8 + cl;
   float s = 0.0f;
   if (c < H)
-#pragma unroll 8
-    for (int b = w; b < nblk; b += 8) s += p[(int64_t)b * H + c];
-  sh[w][lane] = s;
+#pragma unroll 4
+    for (int b = rl; b < nblk; b += 32) s += p[(int64_t)b * H + c];
+  sh[rl][cl] = s;
   __syncthreads();
-  if (w == 0 && c < H) {
+  if (threadIdx.x < 8 && c < H) {
     float t = 0.0f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += sh[k][lane];
+    for (int k = 0; k < 32; ++k) t += sh[k][cl];
     out[c] = __float2bfloat16_rn(t);
   }
 }
 
 void k_colsum_to_bf16(const float* partial, int nblk, int H, void* out, cudaStream_t st) {
-  colsum_kernel<<<(H + 31) / 32, 256, 0, st>>>(partial, nblk, H, (bf16*)out);
+  colsum_kernel<<<(H + 7) / 8, 256, 0, st>>>(partial, nblk, H, (bf16*)out);
   count_launch();
 }
 
