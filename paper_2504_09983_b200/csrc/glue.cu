@@ -230,12 +230,13 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_dx_kernel(const bf16* __restr
 
 // One-pass form (default when H = 256 V G, V in {1, 2, 4}, G in {1, 2, 4, 8}):
 // a row group of G warps owns one row at a time, lane l of warp w of the group
-// owns the V chunks of 8 columns c = ((k G + w) 32 + l) 8, k < V.  The row's dh
-// and x stay in registers between the two halves of the row: (1) dot partials
-// and the dg column partials (dh n, n = x rstd: needs no dot) in registers,
-// the dot summed over the group (shuffle tree, then the G warp sums in warp
-// order through shared memory, one named barrier per row, slot double
-// buffered); (2) dx = dres + rstd (dh g - n dot / H) from the same registers.
+// owns the V chunks of 8 columns c = ((k G + w) 32 + l) 8, k < V.  The row's dh,
+// x and dres are loaded in one round trip and stay in registers between the
+// two halves of the row: (1) the dot partial in a register and the dg column
+// partials (dh n, n = x rstd: needs no dot) added into the group's shared-memory
+// row (lane-private columns), the dot summed over the group (shuffle tree, then
+// the G warp sums in warp order through shared memory, one named barrier per
+// row, slot double buffered); (2) dx = dres + rstd (dh g - n dot / H).
 // So dh, x and dres are read once and dx written once (4 T H 2 B, the
 // algorithmic bytes); each CTA of R = 8 / G row groups strides over rows and
 // adds its groups' dg partials in group order into one partial row.
