@@ -83,6 +83,36 @@ def test_hidden_sizes_match_oracle(hidden, heads, kv):
     check_step(ranks, table, cfg, 1, 1, LR, lambda: rt.step(ranks, 1))
 
 
+@pytest.mark.parametrize("world", [1, 2])
+def test_device_memory_within_plan(world):
+    """P_mem fidelity: every device buffer of a run is a torch
+    allocation, so the allocator's peak over two planned steps is bounded by
+    the plan's peak (P_mem + transient, m / v added back as M_opt) per rank.
+    At N = 1 a gather aliases the shard, so the device may sit below the plan
+    by at most the bf16 weight bytes the plan counts as gathered; at N > 1 the
+    arena is one allocation of the plan's capacity."""
+    cfg = synth.small_llama(layers=2, seq=256)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    torch.cuda.reset_peak_memory_stats()
+    base = torch.cuda.memory_allocated()
+    table, ranks = _setup(cfg, world, dc.DC_PASS_SHARD | dc.DC_PASS_PREFETCH | dc.DC_PASS_UNSHARD)
+    for t in (1, 2):
+        rt.step(ranks, t)
+    torch.cuda.synchronize()
+    rt.poll(ranks)
+    dev = torch.cuda.max_memory_allocated() - base
+    plan = json.loads(dc.schedule_json(ranks[0].sched))
+    # M_opt: Adam m / v (reading D14; the plan adds it only when the profile lists state fragments)
+    m_opt = plan["m_opt"] or 2 * 4 * ranks[0].tensors["m"].numel()
+    per_rank = plan["peak_no_opt"] + m_opt
+    small = 8 << 20          # flag tables, loss / scalar words, allocator rounding
+    assert dev <= world * per_rank + world * small, (dev, per_rank)
+    weights = sum(nx.shard_len(p.numel, world) * world * 2 for p in table)
+    slack = weights if world == 1 else plan["capacity"]
+    assert dev >= world * (per_rank - slack) - world * small, (dev, per_rank, slack)
+
+
 def test_layer_outputs_and_two_steps():
     cfg = synth.small_llama(layers=2, seq=256)
     table, ranks = _setup(cfg, 1, dc.DC_PASS_SHARD)
