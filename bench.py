@@ -164,8 +164,15 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].strip() == "Active"})
         load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        pw = []
+        for r in rows:
+            try:
+                pw.append(float(r[3]))
+            except ValueError:
+                pass
         return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows),
+                "power_w": {"median": statistics.median(pw), "max": max(pw)} if pw else None}
 
 
 BAD_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}

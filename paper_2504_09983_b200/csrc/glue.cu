@@ -344,7 +344,8 @@ __global__ void __launch_bounds__(RF_WARPS * 32, 2) rmsnorm_bwd_fused_kernel(
 static void rmsnorm_fused_shape(int H, int& V, int& G) {
   V = 0;
   G = 0;
-  if (H <= 0 || H % 256 != 0 || std::getenv("DC_RMSNORM_TWO_PASS")) return;   // A/B: previous kernels
+  static const bool two_pass = std::getenv("DC_RMSNORM_TWO_PASS") != nullptr;   // A/B: previous kernels
+  if (H <= 0 || H % 256 != 0 || two_pass) return;
   const int c = H / 256;
   for (int v = 4; v >= 1; v /= 2) {            // largest V in {4, 2, 1} with G = c / V in {1, 2, 4, 8}
     if (c % v) continue;

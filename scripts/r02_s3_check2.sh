@@ -1,0 +1,11 @@
+#!/bin/bash
+# final-build check: GPU suite, smoke, default bench (with power draw), N = 2 launch path (processes sharing one GPU)
+O=gpurun_out/r02s3check2; mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1
+echo "gpu suite rc=$? $(grep -E 'passed|failed' $O/pytest_gpu.log | tail -1)" > $O/summary.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+echo "smoke rc=$? $(tail -1 $O/smoke.log)" >> $O/summary.txt
+timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err
+echo "bench rc=$?" >> $O/summary.txt
+timeout 900 python bench.py --gpus 2 --share-gpu --layers 4 --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_share2.json 2> $O/bench_share2.err
+echo "share-gpu N=2 rc=$?" >> $O/summary.txt
