@@ -412,7 +412,12 @@ dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t which, void
  * "stream_k" (default 1 unless N > 1 virtual ranks share the GPU): the layer
  * GEMMs split their last waves with stream-K (dc_gemm_args.stream_k).
  * "rs_overlap" (default 1 at N > 1, 0 at N = 1): reduce-scatter + Adam on the rs stream beside the
- * backward GEMMs; 0 runs it in compute-stream order. */
+ * backward GEMMs; 0 runs it in compute-stream order.
+ * "dw_stream" / "wb_stream" (value = a cudaStream_t, caller-owned, must outlive
+ * the model): the stream of the concurrent dW GEMMs / of the host-state
+ * write-backs instead of one the model creates (DC_EINVAL for 0, DC_ESTATE
+ * after graph capture).  Virtual ranks sharing one GPU pass streams from one
+ * pool so that no two ranks share a hardware queue. */
 dc_status dc_model_set_option(dc_model* m, const char* key, int64_t value);
 /* Host-resident optimizer states (reading D28; §4.4 P:370-408 with
  * the update fused per layer, D17).  After dc_bind_schedule of a plan whose

@@ -607,6 +607,8 @@ cudaError_t preload_glue_kernels() {
   const void* fns[] = {(const void*)init_param_kernel, (const void*)rmsnorm_fwd_kernel,
                        (const void*)colsum_kernel,
                        (const void*)rmsnorm_bwd_dot_kernel, (const void*)rmsnorm_bwd_dx_kernel,
+                       (const void*)rmsnorm_bwd_fused_kernel<1>, (const void*)rmsnorm_bwd_fused_kernel<2>,
+                       (const void*)rmsnorm_bwd_fused_kernel<4>,
                        (const void*)rmsnorm_fwd_warp_kernel,
                        (const void*)attn_mix_fwd_kernel, (const void*)attn_mix_bwd_kernel,
                        (const void*)act_fwd_kernel, (const void*)act_bwd_kernel,

@@ -133,6 +133,7 @@ struct dc_model {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   cudaStream_t cs2 = nullptr;
+  bool cs2_own = true;                // false: the caller's (option "dw_stream")
   cudaEvent_t ev_fork = nullptr, ev_joinw = nullptr;
   int fuse_act = 0;                  // bit 0: SiLU*up in the gate|up GEMM epilogue; bit 1: its backward
                                      // in the down dX epilogue.  Bit-identical; measured no faster in
@@ -148,6 +149,7 @@ struct dc_model {
   // (H2D, copy stream): PCIe is full duplex.  wb_ev[f] = f's last write-back;
   // a reload waits for every write-back of its ring slot (and of itself)
   cudaStream_t wb_stream = nullptr;
+  bool wb_own = true;                 // false: the caller's (option "wb_stream")
   std::vector<cudaEvent_t> wb_ev;
   std::vector<int> frag_slot;
   std::string err;
@@ -374,10 +376,10 @@ extern "C" dc_status dc_model_destroy(dc_model* m) {
   }
   for (auto& e : m->ev_join) if (e) cudaEventDestroy(e);
   for (auto& e : m->wb_ev) cudaEventDestroy(e);
-  if (m->wb_stream) cudaStreamDestroy(m->wb_stream);
+  if (m->wb_stream && m->wb_own) cudaStreamDestroy(m->wb_stream);
   if (m->graph_exec) cudaGraphExecDestroy(m->graph_exec);
   if (m->graph) cudaGraphDestroy(m->graph);
-  if (m->cs2) cudaStreamDestroy(m->cs2);
+  if (m->cs2 && m->cs2_own) cudaStreamDestroy(m->cs2);
   if (m->ev_fork) cudaEventDestroy(m->ev_fork);
   if (m->ev_joinw) cudaEventDestroy(m->ev_joinw);
   sm_partition_destroy(&m->part);
@@ -1103,6 +1105,25 @@ extern "C" dc_status dc_model_act_ptr(const dc_model* m, int32_t layer, int32_t 
 
 extern "C" dc_status dc_model_set_option(dc_model* m, const char* key, int64_t value) {
   if (!m || !key) return mfail(nullptr, DC_EINVAL, "dc_model_set_option: null argument");
+  if (!strcmp(key, "dw_stream") || !strcmp(key, "wb_stream")) {
+    // caller-supplied (not owned) stream for the concurrent dW GEMMs / the
+    // host-state write-backs instead of one the library creates: several
+    // virtual ranks in one process then draw every stream from one pool whose
+    // streams sit on distinct hardware queues, so no rank's spin-wait can
+    // block a peer's dW GEMM or copy (profiles/r02/stalls/)
+    if (!value) return mfail(m, DC_EINVAL, "dw_stream / wb_stream: null stream");
+    if (m->graph_exec) return mfail(m, DC_ESTATE, "dw_stream / wb_stream: set before graph capture");
+    cudaStream_t sv = reinterpret_cast<cudaStream_t>(static_cast<intptr_t>(value));
+    cudaStream_t& slot = key[0] == 'd' ? m->cs2 : m->wb_stream;
+    bool& own = key[0] == 'd' ? m->cs2_own : m->wb_own;
+    if (slot && own) {
+      cudaStreamSynchronize(slot);
+      cudaStreamDestroy(slot);
+    }
+    slot = sv;
+    own = false;
+    return DC_OK;
+  }
   if (!strcmp(key, "side_adam")) {
     if (value && ctx_world(m->ctx) != 1) return mfail(m, DC_EINVAL, "side_adam needs N == 1");
     if (value && m->E) return mfail(m, DC_EINVAL, "side_adam: Llama-shaped layers only");

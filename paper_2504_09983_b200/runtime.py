@@ -43,6 +43,7 @@ class RankState:
         self.peer_keep = {}     # per symmetric buffer: imported peer mappings (IPC storages / symm_mem handle)
         self.nvls = None        # what bind_multicast selected (N > 1, DC_NVLS)
         self.streams = None
+        self.aux_streams = []    # virtual ranks: the model's dW / write-back streams (from the pool)
         self.sched = None
         self.micro_steps = 1
 
@@ -261,6 +262,16 @@ def attach_model(ranks, cfg, xs, targets, checkpoint=False):
                                       targets[r].data_ptr()))
         if len(ranks) >= 8:      # virtual ranks: no second GEMM stream (see create_ranks)
             dc.check(dc.lib.dc_model_set_option(m, b"dw_concurrent", 0))
+            st.aux_streams = [st.streams[2]]
+        elif len(ranks) > 1:
+            # virtual ranks: the dW and write-back streams come from torch's stream pool
+            # like the rank's other streams (distinct hardware queues), not from
+            # cudaStreamCreate inside the library, whose queue is whichever one the
+            # process-wide round robin reached — possibly one a peer's spin-wait holds
+            st.aux_streams = [torch.cuda.Stream(device=st.device) for _ in range(2)]
+        if len(ranks) > 1:
+            dc.check(dc.lib.dc_model_set_option(m, b"dw_stream", st.aux_streams[0].cuda_stream), st.ctx)
+            dc.check(dc.lib.dc_model_set_option(m, b"wb_stream", st.aux_streams[-1].cuda_stream), st.ctx)
 
 
 def bind(ranks, sched_by_rank, group=None):
@@ -451,9 +462,16 @@ def step(ranks, t, profile=False):
 
 
 def poll(ranks):
-    """Raise if any rank's device flag wait timed out (sticky error word)."""
+    """Raise if any rank's device flag wait timed out (sticky error word); the
+    message carries every failing rank's record (which flag each one waited
+    on), so a cross-rank stall shows both ends."""
+    errs = []
     for st in ranks.values():
-        dc.check(dc.lib.dc_poll(st.ctx), st.ctx)
+        status = dc.lib.dc_poll(st.ctx)
+        if status != dc.DC_OK:
+            errs.append((status, dc.last_error(st.ctx)))
+    if errs:
+        raise dc.DCError(errs[0][0], " | ".join(m for _, m in errs))
 
 
 def loss_ptr(st):

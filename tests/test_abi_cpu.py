@@ -184,3 +184,23 @@ def test_hot_kernels_have_no_local_memory():
     assert len(hot) >= 8, [f[0] for f in hot]
     bad = [(f[0], f[2], f[3]) for f in hot if int(f[2]) or int(f[3])]
     assert not bad, bad
+
+
+def test_every_kernel_is_preloaded():
+    """Every __global__ kernel of the library is force-loaded at dc_init
+    (preload_*_kernels: cudaFuncGetAttributes / cudaFuncSetAttribute).  With
+    CUDA lazy loading a kernel's first launch loads its module, which can
+    block behind another virtual rank's spinning wait kernel — a cross-rank
+    stall (r02 session 3: the new one-pass RMSNorm backward kernel was not in
+    the list; 2-rank tests stalled in 5 of 16 runs until it was)."""
+    import glob
+    src = {f: open(f).read() for f in glob.glob(os.path.join(ROOT, "paper_2504_09983_b200", "csrc", "*.cu"))}
+    kernels = set()
+    for f, s in src.items():
+        for m in re.finditer(r"__global__\s+void\s+((?:__\w+__\([^)]*\)\s+)*)(\w+)\s*\(", s):
+            kernels.add((os.path.basename(f), m.group(2)))
+    assert len(kernels) > 20, kernels
+    pre = "".join(m.group(1) for s in src.values()
+                  for m in re.finditer(r"cudaError_t preload_\w+\(\)\s*\{(.*?)\n\}", s, re.S))
+    missing = sorted(k for k in kernels if not re.search(r"\b%s\b" % k[1], pre))
+    assert not missing, missing
