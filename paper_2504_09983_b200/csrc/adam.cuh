@@ -17,13 +17,30 @@ namespace dc {
 
 struct AdamScalars {
   float w1, w2, b2, neg_s, c, eps, invN;
+  float rc;            // RN(1 / c), once per thread (DC_ADAM_RCP_DIV)
 };
+
+__device__ __forceinline__ AdamScalars adam_scalars(float w1, float w2, float b2, float neg_s, float c, float eps,
+                                                    float invN) {
+  return AdamScalars{w1, w2, b2, neg_s, c, eps, invN, __frcp_rn(c)};
+}
 
 __device__ __forceinline__ void adam_elem(float gsum, float& p, float& m, float& v, const AdamScalars& a) {
   const float g = __fmul_rn(gsum, a.invN);
   m = __fadd_rn(m, __fmul_rn(a.w1, __fsub_rn(g, m)));
   v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(__fmul_rn(a.w2, g), g));
+#ifdef DC_ADAM_RCP_DIV
+  // sqrt(v) / c with the step constant's reciprocal rc = RN(1/c) and two FMA
+  // residual corrections (Markstein): equal to div.rn for every x in
+  // [2^-75, 2^64], which holds every sqrt of a finite v >= 0 except 0, where
+  // both give 0 (exhaustive check: profiles/r01g/adam_div/)
+  const float x = __fsqrt_rn(v), rc = a.rc;
+  const float q0 = __fmul_rn(x, rc);
+  const float q1 = __fmaf_rn(__fmaf_rn(-a.c, q0, x), rc, q0);
+  const float d = __fadd_rn(__fmaf_rn(__fmaf_rn(-a.c, q1, x), rc, q1), a.eps);
+#else
   const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), a.c), a.eps);
+#endif
   p = __fadd_rn(p, __fdiv_rn(__fmul_rn(a.neg_s, m), d));
 }
 

@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(256, DC_RS_MINB) rs_adam_kernel(const RsParams
   constexpr int RS_UNR = RsUnr<MAXQ, MODE>::value;
   {   // grad-ready of every rank was awaited by the preceding wait kernel
     const uint64_t pol = policy_evict_first();
-    const AdamScalars a{p.w1, p.w2, p.b2, p.scal ? -p.scal[0] : p.neg_s, p.scal ? p.scal[1] : p.c, p.eps, p.invN};
+    const AdamScalars a = adam_scalars(p.w1, p.w2, p.b2, p.scal ? -p.scal[0] : p.neg_s, p.scal ? p.scal[1] : p.c, p.eps, p.invN);
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     for (int mi = 0; mi < p.nm; ++mi) {
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(RSB_THREADS, RSB_CTAS_PER_SM) rs_adam_bulk_ker
       }
     }
   } else {                                     // consumers
-    const AdamScalars a{p.w1, p.w2, p.b2, p.scal ? -p.scal[0] : p.neg_s, p.scal ? p.scal[1] : p.c, p.eps, p.invN};
+    const AdamScalars a = adam_scalars(p.w1, p.w2, p.b2, p.scal ? -p.scal[0] : p.neg_s, p.scal ? p.scal[1] : p.c, p.eps, p.invN);
     const int t = threadIdx.x;
     int k = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++k) {

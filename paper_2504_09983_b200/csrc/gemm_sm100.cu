@@ -607,7 +607,7 @@ __device__ __forceinline__ void side_job(const SideJob& sj, int side_warp, int l
   const int64_t nthr = (int64_t)gridDim.x * SIDE_WARPS * 32;
   const int64_t t = (int64_t)blockIdx.x * SIDE_WARPS * 32 + side_warp * 32 + lane;
   const uint64_t pol = policy_evict_first();
-  const AdamScalars a{sj.w1, sj.w2, sj.b2, sj.neg_s, sj.c, sj.eps, 1.0f};
+  const AdamScalars a = adam_scalars(sj.w1, sj.w2, sj.b2, sj.neg_s, sj.c, sj.eps, 1.0f);
   for (int64_t g = sj.g0 + t; g < sj.g1; g += 2 * nthr) {
     Group8<1> x[2];
     int mi[2];

@@ -125,7 +125,7 @@ struct RsMcParams {
 template <int MODE>
 __global__ void __launch_bounds__(RSN_THREADS) rs_adam_nvls_kernel(const RsMcParams p) {
   const uint64_t pol = policy_evict_first();
-  const AdamScalars a{p.w1, p.w2, p.b2, p.scal ? -p.scal[0] : p.neg_s, p.scal ? p.scal[1] : p.c, p.eps, p.invN};
+  const AdamScalars a = adam_scalars(p.w1, p.w2, p.b2, p.scal ? -p.scal[0] : p.neg_s, p.scal ? p.scal[1] : p.c, p.eps, p.invN);
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   for (int mi = 0; mi < p.nm; ++mi) {
