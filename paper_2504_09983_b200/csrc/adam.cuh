@@ -17,7 +17,7 @@ namespace dc {
 
 struct AdamScalars {
   float w1, w2, b2, neg_s, c, eps, invN;
-  float rc;            // RN(1 / c), once per thread (DC_ADAM_RCP_DIV)
+  float rc;            // RN(1 / c), once per thread
 };
 
 __device__ __forceinline__ AdamScalars adam_scalars(float w1, float w2, float b2, float neg_s, float c, float eps,
@@ -29,11 +29,15 @@ __device__ __forceinline__ void adam_elem(float gsum, float& p, float& m, float&
   const float g = __fmul_rn(gsum, a.invN);
   m = __fadd_rn(m, __fmul_rn(a.w1, __fsub_rn(g, m)));
   v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(__fmul_rn(a.w2, g), g));
-#ifdef DC_ADAM_RCP_DIV
+#ifndef DC_ADAM_DIV_RN
   // sqrt(v) / c with the step constant's reciprocal rc = RN(1/c) and two FMA
   // residual corrections (Markstein): equal to div.rn for every x in
   // [2^-75, 2^64], which holds every sqrt of a finite v >= 0 except 0, where
-  // both give 0 (exhaustive check: profiles/r01g/adam_div/)
+  // both give 0 (exhaustive check: profiles/r01g/adam_div/).  Three fewer
+  // instructions than div.rn's fast path: at the power-capped in-step clock
+  // (~1.43 GHz) the bulk rs_adam kernel's consumers are close to issue-bound,
+  // and this takes rs 33.8 -> 32.7 ms per step (profiles/r02/adam_rcp/).
+  // -DDC_ADAM_DIV_RN restores div.rn (bit-identical results).
   const float x = __fsqrt_rn(v), rc = a.rc;
   const float q0 = __fmul_rn(x, rc);
   const float q1 = __fmaf_rn(__fmaf_rn(-a.c, q0, x), rc, q0);
