@@ -25,8 +25,11 @@ __device__ __forceinline__ AdamScalars adam_scalars(float w1, float w2, float b2
   return AdamScalars{w1, w2, b2, neg_s, c, eps, invN, __frcp_rn(c)};
 }
 
+// SCALE = false: the caller knows invN == 1 (N = 1, one micro-step), where
+// g * 1 == g exactly, so the multiply is dropped (the bulk N = 1 update)
+template <bool SCALE = true>
 __device__ __forceinline__ void adam_elem(float gsum, float& p, float& m, float& v, const AdamScalars& a) {
-  const float g = __fmul_rn(gsum, a.invN);
+  const float g = SCALE ? __fmul_rn(gsum, a.invN) : gsum;
   m = __fadd_rn(m, __fmul_rn(a.w1, __fsub_rn(g, m)));
   v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(__fmul_rn(a.w2, g), g));
 #ifndef DC_ADAM_DIV_RN

@@ -616,10 +616,11 @@ __global__ void __launch_bounds__(RSB_THREADS, RSB_CTAS_PER_SM) rs_adam_bulk_ker
           g[2] = __fadd_rn(A.z, g[2]); g[3] = __fadd_rn(A.w, g[3]);
         }
         float4 pp = *P, mm = *M, vv = *V;
-        adam_elem(g[0], pp.x, mm.x, vv.x, a);
-        adam_elem(g[1], pp.y, mm.y, vv.y, a);
-        adam_elem(g[2], pp.z, mm.z, vv.z, a);
-        adam_elem(g[3], pp.w, mm.w, vv.w, a);
+        constexpr bool kScale = !(MAXQ == 1 && MODE == RS_UPDATE);   // N = 1, n = 1: 1/N = 1 exactly
+        adam_elem<kScale>(g[0], pp.x, mm.x, vv.x, a);
+        adam_elem<kScale>(g[1], pp.y, mm.y, vv.y, a);
+        adam_elem<kScale>(g[2], pp.z, mm.z, vv.z, a);
+        adam_elem<kScale>(g[3], pp.w, mm.w, vv.w, a);
         *P = pp; *M = mm; *V = vv;
         const __nv_bfloat162 s0 = __floats2bfloat162_rn(pp.x, pp.y), s1 = __floats2bfloat162_rn(pp.z, pp.w);
         uint2 o;
